@@ -1,0 +1,178 @@
+/*
+ * uniprefill_b200.h -- C ABI of the B200-native UniPrefill token-selection hot path.
+ *
+ * One entry point per reference operation on the path.  The reference
+ * exposes a C++ namespace API over host matrices (/root/reference/proj/core/include/
+ * uniprefill/*.hpp); this ABI replaces it for device-resident, continuous-batching varlen
+ * batches indexed by cu_seqlens:
+ *
+ *   up_score_blocks        replaces score_tokens / score_tokens_heads
+ *                          (importance.hpp:42-47, importance.cpp:17-132) and, through the
+ *                          head range, sharded_block_scores (tp_sim.hpp:25-26)
+ *   up_reduce_block_scores replaces allreduce_scores (tp_sim.hpp:31, tp_sim.cpp:29-49)
+ *                          for shard partials that are device-addressable from one GPU
+ *   up_select              replaces top_p_select + expand_mask (selection.hpp:46-54,
+ *                          selection.cpp:36-122) and the no-readmission veto
+ *                          (restrict_selection, propagation.cpp:116-136, :173-183)
+ *   up_compact             replaces apply_drop + gather_rows + patch_metadata
+ *                          (propagation.cpp:47-77, :105-112; scheduler.cpp:50-90)
+ *   up_drop_layer          the three above back to back (prefill_layer_step's
+ *                          score -> select -> compact section, propagation.cpp:163-202)
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; every data pointer is DEVICE memory owned by the
+ *     caller unless stated otherwise.  `stream` is a cudaStream_t (NULL = legacy stream).
+ *   - All work is stream-ordered and asynchronous; no entry point synchronizes.
+ *   - Shapes are data-dependent after a drop, so launch sizing never needs the segment
+ *     lengths on the host: callers pass capacities (max_tokens) and the device-resident
+ *     cu_seqlens.  The whole layer step can be captured in a CUDA graph.
+ *   - Errors: host-detectable problems return a status immediately (ConfigError ->
+ *     UP_ERR_CONFIG, ContractViolation -> UP_ERR_CONTRACT, errors.hpp:13-42).  Problems
+ *     only visible on the device (negative / non-finite block scores, malformed
+ *     cu_seqlens) raise a sticky flag in the workspace; up_device_status() reads and
+ *     clears it.  No exception crosses the ABI.
+ *   - Re-entrant: distinct workspaces may be used concurrently on distinct streams.
+ */
+#ifndef UNIPREFILL_B200_H
+#define UNIPREFILL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UP_ABI_VERSION 1
+
+typedef enum {
+    UP_OK = 0,
+    UP_ERR_CONFIG = 1,         /* ConfigError (errors.hpp:15-18) */
+    UP_ERR_CONTRACT = 2,       /* ContractViolation (errors.hpp:22-25) */
+    UP_ERR_UNSUPPORTED = 3,    /* valid input outside the implemented envelope */
+    UP_ERR_WORKSPACE = 4,      /* workspace missing or too small */
+    UP_ERR_CUDA = 5,           /* CUDA runtime / driver failure */
+    UP_ERR_INVALID_ARGUMENT = 6
+} up_status;
+
+/* ScoreConfig (config.hpp:53-63).  Defaults: n=128, G=64, A=128, p=0.99. */
+typedef struct {
+    int32_t query_window_n; /* n: last-n query rows per request */
+    int32_t block_size_g;   /* G: tokens per selection block */
+    int32_t sink_count_a;   /* A: always-kept attention sinks */
+    float top_p;            /* p in (0, 1] */
+} up_score_config;
+
+/* A continuous-batching varlen batch (PackedBatch, scheduler.hpp:33-46). */
+typedef struct {
+    int32_t num_requests;        /* R >= 1 */
+    int64_t max_tokens;          /* capacity: rows allocated in every [T, ...] buffer */
+    const int32_t* cu_seqlens;   /* device int32[R+1]: 0 = cu[0] < cu[1] < ... <= max_tokens */
+    const uint8_t* drop_enabled; /* device uint8[R] or NULL (all enabled).  0 marks a
+                                    segment that passes through untouched (decode phase,
+                                    scheduler.cpp:59-62) */
+} up_batch;
+
+/* Head layout of q / k as held by this rank.  Local q-head hl is global head
+ * q_head_offset + hl and reads local kv-head (q_head_offset + hl) / gqa_group -
+ * kv_head_offset.  With TP, a rank holds a contiguous head slice (tp_sim.cpp:12-27). */
+typedef struct {
+    int32_t num_q_heads;    /* q heads present in q */
+    int32_t num_kv_heads;   /* kv heads present in k */
+    int32_t head_dim;       /* D */
+    int32_t gqa_group;      /* global Hq / Hkv (1 for MHA) */
+    int32_t q_head_offset;  /* global index of local q-head 0 */
+    int32_t kv_head_offset; /* global index of local kv-head 0 */
+    int64_t q_row_stride;   /* elements between consecutive token rows of q (>= Hq*D) */
+    int64_t k_row_stride;   /* elements between consecutive token rows of k (>= Hkv*D) */
+} up_heads;
+
+/* One row-major plane compacted by up_compact (hidden states, K, V, Q, positions ...). */
+typedef struct {
+    const void* src;  /* device, max_tokens rows */
+    void* dst;        /* device, max_tokens rows (only the retained prefix is written) */
+    int64_t row_bytes;
+    int64_t src_stride_bytes; /* 0 = row_bytes */
+    int64_t dst_stride_bytes; /* 0 = row_bytes */
+} up_plane;
+
+/* Per-request selection results (Selection, selection.hpp:34-57). */
+typedef struct {
+    int64_t* cutoff_rank;     /* int64[R]: k*, nb if degenerate, -1 for pass-through segments */
+    int64_t* retained_count;  /* int64[R] (optional) */
+    double* covered_mass;     /* double[R] (optional) */
+    uint8_t* degenerate;      /* uint8[R] (optional): zero total mass -> keep-all */
+} up_selection_out;
+
+int up_abi_version(void);
+const char* up_status_string(up_status status);
+
+/* ScoreConfig::validate (config.cpp:98-103). */
+up_status up_config_validate(const up_score_config* cfg);
+
+/* Upper bound of Σ_r ceil(N_r / G) for any batch that fits the capacities. */
+int64_t up_max_blocks(const up_batch* batch, const up_score_config* cfg);
+
+/* Bytes of device workspace needed by every entry point for this batch capacity and head
+ * layout (one workspace serves all of them).  The workspace must be zeroed once before
+ * first use (cudaMemset) and then belongs to one stream at a time. */
+size_t up_workspace_bytes(const up_batch* batch, const up_heads* heads, const up_score_config* cfg);
+
+/* Importance scores per block (a3-a6).  q: bf16 [max_tokens, Hq_local, D] (row stride
+ * q_row_stride), k: bf16 [max_tokens, Hkv_local, D].  Writes
+ *   block_scores[Σ_r ceil(N_r/G)] fp32 (segment-major; zeros for pass-through segments)
+ *   cu_blocks[R+1] int32 (block offsets of each segment),
+ *   token_scores[max_tokens] fp32 when non-NULL (reference token_scores, importance.hpp:18-23).
+ * block_scores holds the PARTIAL sum over this rank's heads; reduce over TP ranks before
+ * up_select (Eq. 15). */
+up_status up_score_blocks(void* stream, const up_batch* batch, const up_heads* heads,
+                          const up_score_config* cfg, const void* q, const void* k,
+                          float* block_scores, int32_t* cu_blocks, float* token_scores,
+                          void* workspace, size_t workspace_bytes);
+
+/* Elementwise sum of tp partial block-score vectors in ascending shard order
+ * (allreduce_scores, tp_sim.cpp:43-47): out[g] = ((0 + s_0[g]) + s_1[g]) + ...
+ * shards: HOST array of tp device pointers (peer-mapped or local). */
+up_status up_reduce_block_scores(void* stream, const float* const* shards, int32_t tp,
+                                 int64_t count, float* out);
+
+/* Top-p keep mask (a9-a13).  block_scores / cu_blocks as produced by up_score_blocks
+ * (after any TP reduction).  veto: device uint8[max_tokens] or NULL -- rows that may not
+ * be re-admitted.  Writes keep[max_tokens] (1 = retained; pass-through segments all 1). */
+up_status up_select(void* stream, const up_batch* batch, const up_score_config* cfg,
+                    const float* block_scores, const int32_t* cu_blocks, const uint8_t* veto,
+                    uint8_t* keep, const up_selection_out* out, void* workspace,
+                    size_t workspace_bytes);
+
+/* Segmented prefix sum + gather compaction (a14-a16).  Retained rows of every plane are
+ * written contiguously in order (drop-enabled segments keep rows with keep != 0, the
+ * others keep all rows).  Writes cu_seqlens_out[R+1], retained_index[num_out] (source row
+ * of each output row; may be NULL) and *num_tokens_out (device int32). */
+up_status up_compact(void* stream, const up_batch* batch, const uint8_t* keep,
+                     const up_plane* planes, int32_t num_planes, int32_t* cu_seqlens_out,
+                     int32_t* retained_index, int32_t* num_tokens_out, void* workspace,
+                     size_t workspace_bytes);
+
+/* up_score_blocks -> up_select -> up_compact for a single-rank (non-TP) layer. */
+up_status up_drop_layer(void* stream, const up_batch* batch, const up_heads* heads,
+                        const up_score_config* cfg, const void* q, const void* k,
+                        const uint8_t* veto, float* block_scores, int32_t* cu_blocks,
+                        uint8_t* keep, const up_selection_out* sel, const up_plane* planes,
+                        int32_t num_planes, int32_t* cu_seqlens_out, int32_t* retained_index,
+                        int32_t* num_tokens_out, void* workspace, size_t workspace_bytes);
+
+/* Synchronizes `stream`, returns the sticky device-side status raised since the last call
+ * (UP_OK if none) and clears it. */
+up_status up_device_status(void* stream, void* workspace);
+
+/* Which scorer implementation up_score_blocks uses for this shape: 1 = tcgen05 tensor-core
+ * kernel, 2 = SIMT kernel (generic shapes or when token_scores are requested). */
+int up_scorer_kind(const up_heads* heads, const up_score_config* cfg, int want_token_scores);
+
+/* Kernel launches issued by the most recent entry point on this thread (for accounting). */
+int up_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNIPREFILL_B200_H */

@@ -1,0 +1,367 @@
+"""CPU oracle for the UniPrefill token-selection hot path -- TEST INFRASTRUCTURE ONLY.
+
+Two checkers live here, both reached through ctypes:
+
+* ``port``: the plain-C restatement in ``uniprefill_oracle.c`` (each function cites the
+  reference file:line it restates), built to ``_build/liboracle_port.so``;
+* ``ref``: the unmodified reference core compiled from ``/root/reference/proj/core/src``
+  plus ``ref_shim.cpp`` into ``_ref/libuniprefill_ref.so`` (absent on machines where it
+  was never built; the GPU box receives the prebuilt file with the repo snapshot).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package, and only as the checker or the timed
+CPU baseline -- never on the product path (``paper_2605_06221_b200``), which has no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_SO = os.path.join(HERE, "_build", "liboracle_port.so")
+REF_SO = os.path.join(HERE, "_ref", "libuniprefill_ref.so")
+
+OK, ERR_CONFIG, ERR_CONTRACT = 0, 1, 2
+
+
+class OracleConfigError(Exception):
+    """Reference ConfigError (errors.hpp:15-18)."""
+
+
+class OracleContractViolation(Exception):
+    """Reference ContractViolation (errors.hpp:22-25)."""
+
+
+def _raise(status: int, what: str) -> None:
+    if status == OK:
+        return
+    if status == ERR_CONFIG:
+        raise OracleConfigError(what)
+    if status == ERR_CONTRACT:
+        raise OracleContractViolation(what)
+    raise RuntimeError(f"{what}: oracle status {status}")
+
+
+class _Cfg(ctypes.Structure):
+    _fields_ = [("query_window_n", ctypes.c_int32), ("block_size_g", ctypes.c_int32),
+                ("sink_count_a", ctypes.c_int32), ("top_p", ctypes.c_float)]
+
+
+class _SelInfo(ctypes.Structure):
+    _fields_ = [("cutoff_rank", ctypes.c_int64), ("retained_count", ctypes.c_int64),
+                ("retention_ratio", ctypes.c_double), ("covered_mass", ctypes.c_double),
+                ("degenerate_keep_all", ctypes.c_int32)]
+
+
+@dataclass
+class OracleSelection:
+    keep_mask: np.ndarray
+    cutoff_rank: int
+    retained_count: int
+    retention_ratio: float
+    covered_mass: float
+    degenerate_keep_all: bool
+
+    @property
+    def retained_indices(self) -> np.ndarray:
+        return np.flatnonzero(self.keep_mask).astype(np.int64)
+
+
+def build() -> None:
+    """Compile the port (and, when the reference sources are present, the reference)."""
+    subprocess.run(["make", "-s", "-C", HERE, "-j8"], check=True)
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def _cfg(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99) -> _Cfg:
+    return _Cfg(int(query_window_n), int(block_size_g), int(sink_count_a), float(top_p))
+
+
+class _Lib:
+    """Common ctypes surface of the port (orc_*) and the reference shim (ref_*)."""
+
+    def __init__(self, path: str, prefix: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.path = path
+        self.lib = ctypes.CDLL(path)
+        self.prefix = prefix
+        f = self._fn
+        P = ctypes.POINTER
+        f("phi_encode", [ctypes.c_float, P(ctypes.c_uint32)])
+        f("phi_decode", [ctypes.c_uint32], ctypes.c_float)
+        f("score_tokens_heads", [P(ctypes.c_float), ctypes.c_int64, P(ctypes.c_float), ctypes.c_int64,
+                                 ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_int, P(_Cfg), P(ctypes.c_float), P(ctypes.c_float),
+                                 P(ctypes.c_int32)])
+        f("top_p_select", [P(ctypes.c_float), ctypes.c_int64, P(_Cfg), ctypes.c_int64,
+                           P(ctypes.c_uint8), P(_SelInfo)])
+        f("expand_mask", [P(ctypes.c_uint8), ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
+                          ctypes.c_int64, ctypes.c_int64, P(ctypes.c_uint8)])
+        f("allreduce_scores", [P(P(ctypes.c_float)), P(ctypes.c_int32), ctypes.c_int32,
+                               ctypes.c_int64, P(ctypes.c_float)])
+
+    def _fn(self, name, argtypes, restype=ctypes.c_int):
+        fn = getattr(self.lib, f"{self.prefix}_{name}")
+        fn.argtypes = argtypes
+        fn.restype = restype
+        return fn
+
+    def _call(self, name):
+        return getattr(self.lib, f"{self.prefix}_{name}")
+
+    # ---- phi -------------------------------------------------------------
+    def phi_encode(self, x: float) -> int:
+        out = ctypes.c_uint32(0)
+        _raise(self._call("phi_encode")(ctypes.c_float(x), ctypes.byref(out)), "phi_encode")
+        return int(out.value)
+
+    def phi_decode(self, bits: int) -> float:
+        return float(self._call("phi_decode")(ctypes.c_uint32(bits)))
+
+    # ---- scorer ----------------------------------------------------------
+    def score_tokens_heads(self, q: np.ndarray, k: np.ndarray, num_heads: int, num_kv_heads: int,
+                           head_begin: int, head_end: int, want_tokens: bool = True, **cfg):
+        """q: N x (H*D), k: N x (Hkv*D) float32.  Returns (token_scores, block_scores, n_eff)."""
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        k = np.ascontiguousarray(k, dtype=np.float32)
+        N = q.shape[0]
+        D = q.shape[1] // num_heads
+        c = _cfg(**cfg)
+        G = c.block_size_g
+        nb = (N + G - 1) // G if G > 0 else 0
+        tok = np.zeros(max(N, 1), np.float32)
+        blk = np.zeros(max(nb, 1), np.float32)
+        n_eff = ctypes.c_int32(0)
+        st = self._call("score_tokens_heads")(
+            _ptr(q, ctypes.c_float), q.shape[1], _ptr(k, ctypes.c_float), k.shape[1], N, num_heads,
+            num_kv_heads, D, head_begin, head_end, ctypes.byref(c),
+            _ptr(tok, ctypes.c_float) if want_tokens else None, _ptr(blk, ctypes.c_float),
+            ctypes.byref(n_eff))
+        _raise(st, "score_tokens_heads")
+        return tok[:N], blk[:nb], int(n_eff.value)
+
+    def score_tokens(self, q, k, num_heads, num_kv_heads=None, **cfg):
+        kvh = num_heads if num_kv_heads is None else num_kv_heads
+        return self.score_tokens_heads(q, k, num_heads, kvh, 0, num_heads, **cfg)
+
+    # ---- selection -------------------------------------------------------
+    def top_p_select(self, block_scores, num_tokens: int, **cfg) -> OracleSelection:
+        b = np.ascontiguousarray(block_scores, dtype=np.float32)
+        keep = np.zeros(max(num_tokens, 1), np.uint8)
+        info = _SelInfo()
+        c = _cfg(**cfg)
+        st = self._call("top_p_select")(_ptr(b, ctypes.c_float), b.size, ctypes.byref(c), num_tokens,
+                                        _ptr(keep, ctypes.c_uint8), ctypes.byref(info))
+        _raise(st, "top_p_select")
+        return OracleSelection(keep[:num_tokens].copy(), info.cutoff_rank, info.retained_count,
+                               info.retention_ratio, info.covered_mass,
+                               bool(info.degenerate_keep_all))
+
+    def expand_mask(self, block_mask, block_size, num_tokens, sink_count, window_n) -> np.ndarray:
+        bm = np.ascontiguousarray(block_mask, dtype=np.uint8)
+        keep = np.zeros(max(num_tokens, 1), np.uint8)
+        st = self._call("expand_mask")(_ptr(bm, ctypes.c_uint8), bm.size, block_size, num_tokens,
+                                       sink_count, window_n, _ptr(keep, ctypes.c_uint8))
+        _raise(st, "expand_mask")
+        return keep[:num_tokens]
+
+    def allreduce_scores(self, shards, shard_ids) -> np.ndarray:
+        arrs = [np.ascontiguousarray(s, dtype=np.float32) for s in shards]
+        length = arrs[0].size if arrs else 0
+        ptrs = (ctypes.POINTER(ctypes.c_float) * max(len(arrs), 1))(*[_ptr(a, ctypes.c_float) for a in arrs])
+        ids = np.ascontiguousarray(shard_ids, dtype=np.int32)
+        out = np.zeros(max(length, 1), np.float32)
+        st = self._call("allreduce_scores")(ptrs, _ptr(ids, ctypes.c_int32), len(arrs), length,
+                                            _ptr(out, ctypes.c_float))
+        _raise(st, "allreduce_scores")
+        return out[:length]
+
+
+class Port(_Lib):
+    """The C restatement (uniprefill_oracle.c)."""
+
+    def __init__(self, path: str = PORT_SO):
+        super().__init__(path, "orc")
+        P = ctypes.POINTER
+        self._fn("restrict_selection", [P(ctypes.c_uint8), P(ctypes.c_uint8), ctypes.c_int64,
+                                        P(ctypes.c_float), ctypes.c_int64, ctypes.c_int, P(_SelInfo)])
+        self._fn("compact", [P(ctypes.c_uint8), P(ctypes.c_int64), ctypes.c_int32, P(ctypes.c_uint8),
+                             ctypes.c_int32, P(ctypes.c_void_p), P(ctypes.c_void_p), P(ctypes.c_int64),
+                             P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64)])
+        self._fn("rng_key", [ctypes.c_uint64, ctypes.c_uint64], ctypes.c_uint64)
+        self._fn("rng_bits", [ctypes.c_uint64, ctypes.c_uint64], ctypes.c_uint64)
+        self._fn("rng_uniform", [ctypes.c_uint64, ctypes.c_uint64], ctypes.c_double)
+        self._fn("rng_normal", [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double], ctypes.c_float)
+        self._fn("scoring_flops", [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int],
+                 ctypes.c_uint64)
+
+    def restrict_selection(self, sel: OracleSelection, veto, block_scores, block_size) -> OracleSelection:
+        keep = sel.keep_mask.astype(np.uint8).copy()
+        v = np.ascontiguousarray(veto, dtype=np.uint8)
+        b = np.ascontiguousarray(block_scores, dtype=np.float32)
+        info = _SelInfo(sel.cutoff_rank, sel.retained_count, sel.retention_ratio, sel.covered_mass,
+                        int(sel.degenerate_keep_all))
+        st = self.lib.orc_restrict_selection(_ptr(keep, ctypes.c_uint8), _ptr(v, ctypes.c_uint8),
+                                             keep.size, _ptr(b, ctypes.c_float), b.size, block_size,
+                                             ctypes.byref(info))
+        _raise(st, "restrict_selection")
+        return OracleSelection(keep, info.cutoff_rank, info.retained_count, info.retention_ratio,
+                               info.covered_mass, bool(info.degenerate_keep_all))
+
+    def compact(self, keep, cu_seqlens, planes, selected=None):
+        """planes: list of 2-D arrays with T rows.  Returns (outs, cu_out, retained_index)."""
+        keep = np.ascontiguousarray(keep, dtype=np.uint8)
+        cu = np.ascontiguousarray(cu_seqlens, dtype=np.int64)
+        R = cu.size - 1
+        srcs = [np.ascontiguousarray(p) for p in planes]
+        T = int(cu[-1])
+        dsts = [np.zeros_like(s) for s in srcs]
+        rb = np.array([s.strides[0] if s.ndim > 1 else s.itemsize for s in srcs], np.int64)
+        sp = (ctypes.c_void_p * max(len(srcs), 1))(*[s.ctypes.data for s in srcs])
+        dp = (ctypes.c_void_p * max(len(dsts), 1))(*[d.ctypes.data for d in dsts])
+        sel = None if selected is None else np.ascontiguousarray(selected, dtype=np.uint8)
+        cu_out = np.zeros(R + 1, np.int64)
+        ridx = np.zeros(max(T, 1), np.int64)
+        nout = ctypes.c_int64(0)
+        st = self.lib.orc_compact(_ptr(keep, ctypes.c_uint8), _ptr(cu, ctypes.c_int64), R,
+                                  _ptr(sel, ctypes.c_uint8) if sel is not None else None, len(srcs),
+                                  sp, dp, _ptr(rb, ctypes.c_int64), _ptr(cu_out, ctypes.c_int64),
+                                  _ptr(ridx, ctypes.c_int64), ctypes.byref(nout))
+        _raise(st, "compact")
+        n = int(nout.value)
+        return [d[:n] for d in dsts], cu_out, ridx[:n]
+
+    def rng_normal_array(self, seed: int, stream: int, count: int, stddev: float) -> np.ndarray:
+        key = self.lib.orc_rng_key(seed, stream)
+        fn = self.lib.orc_rng_normal
+        return np.fromiter((fn(key, i, stddev) for i in range(count)), np.float32, count)
+
+    def rng_uniform(self, seed: int, stream: int, i: int) -> float:
+        return float(self.lib.orc_rng_uniform(self.lib.orc_rng_key(seed, stream), i))
+
+    def rng_bits(self, seed: int, stream: int, i: int) -> int:
+        return int(self.lib.orc_rng_bits(self.lib.orc_rng_key(seed, stream), i))
+
+
+class Ref(_Lib):
+    """The unmodified reference core (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        super().__init__(path, "ref")
+        P = ctypes.POINTER
+        self._fn("apply_drop", [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, P(ctypes.c_uint8),
+                                P(ctypes.c_float), P(ctypes.c_int64), P(ctypes.c_int64)])
+        self._fn("patch_metadata", [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, P(ctypes.c_int64),
+                                    ctypes.c_int32, P(ctypes.c_uint8), P(ctypes.c_uint8),
+                                    P(ctypes.c_uint8), P(ctypes.c_float), P(ctypes.c_int64)])
+        self._fn("sharded_allreduce", [P(ctypes.c_float), ctypes.c_int64, P(ctypes.c_float),
+                                       ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, P(_Cfg), ctypes.c_int, P(ctypes.c_float),
+                                       P(ctypes.c_float)])
+        self._fn("drop_layer_varlen", [P(ctypes.c_float), ctypes.c_int64, P(ctypes.c_float),
+                                       ctypes.c_int64, P(ctypes.c_float), ctypes.c_int64,
+                                       P(ctypes.c_int64), ctypes.c_int32, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, P(_Cfg), ctypes.c_int, P(ctypes.c_float),
+                                       P(ctypes.c_uint8), P(ctypes.c_float), P(ctypes.c_int64)])
+
+    def apply_drop(self, states: np.ndarray, keep):
+        s = np.ascontiguousarray(states, dtype=np.float32)
+        k = np.ascontiguousarray(keep, dtype=np.uint8)
+        out = np.zeros_like(s)
+        pos = np.zeros(s.shape[0], np.int64)
+        n = ctypes.c_int64(0)
+        st = self.lib.ref_apply_drop(_ptr(s, ctypes.c_float), s.shape[0], s.shape[1],
+                                     _ptr(k, ctypes.c_uint8), _ptr(out, ctypes.c_float),
+                                     _ptr(pos, ctypes.c_int64), ctypes.byref(n))
+        _raise(st, "apply_drop")
+        return out[: n.value], pos[: n.value]
+
+    def patch_metadata(self, tokens: np.ndarray, cu_seqlens, keep, selected, is_decode=None):
+        t = np.ascontiguousarray(tokens, dtype=np.float32)
+        cu = np.ascontiguousarray(cu_seqlens, dtype=np.int64)
+        R = cu.size - 1
+        k = np.ascontiguousarray(keep, dtype=np.uint8)
+        sel = np.ascontiguousarray(selected, dtype=np.uint8)
+        dec = None if is_decode is None else np.ascontiguousarray(is_decode, dtype=np.uint8)
+        out = np.zeros_like(t)
+        cu_out = np.zeros(R + 1, np.int64)
+        st = self.lib.ref_patch_metadata(_ptr(t, ctypes.c_float), t.shape[0], t.shape[1],
+                                         _ptr(cu, ctypes.c_int64), R, _ptr(k, ctypes.c_uint8),
+                                         _ptr(sel, ctypes.c_uint8),
+                                         _ptr(dec, ctypes.c_uint8) if dec is not None else None,
+                                         _ptr(out, ctypes.c_float), _ptr(cu_out, ctypes.c_int64))
+        _raise(st, "patch_metadata")
+        return out[: cu_out[-1]], cu_out
+
+    def sharded_allreduce(self, q, k, num_heads, num_kv_heads, tp_degree, **cfg):
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        k = np.ascontiguousarray(k, dtype=np.float32)
+        N = q.shape[0]
+        D = q.shape[1] // num_heads
+        c = _cfg(**cfg)
+        nb = (N + c.block_size_g - 1) // c.block_size_g
+        shards = np.zeros((tp_degree, nb), np.float32)
+        red = np.zeros(nb, np.float32)
+        st = self.lib.ref_sharded_allreduce(_ptr(q, ctypes.c_float), q.shape[1], _ptr(k, ctypes.c_float),
+                                            k.shape[1], N, num_heads, num_kv_heads, D, ctypes.byref(c),
+                                            tp_degree, _ptr(shards, ctypes.c_float),
+                                            _ptr(red, ctypes.c_float))
+        _raise(st, "sharded_allreduce")
+        return shards, red
+
+    def drop_layer_varlen(self, q, k, hidden, cu_seqlens, num_heads, num_kv_heads, threads=1, **cfg):
+        """The reference's per-layer hot path over a varlen batch (score -> select -> compact)."""
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        k = np.ascontiguousarray(k, dtype=np.float32)
+        hid = np.ascontiguousarray(hidden, dtype=np.float32)
+        cu = np.ascontiguousarray(cu_seqlens, dtype=np.int64)
+        R = cu.size - 1
+        T = int(cu[-1])
+        D = q.shape[1] // num_heads
+        c = _cfg(**cfg)
+        G = c.block_size_g
+        nbt = int(sum((int(cu[s + 1] - cu[s]) + G - 1) // G for s in range(R)))
+        blk = np.zeros(max(nbt, 1), np.float32)
+        keep = np.zeros(max(T, 1), np.uint8)
+        hout = np.zeros_like(hid)
+        cu_out = np.zeros(R + 1, np.int64)
+        st = self.lib.ref_drop_layer_varlen(
+            _ptr(q, ctypes.c_float), q.shape[1], _ptr(k, ctypes.c_float), k.shape[1],
+            _ptr(hid, ctypes.c_float), hid.shape[1], _ptr(cu, ctypes.c_int64), R, num_heads,
+            num_kv_heads, D, ctypes.byref(c), threads, _ptr(blk, ctypes.c_float),
+            _ptr(keep, ctypes.c_uint8), _ptr(hout, ctypes.c_float), _ptr(cu_out, ctypes.c_int64))
+        _raise(st, "drop_layer_varlen")
+        return blk[:nbt], keep[:T], hout[: cu_out[-1]], cu_out
+
+
+_port = None
+_ref = None
+
+
+def port() -> Port:
+    global _port
+    if _port is None:
+        if not os.path.exists(PORT_SO):
+            build()
+        _port = Port()
+    return _port
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref() -> Ref:
+    global _ref
+    if _ref is None:
+        _ref = Ref()
+    return _ref

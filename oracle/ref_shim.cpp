@@ -1,0 +1,295 @@
+// ref_shim.cpp -- extern "C" entry points over the UNMODIFIED reference implementation.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together with the
+// reference's own sources where they lie (/root/reference/proj/core/src/*.cpp) into
+// oracle/_ref/libuniprefill_ref.so.  Nothing of the reference is copied into this repo;
+// this file only converts plain arrays to the reference's types, calls its public API
+// (core/include/uniprefill/*.hpp) and maps its exceptions to status codes:
+//   0 ok, 1 ConfigError, 2 ContractViolation, 9 any other exception.
+#include "uniprefill/errors.hpp"
+#include "uniprefill/importance.hpp"
+#include "uniprefill/propagation.hpp"
+#include "uniprefill/scheduler.hpp"
+#include "uniprefill/selection.hpp"
+#include "uniprefill/tp_sim.hpp"
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <thread>
+#include <vector>
+
+using namespace uniprefill;
+
+namespace {
+
+struct RefScoreConfig {
+    int32_t query_window_n;
+    int32_t block_size_g;
+    int32_t sink_count_a;
+    float top_p;
+};
+
+ScoreConfig to_cfg(const RefScoreConfig* c) {
+    ScoreConfig s;
+    s.query_window_n = c->query_window_n;
+    s.block_size_g = c->block_size_g;
+    s.sink_count_a = c->sink_count_a;
+    s.top_p = c->top_p;
+    return s;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ConfigError&) {
+        return 1;
+    } catch (const ContractViolation&) {
+        return 2;
+    } catch (...) {
+        return 9;
+    }
+}
+
+// MHA view of a GQA tensor: kv-head columns replicated H / H_kv times.
+Matrix expand_heads(const float* src, int64_t ld, int64_t rows, int heads_in, int heads_out,
+                    int head_dim) {
+    Matrix m(rows, static_cast<int64_t>(heads_out) * head_dim);
+    const int group = heads_out / heads_in;
+    for (int64_t r = 0; r < rows; ++r) {
+        for (int h = 0; h < heads_out; ++h) {
+            std::memcpy(m.row(r) + static_cast<int64_t>(h) * head_dim,
+                        src + r * ld + static_cast<int64_t>(h / group) * head_dim,
+                        sizeof(float) * static_cast<size_t>(head_dim));
+        }
+    }
+    return m;
+}
+
+struct RefSelectionInfo {
+    int64_t cutoff_rank;
+    int64_t retained_count;
+    double retention_ratio;
+    double covered_mass;
+    int32_t degenerate_keep_all;
+};
+
+} // namespace
+
+extern "C" {
+
+int ref_phi_encode(float x, uint32_t* out) {
+    return guarded([&] { *out = phi_encode(x); });
+}
+
+float ref_phi_decode(uint32_t bits) { return phi_decode(bits); }
+
+// score_tokens_heads (importance.hpp:42-43) over one request.
+int ref_score_tokens_heads(const float* q, int64_t q_ld, const float* k, int64_t k_ld, int64_t N,
+                           int num_heads, int num_kv_heads, int head_dim, int head_begin,
+                           int head_end, const RefScoreConfig* cfg, float* token_scores,
+                           float* block_scores, int32_t* effective_n) {
+    return guarded([&] {
+        const Matrix qm = expand_heads(q, q_ld, N, num_heads, num_heads, head_dim);
+        const Matrix km = expand_heads(k, k_ld, N, num_kv_heads, num_heads, head_dim);
+        const ImportanceScores s =
+            score_tokens_heads(qm, km, num_heads, head_begin, head_end, to_cfg(cfg));
+        if (token_scores) std::memcpy(token_scores, s.token_scores.data(), s.token_scores.size() * 4);
+        std::memcpy(block_scores, s.block_scores.data(), s.block_scores.size() * 4);
+        if (effective_n) *effective_n = s.effective_n;
+    });
+}
+
+// sharded_block_scores + allreduce_scores (tp_sim.hpp:25-31).
+int ref_sharded_allreduce(const float* q, int64_t q_ld, const float* k, int64_t k_ld, int64_t N,
+                          int num_heads, int num_kv_heads, int head_dim, const RefScoreConfig* cfg,
+                          int tp_degree, float* shard_out /* tp x nb or NULL */, float* reduced) {
+    return guarded([&] {
+        const Matrix qm = expand_heads(q, q_ld, N, num_heads, num_heads, head_dim);
+        const Matrix km = expand_heads(k, k_ld, N, num_kv_heads, num_heads, head_dim);
+        const auto shards = sharded_block_scores(qm, km, num_heads, to_cfg(cfg), tp_degree);
+        if (shard_out) {
+            size_t off = 0;
+            for (const auto& s : shards) {
+                std::memcpy(shard_out + off, s.block_scores.data(), s.block_scores.size() * 4);
+                off += s.block_scores.size();
+            }
+        }
+        const std::vector<float> r = allreduce_scores(shards);
+        std::memcpy(reduced, r.data(), r.size() * 4);
+    });
+}
+
+// allreduce_scores (tp_sim.hpp:31) on explicit shards.
+int ref_allreduce_scores(const float* const* shards, const int32_t* shard_ids, int32_t tp,
+                         int64_t length, float* out) {
+    return guarded([&] {
+        std::vector<ShardScores> v;
+        for (int32_t t = 0; t < tp; ++t) {
+            v.push_back(ShardScores{shard_ids[t], std::vector<float>(shards[t], shards[t] + length)});
+        }
+        const std::vector<float> r = allreduce_scores(v);
+        std::memcpy(out, r.data(), r.size() * 4);
+    });
+}
+
+// top_p_select (selection.hpp:53-54).
+int ref_top_p_select(const float* block_scores, int64_t num_blocks, const RefScoreConfig* cfg,
+                     int64_t num_tokens, uint8_t* keep, RefSelectionInfo* info) {
+    return guarded([&] {
+        const Selection sel = top_p_select(
+            std::span<const float>(block_scores, static_cast<size_t>(num_blocks)), to_cfg(cfg),
+            num_tokens);
+        std::memcpy(keep, sel.keep_mask.data(), sel.keep_mask.size());
+        info->cutoff_rank = sel.cutoff_rank;
+        info->retained_count = sel.retained_count();
+        info->retention_ratio = sel.retention_ratio;
+        info->covered_mass = sel.covered_mass;
+        info->degenerate_keep_all = sel.degenerate_keep_all ? 1 : 0;
+    });
+}
+
+// expand_mask (selection.hpp:46-47).
+int ref_expand_mask(const uint8_t* block_mask, int64_t num_blocks, int block_size,
+                    int64_t num_tokens, int64_t sink_count, int64_t window_n, uint8_t* keep) {
+    return guarded([&] {
+        const std::vector<uint8_t> bm(block_mask, block_mask + num_blocks);
+        const std::vector<uint8_t> k = expand_mask(bm, block_size, num_tokens, sink_count, window_n);
+        std::memcpy(keep, k.data(), k.size());
+    });
+}
+
+// apply_drop (propagation.hpp:415) on one request's stream; returns compacted rows and
+// logical positions, and checks the parked map partitions the sequence.
+int ref_apply_drop(const float* states, int64_t rows, int64_t cols, const uint8_t* keep,
+                   float* out_states, int64_t* out_positions, int64_t* out_rows) {
+    return guarded([&] {
+        Matrix prompt(rows, cols);
+        std::memcpy(prompt.data.data(), states, sizeof(float) * static_cast<size_t>(rows * cols));
+        TokenStream stream = TokenStream::from_prompt(prompt);
+        Selection sel;
+        sel.keep_mask.assign(keep, keep + rows);
+        for (int64_t i = 0; i < rows; ++i) {
+            if (keep[i]) sel.retained_indices.push_back(i);
+        }
+        DropHistory history;
+        history.original_length = rows;
+        apply_drop(stream, sel, 0, history);
+        stream.validate();
+        std::memcpy(out_states, stream.active_states.data.data(),
+                    sizeof(float) * stream.active_states.data.size());
+        std::memcpy(out_positions, stream.logical_positions.data(),
+                    sizeof(int64_t) * stream.logical_positions.size());
+        *out_rows = stream.active_count();
+    });
+}
+
+// patch_metadata (scheduler.hpp:52-53) over a packed batch.  selected[s] != 0 attaches a
+// Selection built from keep; is_decode[s] marks decode-phase segments.
+int ref_patch_metadata(const float* tokens, int64_t total_rows, int64_t cols,
+                       const int64_t* cu_seqlens, int32_t num_requests, const uint8_t* keep,
+                       const uint8_t* selected, const uint8_t* is_decode, float* out_tokens,
+                       int64_t* out_cu) {
+    return guarded([&] {
+        PackedBatch batch;
+        batch.tokens = Matrix(total_rows, cols);
+        std::memcpy(batch.tokens.data.data(), tokens,
+                    sizeof(float) * static_cast<size_t>(total_rows * cols));
+        batch.cu_seqlens.assign(cu_seqlens, cu_seqlens + num_requests + 1);
+        std::vector<std::optional<Selection>> sels(static_cast<size_t>(num_requests));
+        for (int32_t s = 0; s < num_requests; ++s) {
+            batch.request_ids.push_back(s);
+            batch.phases.push_back(is_decode && is_decode[s] ? Phase::Decode : Phase::Prefill);
+            if (selected && selected[s]) {
+                Selection sel;
+                const int64_t b = cu_seqlens[s], e = cu_seqlens[s + 1];
+                sel.keep_mask.assign(keep + b, keep + e);
+                for (int64_t i = 0; i < e - b; ++i) {
+                    if (keep[b + i]) sel.retained_indices.push_back(i);
+                }
+                sels[static_cast<size_t>(s)] = sel;
+            }
+        }
+        patch_metadata(batch, sels, 0);
+        std::memcpy(out_tokens, batch.tokens.data.data(), sizeof(float) * batch.tokens.data.size());
+        std::memcpy(out_cu, batch.cu_seqlens.data(), sizeof(int64_t) * batch.cu_seqlens.size());
+    });
+}
+
+// The reference hot path over a varlen batch, exactly as Engine::run_batch drives it per
+// drop layer (scheduler.cpp:293-332): per segment score_tokens -> top_p_select, then the
+// segment's rows are compacted (patch_metadata).  Segments are independent units
+// (SPEC.md:202,265), so `threads` workers process segments concurrently; each segment's
+// arithmetic is unchanged.  block_scores_out is Σ ceil(N_r/G) floats (segment-major),
+// keep_out T bytes.  hidden (T x hidden_cols) is compacted into hidden_out.
+int ref_drop_layer_varlen(const float* q, int64_t q_ld, const float* k, int64_t k_ld,
+                          const float* hidden, int64_t hidden_cols, const int64_t* cu_seqlens,
+                          int32_t num_requests, int num_heads, int num_kv_heads, int head_dim,
+                          const RefScoreConfig* cfg, int threads, float* block_scores_out,
+                          uint8_t* keep_out, float* hidden_out, int64_t* cu_out) {
+    return guarded([&] {
+        const ScoreConfig sc = to_cfg(cfg);
+        const int G = sc.block_size_g;
+        std::vector<int64_t> cu_blocks(static_cast<size_t>(num_requests) + 1, 0);
+        for (int32_t s = 0; s < num_requests; ++s) {
+            const int64_t n = cu_seqlens[s + 1] - cu_seqlens[s];
+            cu_blocks[s + 1] = cu_blocks[s] + (n + G - 1) / G;
+        }
+        std::vector<int> status(static_cast<size_t>(num_requests), 0);
+        auto work = [&](int32_t s) {
+            status[static_cast<size_t>(s)] = guarded([&] {
+                const int64_t b = cu_seqlens[s], n = cu_seqlens[s + 1] - cu_seqlens[s];
+                const Matrix qm = expand_heads(q + b * q_ld, q_ld, n, num_heads, num_heads, head_dim);
+                const Matrix km = expand_heads(k + b * k_ld, k_ld, n, num_kv_heads, num_heads, head_dim);
+                const ImportanceScores scores = score_tokens(qm, km, num_heads, sc);
+                const Selection sel = top_p_select(scores.block_scores, sc, n);
+                std::memcpy(block_scores_out + cu_blocks[s], scores.block_scores.data(),
+                            scores.block_scores.size() * 4);
+                std::memcpy(keep_out + b, sel.keep_mask.data(), sel.keep_mask.size());
+            });
+        };
+        const int nt = threads < 1 ? 1 : threads;
+        if (nt == 1 || num_requests <= 1) {
+            for (int32_t s = 0; s < num_requests; ++s) work(s);
+        } else {
+            std::vector<std::thread> pool;
+            std::atomic<int32_t> next{0};
+            for (int t = 0; t < nt; ++t) {
+                pool.emplace_back([&] {
+                    for (int32_t s = next++; s < num_requests; s = next++) work(s);
+                });
+            }
+            for (auto& th : pool) th.join();
+        }
+        for (int st : status) {
+            if (st == 1) throw ConfigError("segment failed");
+            if (st != 0) throw ContractViolation("segment failed");
+        }
+        // Compaction through the reference's own patch_metadata.
+        PackedBatch batch;
+        const int64_t T = cu_seqlens[num_requests];
+        batch.tokens = Matrix(T, hidden_cols);
+        std::memcpy(batch.tokens.data.data(), hidden, sizeof(float) * static_cast<size_t>(T * hidden_cols));
+        batch.cu_seqlens.assign(cu_seqlens, cu_seqlens + num_requests + 1);
+        std::vector<std::optional<Selection>> sels(static_cast<size_t>(num_requests));
+        for (int32_t s = 0; s < num_requests; ++s) {
+            batch.request_ids.push_back(s);
+            batch.phases.push_back(Phase::Prefill);
+            Selection sel;
+            const int64_t b = cu_seqlens[s], e = cu_seqlens[s + 1];
+            sel.keep_mask.assign(keep_out + b, keep_out + e);
+            for (int64_t i = 0; i < e - b; ++i) {
+                if (keep_out[b + i]) sel.retained_indices.push_back(i);
+            }
+            sels[static_cast<size_t>(s)] = sel;
+        }
+        patch_metadata(batch, sels, 0);
+        std::memcpy(hidden_out, batch.tokens.data.data(), sizeof(float) * batch.tokens.data.size());
+        std::memcpy(cu_out, batch.cu_seqlens.data(), sizeof(int64_t) * batch.cu_seqlens.size());
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,374 @@
+/*
+ * uniprefill_oracle.c -- CPU restatement of the UniPrefill token-selection hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY (see uniprefill_oracle.h).  Parity is pinned against the
+ * reference itself (oracle/_ref/libuniprefill_ref.so, built from
+ * /root/reference/proj/core/src by oracle/Makefile) and against the golden vectors in
+ * tests/golden/.  Build with -O2 -ffp-contract=off: the arithmetic order and rounding
+ * below are the reference's, and FMA contraction would change the last bits.
+ */
+#include "uniprefill_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ config */
+
+/* ScoreConfig::validate (config.cpp:98-103). */
+int orc_config_validate(const orc_score_config* cfg) {
+    if (cfg->query_window_n <= 0) return ORC_ERR_CONFIG;
+    if (cfg->block_size_g <= 0) return ORC_ERR_CONFIG;
+    if (cfg->sink_count_a < 0) return ORC_ERR_CONFIG;
+    if (!(cfg->top_p > 0.0f && cfg->top_p <= 1.0f)) return ORC_ERR_CONFIG;
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ phi / packing */
+
+static uint32_t f2u(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    return u;
+}
+static float u2f(uint32_t u) {
+    float x;
+    memcpy(&x, &u, 4);
+    return x;
+}
+
+/* phi_encode (selection.cpp:14-19): -0 collapses to +0, then a sign-dependent xor. */
+int orc_phi_encode(float x, uint32_t* out) {
+    if (!isfinite(x)) return ORC_ERR_CONTRACT;
+    if (x == 0.0f) x = 0.0f;
+    const uint32_t bits = f2u(x);
+    *out = x >= 0.0f ? (bits ^ 0x80000000u) : (bits ^ 0xFFFFFFFFu);
+    return ORC_OK;
+}
+
+/* phi_decode (selection.cpp:21-25). */
+float orc_phi_decode(uint32_t bits) {
+    const uint32_t raw = (bits & 0x80000000u) ? (bits ^ 0x80000000u) : (bits ^ 0xFFFFFFFFu);
+    return u2f(raw);
+}
+
+/* PackedScore::pack (selection.cpp:27-30): phi(s) << 32 | ~g (ones' complement, so the
+ * lower block index wins ties in descending order). */
+int orc_pack_score(float score, uint32_t block_index, uint64_t* out) {
+    uint32_t e;
+    const int st = orc_phi_encode(score, &e);
+    if (st != ORC_OK) return st;
+    *out = ((uint64_t)e << 32) | (uint64_t)(~block_index);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ rng */
+
+/* hash_mix / hash_combine / CounterRng (rng.cpp:10-40). */
+uint64_t orc_hash_mix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+static uint64_t hash_combine(uint64_t a, uint64_t b) {
+    return orc_hash_mix(a ^ (0x9e3779b97f4a7c15ULL + (b << 6) + (b >> 2) + orc_hash_mix(b)));
+}
+
+uint64_t orc_rng_key(uint64_t seed, uint64_t stream) { return hash_combine(seed, stream); }
+
+uint64_t orc_rng_bits(uint64_t key, uint64_t i) {
+    return orc_hash_mix(key ^ (i * 0xd1342543de82ef95ULL + 0x2545f4914f6cdd1dULL));
+}
+
+double orc_rng_uniform(uint64_t key, uint64_t i) {
+    const double u = (double)(orc_rng_bits(key, i) >> 11) * 0x1.0p-53;
+    return u > 0.0 ? u : 0x1.0p-53;
+}
+
+float orc_rng_normal(uint64_t key, uint64_t i, double stddev) {
+    const double u1 = orc_rng_uniform(key, 2 * i);
+    const double u2 = orc_rng_uniform(key, 2 * i + 1);
+    const double r = sqrt(-2.0 * log(u1));
+    const double z = r * cos(2.0 * 3.14159265358979323846 * u2);
+    return (float)(z * stddev);
+}
+
+/* ------------------------------------------------------------------ scorer */
+
+/* block_reduce (importance.cpp:76-90): float token scores summed in double in index order,
+ * divided by the member count (ragged tail uses its real size), rounded to float. */
+int orc_block_reduce(const float* token_scores, int64_t N, int block_size, float* out) {
+    if (N <= 0) return ORC_ERR_CONTRACT;
+    if (block_size <= 0) return ORC_ERR_CONTRACT;
+    const int64_t nb = (N + block_size - 1) / block_size;
+    for (int64_t g = 0; g < nb; ++g) {
+        const int64_t b = g * block_size;
+        const int64_t e = (b + block_size < N) ? b + block_size : N;
+        double sum = 0.0;
+        for (int64_t i = b; i < e; ++i) sum += token_scores[i];
+        out[g] = (float)(sum / (double)(e - b));
+    }
+    return ORC_OK;
+}
+
+/* score_tokens_heads (importance.cpp:92-127) with partial_scores (:17-33) and
+ * online_softmax_reduce (:35-74) fused per query row.  The reference materialises every
+ * head's n x N raw matrix first; the arithmetic per element and the order in which the
+ * shared double accumulator acc[] is updated (head, then row, then key) are identical, so
+ * the results are bit-identical while memory stays O(N). */
+int orc_score_tokens_heads(const float* q, int64_t q_ld, const float* k, int64_t k_ld, int64_t N,
+                           int num_heads, int num_kv_heads, int head_dim, int head_begin,
+                           int head_end, const orc_score_config* cfg, float* token_scores,
+                           float* block_scores, int32_t* effective_n) {
+    if (num_heads <= 0 || num_kv_heads <= 0 || head_dim <= 0) return ORC_ERR_CONTRACT;
+    if (num_heads % num_kv_heads != 0) return ORC_ERR_CONTRACT;
+    if (head_begin < 0 || head_end > num_heads || head_begin >= head_end) return ORC_ERR_CONTRACT;
+    if (N <= 0) return ORC_ERR_CONTRACT; /* block_reduce rejects empty scores */
+    if (cfg->query_window_n <= 0) return ORC_ERR_CONFIG;
+    if (cfg->block_size_g <= 0) return ORC_ERR_CONTRACT;
+    const int group = num_heads / num_kv_heads;
+    const int64_t n_eff = cfg->query_window_n < N ? cfg->query_window_n : N;
+    if (effective_n) *effective_n = (int32_t)n_eff;
+
+    const double scale = 1.0 / sqrt((double)head_dim);
+    const double inv_n = 1.0 / (double)n_eff;
+    double* acc = (double*)calloc((size_t)N, sizeof(double));
+    float* raw = (float*)malloc((size_t)N * sizeof(float));
+    if (!acc || !raw) {
+        free(acc);
+        free(raw);
+        return ORC_ERR_CONTRACT;
+    }
+    int status = ORC_OK;
+    for (int h = head_begin; h < head_end && status == ORC_OK; ++h) {
+        const int kvh = h / group;
+        for (int64_t j = 0; j < n_eff; ++j) {
+            const float* qrow = q + (N - n_eff + j) * q_ld + (int64_t)h * head_dim;
+            const int64_t query_pos = N - n_eff + j;
+            /* partial_scores row j: float(double dot * scale), -inf past the query. */
+            for (int64_t i = 0; i < N; ++i) {
+                if (i > query_pos) {
+                    raw[i] = -INFINITY;
+                    continue;
+                }
+                const float* krow = k + i * k_ld + (int64_t)kvh * head_dim;
+                double dot = 0.0;
+                for (int c = 0; c < head_dim; ++c) dot += (double)qrow[c] * (double)krow[c];
+                raw[i] = (float)(dot * scale);
+            }
+            /* Pass 1: running max and denominator in index order (importance.cpp:45-56). */
+            double max_logit = -INFINITY;
+            double denom = 0.0;
+            for (int64_t i = 0; i < N; ++i) {
+                const double x = raw[i];
+                if (x == -INFINITY) continue;
+                if (x > max_logit) {
+                    denom = denom * exp(max_logit - x) + 1.0;
+                    max_logit = x;
+                } else {
+                    denom += exp(x - max_logit);
+                }
+            }
+            if (denom <= 0.0 || !isfinite(max_logit)) {
+                status = ORC_ERR_CONTRACT; /* fully masked query row (:57-59) */
+                break;
+            }
+            /* Pass 2: normalized weights into the shared accumulator (:61-66). */
+            for (int64_t i = 0; i < N; ++i) {
+                const double x = raw[i];
+                if (x == -INFINITY) continue;
+                acc[i] += exp(x - max_logit) / denom * inv_n;
+            }
+        }
+    }
+    if (status == ORC_OK) {
+        float* ts = token_scores ? token_scores : (float*)malloc((size_t)N * sizeof(float));
+        for (int64_t i = 0; i < N; ++i) ts[i] = (float)acc[i];
+        status = orc_block_reduce(ts, N, cfg->block_size_g, block_scores);
+        if (!token_scores) free(ts);
+    }
+    free(acc);
+    free(raw);
+    return status;
+}
+
+/* ------------------------------------------------------------------ TP reduction */
+
+/* allreduce_scores (tp_sim.cpp:29-49): ids must be exactly 0..T-1; fp32 sum in ascending
+ * shard id starting from 0.0f. */
+int orc_allreduce_scores(const float* const* shards, const int32_t* shard_ids, int32_t tp,
+                         int64_t length, float* out) {
+    if (tp <= 0) return ORC_ERR_CONTRACT;
+    const float** by_id = (const float**)calloc((size_t)tp, sizeof(float*));
+    for (int32_t t = 0; t < tp; ++t) {
+        const int32_t id = shard_ids[t];
+        if (id < 0 || id >= tp || by_id[id] != NULL) {
+            free(by_id);
+            return ORC_ERR_CONTRACT;
+        }
+        by_id[id] = shards[t];
+    }
+    for (int64_t g = 0; g < length; ++g) out[g] = 0.0f;
+    for (int32_t t = 0; t < tp; ++t) {
+        const float* b = by_id[t];
+        for (int64_t g = 0; g < length; ++g) out[g] += b[g];
+    }
+    free(by_id);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ selection */
+
+/* expand_mask (selection.cpp:36-49). */
+int orc_expand_mask(const uint8_t* block_mask, int64_t num_blocks, int block_size,
+                    int64_t num_tokens, int64_t sink_count, int64_t window_n, uint8_t* keep) {
+    if (block_size <= 0) return ORC_ERR_CONTRACT;
+    if (num_blocks != (num_tokens + block_size - 1) / block_size) return ORC_ERR_CONTRACT;
+    for (int64_t i = 0; i < num_tokens; ++i) {
+        const int block_kept = block_mask[i / block_size] != 0;
+        keep[i] = (block_kept || i < sink_count || i >= num_tokens - window_n) ? 1 : 0;
+    }
+    return ORC_OK;
+}
+
+static int cmp_u64_desc(const void* a, const void* b) {
+    const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? 1 : (x > y ? -1 : 0);
+}
+
+/* Token-level covered mass (selection.cpp:108-120, propagation.cpp:126-135). */
+static double covered_sum(const uint8_t* keep, int64_t num_tokens, const float* block_scores,
+                          int64_t num_blocks, int G) {
+    double covered = 0.0;
+    for (int64_t g = 0; g < num_blocks; ++g) {
+        const int64_t b = g * G;
+        const int64_t e = (b + G < num_tokens) ? b + G : num_tokens;
+        int64_t kept = 0;
+        for (int64_t i = b; i < e; ++i) kept += keep[i];
+        covered += (double)block_scores[g] * ((double)kept / (double)(e - b));
+    }
+    return covered;
+}
+
+/* top_p_select (selection.cpp:51-122). */
+int orc_top_p_select(const float* block_scores, int64_t num_blocks, const orc_score_config* cfg,
+                     int64_t num_tokens, uint8_t* keep, orc_selection_info* info) {
+    int st = orc_config_validate(cfg);
+    if (st != ORC_OK) return st;
+    if (num_tokens < 1) return ORC_ERR_CONTRACT;
+    const int G = cfg->block_size_g;
+    const int64_t nb = (num_tokens + G - 1) / G;
+    if (num_blocks != nb) return ORC_ERR_CONTRACT;
+
+    /* total: sequential double sum in block-index order (:61-67). */
+    double total = 0.0;
+    for (int64_t g = 0; g < nb; ++g) {
+        const float s = block_scores[g];
+        if (!(s >= 0.0f) || !isfinite(s)) return ORC_ERR_CONTRACT;
+        total += s;
+    }
+    const int64_t n_eff = cfg->query_window_n < num_tokens ? cfg->query_window_n : num_tokens;
+    uint8_t* block_mask = (uint8_t*)calloc((size_t)nb, 1);
+    int degenerate = 0;
+    int64_t k_star = 0;
+    if (total <= 0.0) {
+        degenerate = 1;
+        k_star = nb;
+        memset(block_mask, 1, (size_t)nb);
+    } else {
+        uint64_t* packed = (uint64_t*)malloc((size_t)nb * sizeof(uint64_t));
+        for (int64_t g = 0; g < nb; ++g) orc_pack_score(block_scores[g], (uint32_t)g, &packed[g]);
+        qsort(packed, (size_t)nb, sizeof(uint64_t), cmp_u64_desc);
+        /* cum: sequential double sum of decoded floats in sorted order; the threshold is
+         * compared as cum/total >= double(top_p) (:80-93). */
+        double cumulative = 0.0;
+        const double threshold = (double)cfg->top_p;
+        for (int64_t r = 0; r < nb; ++r) {
+            const uint64_t w = packed[r];
+            cumulative += (double)orc_phi_decode((uint32_t)(w >> 32));
+            block_mask[~(uint32_t)(w & 0xFFFFFFFFu)] = 1;
+            k_star = r + 1;
+            if (cumulative / total >= threshold) break;
+        }
+        free(packed);
+    }
+    orc_expand_mask(block_mask, nb, G, num_tokens, cfg->sink_count_a, n_eff, keep);
+    free(block_mask);
+
+    int64_t retained = 0;
+    for (int64_t i = 0; i < num_tokens; ++i) retained += keep[i];
+    info->cutoff_rank = k_star;
+    info->retained_count = retained;
+    info->retention_ratio = (double)retained / (double)num_tokens;
+    info->degenerate_keep_all = degenerate;
+    if (degenerate || total <= 0.0) {
+        info->covered_mass = 1.0;
+    } else {
+        info->covered_mass = covered_sum(keep, num_tokens, block_scores, nb, G) / total;
+    }
+    return ORC_OK;
+}
+
+/* Veto + restrict_selection (propagation.cpp:116-136, :173-183): only when the veto
+ * actually removes a kept row are retained/ratio/covered recomputed. */
+int orc_restrict_selection(uint8_t* keep, const uint8_t* veto, int64_t num_tokens,
+                           const float* block_scores, int64_t num_blocks, int block_size,
+                           orc_selection_info* info) {
+    int changed = 0;
+    for (int64_t i = 0; i < num_tokens; ++i) {
+        if (keep[i] && veto[i]) {
+            keep[i] = 0;
+            changed = 1;
+        }
+    }
+    if (!changed) return ORC_OK;
+    int64_t retained = 0;
+    for (int64_t i = 0; i < num_tokens; ++i) retained += keep[i];
+    info->retained_count = retained;
+    info->retention_ratio = (double)retained / (double)num_tokens;
+    double total = 0.0;
+    for (int64_t g = 0; g < num_blocks; ++g) total += block_scores[g];
+    const double covered = covered_sum(keep, num_tokens, block_scores, num_blocks, block_size);
+    info->covered_mass = total > 0.0 ? covered / total : 1.0;
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ compaction */
+
+/* patch_metadata (scheduler.cpp:50-90) + apply_drop's stable row compaction
+ * (propagation.cpp:47-77): kept rows of selected segments, all rows of the others, in
+ * order; new_cu[s+1] = new_cu[s] + kept_s. */
+int orc_compact(const uint8_t* keep, const int64_t* cu_seqlens, int32_t num_requests,
+                const uint8_t* selected, int32_t n_planes, const void* const* src,
+                void* const* dst, const int64_t* row_bytes, int64_t* cu_out,
+                int64_t* retained_index, int64_t* num_out) {
+    if (num_requests < 0 || cu_seqlens[0] != 0) return ORC_ERR_CONTRACT;
+    for (int32_t s = 0; s < num_requests; ++s) {
+        if (cu_seqlens[s + 1] <= cu_seqlens[s]) return ORC_ERR_CONTRACT;
+    }
+    int64_t out = 0;
+    cu_out[0] = 0;
+    for (int32_t s = 0; s < num_requests; ++s) {
+        const int sel = selected == NULL || selected[s] != 0;
+        for (int64_t i = cu_seqlens[s]; i < cu_seqlens[s + 1]; ++i) {
+            if (sel && !keep[i]) continue;
+            for (int32_t p = 0; p < n_planes; ++p) {
+                memcpy((char*)dst[p] + out * row_bytes[p], (const char*)src[p] + i * row_bytes[p],
+                       (size_t)row_bytes[p]);
+            }
+            if (retained_index) retained_index[out] = i;
+            ++out;
+        }
+        cu_out[s + 1] = out;
+    }
+    *num_out = out;
+    return ORC_OK;
+}
+
+/* scoring_flops (flops.cpp:35-39). */
+uint64_t orc_scoring_flops(int64_t effective_n, int64_t num_keys, int head_dim, int num_heads) {
+    return 2ULL * (uint64_t)effective_n * (uint64_t)num_keys * (uint64_t)head_dim *
+           (uint64_t)num_heads;
+}

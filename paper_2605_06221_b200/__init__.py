@@ -1,0 +1,22 @@
+"""B200-native UniPrefill token-selection hot path (score -> top-p keep mask -> compact).
+
+The compute lives in hand-written sm_100a kernels behind the C ABI in
+``include/uniprefill_b200.h`` (``_lib/libuniprefill_b200.so``); this package is the host-side
+mirror of the reference's operator API (see ``api.py``).
+"""
+from .api import (BlockScores, Compacted, ConfigError, ContractViolation, CudaError, DropEvent,
+                  DropHistory, DropLayer, HeadLayout, ImportanceScores, PackedBatch, ScoreConfig,
+                  Selection, ShardScores, TokenStream, UnsupportedError, VarlenSelection, Workspace,
+                  allreduce_scores, apply_drop, compact_varlen, patch_metadata, reduce_block_scores,
+                  score_blocks_varlen, score_tokens, score_tokens_heads, select_varlen,
+                  sharded_block_scores, top_p_select)
+from ._capi import LIB_PATH, lib
+
+__all__ = [
+    "BlockScores", "Compacted", "ConfigError", "ContractViolation", "CudaError", "DropEvent",
+    "DropHistory", "DropLayer", "HeadLayout", "ImportanceScores", "PackedBatch", "ScoreConfig",
+    "Selection", "ShardScores", "TokenStream", "UnsupportedError", "VarlenSelection", "Workspace",
+    "allreduce_scores", "apply_drop", "compact_varlen", "patch_metadata", "reduce_block_scores",
+    "score_blocks_varlen", "score_tokens", "score_tokens_heads", "select_varlen",
+    "sharded_block_scores", "top_p_select", "LIB_PATH", "lib",
+]

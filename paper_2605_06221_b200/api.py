@@ -1,0 +1,605 @@
+"""Host-side mirror of the reference operator API for the token-selection hot path.
+
+Every function here validates its arguments, then calls the C ABI
+(``include/uniprefill_b200.h``) on device buffers; all compute runs in the sm_100a kernels
+of ``_lib/libuniprefill_b200.so``.  PyTorch only supplies device memory and the current CUDA
+stream.  There is no CPU fallback: without the library, importing this package fails.
+
+Two layers:
+
+* varlen entry points used by an engine (``score_blocks_varlen``, ``select_varlen``,
+  ``compact_varlen``, ``DropLayer``) -- device-resident metadata, no host syncs;
+* reference-named mirrors with the reference's argument meaning and error behaviour
+  (``score_tokens``, ``score_tokens_heads``, ``top_p_select``, ``sharded_block_scores``,
+  ``allreduce_scores``, ``apply_drop``, ``patch_metadata``), each citing the reference
+  declaration it mirrors, so parity tests read like ``/root/reference/proj/tests``.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _capi
+from ._capi import (BatchC, HeadsC, PlaneC, ScoreConfigC, SelectionOutC, lib)
+
+
+# --------------------------------------------------------------------------- errors
+class ConfigError(ValueError):
+    """Reference ConfigError (errors.hpp:15-18)."""
+
+
+class ContractViolation(RuntimeError):
+    """Reference ContractViolation (errors.hpp:22-25)."""
+
+
+class UnsupportedError(RuntimeError):
+    """Valid input outside the implemented envelope."""
+
+
+class CudaError(RuntimeError):
+    """CUDA runtime / driver failure."""
+
+
+def _check(status: int, what: str) -> None:
+    if status == _capi.UP_OK:
+        return
+    msg = f"{what}: {_capi.status_string(status)}"
+    if status == _capi.UP_ERR_CONFIG:
+        raise ConfigError(msg)
+    if status == _capi.UP_ERR_CONTRACT:
+        raise ContractViolation(msg)
+    if status == _capi.UP_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    if status == _capi.UP_ERR_CUDA:
+        raise CudaError(msg)
+    raise RuntimeError(msg)
+
+
+# --------------------------------------------------------------------------- config
+@dataclass
+class ScoreConfig:
+    """ScoreConfig (config.hpp:53-63): n=128, G=64, A=128, p=0.99."""
+
+    query_window_n: int = 128
+    block_size_g: int = 64
+    sink_count_a: int = 128
+    top_p: float = 0.99
+
+    def c(self) -> ScoreConfigC:
+        return ScoreConfigC(int(self.query_window_n), int(self.block_size_g),
+                            int(self.sink_count_a), float(self.top_p))
+
+    def validate(self) -> None:
+        """ScoreConfig::validate (config.cpp:98-103) -> ConfigError."""
+        _check(lib.up_config_validate(ctypes.byref(self.c())), "ScoreConfig.validate")
+
+
+@dataclass
+class HeadLayout:
+    """Head layout of q / k on this rank (up_heads)."""
+
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int
+    gqa_group: Optional[int] = None  # global Hq / Hkv; defaults to local Hq / Hkv
+    q_head_offset: int = 0
+    kv_head_offset: int = 0
+
+    def c(self, q_row_stride: int, k_row_stride: int) -> HeadsC:
+        group = self.gqa_group if self.gqa_group is not None else self.num_q_heads // self.num_kv_heads
+        return HeadsC(self.num_q_heads, self.num_kv_heads, self.head_dim, group, self.q_head_offset,
+                      self.kv_head_offset, q_row_stride, k_row_stride)
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _as_i32_cuda(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.int32).contiguous()
+    return torch.tensor(list(x), dtype=torch.int32, device=device)
+
+
+def _batch(cu: torch.Tensor, max_tokens: int, drop_enabled: Optional[torch.Tensor]) -> BatchC:
+    return BatchC(cu.numel() - 1, int(max_tokens), ctypes.c_void_p(cu.data_ptr()),
+                  None if drop_enabled is None else ctypes.c_void_p(drop_enabled.data_ptr()))
+
+
+class Workspace:
+    """Device scratch shared by all entry points; grows on demand, zeroed once."""
+
+    def __init__(self, device=None):
+        self.device = torch.device(device if device is not None else "cuda")
+        self.buf: Optional[torch.Tensor] = None
+
+    def get(self, batch: BatchC, heads: Optional[HeadsC], cfg: ScoreConfigC) -> torch.Tensor:
+        need = lib.up_workspace_bytes(ctypes.byref(batch),
+                                      ctypes.byref(heads) if heads is not None else None,
+                                      ctypes.byref(cfg))
+        if self.buf is None or self.buf.numel() < need:
+            self.buf = torch.zeros(max(int(need), 256), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+    def device_status(self) -> None:
+        """Raise the sticky device-side error (ContractViolation / UnsupportedError), if any."""
+        if self.buf is None:
+            return
+        _check(lib.up_device_status(_stream_ptr(self.device), ctypes.c_void_p(self.buf.data_ptr())),
+               "device status")
+
+
+_default_ws: dict = {}
+
+
+def _ws(device) -> Workspace:
+    key = str(torch.device(device))
+    if key not in _default_ws:
+        _default_ws[key] = Workspace(device)
+    return _default_ws[key]
+
+
+# --------------------------------------------------------------------------- varlen API
+@dataclass
+class BlockScores:
+    block_scores: torch.Tensor          # fp32 [>= Σ ceil(N_r/G)]
+    cu_blocks: torch.Tensor             # int32 [R+1]
+    token_scores: Optional[torch.Tensor] = None
+
+
+def _heads_view(x: torch.Tensor, num_heads: int):
+    """Accept [T, H, D] or [T, H*D]; return (tensor, row_stride_elements, D)."""
+    if x.dim() == 3:
+        if x.stride(2) != 1 or x.stride(1) != x.shape[2]:
+            raise ContractViolation("q/k heads must be contiguous within a row")
+        return x, x.stride(0), x.shape[2]
+    if x.dim() == 2:
+        if x.stride(1) != 1 or x.shape[1] % num_heads != 0:
+            raise ContractViolation("score_tokens: bad head layout")
+        return x, x.stride(0), x.shape[1] // num_heads
+    raise ContractViolation("q/k must be [T, H, D] or [T, H*D]")
+
+
+def score_blocks_varlen(q: torch.Tensor, k: torch.Tensor, cu_seqlens, config: ScoreConfig,
+                        heads: Optional[HeadLayout] = None, drop_enabled=None,
+                        want_token_scores: bool = False, max_tokens: Optional[int] = None,
+                        workspace: Optional[Workspace] = None, out: Optional[BlockScores] = None,
+                        check: bool = False) -> BlockScores:
+    """Block scores of every drop-enabled segment (up_score_blocks).
+
+    q: bf16 [T, Hq, D] (or [T, Hq*D]); k: bf16 [T, Hkv, D].  Returns the PARTIAL scores over
+    the local heads (reduce across TP ranks before selection)."""
+    if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16:
+        raise ContractViolation("q and k must be bfloat16")
+    dev = q.device
+    cu = _as_i32_cuda(cu_seqlens, dev)
+    R = cu.numel() - 1
+    T = int(max_tokens if max_tokens is not None else q.shape[0])
+    if heads is None:
+        if q.dim() != 3 or k.dim() != 3:
+            raise ContractViolation("pass heads= for 2-D q/k")
+        heads = HeadLayout(q.shape[1], k.shape[1], q.shape[2])
+    qv, qs, D = _heads_view(q, heads.num_q_heads)
+    kv, ks, _ = _heads_view(k, heads.num_kv_heads)
+    if D != heads.head_dim:
+        raise ContractViolation("partial_scores: head dim mismatch")
+    en = None if drop_enabled is None else drop_enabled.to(device=dev, dtype=torch.uint8).contiguous()
+    b = _batch(cu, T, en)
+    hc = heads.c(qs, ks)
+    cfg = config.c()
+    ws = workspace or _ws(dev)
+    buf = ws.get(b, hc, cfg)
+    nbmax = int(lib.up_max_blocks(ctypes.byref(b), ctypes.byref(cfg)))
+    if out is None:
+        out = BlockScores(torch.empty(nbmax, dtype=torch.float32, device=dev),
+                          torch.empty(R + 1, dtype=torch.int32, device=dev),
+                          torch.empty(T, dtype=torch.float32, device=dev) if want_token_scores else None)
+    st = lib.up_score_blocks(_stream_ptr(dev), ctypes.byref(b), ctypes.byref(hc), ctypes.byref(cfg),
+                             _ptr(qv), _ptr(kv), _ptr(out.block_scores), _ptr(out.cu_blocks),
+                             _ptr(out.token_scores), ctypes.c_void_p(buf.data_ptr()), buf.numel())
+    _check(st, "score_blocks")
+    if check:
+        ws.device_status()
+    return out
+
+
+@dataclass
+class VarlenSelection:
+    keep: torch.Tensor             # uint8 [T]
+    cutoff_rank: torch.Tensor      # int64 [R] (-1 for pass-through segments)
+    retained_count: torch.Tensor   # int64 [R]
+    covered_mass: torch.Tensor     # float64 [R]
+    degenerate: torch.Tensor       # uint8 [R]
+
+
+def select_varlen(block_scores: torch.Tensor, cu_blocks: torch.Tensor, cu_seqlens, config: ScoreConfig,
+                  veto: Optional[torch.Tensor] = None, drop_enabled=None,
+                  max_tokens: Optional[int] = None, workspace: Optional[Workspace] = None,
+                  out: Optional[VarlenSelection] = None, check: bool = False) -> VarlenSelection:
+    """Top-p keep mask of every drop-enabled segment (up_select)."""
+    dev = block_scores.device
+    cu = _as_i32_cuda(cu_seqlens, dev)
+    R = cu.numel() - 1
+    T = int(max_tokens) if max_tokens is not None else int(cu[-1].item())
+    en = None if drop_enabled is None else drop_enabled.to(device=dev, dtype=torch.uint8).contiguous()
+    b = _batch(cu, T, en)
+    cfg = config.c()
+    ws = workspace or _ws(dev)
+    buf = ws.get(b, None, cfg)
+    if out is None:
+        out = VarlenSelection(torch.empty(T, dtype=torch.uint8, device=dev),
+                              torch.empty(R, dtype=torch.int64, device=dev),
+                              torch.empty(R, dtype=torch.int64, device=dev),
+                              torch.empty(R, dtype=torch.float64, device=dev),
+                              torch.empty(R, dtype=torch.uint8, device=dev))
+    so = SelectionOutC(_ptr(out.cutoff_rank), _ptr(out.retained_count), _ptr(out.covered_mass),
+                       _ptr(out.degenerate))
+    vt = None if veto is None else veto.to(device=dev, dtype=torch.uint8).contiguous()
+    st = lib.up_select(_stream_ptr(dev), ctypes.byref(b), ctypes.byref(cfg), _ptr(block_scores),
+                       _ptr(cu_blocks), _ptr(vt), _ptr(out.keep), ctypes.byref(so),
+                       ctypes.c_void_p(buf.data_ptr()), buf.numel())
+    _check(st, "select")
+    if check:
+        ws.device_status()
+    return out
+
+
+@dataclass
+class Compacted:
+    planes: List[torch.Tensor]     # compacted copies (capacity rows; first num_out valid)
+    cu_seqlens: torch.Tensor       # int32 [R+1]
+    retained_index: torch.Tensor   # int32 [capacity]
+    num_out: torch.Tensor          # int32 [1] (device)
+
+    def trimmed(self) -> "Compacted":
+        n = int(self.num_out.item())
+        return Compacted([p[:n] for p in self.planes], self.cu_seqlens, self.retained_index[:n],
+                         self.num_out)
+
+
+def compact_varlen(keep: torch.Tensor, cu_seqlens, planes: Sequence[torch.Tensor], drop_enabled=None,
+                   max_tokens: Optional[int] = None, outs: Optional[Sequence[torch.Tensor]] = None,
+                   workspace: Optional[Workspace] = None, result: Optional[Compacted] = None,
+                   check: bool = False) -> Compacted:
+    """Segmented prefix sum + gather of retained rows (up_compact).  planes: [T, ...] tensors."""
+    dev = keep.device
+    cu = _as_i32_cuda(cu_seqlens, dev)
+    R = cu.numel() - 1
+    T = int(max_tokens) if max_tokens is not None else int(keep.numel())
+    en = None if drop_enabled is None else drop_enabled.to(device=dev, dtype=torch.uint8).contiguous()
+    b = _batch(cu, T, en)
+    ws = workspace or _ws(dev)
+    buf = ws.get(b, None, ScoreConfig(1, 1, 0, 1.0).c())
+    if result is None:
+        if outs is None:
+            outs = [torch.empty_like(p) for p in planes]
+        result = Compacted(list(outs), torch.empty(R + 1, dtype=torch.int32, device=dev),
+                           torch.empty(T, dtype=torch.int32, device=dev),
+                           torch.empty(1, dtype=torch.int32, device=dev))
+    arr = (PlaneC * max(len(planes), 1))()
+    for i, (src, dst) in enumerate(zip(planes, result.planes)):
+        if not (src.is_contiguous() and dst.is_contiguous()):
+            raise ContractViolation("compact planes must be contiguous")
+        rb = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
+        arr[i] = PlaneC(src.data_ptr(), dst.data_ptr(), rb, 0, 0)
+    st = lib.up_compact(_stream_ptr(dev), ctypes.byref(b), _ptr(keep), arr, len(planes),
+                        _ptr(result.cu_seqlens), _ptr(result.retained_index), _ptr(result.num_out),
+                        ctypes.c_void_p(buf.data_ptr()), buf.numel())
+    _check(st, "compact")
+    if check:
+        ws.device_status()
+    return result
+
+
+def reduce_block_scores(shards: Sequence[torch.Tensor], out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Ascending-shard fp32 sum (up_reduce_block_scores), bitwise like allreduce_scores."""
+    if len(shards) == 0:
+        raise ContractViolation("allreduce_scores: no shards")
+    n = shards[0].numel()
+    if any(s.numel() != n for s in shards):
+        raise ContractViolation("allreduce_scores: shard length mismatch")
+    dev = shards[0].device
+    out = torch.empty(n, dtype=torch.float32, device=dev) if out is None else out
+    ptrs = (ctypes.c_void_p * len(shards))(*[s.data_ptr() for s in shards])
+    _check(lib.up_reduce_block_scores(_stream_ptr(dev), ptrs, len(shards), n, _ptr(out)),
+           "reduce_block_scores")
+    return out
+
+
+# --------------------------------------------------------------------------- engine hook
+class DropLayer:
+    """score -> select -> compact for one full-attention drop layer over a varlen batch.
+
+    Buffers are preallocated for a capacity of ``max_tokens`` rows and ``num_requests``
+    segments, so a layer step issues only kernel launches (capturable in a CUDA graph).
+    Mirrors prefill_layer_step's drop section (propagation.cpp:163-202) followed by
+    patch_metadata (scheduler.cpp:332)."""
+
+    def __init__(self, config: ScoreConfig, heads: HeadLayout, max_tokens: int, num_requests: int,
+                 plane_shapes: Sequence[tuple], plane_dtypes: Sequence[torch.dtype], device=None):
+        config.validate()
+        self.config = config
+        self.heads = heads
+        self.device = torch.device(device if device is not None else "cuda")
+        self.max_tokens = int(max_tokens)
+        self.R = int(num_requests)
+        dev = self.device
+        self.ws = Workspace(dev)
+        cfg = config.c()
+        G = config.block_size_g
+        nb = self.max_tokens // G + self.R + 1
+        self.scores = BlockScores(torch.empty(nb, dtype=torch.float32, device=dev),
+                                  torch.empty(self.R + 1, dtype=torch.int32, device=dev))
+        self.sel = VarlenSelection(torch.empty(self.max_tokens, dtype=torch.uint8, device=dev),
+                                   torch.empty(self.R, dtype=torch.int64, device=dev),
+                                   torch.empty(self.R, dtype=torch.int64, device=dev),
+                                   torch.empty(self.R, dtype=torch.float64, device=dev),
+                                   torch.empty(self.R, dtype=torch.uint8, device=dev))
+        self.out = Compacted([torch.empty((self.max_tokens, *s), dtype=d, device=dev)
+                              for s, d in zip(plane_shapes, plane_dtypes)],
+                             torch.empty(self.R + 1, dtype=torch.int32, device=dev),
+                             torch.empty(self.max_tokens, dtype=torch.int32, device=dev),
+                             torch.empty(1, dtype=torch.int32, device=dev))
+        self._cfg = cfg
+        self.last_launches = 0
+
+    def __call__(self, q: torch.Tensor, k: torch.Tensor, cu_seqlens: torch.Tensor,
+                 planes: Sequence[torch.Tensor], drop_enabled: Optional[torch.Tensor] = None,
+                 veto: Optional[torch.Tensor] = None, block_scores_hook=None) -> Compacted:
+        """block_scores_hook(block_scores) runs between scoring and selection (TP all-reduce)."""
+        score_blocks_varlen(q, k, cu_seqlens, self.config, self.heads, drop_enabled,
+                            max_tokens=self.max_tokens, workspace=self.ws, out=self.scores)
+        n = lib.up_last_launch_count()
+        if block_scores_hook is not None:
+            block_scores_hook(self.scores.block_scores)
+        select_varlen(self.scores.block_scores, self.scores.cu_blocks, cu_seqlens, self.config, veto,
+                      drop_enabled, max_tokens=self.max_tokens, workspace=self.ws, out=self.sel)
+        n += lib.up_last_launch_count()
+        compact_varlen(self.sel.keep, cu_seqlens, planes, drop_enabled, max_tokens=self.max_tokens,
+                       workspace=self.ws, result=self.out)
+        n += lib.up_last_launch_count()
+        self.last_launches = n
+        return self.out
+
+    def check(self) -> None:
+        self.ws.device_status()
+
+
+# --------------------------------------------------------------------------- reference mirrors
+@dataclass
+class ImportanceScores:
+    """ImportanceScores (importance.hpp:18-23)."""
+
+    token_scores: torch.Tensor
+    block_scores: torch.Tensor
+    num_tokens: int
+    effective_n: int
+
+
+def score_tokens_heads(q: torch.Tensor, k: torch.Tensor, num_heads: int, head_begin: int,
+                       head_end: int, config: ScoreConfig, num_kv_heads: Optional[int] = None,
+                       want_token_scores: bool = True) -> ImportanceScores:
+    """score_tokens_heads (importance.hpp:42-43) on one request.
+
+    q: bf16 [N, num_heads*D] (head-blocked columns, already rotated); k: bf16
+    [N, num_kv_heads*D] (num_kv_heads defaults to num_heads, as in the MHA reference)."""
+    kvh = num_heads if num_kv_heads is None else num_kv_heads
+    if q.dim() != 2 or k.dim() != 2 or q.shape[1] % num_heads != 0 or k.shape[1] % kvh != 0:
+        raise ContractViolation("score_tokens: bad head layout")
+    D = q.shape[1] // num_heads
+    if k.shape[1] // kvh != D or num_heads % kvh != 0:
+        raise ContractViolation("score_tokens: bad head layout")
+    if head_begin < 0 or head_end > num_heads or head_begin >= head_end:
+        raise ContractViolation("score_tokens: bad head range")
+    if k.shape[0] != q.shape[0]:
+        raise ContractViolation("score_tokens: q/k row mismatch")
+    N = k.shape[0]
+    if N < 1:
+        raise ContractViolation("block_reduce: empty scores")
+    if config.block_size_g <= 0:
+        raise ContractViolation("block_reduce: block size must be positive")
+    group = num_heads // kvh
+    heads = HeadLayout(head_end - head_begin, kvh, D, group, head_begin, 0)
+    qs = q[:, head_begin * D: head_end * D]
+    res = score_blocks_varlen(qs, k, [0, N], config, heads, want_token_scores=want_token_scores,
+                              check=True)
+    nb = (N + config.block_size_g - 1) // config.block_size_g
+    return ImportanceScores(res.token_scores[:N] if res.token_scores is not None else None,
+                            res.block_scores[:nb], N, min(config.query_window_n, N))
+
+
+def score_tokens(q: torch.Tensor, k: torch.Tensor, num_heads: int, config: ScoreConfig,
+                 num_kv_heads: Optional[int] = None, want_token_scores: bool = True) -> ImportanceScores:
+    """score_tokens (importance.hpp:46-47): all heads."""
+    return score_tokens_heads(q, k, num_heads, 0, num_heads, config, num_kv_heads, want_token_scores)
+
+
+@dataclass
+class ShardScores:
+    """ShardScores (tp_sim.hpp:16-19)."""
+
+    shard_id: int
+    block_scores: torch.Tensor
+
+
+def sharded_block_scores(q: torch.Tensor, k: torch.Tensor, num_heads: int, config: ScoreConfig,
+                         tp_degree: int, num_kv_heads: Optional[int] = None) -> List[ShardScores]:
+    """sharded_block_scores (tp_sim.hpp:25-26): shard t scores heads [tH/T, (t+1)H/T)."""
+    if tp_degree <= 0:
+        raise ConfigError("tp_degree must be positive")
+    if num_heads % tp_degree != 0:
+        raise ConfigError("num_heads must be divisible by tp_degree")
+    hps = num_heads // tp_degree
+    return [ShardScores(t, score_tokens_heads(q, k, num_heads, t * hps, (t + 1) * hps, config,
+                                              num_kv_heads, want_token_scores=False).block_scores.clone())
+            for t in range(tp_degree)]
+
+
+def allreduce_scores(shards: Sequence[ShardScores]) -> torch.Tensor:
+    """allreduce_scores (tp_sim.hpp:31, tp_sim.cpp:29-49): ids exactly 0..T-1, fp32 ascending sum."""
+    if len(shards) == 0:
+        raise ContractViolation("allreduce_scores: no shards")
+    T = len(shards)
+    by_id: List[Optional[ShardScores]] = [None] * T
+    for s in shards:
+        if s.shard_id < 0 or s.shard_id >= T or by_id[s.shard_id] is not None:
+            raise ContractViolation("allreduce_scores: shard ids must be exactly 0..T-1")
+        if s.block_scores.numel() != shards[0].block_scores.numel():
+            raise ContractViolation("allreduce_scores: shard length mismatch")
+        by_id[s.shard_id] = s
+    return reduce_block_scores([s.block_scores.contiguous() for s in by_id])
+
+
+@dataclass
+class Selection:
+    """Selection (selection.hpp:34-57), device-resident."""
+
+    keep_mask: torch.Tensor
+    retained_indices: torch.Tensor
+    retention_ratio: float
+    covered_mass: float
+    cutoff_rank: int
+    degenerate_keep_all: bool
+
+    def num_tokens(self) -> int:
+        return int(self.keep_mask.numel())
+
+    def retained_count(self) -> int:
+        return int(self.retained_indices.numel())
+
+
+def top_p_select(block_scores, config: ScoreConfig, num_tokens: int,
+                 veto: Optional[torch.Tensor] = None, device=None) -> Selection:
+    """top_p_select (selection.hpp:53-54) on one request (+ optional no-readmission veto)."""
+    config.validate()
+    if num_tokens < 1:
+        raise ContractViolation("top_p_select: num_tokens must be positive")
+    dev = torch.device(device) if device is not None else (
+        block_scores.device if isinstance(block_scores, torch.Tensor) and block_scores.is_cuda
+        else torch.device("cuda"))
+    bs = torch.as_tensor(block_scores, dtype=torch.float32).to(dev).contiguous()
+    nb = (num_tokens + config.block_size_g - 1) // config.block_size_g
+    if bs.numel() != nb:
+        raise ContractViolation("top_p_select: block score length must be ceil(N/G)")
+    cu = torch.tensor([0, num_tokens], dtype=torch.int32, device=dev)
+    cub = torch.tensor([0, nb], dtype=torch.int32, device=dev)
+    sel = select_varlen(bs, cub, cu, config, veto=veto, max_tokens=num_tokens, check=True)
+    idx = compact_varlen(sel.keep, cu, [], max_tokens=num_tokens, check=True)
+    n_ret = int(idx.num_out.item())
+    return Selection(sel.keep, idx.retained_index[:n_ret].to(torch.int64), n_ret / num_tokens,
+                     float(sel.covered_mass[0].item()), int(sel.cutoff_rank[0].item()),
+                     bool(sel.degenerate[0].item()))
+
+
+# ---- propagation / scheduler mirrors ------------------------------------------------
+@dataclass
+class DropEvent:
+    """DropEvent (drop_history.hpp:14-18)."""
+
+    layer: int
+    retained_length: int
+    retained_positions: torch.Tensor
+
+
+@dataclass
+class DropHistory:
+    """DropHistory (drop_history.hpp:20-31)."""
+
+    events: List[DropEvent] = field(default_factory=list)
+    original_length: int = 0
+    decode_appended: int = 0
+
+
+@dataclass
+class TokenStream:
+    """TokenStream (propagation.hpp:21-39).  Parked rows are kept as (positions, states)
+    gathered out of the pre-drop buffer; the pre-drop buffer itself is left untouched
+    (out-of-place compaction, propagation.cpp:64-67)."""
+
+    active_states: torch.Tensor
+    logical_positions: torch.Tensor
+    parked_positions: List[torch.Tensor] = field(default_factory=list)
+    parked_states: List[torch.Tensor] = field(default_factory=list)
+    original_length: int = 0
+
+    @staticmethod
+    def from_prompt(prompt: torch.Tensor) -> "TokenStream":
+        if prompt.shape[0] < 1:
+            raise ContractViolation("TokenStream: prompt must be non-empty")
+        pos = torch.arange(prompt.shape[0], dtype=torch.int64, device=prompt.device)
+        return TokenStream(prompt, pos, [], [], prompt.shape[0])
+
+    def active_count(self) -> int:
+        return int(self.logical_positions.numel())
+
+
+def apply_drop(stream: TokenStream, selection: Selection, layer: int, history: DropHistory) -> None:
+    """apply_drop (propagation.hpp:415, propagation.cpp:47-77) through up_compact."""
+    rows = stream.active_count()
+    if selection.num_tokens() != rows:
+        raise ContractViolation("apply_drop: selection length disagrees with the active stream")
+    keep = selection.keep_mask
+    cu = torch.tensor([0, rows], dtype=torch.int32, device=keep.device)
+    states = stream.active_states.contiguous()
+    pos = stream.logical_positions.contiguous()
+    res = compact_varlen(keep, cu, [states, pos], max_tokens=rows, check=True).trimmed()
+    dropped = (keep == 0)
+    if bool(dropped.any()):
+        inv = (1 - keep).to(torch.uint8)
+        park = compact_varlen(inv, cu, [states, pos], max_tokens=rows, check=True).trimmed()
+        stream.parked_states.append(park.planes[0])
+        stream.parked_positions.append(park.planes[1])
+    stream.active_states = res.planes[0]
+    stream.logical_positions = res.planes[1]
+    history.events.append(DropEvent(layer, int(res.planes[1].numel()), res.planes[1]))
+
+
+@dataclass
+class PackedBatch:
+    """PackedBatch (scheduler.hpp:33-46)."""
+
+    tokens: torch.Tensor
+    cu_seqlens: torch.Tensor       # int64 or int32 [R+1]
+    phases: List[str]              # "prefill" / "decode"
+
+    def num_requests(self) -> int:
+        return len(self.phases)
+
+
+def patch_metadata(batch: PackedBatch, selections: Sequence[Optional[Selection]], layer: int) -> None:
+    """patch_metadata (scheduler.hpp:52-53, scheduler.cpp:50-90) through up_compact."""
+    del layer
+    R = batch.num_requests()
+    if len(selections) != R:
+        raise ContractViolation("patch_metadata: one selection slot per request required")
+    cu_h = [int(x) for x in batch.cu_seqlens.tolist()]
+    if len(cu_h) != R + 1 or cu_h[0] != 0:
+        raise ContractViolation("PackedBatch: cu_seqlens must start at 0")
+    if any(cu_h[i] <= cu_h[i - 1] for i in range(1, len(cu_h))):
+        raise ContractViolation("PackedBatch: cu_seqlens must be strictly increasing")
+    if cu_h[-1] != batch.tokens.shape[0]:
+        raise ContractViolation("PackedBatch: cu_seqlens must end at the total token count")
+    dev = batch.tokens.device
+    T = cu_h[-1]
+    keep = torch.ones(T, dtype=torch.uint8, device=dev)
+    enabled = torch.zeros(R, dtype=torch.uint8, device=dev)
+    for s, sel in enumerate(selections):
+        if sel is None:
+            continue
+        if batch.phases[s] != "prefill":
+            raise ContractViolation("patch_metadata: drops apply only to prefill segments")
+        if sel.num_tokens() != cu_h[s + 1] - cu_h[s]:
+            raise ContractViolation("patch_metadata: selection length disagrees with segment")
+        keep[cu_h[s]:cu_h[s + 1]] = sel.keep_mask.to(dev)
+        enabled[s] = 1
+    res = compact_varlen(keep, batch.cu_seqlens, [batch.tokens.contiguous()], drop_enabled=enabled,
+                         max_tokens=T, check=True).trimmed()
+    batch.tokens = res.planes[0]
+    batch.cu_seqlens = res.cu_seqlens.to(torch.int64)

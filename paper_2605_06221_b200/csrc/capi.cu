@@ -1,0 +1,460 @@
+// capi.cu -- the C ABI (include/uniprefill_b200.h): host-side validation, workspace
+// carve-up, TMA descriptor encoding and kernel launches.  No CPU fallback: every entry
+// point either launches its sm_100a kernels or returns an error status.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace up {
+
+// Launchers defined in the kernel translation units.
+struct ScoreTcParams;
+struct ScoreSimtParams;
+struct SelectParams;
+struct CompactParams;
+int tc_max_hpc(int D);
+cudaError_t launch_score_tc(int D, int HPC, const CUtensorMap& qm, const CUtensorMap& km,
+                            const ScoreTcParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_score_plan(const int32_t* cu, const uint8_t* en, int R, int64_t max_tokens,
+                              int G, int unit_tiles, int nhg, int target_items, int32_t* cu_blocks,
+                              int32_t* cu_chunks, int32_t* cu_items, int32_t* plan, uint32_t* err,
+                              cudaStream_t stream);
+cudaError_t launch_row_weights(const int32_t* cu, const uint8_t* en, const int32_t* cu_chunks,
+                               const float* stat_m, const float* stat_l, float* stat_w, int R,
+                               int num_heads, int n, int64_t max_chunks, uint32_t* err,
+                               cudaStream_t stream);
+cudaError_t launch_block_combine(const int32_t* cu, const uint8_t* en, const int32_t* cu_blocks,
+                                 const int32_t* cu_chunks, const int32_t* plan, const float* P,
+                                 const float* stat_w, float* block_scores, int R, int G,
+                                 int num_heads, int64_t max_blocks, int64_t max_chunks, int grid,
+                                 cudaStream_t stream);
+cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int num_sms,
+                              cudaStream_t stream);
+cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request,
+                          cudaStream_t stream);
+cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t count, float* out,
+                                 int num_sms, cudaStream_t stream);
+cudaError_t launch_compact(const CompactParams& p, cudaStream_t stream);
+int64_t compact_tiles(int64_t max_tokens);
+int compact_max_planes();
+
+}  // namespace up
+
+// Full parameter structs (shared with the kernel TUs through identical definitions).
+#include "params.cuh"
+
+using namespace up;
+
+namespace {
+
+thread_local int g_launches = 0;
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+up_status cuda_status(cudaError_t e) { return e == cudaSuccess ? UP_OK : UP_ERR_CUDA; }
+
+// ---- workspace layout --------------------------------------------------------------
+struct Layout {
+    size_t err, plan, cu_chunks, cu_items, P, stat_m, stat_l, stat_w, simt_m, simt_l, simt_tok,
+        tile_counts, total;
+    int64_t max_blocks, max_chunks;
+    int32_t simt_n;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c) {
+    Layout L{};
+    const int64_t T = b->max_tokens;
+    const int64_t R = b->num_requests;
+    const int64_t G = c->block_size_g > 0 ? c->block_size_g : 1;
+    const int64_t H = h ? h->num_q_heads : 0;
+    L.max_blocks = T / G + R + 1;
+    L.max_chunks = T / kTileKeys + R + 1;
+    const int64_t n = c->query_window_n < T ? c->query_window_n : T;
+    L.simt_n = static_cast<int32_t>(n > 0 ? n : 1);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        off = align_up(off, 256);
+        const size_t at = off;
+        off += bytes;
+        return at;
+    };
+    L.err = take(256);
+    L.plan = take(64);
+    L.cu_chunks = take(sizeof(int32_t) * (R + 1));
+    L.cu_items = take(sizeof(int32_t) * (R + 1));
+    L.P = take(sizeof(float) * H * L.max_blocks * kRows);
+    L.stat_m = take(sizeof(float) * H * L.max_chunks * kRows);
+    L.stat_l = take(sizeof(float) * H * L.max_chunks * kRows);
+    L.stat_w = take(sizeof(float) * H * L.max_chunks * kRows);
+    L.simt_m = take(sizeof(float) * H * R * L.simt_n);
+    L.simt_l = take(sizeof(float) * H * R * L.simt_n);
+    L.simt_tok = take(sizeof(float) * (T + 1));
+    L.tile_counts = take(sizeof(int32_t) * (compact_tiles(T) + 1));
+    L.total = align_up(off, 256);
+    return L;
+}
+
+template <class T>
+T* at(void* ws, size_t off) {
+    return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + off);
+}
+
+up_status check_batch(const up_batch* b) {
+    if (b == nullptr || b->cu_seqlens == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (b->num_requests < 1 || b->max_tokens < 1) return UP_ERR_CONTRACT;
+    if (b->max_tokens > (int64_t{1} << 31) - 1) return UP_ERR_UNSUPPORTED;
+    return UP_OK;
+}
+
+up_status check_heads(const up_heads* h) {
+    if (h == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (h->num_q_heads < 1 || h->num_kv_heads < 1 || h->head_dim < 1 || h->gqa_group < 1)
+        return UP_ERR_CONTRACT;
+    if (h->q_head_offset < 0 || h->kv_head_offset < 0) return UP_ERR_CONTRACT;
+    if (h->q_row_stride < static_cast<int64_t>(h->num_q_heads) * h->head_dim) return UP_ERR_CONTRACT;
+    if (h->k_row_stride < static_cast<int64_t>(h->num_kv_heads) * h->head_dim) return UP_ERR_CONTRACT;
+    // Every local q-head must map to a local kv-head.
+    const int first_kv = h->q_head_offset / h->gqa_group - h->kv_head_offset;
+    const int last_kv = (h->q_head_offset + h->num_q_heads - 1) / h->gqa_group - h->kv_head_offset;
+    if (first_kv < 0 || last_kv >= h->num_kv_heads) return UP_ERR_CONTRACT;
+    return UP_OK;
+}
+
+// ---- TMA descriptors ------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 view [rows, cols] with row stride `ld` elements, box 64 cols x 128 rows, 128B swizzle.
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+    EncodeTiledFn fn = encode_fn();
+    if (fn == nullptr) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    const cuuint32_t box[2] = {64, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int pick_hpc(const up_heads* h) {
+    int hpc = tc_max_hpc(h->head_dim);
+    if (hpc > h->gqa_group) hpc = h->gqa_group;
+    while (hpc > 1 && (h->num_q_heads % hpc || h->q_head_offset % hpc || h->gqa_group % hpc)) hpc >>= 1;
+    return hpc < 1 ? 1 : hpc;
+}
+
+bool tc_eligible(const up_heads* h, const up_score_config* c, int want_tokens) {
+    const int D = h->head_dim;
+    if (want_tokens) return false;
+    if (!(D == 64 || D == 128 || D == 256)) return false;
+    if (c->query_window_n > kRows) return false;
+    if (c->block_size_g % 32 != 0) return false;
+    if ((static_cast<int64_t>(h->q_row_stride) * 2) % 16 || (static_cast<int64_t>(h->k_row_stride) * 2) % 16)
+        return false;
+    return true;
+}
+
+int64_t lcm64(int64_t a, int64_t b) {
+    int64_t x = a, y = b;
+    while (y) { const int64_t t = x % y; x = y; y = t; }
+    return a / x * b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int up_abi_version(void) { return UP_ABI_VERSION; }
+
+const char* up_status_string(up_status s) {
+    switch (s) {
+    case UP_OK: return "ok";
+    case UP_ERR_CONFIG: return "ConfigError: invalid score configuration";
+    case UP_ERR_CONTRACT: return "ContractViolation: operation precondition broken";
+    case UP_ERR_UNSUPPORTED: return "unsupported: valid input outside the implemented envelope";
+    case UP_ERR_WORKSPACE: return "workspace missing or too small";
+    case UP_ERR_CUDA: return "CUDA error";
+    case UP_ERR_INVALID_ARGUMENT: return "invalid argument";
+    }
+    return "unknown status";
+}
+
+int up_last_launch_count(void) { return g_launches; }
+
+up_status up_config_validate(const up_score_config* c) {
+    if (c == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (c->query_window_n <= 0) return UP_ERR_CONFIG;
+    if (c->block_size_g <= 0) return UP_ERR_CONFIG;
+    if (c->sink_count_a < 0) return UP_ERR_CONFIG;
+    if (!(c->top_p > 0.0f && c->top_p <= 1.0f)) return UP_ERR_CONFIG;
+    return UP_OK;
+}
+
+int64_t up_max_blocks(const up_batch* b, const up_score_config* c) {
+    if (b == nullptr || c == nullptr || c->block_size_g <= 0) return 0;
+    return b->max_tokens / c->block_size_g + b->num_requests + 1;
+}
+
+size_t up_workspace_bytes(const up_batch* b, const up_heads* h, const up_score_config* c) {
+    if (b == nullptr || c == nullptr) return 0;
+    return layout_for(b, h, c).total;
+}
+
+int up_scorer_kind(const up_heads* h, const up_score_config* c, int want_token_scores) {
+    if (h == nullptr || c == nullptr) return 0;
+    return tc_eligible(h, c, want_token_scores) ? 1 : 2;
+}
+
+up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
+                          const up_score_config* c, const void* q, const void* k,
+                          float* block_scores, int32_t* cu_blocks, float* token_scores, void* ws,
+                          size_t ws_bytes) {
+    g_launches = 0;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    up_status st = up_config_validate(c);
+    if (st != UP_OK) return st;
+    if ((st = check_batch(b)) != UP_OK) return st;
+    if ((st = check_heads(h)) != UP_OK) return st;
+    if (q == nullptr || k == nullptr || block_scores == nullptr || cu_blocks == nullptr)
+        return UP_ERR_INVALID_ARGUMENT;
+    const Layout L = layout_for(b, h, c);
+    if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
+    const int R = b->num_requests;
+    const int G = c->block_size_g;
+    uint32_t* err = at<uint32_t>(ws, L.err);
+    int32_t* plan = at<int32_t>(ws, L.plan);
+    int32_t* cu_chunks = at<int32_t>(ws, L.cu_chunks);
+    int32_t* cu_items = at<int32_t>(ws, L.cu_items);
+
+    if (tc_eligible(h, c, token_scores != nullptr)) {
+        const int D = h->head_dim;
+        const int hpc = pick_hpc(h);
+        const int nhg = h->num_q_heads / hpc;
+        const int unit_tiles = static_cast<int>(lcm64(G, kTileKeys) / kTileKeys);
+        cudaError_t e = launch_score_plan(b->cu_seqlens, b->drop_enabled, R, b->max_tokens, G,
+                                          unit_tiles, nhg, num_sms() * 3, cu_blocks, cu_chunks,
+                                          cu_items, plan, err, stream);
+        if (e != cudaSuccess) return UP_ERR_CUDA;
+        CUtensorMap qm, km;
+        if (!make_map(&qm, q, b->max_tokens, static_cast<int64_t>(h->num_q_heads) * D, h->q_row_stride) ||
+            !make_map(&km, k, b->max_tokens, static_cast<int64_t>(h->num_kv_heads) * D, h->k_row_stride))
+            return UP_ERR_CUDA;
+        ScoreTcParams p{};
+        p.cu_seqlens = b->cu_seqlens;
+        p.drop_enabled = b->drop_enabled;
+        p.cu_blocks = cu_blocks;
+        p.cu_chunks = cu_chunks;
+        p.cu_items = cu_items;
+        p.plan = plan;
+        p.P = at<float>(ws, L.P);
+        p.stat_m = at<float>(ws, L.stat_m);
+        p.stat_l = at<float>(ws, L.stat_l);
+        p.num_requests = R;
+        p.query_window_n = c->query_window_n;
+        p.block_size_g = G;
+        p.num_hgroups = nhg;
+        p.q_head_offset = h->q_head_offset;
+        p.kv_head_offset = h->kv_head_offset;
+        p.gqa_group = h->gqa_group;
+        p.max_blocks = L.max_blocks;
+        p.max_chunks = L.max_chunks;
+        p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
+        if ((e = launch_score_tc(D, hpc, qm, km, p, num_sms(), stream)) != cudaSuccess) return UP_ERR_CUDA;
+        if ((e = launch_row_weights(b->cu_seqlens, b->drop_enabled, cu_chunks, p.stat_m, p.stat_l,
+                                    at<float>(ws, L.stat_w), R, h->num_q_heads, c->query_window_n,
+                                    L.max_chunks, err, stream)) != cudaSuccess)
+            return UP_ERR_CUDA;
+        if ((e = launch_block_combine(b->cu_seqlens, b->drop_enabled, cu_blocks, cu_chunks, plan, p.P,
+                                      at<float>(ws, L.stat_w), block_scores, R, G, h->num_q_heads,
+                                      L.max_blocks, L.max_chunks, num_sms() * 4, stream)) != cudaSuccess)
+            return UP_ERR_CUDA;
+        g_launches = 4;
+        return UP_OK;
+    }
+
+    // Generic SIMT path.
+    cudaError_t e = launch_score_plan(b->cu_seqlens, b->drop_enabled, R, b->max_tokens, G, 1, 1,
+                                      num_sms() * 3, cu_blocks, cu_chunks, cu_items, plan, err, stream);
+    if (e != cudaSuccess) return UP_ERR_CUDA;
+    ScoreSimtParams p{};
+    p.cu_seqlens = b->cu_seqlens;
+    p.drop_enabled = b->drop_enabled;
+    p.cu_blocks = cu_blocks;
+    p.q = static_cast<const __nv_bfloat16*>(q);
+    p.k = static_cast<const __nv_bfloat16*>(k);
+    p.row_m = at<float>(ws, L.simt_m);
+    p.row_l = at<float>(ws, L.simt_l);
+    p.token_scores = token_scores ? token_scores : at<float>(ws, L.simt_tok);
+    p.block_scores = block_scores;
+    p.q_row_stride = h->q_row_stride;
+    p.k_row_stride = h->k_row_stride;
+    p.num_requests = R;
+    p.num_heads = h->num_q_heads;
+    p.head_dim = h->head_dim;
+    p.gqa_group = h->gqa_group;
+    p.q_head_offset = h->q_head_offset;
+    p.kv_head_offset = h->kv_head_offset;
+    p.query_window_n = c->query_window_n;
+    p.simt_n = L.simt_n;
+    p.block_size_g = G;
+    p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(h->head_dim)));
+    if ((e = launch_score_simt(p, b->max_tokens, num_sms(), stream)) != cudaSuccess) return UP_ERR_CUDA;
+    g_launches = 4;
+    return UP_OK;
+}
+
+up_status up_reduce_block_scores(void* stream, const float* const* shards, int32_t tp,
+                                 int64_t count, float* out) {
+    g_launches = 0;
+    if (shards == nullptr || out == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (tp < 1 || tp > 16) return tp < 1 ? UP_ERR_CONTRACT : UP_ERR_UNSUPPORTED;
+    if (count < 0) return UP_ERR_CONTRACT;
+    for (int t = 0; t < tp; ++t)
+        if (shards[t] == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (count == 0) return UP_OK;
+    const cudaError_t e = launch_reduce_shards(shards, tp, count, out, num_sms(),
+                                               static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return cuda_status(e);
+}
+
+up_status up_select(void* stream, const up_batch* b, const up_score_config* c,
+                    const float* block_scores, const int32_t* cu_blocks, const uint8_t* veto,
+                    uint8_t* keep, const up_selection_out* out, void* ws, size_t ws_bytes) {
+    g_launches = 0;
+    up_status st = up_config_validate(c);
+    if (st != UP_OK) return st;
+    if ((st = check_batch(b)) != UP_OK) return st;
+    if (block_scores == nullptr || cu_blocks == nullptr || keep == nullptr || out == nullptr ||
+        out->cutoff_rank == nullptr)
+        return UP_ERR_INVALID_ARGUMENT;
+    const Layout L = layout_for(b, nullptr, c);
+    if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
+    SelectParams p{};
+    p.cu_seqlens = b->cu_seqlens;
+    p.drop_enabled = b->drop_enabled;
+    p.block_scores = block_scores;
+    p.cu_blocks = cu_blocks;
+    p.veto = veto;
+    p.keep = keep;
+    p.cutoff_rank = out->cutoff_rank;
+    p.retained_count = out->retained_count;
+    p.covered_mass = out->covered_mass;
+    p.degenerate = out->degenerate;
+    p.err = at<uint32_t>(ws, L.err);
+    p.query_window_n = c->query_window_n;
+    p.block_size_g = c->block_size_g;
+    p.sink_count_a = c->sink_count_a;
+    p.top_p = c->top_p;
+    const int64_t per_req = (b->max_tokens + c->block_size_g - 1) / c->block_size_g;
+    const cudaError_t e = launch_select(p, b->num_requests, static_cast<int>(per_req < kMaxSortBlocks ? per_req : kMaxSortBlocks),
+                                        static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return cuda_status(e);
+}
+
+up_status up_compact(void* stream, const up_batch* b, const uint8_t* keep, const up_plane* planes,
+                     int32_t num_planes, int32_t* cu_out, int32_t* retained_index,
+                     int32_t* num_out, void* ws, size_t ws_bytes) {
+    g_launches = 0;
+    up_status st = check_batch(b);
+    if (st != UP_OK) return st;
+    if (keep == nullptr || cu_out == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (num_planes < 0 || num_planes > compact_max_planes()) return UP_ERR_UNSUPPORTED;
+    if (num_planes > 0 && planes == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    up_score_config dummy{1, 1, 0, 1.0f};
+    const Layout L = layout_for(b, nullptr, &dummy);
+    if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
+    CompactParams p{};
+    p.cu_seqlens = b->cu_seqlens;
+    p.drop_enabled = b->drop_enabled;
+    p.keep = keep;
+    p.cu_out = cu_out;
+    p.retained_index = retained_index;
+    p.num_out = num_out;
+    p.tile_counts = at<int32_t>(ws, L.tile_counts);
+    p.num_requests = b->num_requests;
+    p.num_planes = num_planes;
+    p.max_tokens = b->max_tokens;
+    for (int i = 0; i < num_planes; ++i) {
+        const up_plane& pl = planes[i];
+        if (pl.src == nullptr || pl.dst == nullptr || pl.row_bytes <= 0) return UP_ERR_INVALID_ARGUMENT;
+        p.src[i] = static_cast<const uint8_t*>(pl.src);
+        p.dst[i] = static_cast<uint8_t*>(pl.dst);
+        p.row_bytes[i] = pl.row_bytes;
+        p.src_stride[i] = pl.src_stride_bytes > 0 ? pl.src_stride_bytes : pl.row_bytes;
+        p.dst_stride[i] = pl.dst_stride_bytes > 0 ? pl.dst_stride_bytes : pl.row_bytes;
+        if (p.src_stride[i] < pl.row_bytes || p.dst_stride[i] < pl.row_bytes) return UP_ERR_CONTRACT;
+    }
+    const cudaError_t e = launch_compact(p, static_cast<cudaStream_t>(stream));
+    g_launches = 2;
+    return cuda_status(e);
+}
+
+up_status up_drop_layer(void* stream, const up_batch* b, const up_heads* h,
+                        const up_score_config* c, const void* q, const void* k,
+                        const uint8_t* veto, float* block_scores, int32_t* cu_blocks,
+                        uint8_t* keep, const up_selection_out* sel, const up_plane* planes,
+                        int32_t num_planes, int32_t* cu_out, int32_t* retained_index,
+                        int32_t* num_out, void* ws, size_t ws_bytes) {
+    up_status st = up_score_blocks(stream, b, h, c, q, k, block_scores, cu_blocks, nullptr, ws, ws_bytes);
+    if (st != UP_OK) return st;
+    const int n1 = g_launches;
+    st = up_select(stream, b, c, block_scores, cu_blocks, veto, keep, sel, ws, ws_bytes);
+    if (st != UP_OK) return st;
+    const int n2 = g_launches;
+    st = up_compact(stream, b, keep, planes, num_planes, cu_out, retained_index, num_out, ws, ws_bytes);
+    g_launches += n1 + n2;
+    return st;
+}
+
+up_status up_device_status(void* stream, void* ws) {
+    if (ws == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t flags = 0;
+    if (cudaMemcpyAsync(&flags, ws, sizeof(flags), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return UP_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return UP_ERR_CUDA;
+    if (flags != 0) {
+        if (cudaMemsetAsync(ws, 0, sizeof(uint32_t), s) != cudaSuccess) return UP_ERR_CUDA;
+        if (cudaStreamSynchronize(s) != cudaSuccess) return UP_ERR_CUDA;
+    }
+    if (flags & kErrTooManyBlocks) return UP_ERR_UNSUPPORTED;
+    if (flags & (kErrBadScore | kErrBadSeqlens | kErrMaskedRow)) return UP_ERR_CONTRACT;
+    return UP_OK;
+}
+
+}  // extern "C"

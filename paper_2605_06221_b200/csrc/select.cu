@@ -1,0 +1,309 @@
+// select.cu -- per-request top-p keep mask (sm_100a), bit-exact with the reference.
+//
+// One CTA per request (selection.cpp:51-122):
+//   1. validate block scores (finite, >= 0; :61-66) and total them (double);
+//   2. zero mass -> keep-all with the degenerate flag (:73-76);
+//   3. pack (phi(s) << 32 | ~g, :27-34) and bitonic-sort the words descending in shared
+//      memory (ties: lower block index first);
+//   4. parallel double prefix sum of the decoded scores in sorted order, k* = first rank
+//      with cum / total >= double(p) (:80-93).  The reference sums sequentially; a
+//      parallel sum agrees with it to a few ulps, so the decision is taken in parallel
+//      only when every ratio near the crossing clears p by a proven error margin;
+//      otherwise one thread replays the reference's exact sequential sums (bit-exact by
+//      construction: same IEEE double adds in the same order, correctly rounded division);
+//   5. expand blocks to tokens, force sinks (i < A) and the query window (i >= N - n_eff)
+//      (expand_mask, :36-49), apply the optional no-readmission veto (restrict_selection,
+//      propagation.cpp:116-136) and compute retained count and covered mass (:108-120).
+#include <float.h>
+
+#include "params.cuh"
+
+namespace up {
+
+constexpr int kSelThreads = 512;
+
+__device__ __forceinline__ uint32_t phi_encode_dev(float x) {
+    if (x == 0.0f) x = 0.0f;  // -0 -> +0
+    const uint32_t bits = __float_as_uint(x);
+    return x >= 0.0f ? (bits ^ 0x80000000u) : (bits ^ 0xFFFFFFFFu);
+}
+
+__device__ __forceinline__ float phi_decode_dev(uint32_t bits) {
+    return __uint_as_float((bits & 0x80000000u) ? (bits ^ 0x80000000u) : (bits ^ 0xFFFFFFFFu));
+}
+
+__device__ __forceinline__ float key_score(uint64_t w) {
+    return phi_decode_dev(static_cast<uint32_t>(w >> 32));
+}
+
+template <typename T>
+__device__ T block_sum(T v, T* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    T t = 0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < (blockDim.x >> 5) ? scratch[threadIdx.x] : T(0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0) scratch[0] = t;
+    }
+    __syncthreads();
+    t = scratch[0];
+    __syncthreads();
+    return t;
+}
+
+// Exclusive prefix sum of one double per thread across the CTA.
+__device__ double block_exclusive_scan(double v, double* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) scratch[warp] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double w = threadIdx.x < (blockDim.x >> 5) ? scratch[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        scratch[threadIdx.x] = w;  // inclusive warp totals
+    }
+    __syncthreads();
+    const double warp_base = warp > 0 ? scratch[warp - 1] : 0.0;
+    const double r = warp_base + x - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+select_kernel(const SelectParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ double red_d[32];
+    __shared__ int red_i[32];
+    __shared__ int s_kstar;
+    __shared__ double s_ratio[2];
+
+    const int r = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int seg0 = p.cu_seqlens[r];
+    const int N = p.cu_seqlens[r + 1] - seg0;
+    const int G = p.block_size_g;
+    const int nb = (N + G - 1) / G;
+    const int neff = min(p.query_window_n, N);
+    const int64_t A = p.sink_count_a;
+    const bool enabled = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
+
+    auto keep_all = [&](int64_t cutoff, bool degen) {
+        for (int i = tid; i < N; i += blockDim.x) p.keep[seg0 + i] = 1;
+        if (tid == 0) {
+            p.cutoff_rank[r] = cutoff;
+            if (p.retained_count) p.retained_count[r] = N;
+            if (p.covered_mass) p.covered_mass[r] = 1.0;
+            if (p.degenerate) p.degenerate[r] = degen ? 1 : 0;
+        }
+    };
+
+    if (!enabled) { keep_all(-1, false); return; }
+    if (nb > kMaxSortBlocks) {
+        if (tid == 0) raise_error(p.err, kErrTooManyBlocks);
+        keep_all(-1, false);
+        return;
+    }
+    int P2 = 1;
+    while (P2 < nb) P2 <<= 1;
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+    float* sc = reinterpret_cast<float*>(keys + P2);
+    uint8_t* blk = reinterpret_cast<uint8_t*>(sc + nb);
+    const float* bs = p.block_scores + p.cu_blocks[r];
+
+    // 1. validate, pack, total.
+    bool bad = false;
+    double tsum = 0.0;
+    for (int g = tid; g < P2; g += blockDim.x) {
+        if (g < nb) {
+            const float s = bs[g];
+            if (!(s >= 0.0f) || !isfinite(s)) bad = true;
+            sc[g] = s;
+            tsum += s;
+            keys[g] = (static_cast<uint64_t>(phi_encode_dev(s)) << 32) | static_cast<uint64_t>(~static_cast<uint32_t>(g));
+            blk[g] = 0;
+        } else {
+            keys[g] = 0;
+        }
+    }
+    bad = __syncthreads_or(bad);
+    if (bad) {
+        if (tid == 0) raise_error(p.err, kErrBadScore);
+        keep_all(-1, false);
+        return;
+    }
+    const double total = block_sum<double>(tsum, red_d);
+    const bool degenerate = !(total > 0.0);  // all scores are exactly zero
+    int kstar = nb;
+
+    if (!degenerate) {
+        // 2. bitonic sort, descending.
+        for (int kk = 2; kk <= P2; kk <<= 1) {
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                for (int i = tid; i < P2; i += blockDim.x) {
+                    const int ixj = i ^ jj;
+                    if (ixj > i) {
+                        const uint64_t a = keys[i], b = keys[ixj];
+                        const bool desc = (i & kk) == 0;
+                        if (desc ? (a < b) : (a > b)) { keys[i] = b; keys[ixj] = a; }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // 3. parallel prefix over contiguous rank ranges.
+        const int per = (P2 + blockDim.x - 1) / blockDim.x;
+        const int r0 = tid * per;
+        const int r1 = min(r0 + per, nb);
+        double local = 0.0;
+        for (int q = r0; q < r1; ++q) local += static_cast<double>(key_score(keys[q]));
+        const double base = block_exclusive_scan(local, red_d);
+        const double p_d = static_cast<double>(p.top_p);
+        if (tid == 0) s_kstar = nb + 1;  // nb + 1 = never reached
+        __syncthreads();
+        double cum = base;
+        for (int q = r0; q < r1; ++q) {
+            cum += static_cast<double>(key_score(keys[q]));
+            if (cum / total >= p_d) { atomicMin(&s_kstar, q + 1); break; }
+        }
+        __syncthreads();
+        const int kpar = s_kstar;
+        // Guard.  The sequential ratio (the reference's) is monotone in the rank and lies
+        // within delta of the parallel one at every rank (both double sums are within
+        // (nb + per + log2 threads) ulps of the exact sum).  If the parallel ratio clears
+        // p by more than delta at the crossing rank and at the rank before it, the
+        // sequential crossing is the same rank; if the threshold is never reached, the
+        // last rank must stay below p - delta.  Otherwise fall back to the exact replay.
+        const bool reached = kpar <= nb;
+        const int rc = reached ? kpar - 1 : nb - 1;
+        if (tid == 0) { s_ratio[0] = -1.0; s_ratio[1] = -1.0; }
+        __syncthreads();
+        cum = base;
+        for (int q = r0; q < r1; ++q) {
+            cum += static_cast<double>(key_score(keys[q]));
+            if (q == rc) s_ratio[0] = cum / total;
+            if (q == rc - 1) s_ratio[1] = cum / total;
+        }
+        __syncthreads();
+        const double delta = (4.0 * nb + 256.0) * DBL_EPSILON;
+        bool certain = reached ? (s_ratio[0] - p_d > delta) : (p_d - s_ratio[0] > delta);
+        if (reached && rc >= 1) certain = certain && (p_d - s_ratio[1] > delta);
+        if (certain) {
+            kstar = kpar;
+        } else {
+            // Replay the reference's sequential sums exactly (one thread).
+            if (tid == 0) {
+                double tot = 0.0;
+                for (int g = 0; g < nb; ++g) tot += sc[g];
+                double c = 0.0;
+                int k = nb;
+                for (int q = 0; q < nb; ++q) {
+                    c += static_cast<double>(key_score(keys[q]));
+                    if (c / tot >= p_d) { k = q + 1; break; }
+                }
+                s_kstar = k;
+            }
+            __syncthreads();
+            kstar = s_kstar;
+        }
+        // 4. mark the selected blocks.
+        for (int q = tid; q < kstar; q += blockDim.x) {
+            blk[~static_cast<uint32_t>(keys[q] & 0xFFFFFFFFull)] = 1;
+        }
+    } else {
+        for (int g = tid; g < nb; g += blockDim.x) blk[g] = 1;
+    }
+    __syncthreads();
+
+    // 5. expand, force, veto, count.
+    int retained = 0;
+    double covered = 0.0;
+    bool vetoed = false;
+    for (int i = tid; i < N; i += blockDim.x) {
+        const int g = i / G;
+        bool k = blk[g] != 0 || i < A || i >= N - neff;
+        if (k && p.veto != nullptr && p.veto[seg0 + i]) { k = false; vetoed = true; }
+        p.keep[seg0 + i] = k ? 1 : 0;
+        if (k) {
+            ++retained;
+            const int size = min(G, N - g * G);
+            covered += static_cast<double>(sc[g]) / static_cast<double>(size);
+        }
+    }
+    retained = block_sum<int>(retained, red_i);
+    covered = block_sum<double>(covered, red_d);
+    vetoed = __syncthreads_or(vetoed);
+    if (tid == 0) {
+        p.cutoff_rank[r] = kstar;
+        if (p.retained_count) p.retained_count[r] = retained;
+        // Degenerate selections report 1.0 with or without a veto (selection.cpp:104-106,
+        // propagation.cpp:135: restrict_selection also falls back to 1.0 at zero mass).
+        if (p.covered_mass) p.covered_mass[r] = degenerate ? 1.0 : covered / total;
+        if (p.degenerate) p.degenerate[r] = degenerate ? 1 : 0;
+    }
+}
+
+size_t select_smem_bytes(int max_blocks_per_request) {
+    int P2 = 1;
+    while (P2 < max_blocks_per_request) P2 <<= 1;
+    return static_cast<size_t>(P2) * 8 + static_cast<size_t>(max_blocks_per_request) * 5 + 16;
+}
+
+cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request,
+                          cudaStream_t stream) {
+    const int cap = max_blocks_per_request < kMaxSortBlocks ? max_blocks_per_request : kMaxSortBlocks;
+    const size_t smem = select_smem_bytes(cap < 1 ? 1 : cap);
+    cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    select_kernel<<<R, kSelThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
+// allreduce_scores (tp_sim.cpp:43-47): fp32 sum in ascending shard order from 0.0f.
+struct ReduceParams {
+    const float* shards[16];
+    int32_t tp;
+    int64_t count;
+    float* out;
+};
+
+__global__ void reduce_shards_kernel(const ReduceParams p) {
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < p.count;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float acc = 0.0f;
+        for (int t = 0; t < p.tp; ++t) acc = __fadd_rn(acc, p.shards[t][g]);
+        p.out[g] = acc;
+    }
+}
+
+cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t count, float* out,
+                                 int num_sms, cudaStream_t stream) {
+    ReduceParams p{};
+    for (int t = 0; t < tp; ++t) p.shards[t] = shards[t];
+    p.tp = tp;
+    p.count = count;
+    p.out = out;
+    int64_t grid = (count + 255) / 256;
+    if (grid > num_sms * 4) grid = num_sms * 4;
+    if (grid < 1) grid = 1;
+    reduce_shards_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace up

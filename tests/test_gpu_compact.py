@@ -1,0 +1,111 @@
+"""GPU parity: segmented prefix sum + gather compaction (propagation.cpp:47-77,
+scheduler.cpp:50-90), byte-exact against the oracle and the reference's own KATs."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _sel(up, keep):
+    keep = torch.tensor(keep, dtype=torch.uint8, device="cuda")
+    idx = torch.nonzero(keep).flatten()
+    return up.Selection(keep, idx, idx.numel() / keep.numel(), 1.0, idx.numel(), False)
+
+
+def test_apply_drop_keep_all_identity(up):
+    prompt = torch.randn(6, 32, device="cuda")
+    stream = up.TokenStream.from_prompt(prompt)
+    hist = up.DropHistory(original_length=6)
+    up.apply_drop(stream, _sel(up, [1] * 6), 0, hist)
+    assert stream.active_count() == 6
+    assert torch.equal(stream.active_states, prompt)
+    assert not stream.parked_states
+    assert hist.events[0].retained_length == 6
+
+
+def test_apply_drop_compaction_order(up):
+    prompt = torch.randn(8, 32, device="cuda")
+    stream = up.TokenStream.from_prompt(prompt)
+    hist = up.DropHistory(original_length=8)
+    up.apply_drop(stream, _sel(up, [1, 1, 0, 0, 0, 0, 1, 1]), 0, hist)
+    assert stream.logical_positions.tolist() == [0, 1, 6, 7]
+    assert torch.equal(stream.active_states[2], prompt[6])
+    assert stream.parked_positions[0].tolist() == [2, 3, 4, 5]
+    assert torch.equal(stream.parked_states[0][1], prompt[3])
+
+
+def test_stacked_drops_compose(up):
+    prompt = torch.randn(8, 32, device="cuda")
+    stream = up.TokenStream.from_prompt(prompt)
+    hist = up.DropHistory(original_length=8)
+    m1 = [1, 1, 0, 1, 1, 0, 1, 1]
+    up.apply_drop(stream, _sel(up, m1), 0, hist)
+    m2 = [1, 0, 1, 0, 1, 1]
+    up.apply_drop(stream, _sel(up, m2), 4, hist)
+    first = [i for i in range(8) if m1[i]]
+    survivors = [first[i] for i in range(len(first)) if m2[i]]
+    assert stream.logical_positions.tolist() == survivors
+    parked = sorted(int(x) for p in stream.parked_positions for x in p.tolist())
+    assert parked == sorted(set(range(8)) - set(survivors))
+    assert hist.events[1].retained_length == len(survivors)
+
+
+def test_patch_metadata_kats(up):
+    """test_scheduler.cpp:154-203."""
+    toks = torch.randn(16, 8, device="cuda")
+    b = up.PackedBatch(toks.clone(), torch.tensor([0, 8, 16]), ["prefill", "prefill"])
+    up.patch_metadata(b, [None, None], 0)
+    assert b.cu_seqlens.tolist() == [0, 8, 16] and torch.equal(b.tokens, toks)
+
+    b = up.PackedBatch(toks.clone(), torch.tensor([0, 8, 16]), ["prefill", "prefill"])
+    up.patch_metadata(b, [_sel(up, [1, 0, 1, 0, 1, 0, 1, 0]), None], 0)
+    assert b.cu_seqlens.tolist() == [0, 4, 12]
+    assert torch.equal(b.tokens[1], toks[2]) and torch.equal(b.tokens[4], toks[8])
+
+    t9 = torch.randn(9, 8, device="cuda")
+    b = up.PackedBatch(t9, torch.tensor([0, 8, 9]), ["prefill", "decode"])
+    up.patch_metadata(b, [_sel(up, [1, 1, 1, 1, 0, 0, 0, 0]), None], 0)
+    assert b.cu_seqlens.tolist() == [0, 4, 5]
+    with pytest.raises(up.ContractViolation):
+        up.patch_metadata(b, [None, _sel(up, [0])], 1)
+
+
+@pytest.mark.parametrize("lengths,row_bytes", [
+    ([1000, 1, 77, 4096, 3], (8192, 2048, 2048, 8)),
+    ([300], (4096, 512, 4)),
+    ([5, 2049, 513], (16, 24, 6)),   # odd row sizes exercise the narrow copy paths
+])
+def test_compact_matches_oracle(up, port, lengths, row_bytes):
+    rng = np.random.default_rng(len(lengths))
+    T = sum(lengths)
+    cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    keep = (rng.random(T) < 0.3).astype(np.uint8)
+    en = (rng.random(len(lengths)) < 0.8).astype(np.uint8)
+    planes = [rng.integers(0, 255, (T, rb), dtype=np.uint8) for rb in row_bytes]
+    want, cu_want, idx_want = port.compact(keep, cu, planes, selected=en)
+    res = up.compact_varlen(torch.from_numpy(keep).cuda(), torch.from_numpy(cu).cuda(),
+                            [torch.from_numpy(p).cuda() for p in planes],
+                            drop_enabled=torch.from_numpy(en).cuda(), check=True).trimmed()
+    assert res.cu_seqlens.cpu().tolist() == cu_want.tolist()
+    assert np.array_equal(res.retained_index.cpu().numpy(), idx_want)
+    for g, w in zip(res.planes, want):
+        assert np.array_equal(g.cpu().numpy(), w)
+
+
+def test_compact_capacity_larger_than_batch(up, port):
+    """max_tokens capacity > cu[R]: rows past the batch are ignored."""
+    lengths = [500, 700]
+    T = 1200
+    cap = 4000
+    rng = np.random.default_rng(9)
+    keep = np.zeros(cap, np.uint8)
+    keep[:T] = (rng.random(T) < 0.5)
+    hid = torch.randn(cap, 64, device="cuda").to(torch.bfloat16)
+    cu = torch.tensor([0, 500, 1200], dtype=torch.int32, device="cuda")
+    res = up.compact_varlen(torch.from_numpy(keep).cuda(), cu, [hid], max_tokens=cap, check=True)
+    n = int(res.num_out.item())
+    assert n == int(keep[:T].sum())
+    idx = np.flatnonzero(keep[:T])
+    assert torch.equal(res.planes[0][:n], hid[torch.from_numpy(idx).cuda()])
+    assert res.cu_seqlens.cpu().tolist() == [0, int(keep[:500].sum()), n]

@@ -1,0 +1,125 @@
+"""GPU parity: block-wise importance scorer vs the CPU oracle (importance.cpp:17-132).
+
+Tolerance (north star): block scores within rtol 1e-3 of the oracle on identical bf16
+inputs (GPU: bf16 in / fp32 accumulate; oracle: the same values upcast to fp32, double
+accumulation), plus an absolute floor of 1e-6 x the block-score mass for blocks whose
+score underflows fp32 relative to its row maxima.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2605_06221_b200.synthetic import make_batch
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-3
+
+
+def _oracle_blocks(port, sb, r, Hq, Hkv, cfg):
+    cu = sb.cu_seqlens.cpu().numpy()
+    s, e = int(cu[r]), int(cu[r + 1])
+    q = sb.q[s:e].float().reshape(e - s, -1).cpu().numpy()
+    k = sb.k[s:e].float().reshape(e - s, -1).cpu().numpy()
+    tok, blk, _ = port.score_tokens(q, k, Hq, Hkv, **cfg)
+    return tok, blk
+
+
+def _assert_blocks_close(got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    atol = 1e-6 * max(want.sum(), 1e-30) / max(len(want), 1)
+    err = np.abs(got - want)
+    bad = err > RTOL * np.abs(want) + atol
+    assert not bad.any(), (f"{bad.sum()} / {len(want)} blocks off; worst rel "
+                           f"{(err / np.maximum(np.abs(want), 1e-30)).max():.3e}")
+
+
+@pytest.mark.parametrize("Hq,Hkv,D,lengths,n,G", [
+    (8, 2, 128, [1000], 128, 64),          # GQA 4 -> HPC 4 (LLaMA-like)
+    (8, 2, 128, [700, 129, 64, 2000], 128, 64),  # varlen, short segments
+    (4, 1, 128, [300, 1], 128, 64),        # single-token segment
+    (8, 1, 64, [1500], 128, 64),           # D=64, HPC 8
+    (4, 2, 256, [900, 333], 128, 64),      # D=256 (Gemma / Qwen head dim)
+    (4, 4, 128, [777], 128, 64),           # MHA, HPC 1
+    (8, 2, 128, [1024, 513], 64, 32),      # n=64, G=32
+    (8, 2, 128, [2048], 128, 128),         # G=128
+    (8, 2, 128, [1300], 100, 96),          # n < 128, G not a power of two
+])
+def test_tc_scorer_matches_oracle(up, port, Hq, Hkv, D, lengths, n, G):
+    cfg = dict(query_window_n=n, block_size_g=G, sink_count_a=128, top_p=0.99)
+    sb = make_batch(lengths, Hq, Hkv, D, 64, regime="planted", block_size_g=G, seed=sum(lengths) + D)
+    sc = up.ScoreConfig(**cfg)
+    heads = up.HeadLayout(Hq, Hkv, D)
+    import paper_2605_06221_b200._capi as capi
+    import ctypes
+    assert up.lib.up_scorer_kind(ctypes.byref(heads.c(Hq * D, Hkv * D)), ctypes.byref(sc.c()), 0) == 1
+    res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, sc, heads, check=True)
+    cub = res.cu_blocks.cpu().numpy()
+    bs = res.block_scores.cpu().numpy()
+    for r in range(len(lengths)):
+        _, want = _oracle_blocks(port, sb, r, Hq, Hkv, cfg)
+        got = bs[cub[r]:cub[r + 1]]
+        assert len(got) == len(want)
+        _assert_blocks_close(got, want)
+
+
+@pytest.mark.parametrize("Hq,Hkv,D,lengths,n,G", [
+    (8, 8, 8, [40], 16, 8),              # score_default.json fixture shape (n=16, G=8)
+    (4, 2, 32, [300, 17, 5], 8, 4),
+    (2, 1, 64, [130], 200, 10),          # n > N (clamped), odd G
+])
+def test_simt_scorer_matches_oracle_tokens_and_blocks(up, port, Hq, Hkv, D, lengths, n, G):
+    cfg = dict(query_window_n=n, block_size_g=G, sink_count_a=8, top_p=0.9)
+    sb = make_batch(lengths, Hq, Hkv, D, 16, regime="iid", seed=7)
+    res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg),
+                                 up.HeadLayout(Hq, Hkv, D), want_token_scores=True, check=True)
+    cub = res.cu_blocks.cpu().numpy()
+    cu = sb.cu_seqlens.cpu().numpy()
+    for r in range(len(lengths)):
+        tok, blk = _oracle_blocks(port, sb, r, Hq, Hkv, cfg)
+        got_t = res.token_scores[cu[r]:cu[r + 1]].cpu().numpy()
+        np.testing.assert_allclose(got_t, tok, rtol=RTOL, atol=1e-7)
+        _assert_blocks_close(res.block_scores[cub[r]:cub[r + 1]].cpu().numpy(), blk)
+        # mass conservation: token scores of one request sum to #heads (test_importance.cpp:111-126)
+        assert abs(got_t.sum() - Hq) < 1e-3 * Hq
+
+
+def test_tc_and_simt_agree(up):
+    sb = make_batch([1200, 300], 8, 2, 128, 64, regime="planted", seed=3)
+    sc = up.ScoreConfig()
+    h = up.HeadLayout(8, 2, 128)
+    a = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, sc, h, check=True)
+    b = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, sc, h, want_token_scores=True, check=True)
+    nb = int(a.cu_blocks[-1].item())
+    _assert_blocks_close(a.block_scores[:nb].cpu().numpy(), b.block_scores[:nb].cpu().numpy())
+
+
+def test_drop_disabled_segments_are_skipped(up, port):
+    sb = make_batch([500, 1, 800], 8, 2, 128, 64, regime="planted", seed=11)
+    en = torch.tensor([1, 0, 1], dtype=torch.uint8, device="cuda")
+    res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(), up.HeadLayout(8, 2, 128),
+                                 drop_enabled=en, check=True)
+    cub = res.cu_blocks.cpu().numpy()
+    assert list(cub) == [0, 8, 9, 22]
+    assert float(res.block_scores[8].item()) == 0.0
+    for r in (0, 2):
+        _, want = _oracle_blocks(port, sb, r, 8, 2, dict(query_window_n=128, block_size_g=64,
+                                                         sink_count_a=128, top_p=0.99))
+        _assert_blocks_close(res.block_scores[cub[r]:cub[r + 1]].cpu().numpy(), want)
+
+
+def test_score_tokens_mirror_head_ranges_and_tp_sum(up, port):
+    """score_tokens_heads + allreduce over shards == unsharded (test_tp_sim.cpp:45-58)."""
+    N, H, Hkv, D = 600, 8, 2, 128
+    g = torch.Generator().manual_seed(5)
+    q = torch.randn(N, H * D, generator=g).to(torch.bfloat16).cuda()
+    k = torch.randn(N, Hkv * D, generator=g).to(torch.bfloat16).cuda()
+    cfg = up.ScoreConfig(query_window_n=128, block_size_g=64, sink_count_a=16, top_p=0.9)
+    full = up.score_tokens(q, k, H, cfg, num_kv_heads=Hkv, want_token_scores=False)
+    for tp in (1, 2, 4, 8):
+        shards = up.sharded_block_scores(q, k, H, cfg, tp, num_kv_heads=Hkv)
+        red = up.allreduce_scores(shards).cpu().numpy()
+        _assert_blocks_close(red, full.block_scores.cpu().numpy())
+    with pytest.raises(up.ConfigError):
+        up.sharded_block_scores(q, k, H, cfg, 3, num_kv_heads=Hkv)
