@@ -20,26 +20,17 @@ struct CompactParams;
 int tc_max_hpc(int D);
 cudaError_t launch_score_tc(int D, int HPC, const CUtensorMap& qm, const CUtensorMap& km,
                             const ScoreTcParams& p, int grid, cudaStream_t stream);
-cudaError_t launch_score_plan(const int32_t* cu, const uint8_t* en, int R, int64_t max_tokens,
-                              int G, int unit_tiles, int nhg, int target_items, int32_t* cu_blocks,
-                              int32_t* cu_chunks, int32_t* cu_items, int32_t* plan, uint32_t* err,
-                              cudaStream_t stream);
-cudaError_t launch_row_weights(const int32_t* cu, const uint8_t* en, const int32_t* cu_chunks,
-                               const float* stat_m, const float* stat_l, float* stat_w, int R,
-                               int num_heads, int n, int64_t max_chunks, uint32_t* err,
-                               cudaStream_t stream);
-cudaError_t launch_block_combine(const int32_t* cu, const uint8_t* en, const int32_t* cu_blocks,
-                                 const int32_t* cu_chunks, const int32_t* plan, const float* P,
-                                 const float* stat_w, float* block_scores, int R, int G,
-                                 int num_heads, int64_t max_blocks, int64_t max_chunks, int grid,
-                                 cudaStream_t stream);
+cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int G, int32_t* cu_blocks,
+                               uint32_t* err, cudaStream_t stream);
+struct BlockCombineParams;
+cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int num_sms,
                               cudaStream_t stream);
 cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request,
                           cudaStream_t stream);
 cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t count, float* out,
                                  int num_sms, cudaStream_t stream);
-cudaError_t launch_compact(const CompactParams& p, cudaStream_t stream);
+cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream);
 int64_t compact_tiles(int64_t max_tokens);
 int compact_max_planes();
 
@@ -69,9 +60,9 @@ up_status cuda_status(cudaError_t e) { return e == cudaSuccess ? UP_OK : UP_ERR_
 
 // ---- workspace layout --------------------------------------------------------------
 struct Layout {
-    size_t err, plan, cu_chunks, cu_items, P, stat_m, stat_l, stat_w, simt_m, simt_l, simt_tok,
-        tile_counts, total;
-    int64_t max_blocks, max_chunks;
+    size_t err, cu_units, pair_counters, unit_sid, P, stat_m, stat_l, stat_w, simt_m, simt_l,
+        simt_tok, tile_counts, ret_idx, total;
+    int64_t max_blocks, max_units;
     int32_t simt_n;
 };
 
@@ -84,7 +75,8 @@ Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c
     const int64_t G = c->block_size_g > 0 ? c->block_size_g : 1;
     const int64_t H = h ? h->num_q_heads : 0;
     L.max_blocks = T / G + R + 1;
-    L.max_chunks = T / kTileKeys + R + 1;
+    // Σ_r ceil(N_r / unit) * num_hgroups * HPC <= Hq * (T / 128 + R): bounds the item ids.
+    L.max_units = (H > 0 ? H : 1) * (T / kTileKeys + R + 1);
     const int64_t n = c->query_window_n < T ? c->query_window_n : T;
     L.simt_n = static_cast<int32_t>(n > 0 ? n : 1);
     size_t off = 0;
@@ -95,17 +87,18 @@ Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c
         return at;
     };
     L.err = take(256);
-    L.plan = take(64);
-    L.cu_chunks = take(sizeof(int32_t) * (R + 1));
-    L.cu_items = take(sizeof(int32_t) * (R + 1));
+    L.cu_units = take(sizeof(int32_t) * (R + 1));
+    L.pair_counters = take(sizeof(int32_t) * R * (H > 0 ? H : 1));
+    L.unit_sid = take(sizeof(int32_t) * L.max_units);
     L.P = take(sizeof(float) * H * L.max_blocks * kRows);
-    L.stat_m = take(sizeof(float) * H * L.max_chunks * kRows);
-    L.stat_l = take(sizeof(float) * H * L.max_chunks * kRows);
-    L.stat_w = take(sizeof(float) * H * L.max_chunks * kRows);
+    L.stat_m = take(sizeof(float) * L.max_units * kRows);
+    L.stat_l = take(sizeof(float) * L.max_units * kRows);
+    L.stat_w = take(sizeof(float) * L.max_units * kRows);
     L.simt_m = take(sizeof(float) * H * R * L.simt_n);
     L.simt_l = take(sizeof(float) * H * R * L.simt_n);
     L.simt_tok = take(sizeof(float) * (T + 1));
     L.tile_counts = take(sizeof(int32_t) * (compact_tiles(T) + 1));
+    L.ret_idx = take(sizeof(int32_t) * (T + 1));
     L.total = align_up(off, 256);
     return L;
 }
@@ -255,19 +248,11 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
     const int R = b->num_requests;
     const int G = c->block_size_g;
     uint32_t* err = at<uint32_t>(ws, L.err);
-    int32_t* plan = at<int32_t>(ws, L.plan);
-    int32_t* cu_chunks = at<int32_t>(ws, L.cu_chunks);
-    int32_t* cu_items = at<int32_t>(ws, L.cu_items);
 
     if (tc_eligible(h, c, token_scores != nullptr)) {
         const int D = h->head_dim;
         const int hpc = pick_hpc(h);
         const int nhg = h->num_q_heads / hpc;
-        const int unit_tiles = static_cast<int>(lcm64(G, kTileKeys) / kTileKeys);
-        cudaError_t e = launch_score_plan(b->cu_seqlens, b->drop_enabled, R, b->max_tokens, G,
-                                          unit_tiles, nhg, num_sms() * 3, cu_blocks, cu_chunks,
-                                          cu_items, plan, err, stream);
-        if (e != cudaSuccess) return UP_ERR_CUDA;
         CUtensorMap qm, km;
         if (!make_map(&qm, q, b->max_tokens, static_cast<int64_t>(h->num_q_heads) * D, h->q_row_stride) ||
             !make_map(&km, k, b->max_tokens, static_cast<int64_t>(h->num_kv_heads) * D, h->k_row_stride))
@@ -276,38 +261,48 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
         p.cu_seqlens = b->cu_seqlens;
         p.drop_enabled = b->drop_enabled;
         p.cu_blocks = cu_blocks;
-        p.cu_chunks = cu_chunks;
-        p.cu_items = cu_items;
-        p.plan = plan;
+        p.cu_units_out = at<int32_t>(ws, L.cu_units);
+        p.unit_sid = at<int32_t>(ws, L.unit_sid);
+        p.pair_counters = at<int32_t>(ws, L.pair_counters);
+        p.err = err;
         p.P = at<float>(ws, L.P);
         p.stat_m = at<float>(ws, L.stat_m);
         p.stat_l = at<float>(ws, L.stat_l);
+        p.stat_w = at<float>(ws, L.stat_w);
+        p.max_tokens = b->max_tokens;
+        p.max_blocks = L.max_blocks;
         p.num_requests = R;
         p.query_window_n = c->query_window_n;
         p.block_size_g = G;
+        p.unit_keys = static_cast<int32_t>(lcm64(G, kTileKeys));
         p.num_hgroups = nhg;
         p.q_head_offset = h->q_head_offset;
         p.kv_head_offset = h->kv_head_offset;
         p.gqa_group = h->gqa_group;
-        p.max_blocks = L.max_blocks;
-        p.max_chunks = L.max_chunks;
         p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
-        if ((e = launch_score_tc(D, hpc, qm, km, p, num_sms(), stream)) != cudaSuccess) return UP_ERR_CUDA;
-        if ((e = launch_row_weights(b->cu_seqlens, b->drop_enabled, cu_chunks, p.stat_m, p.stat_l,
-                                    at<float>(ws, L.stat_w), R, h->num_q_heads, c->query_window_n,
-                                    L.max_chunks, err, stream)) != cudaSuccess)
-            return UP_ERR_CUDA;
-        if ((e = launch_block_combine(b->cu_seqlens, b->drop_enabled, cu_blocks, cu_chunks, plan, p.P,
-                                      at<float>(ws, L.stat_w), block_scores, R, G, h->num_q_heads,
-                                      L.max_blocks, L.max_chunks, num_sms() * 4, stream)) != cudaSuccess)
-            return UP_ERR_CUDA;
-        g_launches = 4;
+        cudaError_t e = launch_score_tc(D, hpc, qm, km, p, num_sms(), stream);
+        if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
+        BlockCombineParams bp{};
+        bp.cu_seqlens = b->cu_seqlens;
+        bp.cu_blocks = cu_blocks;
+        bp.cu_units = p.cu_units_out;
+        bp.unit_sid = p.unit_sid;
+        bp.P = p.P;
+        bp.stat_w = p.stat_w;
+        bp.block_scores = block_scores;
+        bp.max_blocks = L.max_blocks;
+        bp.num_requests = R;
+        bp.num_heads = h->num_q_heads;
+        bp.hpc = hpc;
+        bp.block_size_g = G;
+        bp.unit_keys = p.unit_keys;
+        if ((e = launch_block_combine(bp, num_sms() * 8, stream)) != cudaSuccess) return UP_ERR_CUDA;
+        g_launches = 2;
         return UP_OK;
     }
 
     // Generic SIMT path.
-    cudaError_t e = launch_score_plan(b->cu_seqlens, b->drop_enabled, R, b->max_tokens, G, 1, 1,
-                                      num_sms() * 3, cu_blocks, cu_chunks, cu_items, plan, err, stream);
+    cudaError_t e = launch_blocks_plan(b->cu_seqlens, R, b->max_tokens, G, cu_blocks, err, stream);
     if (e != cudaSuccess) return UP_ERR_CUDA;
     ScoreSimtParams p{};
     p.cu_seqlens = b->cu_seqlens;
@@ -403,7 +398,7 @@ up_status up_compact(void* stream, const up_batch* b, const uint8_t* keep, const
     p.drop_enabled = b->drop_enabled;
     p.keep = keep;
     p.cu_out = cu_out;
-    p.retained_index = retained_index;
+    p.retained_index = retained_index ? retained_index : at<int32_t>(ws, L.ret_idx);
     p.num_out = num_out;
     p.tile_counts = at<int32_t>(ws, L.tile_counts);
     p.num_requests = b->num_requests;
@@ -419,8 +414,8 @@ up_status up_compact(void* stream, const up_batch* b, const uint8_t* keep, const
         p.dst_stride[i] = pl.dst_stride_bytes > 0 ? pl.dst_stride_bytes : pl.row_bytes;
         if (p.src_stride[i] < pl.row_bytes || p.dst_stride[i] < pl.row_bytes) return UP_ERR_CONTRACT;
     }
-    const cudaError_t e = launch_compact(p, static_cast<cudaStream_t>(stream));
-    g_launches = 2;
+    const cudaError_t e = launch_compact(p, num_sms(), static_cast<cudaStream_t>(stream));
+    g_launches = num_planes > 0 ? 3 : 2;
     return cuda_status(e);
 }
 

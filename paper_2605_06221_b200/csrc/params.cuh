@@ -10,23 +10,42 @@ namespace up {
 struct ScoreTcParams {
     const int32_t* cu_seqlens;
     const uint8_t* drop_enabled;
-    const int32_t* cu_blocks;
-    const int32_t* cu_chunks;
-    const int32_t* cu_items;
-    const int32_t* plan;
-    float* P;
-    float* stat_m;
+    int32_t* cu_blocks;       // out [R+1] (written by CTA 0)
+    int32_t* cu_units_out;    // out [R+1] (written by CTA 0, read by the combine)
+    int32_t* unit_sid;        // out [total units]: item id (stats row) of every unit
+    int32_t* pair_counters;   // [R * num_hgroups], zero between launches (self-cleaning)
+    uint32_t* err;
+    float* P;                 // [Hq][max_blocks][128]
+    float* stat_m;            // [units * HPC][128]
     float* stat_l;
+    float* stat_w;
+    int64_t max_tokens;
+    int64_t max_blocks;
     int32_t num_requests;
     int32_t query_window_n;
     int32_t block_size_g;
+    int32_t unit_keys;        // lcm(G, 128)
     int32_t num_hgroups;
     int32_t q_head_offset;
     int32_t kv_head_offset;
     int32_t gqa_group;
+    float scale_log2;         // log2(e) / sqrt(D)
+};
+
+struct BlockCombineParams {
+    const int32_t* cu_seqlens;
+    const int32_t* cu_blocks;
+    const int32_t* cu_units;
+    const int32_t* unit_sid;
+    const float* P;
+    const float* stat_w;
+    float* block_scores;
     int64_t max_blocks;
-    int64_t max_chunks;
-    float scale_log2;  // log2(e) / sqrt(D)
+    int32_t num_requests;
+    int32_t num_heads;
+    int32_t hpc;
+    int32_t block_size_g;
+    int32_t unit_keys;
 };
 
 struct ScoreSimtParams {

@@ -9,84 +9,74 @@
 //
 // in one pass over K (no second QK^T for normalisation):
 //
-//  * score_tc_kernel (persistent, warp-specialised).  A work item is (request, key chunk,
-//    group of HPC q-heads sharing one kv-head).  Warp 0 streams K tiles with TMA into a
-//    2-stage SWIZZLE_128B ring (Q tiles of the HPC heads stay resident); warp 1 issues
-//    tcgen05.mma (M=128 query rows x N=128 keys x K=D, bf16 -> fp32 in TMEM, one region of
-//    128 TMEM columns per (tile, head), 4 regions); warps 2..9 (two warpgroups, thread =
-//    query row) drain TMEM and compute e = 2^(s*log2e/sqrt(D) - m) against a per-(row,
-//    chunk) reference m that is only moved when a value would exceed it by 2^20 (rare;
-//    the already-written partials of the chunk are rescaled then).  Per (row, block) the
-//    partial Σ e goes to P, per (row, chunk) (m, l = Σ e) to the stats.
-//  * row_weights_kernel: per (request, head, row) the global max M and denominator
-//    L = Σ_c l_c 2^(m_c - M) over chunks -> weight w_c = 2^(m_c - M) / (L n_eff).
-//  * block_combine_kernel: b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[h][c(g)][j] (warp per block).
+//  * score_tc_kernel -- persistent, one CTA per SM, warp-specialised.
+//    Work decomposition: the key range of every (request, head-group) pair is cut into
+//    units of lcm(G,128) keys; the flattened sequence of (request, head-group, unit) is
+//    split into gridDim.x contiguous, equal ranges (exact load balance for any mix of
+//    lengths), so a CTA reloads Q only when its range crosses into the next pair.  The
+//    plan is computed in every CTA's prologue from the device-resident cu_seqlens (no
+//    host round trip); CTA 0 publishes cu_blocks.
+//    Warp 0 streams K tiles with TMA into a 2-stage SWIZZLE_128B ring while the Q tiles of
+//    the HPC heads of one kv-head stay resident; warp 1 issues tcgen05.mma (M=128 query
+//    rows x N=128 keys x K=D, bf16 -> fp32 in TMEM, 4 regions of 128 columns); warps 2..9
+//    (two warpgroups, thread = query row, alternating heads) drain TMEM and compute
+//    e = 2^(s*log2e/sqrt(D) - m) against a per-(row, item) reference m that moves only
+//    when a value would exceed it by ~2^20 (rare; the item's already-written partials are
+//    rescaled then).  Per (row, block) Σ e goes to P, per (row, item) (m, l = Σ e) to the
+//    stats.  The last CTA to finish an item of a (request, head-group) pair (atomic
+//    counter) turns that pair's stats into per-item row weights
+//    w = 2^(m - M) / (L n_eff), M = max_items m, L = Σ_items l 2^(m - M).
+//  * block_combine_kernel -- b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][j].
 #include "params.cuh"
 
 namespace up {
 
-struct ItemInfo {
-    int r, c, hg;
-    int seg0, N, neff, key0, klen, ntiles;
+// ---------------------------------------------------------------- partition
+struct Part {
+    const int32_t* cu_units;  // smem [R+1]
+    int R;
+    int nhg;
+    int64_t U;
+    int grid;
 };
 
-__device__ __forceinline__ ItemInfo decode_item(const ScoreTcParams& p, int item, int chunk_keys) {
-    ItemInfo it;
-    it.r = find_segment(p.cu_items, p.num_requests, item);
-    const int local = item - p.cu_items[it.r];
-    it.c = local / p.num_hgroups;
-    it.hg = local - it.c * p.num_hgroups;
-    it.seg0 = p.cu_seqlens[it.r];
-    it.N = p.cu_seqlens[it.r + 1] - it.seg0;
-    it.neff = min(p.query_window_n, it.N);
-    it.key0 = it.c * chunk_keys;
-    it.klen = min(chunk_keys, it.N - it.key0);
-    it.ntiles = (it.klen + kTileKeys - 1) / kTileKeys;
-    return it;
+struct Item {
+    int r, hg;
+    int u0, u1;        // unit range inside the pair
+    int64_t sid;       // global unit position of the item start (stats id)
+    int64_t seg_start; // global unit position of the pair's unit 0
+    int units_r;
+};
+
+__device__ __forceinline__ int64_t range_begin(const Part& P, int c) {
+    return static_cast<int64_t>(c) * P.U / P.grid;
 }
 
-// Device-side work plan (no host knowledge of segment lengths needed): validates
-// cu_seqlens, writes cu_blocks, picks the key-chunk length and enumerates work items.
-__global__ void score_plan_kernel(const int32_t* __restrict__ cu, const uint8_t* __restrict__ en,
-                                  int R, int64_t max_tokens, int G, int unit_tiles, int nhg,
-                                  int target_items, int32_t* __restrict__ cu_blocks,
-                                  int32_t* __restrict__ cu_chunks, int32_t* __restrict__ cu_items,
-                                  int32_t* __restrict__ plan, uint32_t* __restrict__ err) {
-    if (threadIdx.x != 0) return;
-    bool ok = cu[0] == 0;
-    int64_t tiles = 0;
-    for (int r = 0; r < R && ok; ++r) {
-        const int64_t n = static_cast<int64_t>(cu[r + 1]) - cu[r];
-        if (n <= 0) ok = false;
-        if (en == nullptr || en[r]) tiles += (n + kTileKeys - 1) / kTileKeys;
+// CTA whose range holds global unit position pos: largest c with c*U/grid <= pos.
+__device__ __forceinline__ int cta_of(const Part& P, int64_t pos) {
+    return static_cast<int>(((pos + 1) * P.grid - 1) / P.U);
+}
+
+__device__ __forceinline__ Item make_item(const Part& P, int64_t pos, int64_t end) {
+    Item it;
+    // request: largest r with cu_units[r]*nhg <= pos (pairs with zero units are skipped)
+    int lo = 0, hi = P.R - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (static_cast<int64_t>(P.cu_units[mid]) * P.nhg <= pos) lo = mid; else hi = mid - 1;
     }
-    if (ok && cu[R] > max_tokens) ok = false;
-    if (!ok) {
-        raise_error(err, kErrBadSeqlens);
-        for (int r = 0; r <= R; ++r) { cu_blocks[r] = 0; cu_chunks[r] = 0; cu_items[r] = 0; }
-        plan[0] = unit_tiles * kTileKeys;
-        plan[1] = 0;
-        return;
-    }
-    int64_t chunk_tiles = (tiles * nhg + target_items - 1) / target_items;
-    if (chunk_tiles < 1) chunk_tiles = 1;
-    if (chunk_tiles > 64) chunk_tiles = 64;
-    chunk_tiles = (chunk_tiles + unit_tiles - 1) / unit_tiles * unit_tiles;
-    const int chunk_keys = static_cast<int>(chunk_tiles) * kTileKeys;
-    int32_t b = 0, c = 0, it = 0;
-    for (int r = 0; r < R; ++r) {
-        cu_blocks[r] = b; cu_chunks[r] = c; cu_items[r] = it;
-        const int n = cu[r + 1] - cu[r];
-        b += (n + G - 1) / G;
-        if (en == nullptr || en[r]) {
-            const int nc = (n + chunk_keys - 1) / chunk_keys;
-            c += nc;
-            it += nc * nhg;
-        }
-    }
-    cu_blocks[R] = b; cu_chunks[R] = c; cu_items[R] = it;
-    plan[0] = chunk_keys;
-    plan[1] = it;
+    it.r = lo;
+    it.units_r = P.cu_units[lo + 1] - P.cu_units[lo];
+    const int64_t base = static_cast<int64_t>(P.cu_units[lo]) * P.nhg;
+    const int64_t rel = pos - base;
+    it.hg = static_cast<int>(rel / it.units_r);
+    it.u0 = static_cast<int>(rel - static_cast<int64_t>(it.hg) * it.units_r);
+    it.seg_start = base + static_cast<int64_t>(it.hg) * it.units_r;
+    const int64_t seg_end = it.seg_start + it.units_r;
+    const int64_t stop = end < seg_end ? end : seg_end;
+    it.u1 = it.u0 + static_cast<int>(stop - pos);
+    it.sid = pos;
+    return it;
 }
 
 template <int D, int HPC>
@@ -99,9 +89,12 @@ struct TcCfg {
     static constexpr int NREG = 4;                    // TMEM regions of 128 columns
     static constexpr int NSLOT = HPC >= 2 ? HPC / 2 : 1;
     static constexpr int NBAR = 2 + 2 * KST + 2 * NREG;
-    static constexpr int SMEM = Q_BYTES + KST * K_STAGE + NBAR * 8 + 16 + 1024;
+    static constexpr int FIXED = Q_BYTES + KST * K_STAGE + NBAR * 8 + 64 + 1024;
     static constexpr int THREADS = 320;
+    static int smem(int R) { return FIXED + 5 * NSLOT * 256 * 4 + 2 * (R + 1) * 4; }
 };
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 template <int D, int HPC>
 __global__ void __launch_bounds__(320, 1)
@@ -120,11 +113,18 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
     uint64_t* k_empty = bars + 2 + C::KST;
     uint64_t* t_full = bars + 2 + 2 * C::KST;
     uint64_t* t_empty = bars + 2 + 2 * C::KST + C::NREG;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(bars + C::NBAR);  // [0] tmem base, [1] flag, [2] last
+    float* s_state = reinterpret_cast<float*>(misc + 16);  // [5][NSLOT][256] epilogue state
+    int32_t* s_cu_units = reinterpret_cast<int32_t*>(s_state + 5 * C::NSLOT * 256);
+    int32_t* s_cu_blocks = s_cu_units + (p.num_requests + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const int R = p.num_requests;
+    const int G = p.block_size_g;
+    const int unit_keys = p.unit_keys;
 
+    // ---- prologue: plan from cu_seqlens (warp 2), barriers (warp 0), TMEM (warp 1) ----
     if (warp == 0 && lane == 0) {
         mbar_init(q_full, 1);
         mbar_init(q_empty, 1);
@@ -134,14 +134,65 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
         prefetch_tensormap(&qmap);
         prefetch_tensormap(&kmap);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (warp == 1) tmem_alloc(misc, 512);
+    if (warp == 2) {
+        // Warp-parallel inclusive scans of per-request unit and block counts; validation
+        // of cu_seqlens (PackedBatch::validate, scheduler.cpp:33-48).
+        bool ok = p.cu_seqlens[0] == 0;
+        int carry_u = 0, carry_b = 0;
+        for (int base = 0; base < R; base += 32) {
+            const int r = base + lane;
+            int units = 0, blocks = 0;
+            if (r < R) {
+                const int n = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+                if (n <= 0) ok = false;
+                blocks = n > 0 ? (n + G - 1) / G : 0;
+                const bool en = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
+                units = en && n > 0 ? (n + unit_keys - 1) / unit_keys : 0;
+            }
+            int x = units, y = blocks;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int a = __shfl_up_sync(0xffffffffu, x, o);
+                const int b = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) { x += a; y += b; }
+            }
+            if (r < R) {
+                s_cu_units[r + 1] = carry_u + x;
+                s_cu_blocks[r + 1] = carry_b + y;
+            }
+            carry_u += __shfl_sync(0xffffffffu, x, 31);
+            carry_b += __shfl_sync(0xffffffffu, y, 31);
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (lane == 0) {
+            s_cu_units[0] = 0;
+            s_cu_blocks[0] = 0;
+            if (ok && p.cu_seqlens[R] > p.max_tokens) ok = false;
+            misc[1] = ok ? 1u : 0u;
+            if (!ok && blockIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
+        }
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = misc[0];
+    if (blockIdx.x == 0) {
+        // Publish the segment block offsets for the combine / select / compact kernels.
+        for (int r = threadIdx.x; r <= R; r += blockDim.x) {
+            p.cu_blocks[r] = misc[1] ? s_cu_blocks[r] : 0;
+            p.cu_units_out[r] = misc[1] ? s_cu_units[r] : 0;
+        }
+    }
 
-    const int chunk_keys = p.plan[0];
-    const int total_items = p.plan[1];
+    Part P;
+    P.cu_units = s_cu_units;
+    P.R = R;
+    P.nhg = p.num_hgroups;
+    P.U = misc[1] ? static_cast<int64_t>(s_cu_units[R]) * p.num_hgroups : 0;
+    P.grid = gridDim.x;
+    const int64_t my_begin = P.U > 0 ? range_begin(P, blockIdx.x) : 0;
+    const int64_t my_end = P.U > 0 ? range_begin(P, blockIdx.x + 1) : 0;
 
     if (warp == 0) {
         // ===== TMA producer =====
@@ -149,31 +200,35 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
             int stage = 0;
             uint32_t phase = 0;
             uint32_t qiter = 0;
-            for (int item = blockIdx.x; item < total_items; item += gridDim.x) {
-                const ItemInfo it = decode_item(p, item, chunk_keys);
-                const int kv_local =
-                    (p.q_head_offset + it.hg * HPC) / p.gqa_group - p.kv_head_offset;
+            for (int64_t pos = my_begin; pos < my_end;) {
+                const Item it = make_item(P, pos, my_end);
+                pos += it.u1 - it.u0;
+                const int seg0 = p.cu_seqlens[it.r];
+                const int N = p.cu_seqlens[it.r + 1] - seg0;
+                const int neff = min(p.query_window_n, N);
+                const int key0 = it.u0 * unit_keys;
+                const int key1 = min(it.u1 * unit_keys, N);
+                const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
+                const int kv_local = (p.q_head_offset + it.hg * HPC) / p.gqa_group - p.kv_head_offset;
                 mbar_wait(q_empty, (qiter & 1) ^ 1);
                 ++qiter;
                 mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-                const int qrow = it.seg0 + it.N - it.neff;
+                const int qrow = seg0 + N - neff;
 #pragma unroll
                 for (int hh = 0; hh < HPC; ++hh) {
 #pragma unroll
-                    for (int kc = 0; kc < C::KC; ++kc) {
+                    for (int kc = 0; kc < C::KC; ++kc)
                         tma_load_2d(sq + (hh * C::KC + kc) * C::SUB, &qmap, q_full,
                                     (it.hg * HPC + hh) * D + kc * 64, qrow);
-                    }
                 }
-                for (int t = 0; t < it.ntiles; ++t) {
+                for (int t = 0; t < ntiles; ++t) {
                     mbar_wait(&k_empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&k_full[stage], C::K_STAGE);
-                    const int krow = it.seg0 + it.key0 + t * kTileKeys;
+                    const int krow = seg0 + key0 + t * kTileKeys;
 #pragma unroll
-                    for (int kc = 0; kc < C::KC; ++kc) {
+                    for (int kc = 0; kc < C::KC; ++kc)
                         tma_load_2d(sk + stage * C::K_STAGE + kc * C::SUB, &kmap, &k_full[stage],
                                     kv_local * D + kc * 64, krow);
-                    }
                     if (++stage == C::KST) { stage = 0; phase ^= 1; }
                 }
             }
@@ -188,12 +243,17 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
             uint32_t seq = 0;
             const uint32_t sq_addr = smem_u32(sq);
             const uint32_t sk_addr = smem_u32(sk);
-            for (int item = blockIdx.x; item < total_items; item += gridDim.x) {
-                const ItemInfo it = decode_item(p, item, chunk_keys);
+            for (int64_t pos = my_begin; pos < my_end;) {
+                const Item it = make_item(P, pos, my_end);
+                pos += it.u1 - it.u0;
+                const int N = p.cu_seqlens[it.r + 1] - p.cu_seqlens[it.r];
+                const int key0 = it.u0 * unit_keys;
+                const int key1 = min(it.u1 * unit_keys, N);
+                const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
                 mbar_wait(q_full, qiter & 1);
                 ++qiter;
                 tc_fence_after();
-                for (int t = 0; t < it.ntiles; ++t) {
+                for (int t = 0; t < ntiles; ++t) {
                     mbar_wait(&k_full[stage], phase);
                     tc_fence_after();
 #pragma unroll
@@ -220,118 +280,186 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
         }
     } else {
         // ===== epilogue: two warpgroups, thread = query row =====
+        const int etid = threadIdx.x - 64;   // 0..255
         const int wg = (warp - 2) >> 2;
-        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int quarter = warp & 3;        // TMEM lane quarter this warp may access
         const int j = quarter * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const float sc = p.scale_log2;
-        const int G = p.block_size_g;
-        uint32_t seq = 0;
-        for (int item = blockIdx.x; item < total_items; item += gridDim.x) {
-            const ItemInfo it = decode_item(p, item, chunk_keys);
-            const bool row_valid = j < it.neff;
-            const int qpos = it.N - it.neff + j;  // last key this row may see (segment-relative)
-            const int gc = p.cu_chunks[it.r] + it.c;
-            const int64_t gb_seg = p.cu_blocks[it.r];  // global index of the segment's block 0
-            const int blk_chunk0 = it.key0 / G;
-            float m[C::NSLOT], l[C::NSLOT], bsum[C::NSLOT];
-#pragma unroll
-            for (int s = 0; s < C::NSLOT; ++s) { m[s] = -INFINITY; l[s] = 0.f; bsum[s] = 0.f; }
+        const int gpb = G / 32;              // 32-column groups per block
+        // Per-(head slot, thread) running state lives in shared memory so that one copy of
+        // the region body serves every head (keeps the hot loop small for the I-cache).
+        float* st_m = s_state;
+        float* st_l = st_m + C::NSLOT * 256;
+        float* st_b = st_l + C::NSLOT * 256;
+        int* st_gib = reinterpret_cast<int*>(st_b + C::NSLOT * 256);
+        int* st_blk = st_gib + C::NSLOT * 256;
+        const int hh_first = HPC >= 2 ? wg : 0;
+        const int hh_step = HPC >= 2 ? 2 : 1;
+        const bool active = HPC >= 2 || wg == 0;
+        uint32_t seq_base = 0;
+        for (int64_t pos = my_begin; pos < my_end;) {
+            const Item it = make_item(P, pos, my_end);
+            pos += it.u1 - it.u0;
+            const int seg0 = p.cu_seqlens[it.r];
+            const int N = p.cu_seqlens[it.r + 1] - seg0;
+            const int neff = min(p.query_window_n, N);
+            const int key0 = it.u0 * unit_keys;
+            const int key1 = min(it.u1 * unit_keys, N);
+            const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
+            const bool row_valid = j < neff;
+            const int qpos = N - neff + j;   // last key this row may see (segment-relative)
+            const int64_t gb_seg = s_cu_blocks[it.r];  // global block index of block 0
+            const int blk0 = key0 / G;
+            for (int s = 0; s < C::NSLOT; ++s) {
+                st_m[s * 256 + etid] = -INFINITY;
+                st_l[s * 256 + etid] = 0.f;
+                st_b[s * 256 + etid] = 0.f;
+                st_gib[s * 256 + etid] = 0;
+                st_blk[s * 256 + etid] = blk0;
+            }
 
-            for (int t = 0; t < it.ntiles; ++t) {
-                const int colbase = it.key0 + t * kTileKeys;
-                const bool tail = colbase + kTileKeys - 1 > it.N - it.neff;  // warp-uniform
-#pragma unroll
-                for (int hh = 0; hh < HPC; ++hh) {
-                    const bool mine = HPC == 1 ? (wg == 0) : ((hh & 1) == wg);
-                    if (mine) {
-                        const int slot = HPC >= 2 ? hh / 2 : 0;
-                        const int h_local = it.hg * HPC + hh;
-                        const uint32_t reg = seq % C::NREG;
-                        mbar_wait(&t_full[reg], (seq / C::NREG) & 1);
-                        tc_fence_after();
-                        float* Prow = p.P + (static_cast<int64_t>(h_local) * p.max_blocks + gb_seg) * kRows + j;
+            for (int t = 0; t < ntiles && active; ++t) {
+                const int colbase = key0 + t * kTileKeys;
+                const bool tail = colbase + kTileKeys - 1 > N - neff;  // warp-uniform
 #pragma unroll 1
-                        for (int q4 = 0; q4 < kTileKeys / 32; ++q4) {
-                            const int c0 = colbase + q4 * 32;
-                            if (c0 >= it.N) break;  // warp-uniform
-                            uint32_t v[32];
-                            tmem_ld32(tmem_base + lane_base + reg * kTileKeys + q4 * 32, v);
-                            tmem_ld_wait();
-                            const float mneg = -m[slot];
-                            float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-                            if (!tail) {
+                for (int hh = hh_first; hh < HPC; hh += hh_step) {
+                    const int si = (HPC >= 2 ? hh >> 1 : 0) * 256 + etid;
+                    const uint32_t sq_ = seq_base + t * HPC + hh;
+                    const uint32_t reg = sq_ % C::NREG;
+                    float* Prow = p.P + (static_cast<int64_t>(it.hg * HPC + hh) * p.max_blocks + gb_seg) * kRows + j;
+                    float m = st_m[si], l = st_l[si], bsum = st_b[si];
+                    int gib = st_gib[si], blk = st_blk[si];
+                    mbar_wait(&t_full[reg], (sq_ / C::NREG) & 1);
+                    tc_fence_after();
+                    const uint32_t taddr = tmem_base + lane_base + reg * kTileKeys;
+#pragma unroll 1
+                    for (int q4 = 0; q4 < kTileKeys / 32; ++q4) {
+                        const int c0 = colbase + q4 * 32;
+                        uint32_t v[32];
+                        tmem_ld32(taddr + q4 * 32, v);
+                        tmem_ld_wait();
+                        if (q4 == kTileKeys / 32 - 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&t_empty[reg]);
+                        }
+                        if (c0 >= N) continue;  // warp-uniform
+                        const float mneg = -m;
+                        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                        if (!tail) {
 #pragma unroll
-                                for (int k = 0; k < 32; k += 4) {
-                                    acc0 += ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, mneg));
-                                    acc1 += ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, mneg));
-                                    acc2 += ex2_approx(fmaf(__uint_as_float(v[k + 2]), sc, mneg));
-                                    acc3 += ex2_approx(fmaf(__uint_as_float(v[k + 3]), sc, mneg));
-                                }
-                            } else {
-#pragma unroll
-                                for (int k = 0; k < 32; k += 4) {
-                                    const float e0 = ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, mneg));
-                                    const float e1 = ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, mneg));
-                                    const float e2 = ex2_approx(fmaf(__uint_as_float(v[k + 2]), sc, mneg));
-                                    const float e3 = ex2_approx(fmaf(__uint_as_float(v[k + 3]), sc, mneg));
-                                    acc0 += (c0 + k + 0 <= qpos) ? e0 : 0.f;
-                                    acc1 += (c0 + k + 1 <= qpos) ? e1 : 0.f;
-                                    acc2 += (c0 + k + 2 <= qpos) ? e2 : 0.f;
-                                    acc3 += (c0 + k + 3 <= qpos) ? e3 : 0.f;
-                                }
+                            for (int k = 0; k < 32; k += 4) {
+                                a0 += ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, mneg));
+                                a1 += ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, mneg));
+                                a2 += ex2_approx(fmaf(__uint_as_float(v[k + 2]), sc, mneg));
+                                a3 += ex2_approx(fmaf(__uint_as_float(v[k + 3]), sc, mneg));
                             }
-                            float gs = (acc0 + acc1) + (acc2 + acc3);
-                            if (!(gs <= 0x1p20f)) {
-                                // Rebase: the reference for this (row, chunk) moves to the max seen.
-                                float gmax = -INFINITY;
+                        } else {
+                            const int lim = qpos - c0;  // column k valid iff k <= lim
 #pragma unroll
-                                for (int k = 0; k < 32; ++k) {
-                                    const bool valid = !tail || (c0 + k <= qpos);
-                                    if (valid) gmax = fmaxf(gmax, __uint_as_float(v[k]) * sc);
-                                }
-                                const float mold = m[slot];
-                                const float mnew = fmaxf(mold, gmax);
-                                if (mold != -INFINITY) {
-                                    const float f = ex2_approx(mold - mnew);
-                                    l[slot] *= f;
-                                    bsum[slot] *= f;
-                                    const int cur_blk = c0 / G;
-                                    for (int g = blk_chunk0; g < cur_blk; ++g) Prow[static_cast<int64_t>(g) * kRows] *= f;
-                                }
-                                m[slot] = mnew;
-                                gs = 0.f;
-#pragma unroll
-                                for (int k = 0; k < 32; ++k) {
-                                    const bool valid = !tail || (c0 + k <= qpos);
-                                    const float e = ex2_approx(fmaf(__uint_as_float(v[k]), sc, -mnew));
-                                    gs += valid ? e : 0.f;
-                                }
-                            }
-                            bsum[slot] += gs;
-                            if (((c0 + 32) % G) == 0 || c0 + 32 >= it.N) {
-                                Prow[static_cast<int64_t>(c0 / G) * kRows] = row_valid ? bsum[slot] : 0.f;
-                                l[slot] += bsum[slot];
-                                bsum[slot] = 0.f;
+                            for (int k = 0; k < 32; k += 4) {
+                                const float e0 = ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, mneg));
+                                const float e1 = ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, mneg));
+                                const float e2 = ex2_approx(fmaf(__uint_as_float(v[k + 2]), sc, mneg));
+                                const float e3 = ex2_approx(fmaf(__uint_as_float(v[k + 3]), sc, mneg));
+                                a0 += (k + 0 <= lim) ? e0 : 0.f;
+                                a1 += (k + 1 <= lim) ? e1 : 0.f;
+                                a2 += (k + 2 <= lim) ? e2 : 0.f;
+                                a3 += (k + 3 <= lim) ? e3 : 0.f;
                             }
                         }
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&t_empty[reg]);
+                        float gs = (a0 + a1) + (a2 + a3);
+                        if (!(gs <= 0x1p20f)) {
+                            // Rebase this (row, item) reference onto the max seen (rare).
+                            const int lim = tail ? qpos - c0 : 31;
+                            float gmax = -INFINITY;
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                if (k <= lim) gmax = fmaxf(gmax, __uint_as_float(v[k]) * sc);
+                            const float mnew = fmaxf(m, gmax);
+                            if (m != -INFINITY) {
+                                const float f = ex2_approx(m - mnew);
+                                l *= f;
+                                bsum *= f;
+                                for (int g = blk0; g < blk; ++g) Prow[static_cast<int64_t>(g) * kRows] *= f;
+                            }
+                            m = mnew;
+                            gs = 0.f;
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) {
+                                const float e = ex2_approx(fmaf(__uint_as_float(v[k]), sc, -mnew));
+                                gs += (k <= lim) ? e : 0.f;
+                            }
+                        }
+                        bsum += gs;
+                        if (++gib == gpb || c0 + 32 >= N) {
+                            Prow[static_cast<int64_t>(blk) * kRows] = row_valid ? bsum : 0.f;
+                            l += bsum;
+                            bsum = 0.f;
+                            gib = 0;
+                            ++blk;
+                        }
                     }
-                    ++seq;
+                    st_m[si] = m; st_l[si] = l; st_b[si] = bsum; st_gib[si] = gib; st_blk[si] = blk;
                 }
             }
-            // Chunk statistics for the owned heads.
-#pragma unroll
-            for (int hh = 0; hh < HPC; ++hh) {
-                const bool mine = HPC == 1 ? (wg == 0) : ((hh & 1) == wg);
-                if (mine) {
-                    const int slot = HPC >= 2 ? hh / 2 : 0;
-                    const int h_local = it.hg * HPC + hh;
-                    const int64_t si = (static_cast<int64_t>(h_local) * p.max_chunks + gc) * kRows + j;
-                    p.stat_m[si] = row_valid ? m[slot] : -INFINITY;
-                    p.stat_l[si] = row_valid ? l[slot] : 0.f;
+            seq_base += ntiles * HPC;
+            // Item statistics for the owned heads: stats[sid][hh][row].
+            if (active) {
+                for (int hh = hh_first; hh < HPC; hh += hh_step) {
+                    const int si = (HPC >= 2 ? hh >> 1 : 0) * 256 + etid;
+                    const int64_t x = (it.sid * HPC + hh) * kRows + j;
+                    p.stat_m[x] = row_valid ? st_m[si] : -INFINITY;
+                    p.stat_l[x] = row_valid ? st_l[si] : 0.f;
+                }
+            }
+            for (int u = it.u0 + etid; u < it.u1; u += 256) p.unit_sid[it.seg_start + u] = static_cast<int32_t>(it.sid);
+
+            // The last CTA to finish an item of this (request, head-group) pair turns the
+            // pair's item statistics into row weights.
+            const int64_t seg_end = it.seg_start + it.units_r;
+            epi_bar();
+            if (etid == 0) {
+                int expected = 0;
+                for (int64_t s = it.seg_start; s < seg_end; ++expected) {
+                    const int64_t e = range_begin(P, cta_of(P, s) + 1);
+                    s = e < seg_end ? e : seg_end;
+                }
+                int32_t* ctr = p.pair_counters + it.r * P.nhg + it.hg;
+                __threadfence();
+                const int old = atomicAdd(ctr, 1);
+                const bool is_last = old == expected - 1;
+                if (is_last) *ctr = 0;  // self-cleaning for the next launch
+                misc[2] = is_last ? 1u : 0u;
+            }
+            epi_bar();
+            if (misc[2]) {
+                __threadfence();
+                for (int x = etid; x < HPC * kRows; x += 256) {
+                    const int hh = x / kRows, jj = x - (x / kRows) * kRows;
+                    const bool valid = jj < neff;
+                    float M = -INFINITY;
+                    for (int64_t s = it.seg_start; s < seg_end;) {
+                        M = fmaxf(M, __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]));
+                        const int64_t e = range_begin(P, cta_of(P, s) + 1);
+                        s = e < seg_end ? e : seg_end;
+                    }
+                    float L = 0.f;
+                    for (int64_t s = it.seg_start; s < seg_end;) {
+                        const float mc = __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]);
+                        if (mc != -INFINITY) L += __ldcg(&p.stat_l[(s * HPC + hh) * kRows + jj]) * ex2_approx(mc - M);
+                        const int64_t e = range_begin(P, cta_of(P, s) + 1);
+                        s = e < seg_end ? e : seg_end;
+                    }
+                    if (valid && !(L > 0.f)) raise_error(p.err, kErrMaskedRow);
+                    const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
+                    for (int64_t s = it.seg_start; s < seg_end;) {
+                        const float mc = __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]);
+                        p.stat_w[(s * HPC + hh) * kRows + jj] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
+                        const int64_t e = range_begin(P, cta_of(P, s) + 1);
+                        s = e < seg_end ? e : seg_end;
+                    }
                 }
             }
         }
@@ -345,68 +473,73 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
     }
 }
 
-// Per (request, head, row): combine chunk statistics into per-chunk weights.
-__global__ void row_weights_kernel(const int32_t* __restrict__ cu, const uint8_t* __restrict__ en,
-                                   const int32_t* __restrict__ cu_chunks,
-                                   const float* __restrict__ stat_m, const float* __restrict__ stat_l,
-                                   float* __restrict__ stat_w, int n, int64_t max_chunks,
-                                   uint32_t* __restrict__ err) {
-    const int r = blockIdx.x;
-    const int h = blockIdx.y;
-    const int j = threadIdx.x;
-    if (en != nullptr && !en[r]) return;
-    const int N = cu[r + 1] - cu[r];
-    const int neff = min(n, N);
-    const int c0 = cu_chunks[r], c1 = cu_chunks[r + 1];
-    const int64_t base = static_cast<int64_t>(h) * max_chunks * kRows + j;
-    float M = -INFINITY;
-    for (int c = c0; c < c1; ++c) M = fmaxf(M, stat_m[base + static_cast<int64_t>(c) * kRows]);
-    float L = 0.f;
-    for (int c = c0; c < c1; ++c) {
-        const float mc = stat_m[base + static_cast<int64_t>(c) * kRows];
-        if (mc != -INFINITY) L += stat_l[base + static_cast<int64_t>(c) * kRows] * ex2_approx(mc - M);
-    }
-    const bool valid = j < neff;
-    if (valid && !(L > 0.f)) raise_error(err, kErrMaskedRow);
-    const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
-    for (int c = c0; c < c1; ++c) {
-        const float mc = stat_m[base + static_cast<int64_t>(c) * kRows];
-        stat_w[base + static_cast<int64_t>(c) * kRows] = (mc != -INFINITY) ? ex2_approx(mc - M) * inv : 0.f;
+// Warp per block: b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][hh][j].
+__global__ void __launch_bounds__(256)
+block_combine_kernel(const BlockCombineParams p) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int R = p.num_requests;
+    const int total = p.cu_blocks[R];
+    const int nhg = p.num_heads / p.hpc;
+    for (int gb = blockIdx.x * (blockDim.x >> 5) + warp; gb < total; gb += gridDim.x * (blockDim.x >> 5)) {
+        const int r = find_segment(p.cu_blocks, R, gb);
+        const int units_r = p.cu_units[r + 1] - p.cu_units[r];
+        if (units_r == 0) {  // pass-through segment
+            if (lane == 0) p.block_scores[gb] = 0.f;
+            continue;
+        }
+        const int g = gb - p.cu_blocks[r];
+        const int N = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+        const int size = min(p.block_size_g, N - g * p.block_size_g);
+        const int u = (g * p.block_size_g) / p.unit_keys;
+        const int64_t pair0 = static_cast<int64_t>(p.cu_units[r]) * nhg;
+        float acc0 = 0.f, acc1 = 0.f;
+        for (int hg = 0; hg < nhg; ++hg) {
+            const int64_t sid = p.unit_sid[pair0 + static_cast<int64_t>(hg) * units_r + u];
+#pragma unroll 4
+            for (int hh = 0; hh < p.hpc; ++hh) {
+                const int h = hg * p.hpc + hh;
+                const float4 pv = __ldcs(reinterpret_cast<const float4*>(
+                    p.P + (static_cast<int64_t>(h) * p.max_blocks + gb) * kRows) + lane);
+                const float4 wv = __ldg(reinterpret_cast<const float4*>(
+                    p.stat_w + (sid * p.hpc + hh) * kRows) + lane);
+                acc0 = fmaf(pv.x, wv.x, fmaf(pv.y, wv.y, acc0));
+                acc1 = fmaf(pv.z, wv.z, fmaf(pv.w, wv.w, acc1));
+            }
+        }
+        float acc = acc0 + acc1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) p.block_scores[gb] = acc / static_cast<float>(size);
     }
 }
 
-// Warp per block: b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[h][c(g)][j].
-__global__ void block_combine_kernel(const int32_t* __restrict__ cu, const uint8_t* __restrict__ en,
-                                     const int32_t* __restrict__ cu_blocks,
-                                     const int32_t* __restrict__ cu_chunks,
-                                     const int32_t* __restrict__ plan, const float* __restrict__ P,
-                                     const float* __restrict__ stat_w, float* __restrict__ block_scores,
-                                     int R, int G, int num_heads, int64_t max_blocks,
-                                     int64_t max_chunks) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int total = cu_blocks[R];
-    const int chunk_keys = plan[0];
-    for (int gb = blockIdx.x * (blockDim.x >> 5) + warp; gb < total; gb += gridDim.x * (blockDim.x >> 5)) {
-        const int r = find_segment(cu_blocks, R, gb);
-        if (en != nullptr && !en[r]) {
-            if (lane == 0) block_scores[gb] = 0.f;
-            continue;
+// SIMT-path plan: validates cu_seqlens and writes cu_blocks (one warp).
+__global__ void blocks_plan_kernel(const int32_t* __restrict__ cu, int R, int64_t max_tokens, int G,
+                                   int32_t* __restrict__ cu_blocks, uint32_t* __restrict__ err) {
+    const int lane = threadIdx.x;
+    bool ok = cu[0] == 0;
+    int carry = 0;
+    for (int base = 0; base < R; base += 32) {
+        const int r = base + lane;
+        int blocks = 0;
+        if (r < R) {
+            const int n = cu[r + 1] - cu[r];
+            if (n <= 0) ok = false;
+            blocks = (n + G - 1) / G;
         }
-        const int g = gb - cu_blocks[r];
-        const int N = cu[r + 1] - cu[r];
-        const int gc = cu_chunks[r] + (g * G) / chunk_keys;
-        const int size = min(G, N - g * G);
-        float acc = 0.f;
-        for (int h = 0; h < num_heads; ++h) {
-            const float4 pv = *reinterpret_cast<const float4*>(
-                P + (static_cast<int64_t>(h) * max_blocks + gb) * kRows + lane * 4);
-            const float4 wv = *reinterpret_cast<const float4*>(
-                stat_w + (static_cast<int64_t>(h) * max_chunks + gc) * kRows + lane * 4);
-            acc += pv.x * wv.x + pv.y * wv.y + pv.z * wv.z + pv.w * wv.w;
-        }
+        int y = blocks;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) block_scores[gb] = acc / static_cast<float>(size);
+        for (int o = 1; o < 32; o <<= 1) {
+            const int b = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += b;
+        }
+        if (r < R) cu_blocks[r + 1] = carry + y;
+        carry += __shfl_sync(0xffffffffu, y, 31);
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (lane == 0) {
+        cu_blocks[0] = 0;
+        if (!ok || cu[R] > max_tokens) raise_error(err, kErrBadSeqlens);
     }
 }
 
@@ -415,10 +548,12 @@ template <int D, int HPC>
 static cudaError_t launch_tc(const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p,
                              int grid, cudaStream_t stream) {
     using C = TcCfg<D, HPC>;
+    const int smem = C::smem(p.num_requests);
+    if (smem > 232448) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<D, HPC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    score_tc_kernel<D, HPC><<<grid, C::THREADS, C::SMEM, stream>>>(qm, km, p);
+    score_tc_kernel<D, HPC><<<grid, C::THREADS, smem, stream>>>(qm, km, p);
     return cudaGetLastError();
 }
 
@@ -435,32 +570,14 @@ cudaError_t launch_score_tc(int D, int HPC, const CUtensorMap& qm, const CUtenso
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_score_plan(const int32_t* cu, const uint8_t* en, int R, int64_t max_tokens,
-                              int G, int unit_tiles, int nhg, int target_items, int32_t* cu_blocks,
-                              int32_t* cu_chunks, int32_t* cu_items, int32_t* plan, uint32_t* err,
-                              cudaStream_t stream) {
-    score_plan_kernel<<<1, 32, 0, stream>>>(cu, en, R, max_tokens, G, unit_tiles, nhg, target_items,
-                                            cu_blocks, cu_chunks, cu_items, plan, err);
+cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int G, int32_t* cu_blocks,
+                               uint32_t* err, cudaStream_t stream) {
+    blocks_plan_kernel<<<1, 32, 0, stream>>>(cu, R, max_tokens, G, cu_blocks, err);
     return cudaGetLastError();
 }
 
-cudaError_t launch_row_weights(const int32_t* cu, const uint8_t* en, const int32_t* cu_chunks,
-                               const float* stat_m, const float* stat_l, float* stat_w, int R,
-                               int num_heads, int n, int64_t max_chunks, uint32_t* err,
-                               cudaStream_t stream) {
-    row_weights_kernel<<<dim3(R, num_heads), kRows, 0, stream>>>(cu, en, cu_chunks, stat_m, stat_l,
-                                                                 stat_w, n, max_chunks, err);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_block_combine(const int32_t* cu, const uint8_t* en, const int32_t* cu_blocks,
-                                 const int32_t* cu_chunks, const int32_t* plan, const float* P,
-                                 const float* stat_w, float* block_scores, int R, int G,
-                                 int num_heads, int64_t max_blocks, int64_t max_chunks, int grid,
-                                 cudaStream_t stream) {
-    block_combine_kernel<<<grid, 256, 0, stream>>>(cu, en, cu_blocks, cu_chunks, plan, P, stat_w,
-                                                   block_scores, R, G, num_heads, max_blocks,
-                                                   max_chunks);
+cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream) {
+    block_combine_kernel<<<grid, 256, 0, stream>>>(p);
     return cudaGetLastError();
 }
 

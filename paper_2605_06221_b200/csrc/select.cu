@@ -230,24 +230,34 @@ select_kernel(const SelectParams p) {
     }
     __syncthreads();
 
-    // 5. expand, force, veto, count.
+    // 5. expand, force, veto, count: warp per block, lanes over its tokens (coalesced bytes).
     int retained = 0;
     double covered = 0.0;
-    bool vetoed = false;
-    for (int i = tid; i < N; i += blockDim.x) {
-        const int g = i / G;
-        bool k = blk[g] != 0 || i < A || i >= N - neff;
-        if (k && p.veto != nullptr && p.veto[seg0 + i]) { k = false; vetoed = true; }
-        p.keep[seg0 + i] = k ? 1 : 0;
-        if (k) {
-            ++retained;
-            const int size = min(G, N - g * G);
-            covered += static_cast<double>(sc[g]) / static_cast<double>(size);
+    {
+        const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+        for (int g = warp; g < nb; g += nwarps) {
+            const int b0 = g * G;
+            const int size = min(G, N - b0);
+            const bool bk = blk[g] != 0;
+            int kept = 0;
+            for (int x = lane; x < size; x += 32) {
+                const int i = b0 + x;
+                bool k = bk || i < A || i >= N - neff;
+                if (k && p.veto != nullptr && p.veto[seg0 + i]) k = false;
+                p.keep[seg0 + i] = k ? 1 : 0;
+                kept += k ? 1 : 0;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+            if (lane == 0) {
+                retained += kept;
+                // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g|.
+                covered += static_cast<double>(sc[g]) * (static_cast<double>(kept) / static_cast<double>(size));
+            }
         }
     }
     retained = block_sum<int>(retained, red_i);
     covered = block_sum<double>(covered, red_d);
-    vetoed = __syncthreads_or(vetoed);
     if (tid == 0) {
         p.cutoff_rank[r] = kstar;
         if (p.retained_count) p.retained_count[r] = retained;
