@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -57,6 +58,16 @@ int num_sms() {
 }
 
 up_status cuda_status(cudaError_t e) { return e == cudaSuccess ? UP_OK : UP_ERR_CUDA; }
+
+// Per-CTA timing of the tensor-core scorer (diagnostics only, enabled by UP_SCORE_DEBUG).
+unsigned long long* score_debug_buffer() {
+    static unsigned long long* d = [] {
+        unsigned long long* x = nullptr;
+        if (std::getenv("UP_SCORE_DEBUG")) cudaMalloc(&x, sizeof(unsigned long long) * 4 * 4096);
+        return x;
+    }();
+    return d;
+}
 
 // ---- workspace layout --------------------------------------------------------------
 struct Layout {
@@ -280,7 +291,13 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
         p.kv_head_offset = h->kv_head_offset;
         p.gqa_group = h->gqa_group;
         p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
-        cudaError_t e = launch_score_tc(D, hpc, qm, km, p, num_sms(), stream);
+        static const int grid_override = [] {
+            const char* s = std::getenv("UP_SCORE_GRID");
+            return s ? std::atoi(s) : 0;
+        }();
+        const int grid = grid_override > 0 ? grid_override : num_sms();
+        p.dbg = score_debug_buffer();
+        cudaError_t e = launch_score_tc(D, hpc, qm, km, p, grid, stream);
         if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
         BlockCombineParams bp{};
         bp.cu_seqlens = b->cu_seqlens;
@@ -453,3 +470,13 @@ up_status up_device_status(void* stream, void* ws) {
 }
 
 }  // extern "C"
+
+// Diagnostics (not part of the ABI header): copy the scorer's per-CTA timing records
+// [cta][start_ns, end_ns, units, smid] of the last launch to host memory.
+extern "C" int up_internal_score_debug(unsigned long long* host, int max_ctas) {
+    unsigned long long* d = score_debug_buffer();
+    if (d == nullptr || host == nullptr) return -1;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+    return cudaMemcpy(host, d, sizeof(unsigned long long) * 4 * max_ctas, cudaMemcpyDeviceToHost) ==
+                   cudaSuccess ? 0 : -3;
+}

@@ -30,6 +30,7 @@ struct ScoreTcParams {
     int32_t kv_head_offset;
     int32_t gqa_group;
     float scale_log2;         // log2(e) / sqrt(D)
+    unsigned long long* dbg;  // optional per-CTA timing [grid][4] (UP_SCORE_DEBUG), else null
 };
 
 struct BlockCombineParams {

@@ -230,10 +230,55 @@ select_kernel(const SelectParams p) {
     }
     __syncthreads();
 
-    // 5. expand, force, veto, count: warp per block, lanes over its tokens (coalesced bytes).
+    // 5. expand, force, veto, count.
     int retained = 0;
     double covered = 0.0;
-    {
+    const int64_t win0 = N - neff;  // first query-window row
+    if (p.veto == nullptr) {
+        // Kept tokens per block follow from the block decision and the forced ranges
+        // [0, A) and [N - n_eff, N) analytically: one thread per block.
+        for (int g = tid; g < nb; g += blockDim.x) {
+            const int64_t b0 = static_cast<int64_t>(g) * G;
+            const int size = min(G, N - g * G);
+            int kept = size;
+            if (!blk[g]) {
+                const int64_t b1 = b0 + size;
+                const int64_t sink_end = b1 < A ? b1 : A;
+                const int64_t win_beg = b0 > win0 ? b0 : win0;
+                const int64_t sink = sink_end > b0 ? sink_end - b0 : 0;
+                const int64_t win = b1 > win_beg ? b1 - win_beg : 0;
+                const int64_t both = sink_end > win_beg ? sink_end - win_beg : 0;
+                kept = static_cast<int>(sink + win - both);
+            }
+            retained += kept;
+            // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g|.
+            covered += static_cast<double>(sc[g]) * (static_cast<double>(kept) / static_cast<double>(size));
+        }
+        // Token bytes, 16 per thread per store where the destination is 16-byte aligned.
+        uint8_t* kp = p.keep + seg0;
+        const int head = min(N, static_cast<int>((16 - (reinterpret_cast<uintptr_t>(kp) & 15)) & 15));
+        auto kbyte = [&](int i) -> uint32_t {
+            return (blk[i / G] != 0 || i < A || i >= win0) ? 1u : 0u;
+        };
+        for (int i = tid; i < head; i += blockDim.x) kp[i] = static_cast<uint8_t>(kbyte(i));
+        const int nchunk = (N - head) >> 4;
+        for (int c = tid; c < nchunk; c += blockDim.x) {
+            const int i0 = head + c * 16;
+            int g = i0 / G;            // one division per 16 tokens; then walk block edges
+            int edge = (g + 1) * G;
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+                const int i = i0 + x;
+                while (i >= edge) { ++g; edge += G; }
+                const uint32_t kb = (blk[g] != 0 || i < A || i >= win0) ? 1u : 0u;
+                w[x >> 2] |= kb << (8 * (x & 3));
+            }
+            *reinterpret_cast<uint4*>(kp + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        for (int i = head + nchunk * 16 + tid; i < N; i += blockDim.x) kp[i] = static_cast<uint8_t>(kbyte(i));
+    } else {
+        // With a veto: warp per block, lanes over its tokens (coalesced bytes).
         const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
         for (int g = warp; g < nb; g += nwarps) {
             const int b0 = g * G;

@@ -1,0 +1,207 @@
+"""CPU: pin the oracle (the C restatement in oracle/uniprefill_oracle.c).
+
+1. The reference's own known-answer tests (test_selection.cpp, test_importance.cpp,
+   test_tp_sim.cpp, test_propagation.cpp, test_scheduler.cpp), restated against the port.
+2. Every golden vector in tests/golden/golden.json (generated from the unmodified
+   reference by tests/golden/make_golden.py) reproduced bit for bit.
+3. When oracle/_ref (the reference compiled from its sources) is present: the port and the
+   reference agree bit for bit on fresh random inputs.
+"""
+import json
+import math
+import os
+import struct
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden.json")
+
+
+def unhex(xs):
+    return np.array([struct.unpack("<f", bytes.fromhex(x))[0] for x in xs], np.float32)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+def cfg(n=1, g=1, a=0, p=0.9):
+    return dict(query_window_n=n, block_size_g=g, sink_count_a=a, top_p=p)
+
+
+# ----------------------------------------------------------------------- KATs
+def test_phi_fixed_points(port):
+    """test_selection.cpp:71-78."""
+    assert port.phi_encode(0.0) == 0x80000000
+    assert port.phi_encode(-0.0) == 0x80000000
+    assert port.phi_encode(1.0) == 0xBF800000
+    assert port.phi_encode(-1.0) == 0x407FFFFF
+    for bad in (math.nan, math.inf, -math.inf):
+        with pytest.raises(oracle.OracleContractViolation):
+            port.phi_encode(bad)
+
+
+def test_phi_monotone_and_inverse(port):
+    """test_selection.cpp:80-121 (sampled)."""
+    rng = np.random.default_rng(13)
+    bits = rng.integers(0, 2 ** 32, 3000, dtype=np.uint64).astype(np.uint32)
+    xs = bits.view(np.float32)
+    xs = xs[np.isfinite(xs)][:1500]
+    xs = np.concatenate([xs, np.array([0.0, -0.0, 1.4e-45, -1.4e-45, 1.2e-38, 3.4e38, -3.4e38], np.float32)])
+    enc = np.array([port.phi_encode(float(x)) for x in xs], np.uint64)
+    order_x = np.argsort(xs, kind="stable")
+    assert np.all(np.diff(enc[order_x].astype(np.int64)) >= 0)
+    for x, e in zip(xs[:300], enc[:300]):
+        back = port.phi_decode(int(e))
+        assert back == x or (x == 0 and back == 0)
+
+
+def test_top_p_worked_example(port):
+    sel = port.top_p_select([0.5, 0.3, 0.15, 0.05], 4, **cfg(p=0.9))
+    assert sel.cutoff_rank == 3 and sel.keep_mask.tolist() == [1, 1, 1, 1]
+
+
+def test_top_p_edge_cases(port):
+    assert port.top_p_select([0.9, 0.05, 0.04, 0.01], 4, **cfg(p=1.0)).cutoff_rank == 4
+    sel = port.top_p_select([0.1] * 10, 10, **cfg(p=0.99))
+    assert sel.cutoff_rank == 10 and sel.retained_count == 10
+    sel = port.top_p_select([0.0] * 5, 5, **cfg(p=0.5))
+    assert sel.degenerate_keep_all and sel.covered_mass == 1.0 and sel.retained_count == 5
+    for bad in ([0.5, -0.1], [0.5, math.nan]):
+        with pytest.raises(oracle.OracleContractViolation):
+            port.top_p_select(bad, 2, **cfg(p=0.9))
+    for badcfg in (cfg(p=0.0), cfg(p=1.5), cfg(n=0), cfg(g=0), cfg(a=-1)):
+        with pytest.raises(oracle.OracleConfigError):
+            port.top_p_select([1.0], 1, **badcfg)
+
+
+def test_expand_mask_kats(port):
+    """test_selection.cpp:178-182."""
+    assert port.expand_mask([1, 0, 1], 2, 6, 0, 0).tolist() == [1, 1, 0, 0, 1, 1]
+    assert port.expand_mask([0, 0, 0], 2, 6, 1, 1).tolist() == [1, 0, 0, 0, 0, 1]
+    assert port.expand_mask([0, 1, 0], 2, 5, 0, 0).tolist() == [0, 0, 1, 1, 0]
+
+
+def test_block_reduce_and_scorer_kats(port):
+    """test_importance.cpp:99-109, 151-159 through score_tokens."""
+    # singleton: one key, one query -> token score 1 per head
+    tok, blk, n = port.score_tokens(np.ones((1, 4), np.float32), np.ones((1, 4), np.float32), 1, **cfg(n=1, g=1))
+    assert tok.tolist() == [1.0] and n == 1
+    # zero queries: the last row sees 4 keys uniformly
+    tok, blk, _ = port.score_tokens(np.zeros((4, 4), np.float32), np.ones((4, 4), np.float32), 1, **cfg(n=1, g=2))
+    assert tok.tolist() == [0.25] * 4 and blk.tolist() == [0.25, 0.25]
+
+
+def test_allreduce_kats(port):
+    """test_tp_sim.cpp:71-94."""
+    assert port.allreduce_scores([[1, 2], [3, 4]], [0, 1]).tolist() == [4.0, 6.0]
+    assert port.allreduce_scores([[3, 4], [1, 2]], [1, 0]).tolist() == [4.0, 6.0]
+    for shards, ids in (([[1.0], [2.0]], [0, 0]), ([[1.0], [2.0]], [0, 2])):
+        with pytest.raises(oracle.OracleContractViolation):
+            port.allreduce_scores(shards, ids)
+
+
+def test_compaction_kats(port):
+    """test_propagation.cpp:97-111 and test_scheduler.cpp:154-203."""
+    rows = np.arange(8 * 4, dtype=np.float32).reshape(8, 4)
+    (out,), cu, idx = port.compact(np.array([1, 1, 0, 0, 0, 0, 1, 1], np.uint8), [0, 8], [rows])
+    assert idx.tolist() == [0, 1, 6, 7] and np.array_equal(out[2], rows[6]) and cu.tolist() == [0, 4]
+    toks = np.arange(16 * 2, dtype=np.float32).reshape(16, 2)
+    (out,), cu, _ = port.compact(np.array([1, 0] * 4 + [1] * 8, np.uint8), [0, 8, 16], [toks], selected=[1, 0])
+    assert cu.tolist() == [0, 4, 12] and np.array_equal(out[1], toks[2]) and np.array_equal(out[4], toks[8])
+
+
+# ----------------------------------------------------------------------- golden vectors
+def test_golden_phi(port, golden):
+    for x, e in golden["phi"].items():
+        assert port.phi_encode(float(x)) == e
+
+
+def test_golden_selection(port, golden):
+    for case in golden["selection"]:
+        s = unhex(case["scores"])
+        sel = port.top_p_select(s, case["num_tokens"], **case["cfg"])
+        assert sel.retained_indices.tolist() == case["retained"], case["kind"]
+        assert sel.cutoff_rank == case["cutoff_rank"]
+        assert sel.covered_mass == float.fromhex(case["covered_mass"])
+        assert sel.degenerate_keep_all == case["degenerate"]
+
+
+def _rng_matrix(port, rows, cols, seed, stream, stddev):
+    return port.rng_normal_array(seed, stream, rows * cols, stddev).reshape(rows, cols)
+
+
+def test_golden_scorer(port, golden):
+    for case in golden["scorer"]:
+        N, H, Hkv, D = case["N"], case["H"], case["Hkv"], case["D"]
+        q = _rng_matrix(port, N, H * D, case["seed"], 0x696D70, case["stddev"])
+        k = _rng_matrix(port, N, Hkv * D, case["seed"], 0x696D71, case["stddev"])
+        tok, blk, n_eff = port.score_tokens(q, k, H, Hkv, **case["cfg"])
+        assert np.array_equal(tok, unhex(case["token_scores"]))
+        assert np.array_equal(blk, unhex(case["block_scores"]))
+        assert n_eff == case["effective_n"]
+        sel = port.top_p_select(blk, N, **case["cfg"])
+        assert sel.retained_indices.tolist() == case["retained"]
+
+
+def test_golden_tp(port, golden):
+    for case in golden["tp"]:
+        q = _rng_matrix(port, case["N"], 64, case["seed_q"], 0x7470, case["stddev"])
+        k = _rng_matrix(port, case["N"], 64, case["seed_k"], 0x7470, case["stddev"])
+        for tp, want in case["tp"].items():
+            tp = int(tp)
+            hps = 8 // tp
+            shards = [port.score_tokens_heads(q, k, 8, 8, t * hps, (t + 1) * hps, want_tokens=False, **case["cfg"])[1]
+                      for t in range(tp)]
+            for s, w in zip(shards, want["shards"]):
+                assert np.array_equal(s, unhex(w))
+            red = port.allreduce_scores(shards, list(range(tp)))
+            assert np.array_equal(red, unhex(want["reduced"]))
+
+
+def test_golden_compact(port, golden):
+    for case in golden["compact"]:
+        if case["name"] == "apply_drop_order":
+            st = unhex(case["states"]).reshape(case["rows"], case["cols"])
+            (out,), cu, idx = port.compact(np.array(case["keep"], np.uint8), [0, case["rows"]], [st])
+            assert np.array_equal(out, unhex(case["out"]).reshape(-1, case["cols"]))
+            assert idx.tolist() == case["positions"]
+            continue
+        toks = unhex(case["tokens"]).reshape(-1, case["cols"])
+        (out,), cu, _ = port.compact(np.array(case["keep"], np.uint8), case["cu"], [toks],
+                                     selected=case["selected"])
+        assert cu.tolist() == case["cu_out"]
+        assert np.array_equal(out, unhex(case["out"]).reshape(-1, case["cols"]))
+
+
+# ----------------------------------------------------------------------- port == reference
+def test_port_matches_reference_random(port, ref):
+    rng = np.random.default_rng(0)
+    for N, H, Hkv, D, c in [(300, 8, 2, 16, cfg(16, 8, 8, 0.9)), (129, 4, 4, 8, cfg(128, 64, 16, 0.99)),
+                            (1000, 4, 1, 32, cfg(128, 64, 128, 0.95))]:
+        q = rng.standard_normal((N, H * D)).astype(np.float32)
+        k = rng.standard_normal((N, Hkv * D)).astype(np.float32)
+        a = port.score_tokens(q, k, H, Hkv, **c)
+        b = ref.score_tokens(q, k, H, Hkv, **c)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        sa, sb = port.top_p_select(a[1], N, **c), ref.top_p_select(b[1], N, **c)
+        assert np.array_equal(sa.keep_mask, sb.keep_mask) and sa.cutoff_rank == sb.cutoff_rank
+        assert sa.covered_mass == sb.covered_mass
+
+
+def test_port_matches_reference_compaction(port, ref):
+    rng = np.random.default_rng(1)
+    lengths = [37, 1, 300, 64]
+    cu = np.concatenate([[0], np.cumsum(lengths)])
+    T = int(cu[-1])
+    toks = rng.standard_normal((T, 16)).astype(np.float32)
+    keep = (rng.random(T) < 0.4).astype(np.uint8)
+    sel = np.array([1, 0, 1, 1], np.uint8)
+    want, cu_want = ref.patch_metadata(toks, cu, keep, sel)
+    (got,), cu_got, _ = port.compact(keep, cu, [toks], selected=sel)
+    assert np.array_equal(got, want) and cu_got.tolist() == cu_want.tolist()
