@@ -1,0 +1,166 @@
+// uniprefill_b200.hpp -- C++ host mirror of the reference operator API over the C ABI.
+//
+// The reference ships its hot path as the C++ namespace `uniprefill`
+// (/root/reference/proj/core/include/uniprefill/*.hpp) over host matrices, throwing
+// ConfigError / ContractViolation (errors.hpp:13-42).  This header keeps those names,
+// argument meanings and error behaviour for device-resident varlen batches:
+//
+//   uniprefill::b200::ScoreConfig          <- ScoreConfig            (config.hpp:53-63)
+//   uniprefill::b200::score_blocks         <- score_tokens[_heads]   (importance.hpp:42-47)
+//   uniprefill::b200::reduce_block_scores  <- allreduce_scores       (tp_sim.hpp:31)
+//   uniprefill::b200::top_p_select         <- top_p_select           (selection.hpp:53-54)
+//   uniprefill::b200::compact              <- apply_drop / patch_metadata
+//                                             (propagation.hpp:415, scheduler.hpp:52-53)
+//   uniprefill::b200::DropLayer            <- prefill_layer_step's drop section
+//                                             (propagation.cpp:163-202)
+//
+// All work is enqueued on the given stream; nothing synchronizes except check_device().
+// Header-only; link libuniprefill_b200.so and cudart.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "uniprefill_b200.h"
+
+namespace uniprefill::b200 {
+
+class ConfigError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class ContractViolation : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class UnsupportedError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class CudaError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(up_status s, const char* what) {
+    if (s == UP_OK) return;
+    const std::string msg = std::string(what) + ": " + up_status_string(s);
+    switch (s) {
+    case UP_ERR_CONFIG: throw ConfigError(msg);
+    case UP_ERR_CONTRACT: throw ContractViolation(msg);
+    case UP_ERR_UNSUPPORTED: throw UnsupportedError(msg);
+    case UP_ERR_CUDA: throw CudaError(msg);
+    default: throw std::runtime_error(msg);
+    }
+}
+
+struct ScoreConfig {
+    int query_window_n = 128;
+    int block_size_g = 64;
+    int sink_count_a = 128;
+    float top_p = 0.99f;
+
+    up_score_config c() const { return {query_window_n, block_size_g, sink_count_a, top_p}; }
+    /// ScoreConfig::validate (config.cpp:98-103): throws ConfigError.
+    void validate() const {
+        const up_score_config x = c();
+        check(up_config_validate(&x), "ScoreConfig::validate");
+    }
+};
+
+/// Device-resident varlen batch (PackedBatch, scheduler.hpp:33-46).
+struct VarlenBatch {
+    int32_t num_requests = 0;
+    int64_t max_tokens = 0;
+    const int32_t* cu_seqlens = nullptr;    // device int32[R+1]
+    const uint8_t* drop_enabled = nullptr;  // device uint8[R] or null
+    up_batch c() const { return {num_requests, max_tokens, cu_seqlens, drop_enabled}; }
+};
+
+struct HeadLayout {
+    int num_q_heads = 0, num_kv_heads = 0, head_dim = 0;
+    int gqa_group = 1, q_head_offset = 0, kv_head_offset = 0;
+    int64_t q_row_stride = 0, k_row_stride = 0;
+    up_heads c() const {
+        return {num_q_heads, num_kv_heads, head_dim, gqa_group, q_head_offset, kv_head_offset,
+                q_row_stride ? q_row_stride : int64_t(num_q_heads) * head_dim,
+                k_row_stride ? k_row_stride : int64_t(num_kv_heads) * head_dim};
+    }
+};
+
+/// Device scratch shared by every entry point (zeroed once).
+class Workspace {
+public:
+    Workspace() = default;
+    Workspace(const VarlenBatch& b, const HeadLayout& h, const ScoreConfig& cfg) { reserve(b, h, cfg); }
+    ~Workspace() { if (ptr_) cudaFree(ptr_); }
+    Workspace(const Workspace&) = delete;
+    Workspace& operator=(const Workspace&) = delete;
+
+    void reserve(const VarlenBatch& b, const HeadLayout& h, const ScoreConfig& cfg) {
+        const up_batch bc = b.c();
+        const up_heads hc = h.c();
+        const up_score_config cc = cfg.c();
+        const size_t need = up_workspace_bytes(&bc, &hc, &cc);
+        if (need <= bytes_) return;
+        if (ptr_) cudaFree(ptr_);
+        if (cudaMalloc(&ptr_, need) != cudaSuccess || cudaMemset(ptr_, 0, need) != cudaSuccess)
+            throw CudaError("Workspace: cudaMalloc failed");
+        bytes_ = need;
+    }
+    void* data() const { return ptr_; }
+    size_t bytes() const { return bytes_; }
+
+private:
+    void* ptr_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+/// Block scores of every drop-enabled segment (importance.cpp:92-132 per segment).
+inline void score_blocks(cudaStream_t s, const VarlenBatch& b, const HeadLayout& h, const ScoreConfig& cfg,
+                         const void* q_bf16, const void* k_bf16, float* block_scores, int32_t* cu_blocks,
+                         Workspace& ws, float* token_scores = nullptr) {
+    const up_batch bc = b.c();
+    const up_heads hc = h.c();
+    const up_score_config cc = cfg.c();
+    check(up_score_blocks(s, &bc, &hc, &cc, q_bf16, k_bf16, block_scores, cu_blocks, token_scores, ws.data(),
+                          ws.bytes()),
+          "score_blocks");
+}
+
+/// allreduce_scores (tp_sim.cpp:29-49) over device-addressable shard partials.
+inline void reduce_block_scores(cudaStream_t s, const std::vector<const float*>& shards, int64_t count,
+                                float* out) {
+    if (shards.empty()) throw ContractViolation("allreduce_scores: no shards");
+    check(up_reduce_block_scores(s, shards.data(), static_cast<int32_t>(shards.size()), count, out),
+          "reduce_block_scores");
+}
+
+/// top_p_select + expand_mask (+ veto) for every drop-enabled segment.
+inline void top_p_select(cudaStream_t s, const VarlenBatch& b, const ScoreConfig& cfg, const float* block_scores,
+                         const int32_t* cu_blocks, uint8_t* keep, const up_selection_out& out, Workspace& ws,
+                         const uint8_t* veto = nullptr) {
+    const up_batch bc = b.c();
+    const up_score_config cc = cfg.c();
+    check(up_select(s, &bc, &cc, block_scores, cu_blocks, veto, keep, &out, ws.data(), ws.bytes()),
+          "top_p_select");
+}
+
+/// apply_drop / patch_metadata: compacts every plane, rebuilds cu_seqlens.
+inline void compact(cudaStream_t s, const VarlenBatch& b, const uint8_t* keep, const std::vector<up_plane>& planes,
+                    int32_t* cu_seqlens_out, int32_t* retained_index, int32_t* num_tokens_out, Workspace& ws) {
+    const up_batch bc = b.c();
+    check(up_compact(s, &bc, keep, planes.data(), static_cast<int32_t>(planes.size()), cu_seqlens_out,
+                     retained_index, num_tokens_out, ws.data(), ws.bytes()),
+          "compact");
+}
+
+/// Synchronizes and raises the sticky device-side ContractViolation (NaN / negative block
+/// scores, malformed cu_seqlens) like the reference's exceptions.
+inline void check_device(cudaStream_t s, Workspace& ws) { check(up_device_status(s, ws.data()), "device"); }
+
+}  // namespace uniprefill::b200

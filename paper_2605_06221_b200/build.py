@@ -29,9 +29,10 @@ def nvcc() -> str:
 
 
 def _flags():
+    extra = os.environ.get("UP_NVCC_FLAGS", "").split()  # e.g. -DUP_POLY_PAIRS=4 for tuning sweeps
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                    "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-                   "-Xptxas", "-v" if os.environ.get("UP_PTXAS_VERBOSE") else "-O3"]
+                   "-Xptxas", "-v" if os.environ.get("UP_PTXAS_VERBOSE") else "-O3"] + extra
 
 
 def _stale(target: str, deps) -> bool:

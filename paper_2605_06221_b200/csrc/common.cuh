@@ -191,6 +191,44 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// ---- packed fp32 pairs (FFMA2 / FADD2 on sm_100a) ---------------------------------
+__device__ __forceinline__ uint64_t pk(float lo, float hi) {
+    return static_cast<uint64_t>(__float_as_uint(lo)) | (static_cast<uint64_t>(__float_as_uint(hi)) << 32);
+}
+__device__ __forceinline__ float lo_f(uint64_t x) { return __uint_as_float(static_cast<uint32_t>(x)); }
+__device__ __forceinline__ float hi_f(uint64_t x) { return __uint_as_float(static_cast<uint32_t>(x >> 32)); }
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// 2^x for a pair on the FMA pipe (offloads MUFU): x clamped to [-126, 64]; round-to-
+// nearest split x = j + f via the 1.5*2^23 magic number, degree-3 minimax polynomial for
+// 2^f on [-0.5, 0.5] (max relative error 7.5e-5), exponent added into the bits.  Values
+// below 2^-126 of the reference come out as denormal-small positives (negligible against
+// the >= 1 row mass); x >= 40 can only occur when the reference must move (rebase).
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+    const float x0 = fminf(fmaxf(lo_f(x), -126.f), 64.f);
+    const float x1 = fminf(fmaxf(hi_f(x), -126.f), 64.f);
+    const uint64_t xc = pk(x0, x1);
+    const uint64_t t = add2(xc, pk(12582912.f, 12582912.f));     // j + 1.5*2^23
+    const uint64_t j = add2(t, pk(-12582912.f, -12582912.f));    // j
+    const uint64_t f = fma2(j, pk(-1.f, -1.f), xc);               // x - j in [-0.5, 0.5]
+    uint64_t p = fma2(pk(0.05517162704803067f, 0.05517162704803067f), f,
+                      pk(0.2426111716750347f, 0.2426111716750347f));
+    p = fma2(p, f, pk(0.693260997791971f, 0.693260997791971f));
+    p = fma2(p, f, pk(0.9999280708313836f, 0.9999280708313836f));
+    const uint32_t r0 = static_cast<uint32_t>(p) + (static_cast<uint32_t>(t) << 23);
+    const uint32_t r1 = static_cast<uint32_t>(p >> 32) + (static_cast<uint32_t>(t >> 32) << 23);
+    return static_cast<uint64_t>(r0) | (static_cast<uint64_t>(r1) << 32);
+}
+
 // Binary search: largest s in [0, R) with cu[s] <= x (cu is non-decreasing, cu[0] = 0).
 __device__ __forceinline__ int find_segment(const int32_t* cu, int R, int64_t x) {
     int lo = 0, hi = R - 1;

@@ -81,6 +81,34 @@ __device__ __forceinline__ Item make_item(const Part& P, int64_t pos, int64_t en
     return it;
 }
 
+#ifndef UP_POLY_PAIRS
+#define UP_POLY_PAIRS 0
+#endif
+// Of the 16 element pairs of a 32-column group, this many evaluate 2^x with the FMA-pipe
+// polynomial (exp2_poly2) instead of MUFU.EX2 (0 measured fastest on B200: the epilogue
+// is issue/latency-limited, not MUFU-limited, at two epilogue warps per SMSP).
+constexpr int kPolyPairs = UP_POLY_PAIRS;
+
+// Σ_k 2^(v_k * sc - m) over 32 TMEM values: packed FFMA2 for the exponent argument, MUFU
+// ex2 (or the FMA-pipe polynomial for the last kPolyPairs pairs), two FADD2 chains.
+__device__ __forceinline__ float group_sum_pk(const uint32_t* v, uint64_t sc2, uint64_t m2) {
+    uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const uint64_t x = fma2(static_cast<uint64_t>(v[2 * i]) | (static_cast<uint64_t>(v[2 * i + 1]) << 32), sc2, m2);
+        const uint64_t e = i < 16 - kPolyPairs ? pk(ex2_approx(lo_f(x)), ex2_approx(hi_f(x))) : exp2_poly2(x);
+        if (i & 1) a1 = add2(a1, e); else a0 = add2(a0, e);
+    }
+    const uint64_t a = add2(a0, a1);
+    return lo_f(a) + hi_f(a);
+}
+
+// Cold path of a rebase: rescale the partials this thread already wrote for the item.
+__device__ __noinline__ void rescale_rows(float* prow, int g0, int g1, float f) {
+#pragma unroll 4
+    for (int g = g0; g < g1; ++g) prow[static_cast<int64_t>(g) * kRows] *= f;
+}
+
 template <int D, int HPC>
 struct TcCfg {
     static constexpr int KC = D / 64;                 // 128-byte K-chunks per row
@@ -350,49 +378,37 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
                             if (lane == 0) mbar_arrive(&t_empty[reg]);
                         }
                         if (c0 >= N) continue;  // warp-uniform
-                        const float mneg = -m;
-                        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                        float gs;
                         if (!tail) {
-#pragma unroll
-                            for (int k = 0; k < 32; k += 4) {
-                                a0 += ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, mneg));
-                                a1 += ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, mneg));
-                                a2 += ex2_approx(fmaf(__uint_as_float(v[k + 2]), sc, mneg));
-                                a3 += ex2_approx(fmaf(__uint_as_float(v[k + 3]), sc, mneg));
-                            }
+                            gs = group_sum_pk(v, pk(sc, sc), pk(-m, -m));
                         } else {
                             const int lim = qpos - c0;  // column k valid iff k <= lim
+                            float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-                            for (int k = 0; k < 32; k += 4) {
-                                const float e0 = ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, mneg));
-                                const float e1 = ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, mneg));
-                                const float e2 = ex2_approx(fmaf(__uint_as_float(v[k + 2]), sc, mneg));
-                                const float e3 = ex2_approx(fmaf(__uint_as_float(v[k + 3]), sc, mneg));
+                            for (int k = 0; k < 32; k += 2) {
+                                const float e0 = ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, -m));
+                                const float e1 = ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, -m));
                                 a0 += (k + 0 <= lim) ? e0 : 0.f;
                                 a1 += (k + 1 <= lim) ? e1 : 0.f;
-                                a2 += (k + 2 <= lim) ? e2 : 0.f;
-                                a3 += (k + 3 <= lim) ? e3 : 0.f;
                             }
+                            gs = a0 + a1;
                         }
-                        float gs = (a0 + a1) + (a2 + a3);
                         // Rebase only when a value exceeds the reference by ~2^40: partial sums
                         // stay < 2^53 (l over <= 2^13 keys) and values down to 2^-166 of the
                         // row max stay representable, so this fires essentially only on the
                         // item's first group (m = -inf).
                         if (!(gs <= 0x1p40f)) {
-                            // Rebase this (row, item) reference onto the max seen (rare).
                             const int lim = tail ? qpos - c0 : 31;
                             float gmax = -INFINITY;
 #pragma unroll
                             for (int k = 0; k < 32; ++k)
-                                if (k <= lim) gmax = fmaxf(gmax, __uint_as_float(v[k]) * sc);
-                            const float mnew = fmaxf(m, gmax);
+                                if (k <= lim) gmax = fmaxf(gmax, __uint_as_float(v[k]));
+                            const float mnew = fmaxf(m, gmax * sc);
                             if (m != -INFINITY) {
                                 const float f = ex2_approx(m - mnew);
                                 l *= f;
                                 bsum *= f;
-#pragma unroll 8
-                                for (int g = blk0; g < blk; ++g) Prow[static_cast<int64_t>(g) * kRows] *= f;
+                                rescale_rows(Prow, blk0, blk, f);
                             }
                             m = mnew;
                             gs = 0.f;
