@@ -21,6 +21,8 @@ struct CompactParams;
 int tc_max_hpc(int D);
 cudaError_t launch_score_tc(int D, int HPC, const CUtensorMap& qm, const CUtensorMap& km,
                             const ScoreTcParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_score_tc4(int D, const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p,
+                             int grid, cudaStream_t stream);
 cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int G, int32_t* cu_blocks,
                                uint32_t* err, cudaStream_t stream);
 struct BlockCombineParams;
@@ -297,7 +299,15 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
         }();
         const int grid = grid_override > 0 ? grid_override : num_sms();
         p.dbg = score_debug_buffer();
-        cudaError_t e = launch_score_tc(D, hpc, qm, km, p, grid, stream);
+        // Four q-heads per kv-head: the four-warpgroup variant (score_tc4.cu); UP_SCORE_TC4=0
+        // selects the two-warpgroup kernel for comparison.
+        static const bool use_tc4 = [] {
+            const char* s = std::getenv("UP_SCORE_TC4");
+            return !(s && s[0] == '0');
+        }();
+        cudaError_t e = (use_tc4 && hpc == 4 && (D == 64 || D == 128))
+                            ? launch_score_tc4(D, qm, km, p, grid, stream)
+                            : launch_score_tc(D, hpc, qm, km, p, grid, stream);
         if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
         BlockCombineParams bp{};
         bp.cu_seqlens = b->cu_seqlens;

@@ -1,0 +1,87 @@
+// score_common.cuh -- pieces shared by the tcgen05 scorer kernels (score_tc.cu,
+// score_tc4.cu): the balanced work partition and the packed exp2 group sums.
+#pragma once
+
+#include "params.cuh"
+
+namespace up {
+
+constexpr int kMaxPairItems = 256;  // item starts of one (request, head-group) pair kept in smem
+
+// ---------------------------------------------------------------- partition
+struct Part {
+    const int32_t* cu_units;  // smem [R+1]
+    int R;
+    int nhg;
+    int64_t U;
+    int grid;
+};
+
+struct Item {
+    int r, hg;
+    int u0, u1;        // unit range inside the pair
+    int64_t sid;       // global unit position of the item start (stats id)
+    int64_t seg_start; // global unit position of the pair's unit 0
+    int units_r;
+};
+
+__device__ __forceinline__ int64_t range_begin(const Part& P, int c) {
+    return static_cast<int64_t>(c) * P.U / P.grid;
+}
+
+// CTA whose range holds global unit position pos: largest c with c*U/grid <= pos.
+__device__ __forceinline__ int cta_of(const Part& P, int64_t pos) {
+    return static_cast<int>(((pos + 1) * P.grid - 1) / P.U);
+}
+
+__device__ __forceinline__ Item make_item(const Part& P, int64_t pos, int64_t end) {
+    Item it;
+    // request: largest r with cu_units[r]*nhg <= pos (pairs with zero units are skipped)
+    int lo = 0, hi = P.R - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (static_cast<int64_t>(P.cu_units[mid]) * P.nhg <= pos) lo = mid; else hi = mid - 1;
+    }
+    it.r = lo;
+    it.units_r = P.cu_units[lo + 1] - P.cu_units[lo];
+    const int64_t base = static_cast<int64_t>(P.cu_units[lo]) * P.nhg;
+    const int64_t rel = pos - base;
+    it.hg = static_cast<int>(rel / it.units_r);
+    it.u0 = static_cast<int>(rel - static_cast<int64_t>(it.hg) * it.units_r);
+    it.seg_start = base + static_cast<int64_t>(it.hg) * it.units_r;
+    const int64_t seg_end = it.seg_start + it.units_r;
+    const int64_t stop = end < seg_end ? end : seg_end;
+    it.u1 = it.u0 + static_cast<int>(stop - pos);
+    it.sid = pos;
+    return it;
+}
+
+#ifndef UP_POLY_PAIRS
+#define UP_POLY_PAIRS 0
+#endif
+// Of the 16 element pairs of a 32-column group, this many evaluate 2^x with the FMA-pipe
+// polynomial (exp2_poly2) instead of MUFU.EX2 (0 measured fastest on B200: the epilogue
+// is issue/latency-limited, not MUFU-limited, at two epilogue warps per SMSP).
+constexpr int kPolyPairs = UP_POLY_PAIRS;
+
+// Σ_k 2^(v_k * sc - m) over 32 TMEM values: packed FFMA2 for the exponent argument, MUFU
+// ex2 (or the FMA-pipe polynomial for the last kPolyPairs pairs), two FADD2 chains.
+__device__ __forceinline__ float group_sum_pk(const uint32_t* v, uint64_t sc2, uint64_t m2) {
+    uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const uint64_t x = fma2(static_cast<uint64_t>(v[2 * i]) | (static_cast<uint64_t>(v[2 * i + 1]) << 32), sc2, m2);
+        const uint64_t e = i < 16 - kPolyPairs ? pk(ex2_approx(lo_f(x)), ex2_approx(hi_f(x))) : exp2_poly2(x);
+        if (i & 1) a1 = add2(a1, e); else a0 = add2(a0, e);
+    }
+    const uint64_t a = add2(a0, a1);
+    return lo_f(a) + hi_f(a);
+}
+
+// Cold path of a rebase: rescale the partials this thread already wrote for the item.
+static __device__ __noinline__ void rescale_rows(float* prow, int g0, int g1, float f) {
+#pragma unroll 4
+    for (int g = g0; g < g1; ++g) prow[static_cast<int64_t>(g) * kRows] *= f;
+}
+
+}  // namespace up

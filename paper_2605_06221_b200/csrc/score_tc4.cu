@@ -1,0 +1,409 @@
+// score_tc4.cu -- tensor-core scorer variant for four q-heads per kv-head (HPC = 4, e.g.
+// LLaMA-3.1-8B: 32 q-heads / 8 kv-heads, D = 128) with four epilogue warpgroups.
+//
+// Same math, work partition, statistics and row-weight epilogue as score_tc.cu (see its
+// header: importance.cpp:17-132 restated as a single pass over K).  What differs is the
+// pipeline shape, chosen because the exp2 epilogue -- not the tensor core -- bounds the
+// scorer (MUFU 16 ex2/clk/SM vs 32 S elements/clk/SM from tcgen05 at D = 128):
+//  * 18 warps: warp 0 TMA, warp 1 MMA, warps 2..17 = four epilogue warpgroups, one per
+//    q-head of the group, so every SMSP runs four exp2 streams (vs two) and each thread
+//    keeps its row's running state (m, l, block partial) in registers;
+//  * every 128-key tile is issued as two N = 64 MMAs per head into eight 64-column TMEM
+//    regions = (head, buffer): a warpgroup drains one buffer while tcgen05 fills the other.
+#include "score_common.cuh"
+
+namespace up {
+
+template <int D>
+struct Tc4Cfg {
+    static constexpr int HPC = 4;
+    static constexpr int KC = D / 64;
+    static constexpr int SUB = 128 * 128;
+    static constexpr int Q_BYTES = HPC * KC * SUB;
+    static constexpr int K_STAGE = KC * SUB;
+    static constexpr int KST = 2;
+    static constexpr int SUBN = 64;                // keys per MMA / TMEM region width
+    static constexpr int NREG = HPC * 2;           // (head, buffer) regions
+    static constexpr int NBAR = 2 + 2 * KST + 2 * NREG;
+    static constexpr int THREADS = 64 + 512;
+    static constexpr int FIXED = Q_BYTES + KST * K_STAGE + NBAR * 8 + 64 + 1024;
+    static int smem(int R) { return FIXED + 2 * (R + 1) * 4 + kMaxPairItems * 4; }
+};
+
+__device__ __forceinline__ void epi_bar512() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
+
+template <int D>
+__global__ void __launch_bounds__(576, 1)
+score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                 const ScoreTcParams p) {
+    using C = Tc4Cfg<D>;
+    constexpr int HPC = C::HPC;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sq = smem;
+    uint8_t* sk = smem + C::Q_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sk + C::KST * C::K_STAGE);
+    uint64_t* q_full = bars + 0;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* k_full = bars + 2;
+    uint64_t* k_empty = bars + 2 + C::KST;
+    uint64_t* t_full = bars + 2 + 2 * C::KST;
+    uint64_t* t_empty = bars + 2 + 2 * C::KST + C::NREG;
+    uint32_t* misc = reinterpret_cast<uint32_t*>(bars + C::NBAR);  // [0] tmem base, [1] ok, [2] last, [3] n
+    int32_t* s_cu_units = reinterpret_cast<int32_t*>(misc + 16);
+    int32_t* s_cu_blocks = s_cu_units + (p.num_requests + 1);
+    int32_t* s_items = s_cu_blocks + (p.num_requests + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int R = p.num_requests;
+    const int G = p.block_size_g;
+    const int unit_keys = p.unit_keys;
+    unsigned long long t_start = 0;
+    if (p.dbg != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int s = 0; s < C::KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
+        for (int s = 0; s < C::NREG; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 4); }
+        fence_barrier_init();
+        prefetch_tensormap(&qmap);
+        prefetch_tensormap(&kmap);
+    }
+    if (warp == 1) tmem_alloc(misc, 512);
+    if (warp == 2) {
+        // Plan from cu_seqlens (PackedBatch::validate, scheduler.cpp:33-48).
+        bool ok = p.cu_seqlens[0] == 0;
+        int carry_u = 0, carry_b = 0;
+        for (int base = 0; base < R; base += 32) {
+            const int r = base + lane;
+            int units = 0, blocks = 0;
+            if (r < R) {
+                const int n = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+                if (n <= 0) ok = false;
+                blocks = n > 0 ? (n + G - 1) / G : 0;
+                const bool en = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
+                units = en && n > 0 ? (n + unit_keys - 1) / unit_keys : 0;
+            }
+            int x = units, y = blocks;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int a = __shfl_up_sync(0xffffffffu, x, o);
+                const int b = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) { x += a; y += b; }
+            }
+            if (r < R) {
+                s_cu_units[r + 1] = carry_u + x;
+                s_cu_blocks[r + 1] = carry_b + y;
+            }
+            carry_u += __shfl_sync(0xffffffffu, x, 31);
+            carry_b += __shfl_sync(0xffffffffu, y, 31);
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (lane == 0) {
+            s_cu_units[0] = 0;
+            s_cu_blocks[0] = 0;
+            if (ok && p.cu_seqlens[R] > p.max_tokens) ok = false;
+            misc[1] = ok ? 1u : 0u;
+            if (!ok && blockIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = misc[0];
+    if (blockIdx.x == 0) {
+        for (int r = threadIdx.x; r <= R; r += blockDim.x) {
+            p.cu_blocks[r] = misc[1] ? s_cu_blocks[r] : 0;
+            p.cu_units_out[r] = misc[1] ? s_cu_units[r] : 0;
+        }
+    }
+
+    Part P;
+    P.cu_units = s_cu_units;
+    P.R = R;
+    P.nhg = p.num_hgroups;
+    P.U = misc[1] ? static_cast<int64_t>(s_cu_units[R]) * p.num_hgroups : 0;
+    P.grid = gridDim.x;
+    const int64_t my_begin = P.U > 0 ? range_begin(P, blockIdx.x) : 0;
+    const int64_t my_end = P.U > 0 ? range_begin(P, blockIdx.x + 1) : 0;
+
+    if (warp == 0) {
+        // ===== TMA producer (identical to score_tc.cu) =====
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t qiter = 0;
+            for (int64_t pos = my_begin; pos < my_end;) {
+                const Item it = make_item(P, pos, my_end);
+                pos += it.u1 - it.u0;
+                const int seg0 = p.cu_seqlens[it.r];
+                const int N = p.cu_seqlens[it.r + 1] - seg0;
+                const int neff = min(p.query_window_n, N);
+                const int key0 = it.u0 * unit_keys;
+                const int key1 = min(it.u1 * unit_keys, N);
+                const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
+                const int kv_local = (p.q_head_offset + it.hg * HPC) / p.gqa_group - p.kv_head_offset;
+                mbar_wait(q_empty, (qiter & 1) ^ 1);
+                ++qiter;
+                mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+                const int qrow = seg0 + N - neff;
+#pragma unroll
+                for (int hh = 0; hh < HPC; ++hh) {
+#pragma unroll
+                    for (int kc = 0; kc < C::KC; ++kc)
+                        tma_load_2d(sq + (hh * C::KC + kc) * C::SUB, &qmap, q_full,
+                                    (it.hg * HPC + hh) * D + kc * 64, qrow);
+                }
+                for (int t = 0; t < ntiles; ++t) {
+                    mbar_wait(&k_empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&k_full[stage], C::K_STAGE);
+                    const int krow = seg0 + key0 + t * kTileKeys;
+#pragma unroll
+                    for (int kc = 0; kc < C::KC; ++kc)
+                        tma_load_2d(sk + stage * C::K_STAGE + kc * C::SUB, &kmap, &k_full[stage],
+                                    kv_local * D + kc * 64, krow);
+                    if (++stage == C::KST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer: per tile, two 64-key halves x four heads, N = 64 =====
+        if (elect_one()) {
+            constexpr uint32_t kIdesc = idesc_bf16_f32(128, C::SUBN);
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t qiter = 0;
+            uint32_t u = 0;  // 64-key sub-tile counter
+            const uint32_t sq_addr = smem_u32(sq);
+            const uint32_t sk_addr = smem_u32(sk);
+            for (int64_t pos = my_begin; pos < my_end;) {
+                const Item it = make_item(P, pos, my_end);
+                pos += it.u1 - it.u0;
+                const int N = p.cu_seqlens[it.r + 1] - p.cu_seqlens[it.r];
+                const int key0 = it.u0 * unit_keys;
+                const int key1 = min(it.u1 * unit_keys, N);
+                const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
+                mbar_wait(q_full, qiter & 1);
+                ++qiter;
+                tc_fence_after();
+                for (int t = 0; t < ntiles; ++t) {
+                    mbar_wait(&k_full[stage], phase);
+                    tc_fence_after();
+#pragma unroll
+                    for (int s = 0; s < 2; ++s, ++u) {
+#pragma unroll
+                        for (int hh = 0; hh < HPC; ++hh) {
+                            const uint32_t reg = hh * 2 + (u & 1);
+                            mbar_wait(&t_empty[reg], ((u >> 1) & 1) ^ 1);
+                            tc_fence_after();
+                            const uint32_t d_tmem = tmem_base + reg * C::SUBN;
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const uint32_t off = (kk >> 2) * C::SUB + (kk & 3) * 32;
+                                const uint64_t a = smem_desc_sw128(sq_addr + hh * C::KC * C::SUB + off);
+                                // rows s*64.. of the K tile: 8 swizzle atoms (8 KB) further
+                                const uint64_t b = smem_desc_sw128(sk_addr + stage * C::K_STAGE + off + s * 8192);
+                                mma_bf16_ss(d_tmem, a, b, kIdesc, kk > 0 ? 1u : 0u);
+                            }
+                            mma_commit(&t_full[reg]);
+                        }
+                    }
+                    mma_commit(&k_empty[stage]);
+                    if (++stage == C::KST) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(q_empty);
+            }
+        }
+    } else {
+        // ===== epilogue: warpgroup w drains head w; thread = query row =====
+        const int etid = threadIdx.x - 64;   // 0..511
+        const int w = (warp - 2) >> 2;       // head within the group
+        const int quarter = warp & 3;        // TMEM lane quarter
+        const int j = quarter * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+        const float sc = p.scale_log2;
+        const int gpb = G / 32;
+        uint32_t u = 0;
+        for (int64_t pos = my_begin; pos < my_end;) {
+            const Item it = make_item(P, pos, my_end);
+            pos += it.u1 - it.u0;
+            const int seg0 = p.cu_seqlens[it.r];
+            const int N = p.cu_seqlens[it.r + 1] - seg0;
+            const int neff = min(p.query_window_n, N);
+            const int key0 = it.u0 * unit_keys;
+            const int key1 = min(it.u1 * unit_keys, N);
+            const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
+            const bool row_valid = j < neff;
+            const int qpos = N - neff + j;
+            const int64_t gb_seg = s_cu_blocks[it.r];
+            const int blk0 = key0 / G;
+            float* Prow = p.P + (static_cast<int64_t>(it.hg * HPC + w) * p.max_blocks + gb_seg) * kRows + j;
+            float m = -INFINITY, l = 0.f, bsum = 0.f;
+            int gib = 0, blk = blk0;
+
+#pragma unroll 1
+            for (int t2 = 0; t2 < 2 * ntiles; ++t2, ++u) {
+                const int cbase = key0 + t2 * C::SUBN;
+                const bool tail = cbase + C::SUBN - 1 > N - neff;  // warp-uniform
+                const uint32_t reg = w * 2 + (u & 1);
+                mbar_wait(&t_full[reg], (u >> 1) & 1);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + lane_base + reg * C::SUBN;
+#pragma unroll 1
+                for (int q2 = 0; q2 < C::SUBN / 32; ++q2) {
+                    const int c0 = cbase + q2 * 32;
+                    uint32_t v[32];
+                    tmem_ld32(taddr + q2 * 32, v);
+                    tmem_ld_wait();
+                    if (q2 == C::SUBN / 32 - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&t_empty[reg]);
+                    }
+                    if (c0 >= N) continue;  // warp-uniform
+                    float gs;
+                    if (!tail) {
+                        gs = group_sum_pk(v, pk(sc, sc), pk(-m, -m));
+                    } else {
+                        const int lim = qpos - c0;
+                        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+                        for (int k = 0; k < 32; k += 2) {
+                            const float e0 = ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, -m));
+                            const float e1 = ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, -m));
+                            a0 += (k + 0 <= lim) ? e0 : 0.f;
+                            a1 += (k + 1 <= lim) ? e1 : 0.f;
+                        }
+                        gs = a0 + a1;
+                    }
+                    if (!(gs <= 0x1p40f)) {  // rebase (see score_tc.cu)
+                        const int lim = tail ? qpos - c0 : 31;
+                        float gmax = -INFINITY;
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            if (k <= lim) gmax = fmaxf(gmax, __uint_as_float(v[k]));
+                        const float mnew = fmaxf(m, gmax * sc);
+                        if (m != -INFINITY) {
+                            const float f = ex2_approx(m - mnew);
+                            l *= f;
+                            bsum *= f;
+                            rescale_rows(Prow, blk0, blk, f);
+                        }
+                        m = mnew;
+                        gs = 0.f;
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) {
+                            const float e = ex2_approx(fmaf(__uint_as_float(v[k]), sc, -mnew));
+                            gs += (k <= lim) ? e : 0.f;
+                        }
+                    }
+                    bsum += gs;
+                    if (++gib == gpb || c0 + 32 >= N) {
+                        Prow[static_cast<int64_t>(blk) * kRows] = row_valid ? bsum : 0.f;
+                        l += bsum;
+                        bsum = 0.f;
+                        gib = 0;
+                        ++blk;
+                    }
+                }
+            }
+            {
+                const int64_t x = (it.sid * HPC + w) * kRows + j;
+                p.stat_m[x] = row_valid ? m : -INFINITY;
+                p.stat_l[x] = row_valid ? l : 0.f;
+            }
+            for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
+
+            const int64_t seg_end = it.seg_start + it.units_r;
+            epi_bar512();
+            if (etid == 0) {
+                int n_items = 0;
+                for (int64_t s = it.seg_start; s < seg_end; ++n_items) {
+                    if (n_items < kMaxPairItems) s_items[n_items] = static_cast<int32_t>(s);
+                    const int64_t e = range_begin(P, cta_of(P, s) + 1);
+                    s = e < seg_end ? e : seg_end;
+                }
+                int32_t* ctr = p.pair_counters + it.r * P.nhg + it.hg;
+                __threadfence();
+                const int old = atomicAdd(ctr, 1);
+                const bool is_last = old == n_items - 1;
+                if (is_last) *ctr = 0;
+                misc[2] = is_last ? 1u : 0u;
+                misc[3] = static_cast<uint32_t>(n_items);
+            }
+            epi_bar512();
+            if (misc[2]) {
+                __threadfence();
+                const int n_items = static_cast<int>(misc[3]);
+                for (int x = etid; x < HPC * kRows; x += 512) {
+                    const int hh = x / kRows, jj = x - (x / kRows) * kRows;
+                    const bool valid = jj < neff;
+                    auto item_at = [&](int k, int64_t& s) {
+                        if (k < kMaxPairItems) { s = s_items[k]; return; }
+                        s = range_begin(P, cta_of(P, s) + 1);
+                    };
+                    float M = -INFINITY;
+                    int64_t s = 0;
+                    for (int k = 0; k < n_items; ++k) {
+                        item_at(k, s);
+                        M = fmaxf(M, __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]));
+                    }
+                    float L = 0.f;
+                    for (int k = 0; k < n_items; ++k) {
+                        item_at(k, s);
+                        const float mc = __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]);
+                        if (mc != -INFINITY) L += __ldcg(&p.stat_l[(s * HPC + hh) * kRows + jj]) * ex2_approx(mc - M);
+                    }
+                    if (valid && !(L > 0.f)) raise_error(p.err, kErrMaskedRow);
+                    const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
+                    for (int k = 0; k < n_items; ++k) {
+                        item_at(k, s);
+                        const float mc = __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]);
+                        p.stat_w[(s * HPC + hh) * kRows + jj] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+    if (p.dbg != nullptr && threadIdx.x == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        p.dbg[blockIdx.x * 4 + 0] = t_start;
+        p.dbg[blockIdx.x * 4 + 1] = t_end;
+        p.dbg[blockIdx.x * 4 + 2] = static_cast<unsigned long long>(my_end - my_begin);
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.dbg[blockIdx.x * 4 + 3] = smid;
+    }
+}
+
+template <int D>
+static cudaError_t launch_tc4(const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p, int grid,
+                             cudaStream_t stream) {
+    using C = Tc4Cfg<D>;
+    const int smem = C::smem(p.num_requests);
+    if (smem > 232448) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(score_tc4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    score_tc4_kernel<D><<<grid, C::THREADS, smem, stream>>>(qm, km, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_score_tc4(int D, const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p,
+                             int grid, cudaStream_t stream) {
+    if (D == 64) return launch_tc4<64>(qm, km, p, grid, stream);
+    if (D == 128) return launch_tc4<128>(qm, km, p, grid, stream);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace up
