@@ -29,7 +29,7 @@ struct BlockCombineParams;
 cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int num_sms,
                               cudaStream_t stream);
-cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request,
+cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request, int num_sms,
                           cudaStream_t stream);
 cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t count, float* out,
                                  int num_sms, cudaStream_t stream);
@@ -71,10 +71,19 @@ unsigned long long* score_debug_buffer() {
     return d;
 }
 
+unsigned long long* select_debug_buffer() {
+    static unsigned long long* d = [] {
+        unsigned long long* x = nullptr;
+        if (std::getenv("UP_SELECT_DEBUG")) cudaMalloc(&x, sizeof(unsigned long long) * 16);
+        return x;
+    }();
+    return d;
+}
+
 // ---- workspace layout --------------------------------------------------------------
 struct Layout {
     size_t err, cu_units, pair_counters, unit_sid, P, stat_m, stat_l, stat_w, simt_m, simt_l,
-        simt_tok, tile_counts, ret_idx, total;
+        simt_tok, tile_counts, ret_idx, blk_keep, total;
     int64_t max_blocks, max_units;
     int32_t simt_n;
 };
@@ -112,6 +121,7 @@ Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c
     L.simt_tok = take(sizeof(float) * (T + 1));
     L.tile_counts = take(sizeof(int32_t) * (compact_tiles(T) + 1));
     L.ret_idx = take(sizeof(int32_t) * (T + 1));
+    L.blk_keep = take(static_cast<size_t>(L.max_blocks));
     L.total = align_up(off, 256);
     return L;
 }
@@ -401,10 +411,13 @@ up_status up_select(void* stream, const up_batch* b, const up_score_config* c,
     p.block_size_g = c->block_size_g;
     p.sink_count_a = c->sink_count_a;
     p.top_p = c->top_p;
+    p.dbg = select_debug_buffer();
+    p.blk_keep = at<uint8_t>(ws, L.blk_keep);
+    p.max_tokens = b->max_tokens;
     const int64_t per_req = (b->max_tokens + c->block_size_g - 1) / c->block_size_g;
     const cudaError_t e = launch_select(p, b->num_requests, static_cast<int>(per_req < kMaxSortBlocks ? per_req : kMaxSortBlocks),
-                                        static_cast<cudaStream_t>(stream));
-    g_launches = 1;
+                                        num_sms(), static_cast<cudaStream_t>(stream));
+    g_launches = 2;
     return cuda_status(e);
 }
 
@@ -480,6 +493,14 @@ up_status up_device_status(void* stream, void* ws) {
 }
 
 }  // extern "C"
+
+// Diagnostics (not part of the ABI header): phase clocks of the select kernel's CTA 0.
+extern "C" int up_internal_select_debug(unsigned long long* host) {
+    unsigned long long* d = select_debug_buffer();
+    if (d == nullptr || host == nullptr) return -1;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+    return cudaMemcpy(host, d, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -3;
+}
 
 // Diagnostics (not part of the ABI header): copy the scorer's per-CTA timing records
 // [cta][start_ns, end_ns, units, smid] of the last launch to host memory.

@@ -89,6 +89,9 @@ struct SelectParams {
     int32_t block_size_g;
     int32_t sink_count_a;
     float top_p;
+    uint8_t* blk_keep;        // workspace [max_blocks]: per-block decisions for the expand kernel
+    int64_t max_tokens;
+    unsigned long long* dbg;  // optional phase clocks of CTA 0 (UP_SELECT_DEBUG), else null
 };
 
 constexpr int kMaxPlanes = 8;

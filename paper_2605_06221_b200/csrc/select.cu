@@ -16,6 +16,8 @@
 //      propagation.cpp:116-136) and compute retained count and covered mass (:108-120).
 #include <float.h>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "params.cuh"
 
 namespace up {
@@ -85,6 +87,238 @@ __device__ double block_exclusive_scan(double v, double* scratch) {
     return r;
 }
 
+#define SEL_STAMP(k)                                                      \
+    if (p.dbg != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {       \
+        unsigned long long c_;                                            \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_));                \
+        p.dbg[k] = c_;                                                    \
+    }
+
+// Per-request epilogue shared by both select kernels: blk[] (smem) holds the block
+// decisions and sc[] the block scores.  Publishes the decisions for the expand kernel and
+// computes retained count / covered mass (selection.cpp:98-120): analytically per block
+// without a veto (a block keeps all tokens, or only the forced sinks [0, A) and query
+// window [N - n_eff, N)), per token with the veto (restrict_selection,
+// propagation.cpp:116-136).
+__device__ void finish_request(const SelectParams& p, int r, int seg0, int N, int nb, int neff,
+                               const uint8_t* blk, const float* sc, int kstar, bool degenerate,
+                               double total, double* red_d, int* red_i) {
+    const int tid = threadIdx.x;
+    const int G = p.block_size_g;
+    const int64_t A = p.sink_count_a;
+    const int64_t win0 = N - neff;
+    uint8_t* out_blk = p.blk_keep + p.cu_blocks[r];
+    int retained = 0;
+    double covered = 0.0;
+    for (int g = tid; g < nb; g += blockDim.x) {
+        out_blk[g] = blk[g];
+        const int64_t b0 = static_cast<int64_t>(g) * G;
+        const int size = min(G, N - g * G);
+        int kept;
+        if (p.veto == nullptr) {
+            kept = size;
+            if (!blk[g]) {
+                const int64_t b1 = b0 + size;
+                const int64_t sink_end = b1 < A ? b1 : A;
+                const int64_t win_beg = b0 > win0 ? b0 : win0;
+                const int64_t sink = sink_end > b0 ? sink_end - b0 : 0;
+                const int64_t win = b1 > win_beg ? b1 - win_beg : 0;
+                const int64_t both = sink_end > win_beg ? sink_end - win_beg : 0;
+                kept = static_cast<int>(sink + win - both);
+            }
+        } else {
+            kept = 0;
+            for (int x = 0; x < size; ++x) {
+                const int64_t i = b0 + x;
+                const bool k = (blk[g] != 0 || i < A || i >= win0) && !p.veto[seg0 + i];
+                kept += k ? 1 : 0;
+            }
+        }
+        retained += kept;
+        // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g|.
+        covered += static_cast<double>(sc[g]) * (static_cast<double>(kept) / static_cast<double>(size));
+    }
+    retained = block_sum<int>(retained, red_i);
+    covered = block_sum<double>(covered, red_d);
+    if (tid == 0) {
+        p.cutoff_rank[r] = kstar;
+        if (p.retained_count) p.retained_count[r] = retained;
+        // Degenerate selections report 1.0 with or without a veto (selection.cpp:104-106,
+        // propagation.cpp:135: restrict_selection also falls back to 1.0 at zero mass).
+        if (p.covered_mass) p.covered_mass[r] = degenerate ? 1.0 : covered / total;
+        if (p.degenerate) p.degenerate[r] = degenerate ? 1 : 0;
+    }
+}
+
+// Error / pass-through requests: every block kept, stats of a keep-all selection.
+__device__ void keep_all_request(const SelectParams& p, int r, int N, int nb, int64_t cutoff) {
+    uint8_t* out_blk = p.blk_keep + p.cu_blocks[r];
+    for (int g = threadIdx.x; g < nb; g += blockDim.x) out_blk[g] = 1;
+    if (threadIdx.x == 0) {
+        p.cutoff_rank[r] = cutoff;
+        if (p.retained_count) p.retained_count[r] = N;
+        if (p.covered_mass) p.covered_mass[r] = 1.0;
+        if (p.degenerate) p.degenerate[r] = 0;
+    }
+}
+
+// The reference's exact sequential sums (selection.cpp:61-67, :84-93) replayed by one
+// thread over the sorted order; returns k*.  Bit-exact by construction.
+__device__ int exact_crossing(const float* sc, int nb, const uint32_t* skey, const int32_t* sval,
+                              double p_d) {
+    double tot = 0.0;
+    for (int g = 0; g < nb; ++g) tot += sc[g];
+    double c = 0.0;
+    for (int q = 0; q < nb; ++q) {
+        c += static_cast<double>(phi_decode_dev(skey[q]));
+        if (c / tot >= p_d) return q + 1;
+    }
+    (void)sval;
+    return nb;
+}
+
+// Guard (see file header): the sequential ratio is monotone in the rank and within delta
+// of the parallel one; accept the parallel crossing only when it clears p by delta.
+__device__ __forceinline__ bool crossing_certain(bool reached, int rc, double ratio_c, double ratio_prev,
+                                                 double p_d, int nb) {
+    const double delta = (4.0 * nb + 256.0) * DBL_EPSILON;
+    bool certain = reached ? (ratio_c - p_d > delta) : (p_d - ratio_c > delta);
+    if (reached && rc >= 1) certain = certain && (p_d - ratio_prev > delta);
+    return certain;
+}
+
+// ---- CUB radix-sort variant (nb <= THREADS * ITEMS) ---------------------------------
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+select_radix_kernel(const SelectParams p) {
+    using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, int32_t>;
+    constexpr int CAP = THREADS * ITEMS;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        struct { uint32_t key[CAP]; int32_t val[CAP]; } sorted;  // fallback replay only
+    } u;
+    __shared__ float sc[CAP];
+    __shared__ uint8_t blk[CAP];
+    __shared__ double red_d[32];
+    __shared__ int red_i[32];
+    __shared__ int s_kstar;
+    __shared__ double s_ratio[2];
+
+    const int r = blockIdx.x;
+    SEL_STAMP(0)
+    const int tid = threadIdx.x;
+    const int seg0 = p.cu_seqlens[r];
+    const int N = p.cu_seqlens[r + 1] - seg0;
+    const int G = p.block_size_g;
+    const int nb = (N + G - 1) / G;
+    const int neff = min(p.query_window_n, N);
+    const bool enabled = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
+    if (!enabled) { keep_all_request(p, r, N, nb, -1); return; }
+    if (nb > CAP) {
+        if (tid == 0) raise_error(p.err, kErrTooManyBlocks);
+        keep_all_request(p, r, N, nb, -1);
+        return;
+    }
+    const float* bs = p.block_scores + p.cu_blocks[r];
+
+    // 1. validate, total, keys (blocked: thread t owns blocks t*ITEMS .. +ITEMS-1).
+    uint32_t key[ITEMS];
+    int32_t val[ITEMS];
+    bool bad = false;
+    double tsum = 0.0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int g = tid * ITEMS + i;
+        if (g < nb) {
+            const float s = bs[g];
+            if (!(s >= 0.0f) || !isfinite(s)) bad = true;
+            sc[g] = s;
+            tsum += s;
+            key[i] = phi_encode_dev(s);  // >= 0x80000000 for every valid score
+            val[i] = g;
+        } else {
+            key[i] = 0;                   // padding sorts last
+            val[i] = -1;
+        }
+    }
+    bad = __syncthreads_or(bad);
+    if (bad) {
+        if (tid == 0) raise_error(p.err, kErrBadScore);
+        keep_all_request(p, r, N, nb, -1);
+        return;
+    }
+    const double total = block_sum<double>(tsum, red_d);
+    const bool degenerate = !(total > 0.0);
+    int kstar = nb;
+    if (degenerate) {
+        for (int g = tid; g < nb; g += THREADS) blk[g] = 1;
+    } else {
+        SEL_STAMP(1)
+        // 2. stable descending radix sort of phi(s): ties keep ascending block index, the
+        //    order of PackedScore's ~g low word (selection.cpp:27-34).
+        Sort(u.sort).SortDescending(key, val);
+        SEL_STAMP(2)
+        // 3. parallel prefix over the thread's ITEMS consecutive ranks.
+        float dec[ITEMS];
+        double local = 0.0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            dec[i] = val[i] >= 0 ? phi_decode_dev(key[i]) : 0.0f;
+            local += static_cast<double>(dec[i]);
+        }
+        const double base = block_exclusive_scan(local, red_d);
+        const double p_d = static_cast<double>(p.top_p);
+        if (tid == 0) { s_kstar = nb + 1; s_ratio[0] = -1.0; s_ratio[1] = -1.0; }
+        __syncthreads();
+        double cum = base;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int q = tid * ITEMS + i;
+            cum += static_cast<double>(dec[i]);
+            if (q < nb && cum / total >= p_d) { atomicMin(&s_kstar, q + 1); break; }
+        }
+        __syncthreads();
+        const int kpar = s_kstar;
+        const bool reached = kpar <= nb;
+        const int rc = reached ? kpar - 1 : nb - 1;
+        cum = base;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int q = tid * ITEMS + i;
+            cum += static_cast<double>(dec[i]);
+            if (q == rc) s_ratio[0] = cum / total;
+            if (q == rc - 1) s_ratio[1] = cum / total;
+        }
+        __syncthreads();
+        if (crossing_certain(reached, rc, s_ratio[0], s_ratio[1], p_d, nb)) {
+            kstar = kpar;
+        } else {
+            __syncthreads();  // u.sort no longer needed
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                u.sorted.key[tid * ITEMS + i] = key[i];
+                u.sorted.val[tid * ITEMS + i] = val[i];
+            }
+            __syncthreads();
+            if (tid == 0) s_kstar = exact_crossing(sc, nb, u.sorted.key, u.sorted.val, p_d);
+            __syncthreads();
+            kstar = s_kstar;
+        }
+        SEL_STAMP(3)
+        // 4. block decisions.
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int q = tid * ITEMS + i;
+            if (val[i] >= 0) blk[val[i]] = q < kstar ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    SEL_STAMP(4)
+    finish_request(p, r, seg0, N, nb, neff, blk, sc, kstar, degenerate, total, red_d, red_i);
+    SEL_STAMP(5)
+}
+
+// ---- bitonic variant for large requests (<= kMaxSortBlocks blocks) ------------------
 __global__ void __launch_bounds__(kSelThreads)
 select_kernel(const SelectParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -100,23 +334,11 @@ select_kernel(const SelectParams p) {
     const int G = p.block_size_g;
     const int nb = (N + G - 1) / G;
     const int neff = min(p.query_window_n, N);
-    const int64_t A = p.sink_count_a;
     const bool enabled = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
-
-    auto keep_all = [&](int64_t cutoff, bool degen) {
-        for (int i = tid; i < N; i += blockDim.x) p.keep[seg0 + i] = 1;
-        if (tid == 0) {
-            p.cutoff_rank[r] = cutoff;
-            if (p.retained_count) p.retained_count[r] = N;
-            if (p.covered_mass) p.covered_mass[r] = 1.0;
-            if (p.degenerate) p.degenerate[r] = degen ? 1 : 0;
-        }
-    };
-
-    if (!enabled) { keep_all(-1, false); return; }
+    if (!enabled) { keep_all_request(p, r, N, nb, -1); return; }
     if (nb > kMaxSortBlocks) {
         if (tid == 0) raise_error(p.err, kErrTooManyBlocks);
-        keep_all(-1, false);
+        keep_all_request(p, r, N, nb, -1);
         return;
     }
     int P2 = 1;
@@ -126,7 +348,6 @@ select_kernel(const SelectParams p) {
     uint8_t* blk = reinterpret_cast<uint8_t*>(sc + nb);
     const float* bs = p.block_scores + p.cu_blocks[r];
 
-    // 1. validate, pack, total.
     bool bad = false;
     double tsum = 0.0;
     for (int g = tid; g < P2; g += blockDim.x) {
@@ -144,15 +365,13 @@ select_kernel(const SelectParams p) {
     bad = __syncthreads_or(bad);
     if (bad) {
         if (tid == 0) raise_error(p.err, kErrBadScore);
-        keep_all(-1, false);
+        keep_all_request(p, r, N, nb, -1);
         return;
     }
     const double total = block_sum<double>(tsum, red_d);
-    const bool degenerate = !(total > 0.0);  // all scores are exactly zero
+    const bool degenerate = !(total > 0.0);
     int kstar = nb;
-
     if (!degenerate) {
-        // 2. bitonic sort, descending.
         for (int kk = 2; kk <= P2; kk <<= 1) {
             for (int jj = kk >> 1; jj > 0; jj >>= 1) {
                 for (int i = tid; i < P2; i += blockDim.x) {
@@ -166,7 +385,6 @@ select_kernel(const SelectParams p) {
                 __syncthreads();
             }
         }
-        // 3. parallel prefix over contiguous rank ranges.
         const int per = (P2 + blockDim.x - 1) / blockDim.x;
         const int r0 = tid * per;
         const int r1 = min(r0 + per, nb);
@@ -174,7 +392,7 @@ select_kernel(const SelectParams p) {
         for (int q = r0; q < r1; ++q) local += static_cast<double>(key_score(keys[q]));
         const double base = block_exclusive_scan(local, red_d);
         const double p_d = static_cast<double>(p.top_p);
-        if (tid == 0) s_kstar = nb + 1;  // nb + 1 = never reached
+        if (tid == 0) { s_kstar = nb + 1; s_ratio[0] = -1.0; s_ratio[1] = -1.0; }
         __syncthreads();
         double cum = base;
         for (int q = r0; q < r1; ++q) {
@@ -183,16 +401,8 @@ select_kernel(const SelectParams p) {
         }
         __syncthreads();
         const int kpar = s_kstar;
-        // Guard.  The sequential ratio (the reference's) is monotone in the rank and lies
-        // within delta of the parallel one at every rank (both double sums are within
-        // (nb + per + log2 threads) ulps of the exact sum).  If the parallel ratio clears
-        // p by more than delta at the crossing rank and at the rank before it, the
-        // sequential crossing is the same rank; if the threshold is never reached, the
-        // last rank must stay below p - delta.  Otherwise fall back to the exact replay.
         const bool reached = kpar <= nb;
         const int rc = reached ? kpar - 1 : nb - 1;
-        if (tid == 0) { s_ratio[0] = -1.0; s_ratio[1] = -1.0; }
-        __syncthreads();
         cum = base;
         for (int q = r0; q < r1; ++q) {
             cum += static_cast<double>(key_score(keys[q]));
@@ -200,13 +410,9 @@ select_kernel(const SelectParams p) {
             if (q == rc - 1) s_ratio[1] = cum / total;
         }
         __syncthreads();
-        const double delta = (4.0 * nb + 256.0) * DBL_EPSILON;
-        bool certain = reached ? (s_ratio[0] - p_d > delta) : (p_d - s_ratio[0] > delta);
-        if (reached && rc >= 1) certain = certain && (p_d - s_ratio[1] > delta);
-        if (certain) {
+        if (crossing_certain(reached, rc, s_ratio[0], s_ratio[1], p_d, nb)) {
             kstar = kpar;
         } else {
-            // Replay the reference's sequential sums exactly (one thread).
             if (tid == 0) {
                 double tot = 0.0;
                 for (int g = 0; g < nb; ++g) tot += sc[g];
@@ -221,95 +427,49 @@ select_kernel(const SelectParams p) {
             __syncthreads();
             kstar = s_kstar;
         }
-        // 4. mark the selected blocks.
-        for (int q = tid; q < kstar; q += blockDim.x) {
-            blk[~static_cast<uint32_t>(keys[q] & 0xFFFFFFFFull)] = 1;
-        }
+        for (int q = tid; q < kstar; q += blockDim.x) blk[~static_cast<uint32_t>(keys[q] & 0xFFFFFFFFull)] = 1;
     } else {
         for (int g = tid; g < nb; g += blockDim.x) blk[g] = 1;
     }
     __syncthreads();
+    finish_request(p, r, seg0, N, nb, neff, blk, sc, kstar, degenerate, total, red_d, red_i);
+}
 
-    // 5. expand, force, veto, count.
-    int retained = 0;
-    double covered = 0.0;
-    const int64_t win0 = N - neff;  // first query-window row
-    if (p.veto == nullptr) {
-        // Kept tokens per block follow from the block decision and the forced ranges
-        // [0, A) and [N - n_eff, N) analytically: one thread per block.
-        for (int g = tid; g < nb; g += blockDim.x) {
-            const int64_t b0 = static_cast<int64_t>(g) * G;
-            const int size = min(G, N - g * G);
-            int kept = size;
-            if (!blk[g]) {
-                const int64_t b1 = b0 + size;
-                const int64_t sink_end = b1 < A ? b1 : A;
-                const int64_t win_beg = b0 > win0 ? b0 : win0;
-                const int64_t sink = sink_end > b0 ? sink_end - b0 : 0;
-                const int64_t win = b1 > win_beg ? b1 - win_beg : 0;
-                const int64_t both = sink_end > win_beg ? sink_end - win_beg : 0;
-                kept = static_cast<int>(sink + win - both);
-            }
-            retained += kept;
-            // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g|.
-            covered += static_cast<double>(sc[g]) * (static_cast<double>(kept) / static_cast<double>(size));
-        }
-        // Token bytes, 16 per thread per store where the destination is 16-byte aligned.
-        uint8_t* kp = p.keep + seg0;
-        const int head = min(N, static_cast<int>((16 - (reinterpret_cast<uintptr_t>(kp) & 15)) & 15));
-        auto kbyte = [&](int i) -> uint32_t {
-            return (blk[i / G] != 0 || i < A || i >= win0) ? 1u : 0u;
-        };
-        for (int i = tid; i < head; i += blockDim.x) kp[i] = static_cast<uint8_t>(kbyte(i));
-        const int nchunk = (N - head) >> 4;
-        for (int c = tid; c < nchunk; c += blockDim.x) {
-            const int i0 = head + c * 16;
-            int g = i0 / G;            // one division per 16 tokens; then walk block edges
-            int edge = (g + 1) * G;
-            uint32_t w[4] = {0u, 0u, 0u, 0u};
+// ---- token expansion (expand_mask, selection.cpp:36-49), grid-wide -------------------
+// keep[i] = block kept | i < A | i >= N - n_eff (segment-relative), minus the veto;
+// pass-through segments keep everything.  16 tokens per thread, one 16-byte store.
+__global__ void __launch_bounds__(256)
+expand_kernel(const SelectParams p, int R) {
+    const int T = p.cu_seqlens[R];
+    const int64_t A = p.sink_count_a;
+    const int G = p.block_size_g;
+    const bool aligned = (reinterpret_cast<uintptr_t>(p.keep) & 15) == 0;
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c * 16 < T;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i0 = static_cast<int>(c * 16);
+        int r = find_segment(p.cu_seqlens, R, i0);
+        int seg0 = p.cu_seqlens[r], seg1 = p.cu_seqlens[r + 1];
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-            for (int x = 0; x < 16; ++x) {
-                const int i = i0 + x;
-                while (i >= edge) { ++g; edge += G; }
-                const uint32_t kb = (blk[g] != 0 || i < A || i >= win0) ? 1u : 0u;
-                w[x >> 2] |= kb << (8 * (x & 3));
+        for (int x = 0; x < 16; ++x) {
+            const int i = i0 + x;
+            if (i >= T) break;
+            while (i >= seg1) { ++r; seg0 = seg1; seg1 = p.cu_seqlens[r + 1]; }
+            uint32_t k = 1;
+            if (p.drop_enabled == nullptr || p.drop_enabled[r]) {
+                const int li = i - seg0;
+                const int N = seg1 - seg0;
+                const int neff = min(p.query_window_n, N);
+                k = (p.blk_keep[p.cu_blocks[r] + li / G] != 0 || li < A || li >= N - neff) ? 1u : 0u;
+                if (k && p.veto != nullptr && p.veto[i]) k = 0;
             }
-            *reinterpret_cast<uint4*>(kp + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+            w[x >> 2] |= k << (8 * (x & 3));
         }
-        for (int i = head + nchunk * 16 + tid; i < N; i += blockDim.x) kp[i] = static_cast<uint8_t>(kbyte(i));
-    } else {
-        // With a veto: warp per block, lanes over its tokens (coalesced bytes).
-        const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-        for (int g = warp; g < nb; g += nwarps) {
-            const int b0 = g * G;
-            const int size = min(G, N - b0);
-            const bool bk = blk[g] != 0;
-            int kept = 0;
-            for (int x = lane; x < size; x += 32) {
-                const int i = b0 + x;
-                bool k = bk || i < A || i >= N - neff;
-                if (k && p.veto != nullptr && p.veto[seg0 + i]) k = false;
-                p.keep[seg0 + i] = k ? 1 : 0;
-                kept += k ? 1 : 0;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
-            if (lane == 0) {
-                retained += kept;
-                // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g|.
-                covered += static_cast<double>(sc[g]) * (static_cast<double>(kept) / static_cast<double>(size));
-            }
+        if (aligned && i0 + 16 <= T) {
+            *reinterpret_cast<uint4*>(p.keep + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+            for (int x = 0; x < 16 && i0 + x < T; ++x) p.keep[i0 + x] = static_cast<uint8_t>(w[x >> 2] >> (8 * (x & 3)));
         }
-    }
-    retained = block_sum<int>(retained, red_i);
-    covered = block_sum<double>(covered, red_d);
-    if (tid == 0) {
-        p.cutoff_rank[r] = kstar;
-        if (p.retained_count) p.retained_count[r] = retained;
-        // Degenerate selections report 1.0 with or without a veto (selection.cpp:104-106,
-        // propagation.cpp:135: restrict_selection also falls back to 1.0 at zero mass).
-        if (p.covered_mass) p.covered_mass[r] = degenerate ? 1.0 : covered / total;
-        if (p.degenerate) p.degenerate[r] = degenerate ? 1 : 0;
     }
 }
 
@@ -319,14 +479,26 @@ size_t select_smem_bytes(int max_blocks_per_request) {
     return static_cast<size_t>(P2) * 8 + static_cast<size_t>(max_blocks_per_request) * 5 + 16;
 }
 
-cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request,
+cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request, int num_sms,
                           cudaStream_t stream) {
-    const int cap = max_blocks_per_request < kMaxSortBlocks ? max_blocks_per_request : kMaxSortBlocks;
-    const size_t smem = select_smem_bytes(cap < 1 ? 1 : cap);
-    cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    select_kernel<<<R, kSelThreads, smem, stream>>>(p);
+    cudaError_t e;
+    if (max_blocks_per_request <= 512) {
+        select_radix_kernel<128, 4><<<R, 128, 0, stream>>>(p);
+    } else if (max_blocks_per_request <= 2048) {
+        select_radix_kernel<512, 4><<<R, 512, 0, stream>>>(p);
+    } else {
+        const int cap = max_blocks_per_request < kMaxSortBlocks ? max_blocks_per_request : kMaxSortBlocks;
+        const size_t smem = select_smem_bytes(cap);
+        e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        select_kernel<<<R, kSelThreads, smem, stream>>>(p);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int64_t chunks = (p.max_tokens + 15) / 16;
+    int64_t grid = (chunks + 255) / 256;
+    if (grid > num_sms * 8) grid = num_sms * 8;
+    if (grid < 1) grid = 1;
+    expand_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(p, R);
     return cudaGetLastError();
 }
 
