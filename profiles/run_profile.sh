@@ -1,8 +1,8 @@
 #!/usr/bin/env bash
 # Profiling recipe (run on the GPU box from the repo root, one GPU):
 #   1. launch list with per-launch device time (cold-cache, serialised: compare SHARES)
-#   2. one `ncu --set full` capture of each hot kernel (score_tc_kernel, compact_scatter_kernel,
-#      select_kernel), imported here with `ncu -i ... --page raw --csv`.
+#   2. one `ncu --set full` capture of each hot kernel (score_tc4_kernel, compact_copy_kernel,
+#      select_radix_kernel, block_combine_kernel, expand_kernel), imported here with `ncu -i ... --page raw --csv`.
 # Outputs go to gpurun_out/ (scratch); summaries are copied into profiles/ by hand.
 set -euo pipefail
 OUT=${OUT:-gpurun_out}
@@ -13,5 +13,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 520 --csv \
     --log-file "$OUT/launches.csv" $BENCH > "$OUT/launches_bench.log" 2>&1 || true
 
 ncu --set full --clock-control none --import-source on \
-    -k regex:'score_tc_kernel|compact_scatter_kernel|select_kernel|block_combine_kernel' -s 7 -c 4 \
+    -k regex:'score_tc|compact_copy|select_radix|block_combine|expand_kernel' -s 7 -c 5 \
     -o "$OUT/prof_full" -f $BENCH > "$OUT/prof_full.log" 2>&1 || true
