@@ -35,15 +35,38 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+SPEC = dict(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99)
 CONFIGS = {
-    # name: (model, lengths, layers, cfg)
-    "c1": ("llama3.1-8b", [4096], 1, dict(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99)),
-    "c2": ("llama3.1-8b", [32768] * 4, 32, dict(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99)),
+    # name: (model shape, request lengths, drop layers per step, ScoreConfig, mode)
+    #   mode "dp": request sharding (each rank its own batch: c1/c2 per rank, c5 LPT split)
+    #   mode "tp": head sharding of one batch over the TP group (c3)
+    "c1": ("llama3.1-8b", [4096], 1, SPEC, "dp"),
+    "c2": ("llama3.1-8b", [32768] * 4, 32, SPEC, "dp"),
+    # Qwen3-Next-80B-A3B: 48 layers, 3:1 linear/full -> 12 full-attention drop layers
+    "c3": ("qwen3-next-80b-a3b", [131072], 12, SPEC, "tp"),
+    # Gemma-3-12B: 48 layers, 5:1 sliding-window/full -> 8 full-attention drop layers, p=0.98
+    "c4": ("gemma3-12b", [65536] * 16, 8, dict(SPEC, top_p=0.98), "dp"),
+    # 64-request stream, N_r log-uniform in [4K, 128K] (seed 5), LPT-sharded over the ranks
+    "c5": ("llama3.1-8b", "loguniform:64:4096:131072:5", 32, SPEC, "dp-split"),
 }
 WORKLOAD_NAME = {
     "c1": "llama3.1-8b layer shape, 1x4096 tokens, 1 drop layer, score+select+compact",
     "c2": "llama3.1-8b layer shape, varlen 4x32768 tokens, 32 full-attn drop layers, score+select+compact",
+    "c3": "qwen3-next-80b-a3b full-attn layer shape, 1x131072 tokens, 12 drop layers, TP=8 head-sharded "
+          "scoring + ordered shard reduce, select, compact",
+    "c4": "gemma3-12b layer shape, varlen 16x65536 tokens, 8 full-attn drop layers (p=0.98), "
+          "score+select+compact",
+    "c5": "llama3.1-8b layer shape, 64-request varlen stream (4K-128K log-uniform), 32 drop layers, "
+          "LPT request-sharded, score+select+compact",
 }
+
+
+def config_lengths(spec):
+    if isinstance(spec, str):
+        _, count, lo, hi, seed = spec.split(":")
+        from paper_2605_06221_b200.synthetic import loguniform_lengths
+        return loguniform_lengths(int(count), int(lo), int(hi), int(seed))
+    return list(spec)
 
 
 def parse():
@@ -136,13 +159,18 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes from the committed ncu --set full summary, if present."""
+def ncu_traffic(prefix):
+    """Per-launch DRAM bytes (read + write) of the first kernel whose name starts with
+    `prefix`, from the committed ncu --set full capture (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f)
-    return {}
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    for name, v in d.items():
+        if name.startswith(prefix):
+            return v
+    return None
 
 
 # --------------------------------------------------------------------------- CPU reference
@@ -197,7 +225,7 @@ class CpuReferenceSample:
 
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
-    model, lengths, layers, cfg = CONFIGS[args.config]
+    model, _, layers, cfg, _ = CONFIGS[args.config]
     if rank != 0:
         return
     sample = CpuReferenceSample(model, cfg, args.regime)
@@ -221,12 +249,112 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
+class LayerRunner:
+    """One drop layer (score -> [shard reduce] -> select -> compact) of the configured
+    workload on this rank, through the public API (paper_2605_06221_b200.api)."""
+
+    def __init__(self, up, torch, mode, shp, lengths, cfg, dev, world, rank):
+        from paper_2605_06221_b200.distributed import head_slice
+
+        self.up, self.torch, self.mode, self.cfg, self.dev = up, torch, mode, cfg, dev
+        Hq, Hkv, D, HID = shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"], shp["hidden"]
+        self.T, self.R = sum(lengths), len(lengths)
+        G = cfg.block_size_g
+        self.nb = sum((n + G - 1) // G for n in lengths)
+        self.world, self.rank = world, rank
+        self.launches = 0
+        if mode == "tp":
+            # TP=8 head sharding (Eq. 15): at N=1 the eight shards are scored one after the
+            # other on this GPU and summed by the ordered shard reduce; at N>1 every rank
+            # scores its own head slice and the partials are all-reduced across ranks.
+            self.tp = 8 if world == 1 else world
+            slices = [head_slice(Hq, Hkv, t, self.tp) for t in range(self.tp)]
+            self.shards = slices if world == 1 else [slices[rank]]
+        else:
+            self.tp, self.shards = 1, [((0, Hq), (0, Hkv))]
+        # planes compacted per layer: hidden, K, V of the local kv-heads, positions
+        kb = min(sh[1][0] for sh in self.shards)
+        ke = max(sh[1][1] for sh in self.shards)
+        self.kv_range = (kb, ke)
+        self.Hkv_local = ke - kb
+        # At N>1 (tp) the activation tensors hold only this rank's heads (localize()).
+        self.local = mode == "tp" and world > 1
+        self.heads = []
+        for (qb, qe), (skb, ske) in self.shards:
+            qi = (0, qe - qb) if self.local else (qb, qe)
+            ki = (0, ske - skb) if self.local else (skb, ske)
+            self.heads.append((qi, ki,
+                               up.HeadLayout(qe - qb, ske - skb, D, gqa_group=Hq // Hkv, q_head_offset=qb,
+                                             kv_head_offset=skb)))
+        self.flops = sum(2 * min(cfg.query_window_n, N) * N * D * (qe - qb)
+                         for N in lengths for (qb, qe), _ in self.shards)
+        self.row_bytes = HID * 2 + 2 * self.Hkv_local * D * 2 + 8
+        plane_shapes = [(HID,), (self.Hkv_local, D), (self.Hkv_local, D), ()]
+        plane_dtypes = [torch.bfloat16, torch.bfloat16, torch.bfloat16, torch.int64]
+        self.layer = up.DropLayer(cfg, up.HeadLayout(Hq, Hkv, D), self.T, self.R, plane_shapes, plane_dtypes,
+                                  device=dev)
+        self.partials = [torch.empty(self.layer.scores.block_scores.numel(), dtype=torch.float32, device=dev)
+                         for _ in range(len(self.shards) if mode == "tp" and world == 1 else 0)]
+
+    def localize(self, sb):
+        """TP rank at N>1: keep only this rank's q-heads and kv-heads (what a rank holds)."""
+        if self.local:
+            (qb, qe), (kb, ke) = self.shards[0]
+            sb.q = sb.q[:, qb:qe].contiguous()
+            sb.k = sb.k[:, kb:ke].contiguous()
+            sb.v = sb.v[:, kb:ke].contiguous()
+        return sb
+
+    def planes(self, sb):
+        if self.local:
+            return [sb.hidden, sb.k, sb.v, sb.positions]
+        kb, ke = self.kv_range
+        return [sb.hidden, sb.k[:, kb:ke], sb.v[:, kb:ke], sb.positions]
+
+    def score(self, sb, cu):
+        up, L = self.up, self.layer
+        if self.mode != "tp":
+            up.score_blocks_varlen(sb.q, sb.k, cu, self.cfg, L.heads, max_tokens=self.T, workspace=L.ws,
+                                   out=L.scores)
+            return up.lib.up_last_launch_count()
+        n = 0
+        if self.world == 1:
+            for ((qb, qe), (kb, ke), h), part in zip(self.heads, self.partials):
+                up.score_blocks_varlen(sb.q[:, qb:qe], sb.k[:, kb:ke], cu, self.cfg, h, max_tokens=self.T,
+                                       workspace=L.ws, out=up.BlockScores(part, L.scores.cu_blocks))
+                n += up.lib.up_last_launch_count()
+            up.reduce_block_scores([p_[:self.nb] for p_ in self.partials], out=L.scores.block_scores[:self.nb])
+            return n + up.lib.up_last_launch_count()
+        from paper_2605_06221_b200.distributed import allreduce_block_scores
+        (qb, qe), (kb, ke), h = self.heads[0]
+        up.score_blocks_varlen(sb.q[:, qb:qe], sb.k[:, kb:ke], cu, self.cfg, h, max_tokens=self.T,
+                               workspace=L.ws, out=L.scores)
+        n = up.lib.up_last_launch_count()
+        allreduce_block_scores(L.scores.block_scores[:self.nb], deterministic=True)
+        return n + up.lib.up_last_launch_count()
+
+    def select(self, cu):
+        L = self.layer
+        self.up.select_varlen(L.scores.block_scores, L.scores.cu_blocks, cu, self.cfg, max_tokens=self.T,
+                              workspace=L.ws, out=L.sel)
+        return self.up.lib.up_last_launch_count()
+
+    def compact(self, sb, cu):
+        L = self.layer
+        self.up.compact_varlen(L.sel.keep, cu, self.planes(sb), max_tokens=self.T, workspace=L.ws,
+                               result=L.out)
+        return self.up.lib.up_last_launch_count()
+
+    def __call__(self, sb, cu):
+        self.launches = self.score(sb, cu) + self.select(cu) + self.compact(sb, cu)
+
+
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2605_06221_b200 as up
+    from paper_2605_06221_b200.distributed import lpt_partition
     from paper_2605_06221_b200.synthetic import MODEL_SHAPES, make_batch
 
     ws, rank, local = dist_env()
@@ -235,42 +363,46 @@ def run_ours(args):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    model, lengths, layers, cfgd = CONFIGS[args.config]
+    model, lspec, layers, cfgd, mode = CONFIGS[args.config]
     shp = MODEL_SHAPES[model]
     Hq, Hkv, D, HID = shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"], shp["hidden"]
     cfg = up.ScoreConfig(**cfgd)
-    R = len(lengths)
-    T = sum(lengths)
+    all_lengths = config_lengths(lspec)
+    if mode == "dp-split":   # a fixed request stream split across the ranks (LPT on N_r)
+        lengths = [all_lengths[i] for i in lpt_partition(all_lengths, ws)[rank]]
+        job_tokens, scaling = sum(all_lengths), "strong"
+    elif mode == "tp":       # one batch, heads split across the ranks
+        lengths = all_lengths
+        job_tokens, scaling = sum(all_lengths), "strong"
+        if ws > 1 and Hq % ws:
+            raise SystemExit(f"--config {args.config}: {Hq} q-heads do not split over {ws} ranks")
+    else:                    # every rank runs its own batch
+        lengths = all_lengths
+        job_tokens, scaling = ws * sum(all_lengths), "weak"
+    R, T = len(lengths), sum(lengths)
     n = cfg.query_window_n
+    runner = LayerRunner(up, torch, mode, shp, lengths, cfg, dev, ws, rank)
 
     # ---- activations: one set per layer (or --layer-sets distinct sets, cycled) ----
     free, _ = torch.cuda.mem_get_info(dev)
     per_set = T * (Hq * D + 2 * Hkv * D + HID) * 2 + T * 8
     n_sets = args.layer_sets or layers
-    n_sets = max(1, min(n_sets, int((free * 0.8 - 3 * per_set) // per_set)))
-    sets = []
-    for s in range(n_sets):
-        sb = make_batch(lengths, Hq, Hkv, D, HID, regime=args.regime, seed=1000 * rank + s, device=dev)
-        sets.append(sb)
+    n_sets = max(1, min(n_sets, int((free * 0.7 - 3 * per_set) // per_set)))
+    sets = [runner.localize(make_batch(lengths, Hq, Hkv, D, HID, regime=args.regime,
+                                       seed=1000 * (rank if mode != "tp" else 0) + s, device=dev))
+            for s in range(n_sets)]
+    torch.cuda.empty_cache()
     cu = sets[0].cu_seqlens
-    heads = up.HeadLayout(Hq, Hkv, D)
-    plane_shapes = [(HID,), (Hkv, D), (Hkv, D), ()]
-    plane_dtypes = [torch.bfloat16, torch.bfloat16, torch.bfloat16, torch.int64]
-    layer = up.DropLayer(cfg, heads, T, R, plane_shapes, plane_dtypes, device=dev)
-
-    def one_layer(sb):
-        return layer(sb.q, sb.k, cu, [sb.hidden, sb.k, sb.v, sb.positions])
 
     def step():
         for l in range(layers):
-            one_layer(sets[l % n_sets])
+            runner(sets[l % n_sets], cu)
 
     # correctness guard on the first layer (device status), then warm-up
-    one_layer(sets[0])
-    layer.check()
-    launches_per_layer = layer.last_launches
-    use_graph = not args.no_graph
-    graph = None
+    runner(sets[0], cu)
+    runner.layer.check()
+    launches_per_layer = runner.launches
+    use_graph = not args.no_graph and not (mode == "tp" and ws > 1)
     stream = torch.cuda.Stream(device=dev)
     if use_graph:
         with torch.cuda.stream(stream):
@@ -287,7 +419,7 @@ def run_ours(args):
         for _ in range(args.warmup):
             run_step()
     torch.cuda.synchronize(dev)
-    layer.check()
+    runner.layer.check()
 
     # ---- timed region (device-resident inputs) ----
     if ws > 1:
@@ -311,84 +443,79 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    tokens_per_step = layers * T
     ms_per_step = ms / args.steps
-    value = ws * tokens_per_step / (ms_per_step / 1e3)
+    value = job_tokens * layers / (ms_per_step / 1e3)
+    rho = float(runner.layer.out.num_out.item()) / T
 
-    # retained fraction (planted regime) from the last layer
-    rho = float(layer.out.num_out.item()) / T
-
-    # ---- per-stage timing (events around each stage, same stream) ----
-    stages = {}
+    # ---- per-stage timing: each stage over all layers captured in its own CUDA graph
+    # (device time only, no host launch gaps), replayed between events on the stream ----
+    stage_info, roofline = {}, None
     if args.profile_stages:
         names = ["score", "select", "compact"]
-        evs = {nm: [] for nm in names}
-        with torch.cuda.stream(stream):
-            for l in range(layers):
-                sb = sets[l % n_sets]
-                e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-                e[0].record(stream)
-                up.score_blocks_varlen(sb.q, sb.k, cu, cfg, heads, max_tokens=T, workspace=layer.ws,
-                                       out=layer.scores)
-                e[1].record(stream)
-                up.select_varlen(layer.scores.block_scores, layer.scores.cu_blocks, cu, cfg, max_tokens=T,
-                                 workspace=layer.ws, out=layer.sel)
-                e[2].record(stream)
-                up.compact_varlen(layer.sel.keep, cu, [sb.hidden, sb.k, sb.v, sb.positions], max_tokens=T,
-                                  workspace=layer.ws, result=layer.out)
-                e[3].record(stream)
-                evs["score"].append((e[0], e[1]))
-                evs["select"].append((e[1], e[2]))
-                evs["compact"].append((e[2], e[3]))
-        torch.cuda.synchronize(dev)
+        fns = {"score": lambda sb: runner.score(sb, cu), "select": lambda sb: runner.select(cu),
+               "compact": lambda sb: runner.compact(sb, cu)}
+        stages = {}
         for nm in names:
-            stages[nm] = sum(a.elapsed_time(b) for a, b in evs[nm]) / layers
-        retained = int(layer.out.num_out.item())
+            def stage_pass(nm=nm):
+                for l in range(layers):
+                    fns[nm](sets[l % n_sets])
+            with torch.cuda.stream(stream):
+                stage_pass()
+            torch.cuda.synchronize(dev)
+            if use_graph:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    stage_pass()
+                run = g.replay
+            else:
+                run = stage_pass
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                run()
+                e0.record(stream)
+                run()
+                e1.record(stream)
+            torch.cuda.synchronize(dev)
+            stages[nm] = e0.elapsed_time(e1) / layers
+            del run
+        retained = int(runner.layer.out.num_out.item())
         hbm_peak, tf_peak, peak_kind = measured_peaks()
-        flops = sum(2 * min(n, N) * N * D * Hq for N in lengths)
-        row_bytes = HID * 2 + 2 * Hkv * D * 2 + 8
-        comp_bytes = T * 1 + (R + 1) * 4 * 2 + retained * (2 * row_bytes + 4)
-        traffic = ncu_traffic()
-        score_ach = flops / (stages["score"] / 1e3) / 1e12
+
+        def prof_traffic(prefix):  # the committed ncu capture is of the c2 workload
+            return ncu_traffic(prefix) if args.config == "c2" else None
+
+        comp_bytes = T * 1 + (R + 1) * 4 * 2 + retained * (2 * runner.row_bytes + 4)
+        score_ach = runner.flops / (stages["score"] / 1e3) / 1e12
         comp_ach = comp_bytes / (stages["compact"] / 1e3) / 1e9
         stage_info = {
             "score": {"bound": "tensor", "achieved": score_ach, "peak": tf_peak, "unit": "TFLOP/s",
                       "frac": score_ach / tf_peak, "ms_per_layer": stages["score"],
-                      "algorithmic_flops_per_layer": flops,
-                      "traffic": traffic.get("score_tc_kernel")},
+                      "algorithmic_flops_per_layer": runner.flops,
+                      "traffic": prof_traffic("score_tc4" if D <= 128 and Hq // Hkv >= 4 else "score_tc_kernel")},
             "select": {"bound": "latency", "us_per_event": stages["select"] * 1e3, "requests": R},
             "compact": {"bound": "hbm", "achieved": comp_ach, "peak": hbm_peak, "unit": "GB/s",
                         "frac": comp_ach / hbm_peak, "ms_per_layer": stages["compact"],
                         "algorithmic_bytes_per_layer": comp_bytes,
-                        "traffic": traffic.get("compact_scatter_kernel")},
+                        "traffic": prof_traffic("compact_copy")},
         }
         dominant = "score" if stages["score"] >= stages["compact"] else "compact"
         d = stage_info[dominant]
         roofline = {"kernel": dominant, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                     "unit": d["unit"], "frac": d["frac"], "traffic": d["traffic"],
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json burst)"}
-    else:
-        stage_info, roofline = {}, None
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if args.e2e_steps > 0:
         src = sets[0]
-        tails = []
         cu_h = cu.cpu().tolist()
-        for r in range(R):
-            s, e_ = cu_h[r], cu_h[r + 1]
-            tails.append((max(s, e_ - n), e_))
+        tails = [(max(cu_h[r], cu_h[r + 1] - n), cu_h[r + 1]) for r in range(R)]
         h_qt = [src.q[a:b].cpu().pin_memory() for a, b in tails]
-        h_k = src.k.cpu().pin_memory()
-        h_v = src.v.cpu().pin_memory()
-        h_hid = src.hidden.cpu().pin_memory()
-        h_pos = src.positions.cpu().pin_memory()
-        h_cu = cu.cpu().pin_memory()
-        d_q = torch.empty_like(src.q)
-        d_k, d_v, d_hid, d_pos, d_cu = (torch.empty_like(src.k), torch.empty_like(src.v),
-                                        torch.empty_like(src.hidden), torch.empty_like(src.positions),
-                                        torch.empty_like(cu))
+        h_k, h_v, h_hid, h_pos, h_cu = (x.cpu().pin_memory() for x in
+                                        (src.k, src.v, src.hidden, src.positions, cu))
+        d_in = type(src)(torch.empty_like(src.q), torch.empty_like(src.k), torch.empty_like(src.v),
+                         torch.empty_like(src.hidden), torch.empty_like(src.positions), torch.empty_like(cu),
+                         src.lengths)
         o_keep = torch.empty(T, dtype=torch.uint8).pin_memory()
         o_cu = torch.empty(R + 1, dtype=torch.int32).pin_memory()
         o_cut = torch.empty(R, dtype=torch.int64).pin_memory()
@@ -399,16 +526,14 @@ def run_ours(args):
         def e2e_step():
             for l in range(layers):
                 for (a, b), t in zip(tails, h_qt):
-                    d_q[a:b].copy_(t, non_blocking=True)
-                d_k.copy_(h_k, non_blocking=True)
-                d_v.copy_(h_v, non_blocking=True)
-                d_hid.copy_(h_hid, non_blocking=True)
-                d_pos.copy_(h_pos, non_blocking=True)
-                d_cu.copy_(h_cu, non_blocking=True)
-                out = layer(d_q, d_k, d_cu, [d_hid, d_k, d_v, d_pos])
-                o_keep.copy_(layer.sel.keep, non_blocking=True)
-                o_cu.copy_(out.cu_seqlens, non_blocking=True)
-                o_cut.copy_(layer.sel.cutoff_rank, non_blocking=True)
+                    d_in.q[a:b].copy_(t, non_blocking=True)
+                for d_, h_ in ((d_in.k, h_k), (d_in.v, h_v), (d_in.hidden, h_hid), (d_in.positions, h_pos),
+                               (d_in.cu_seqlens, h_cu)):
+                    d_.copy_(h_, non_blocking=True)
+                runner(d_in, d_in.cu_seqlens)
+                o_keep.copy_(runner.layer.sel.keep, non_blocking=True)
+                o_cu.copy_(runner.layer.out.cu_seqlens, non_blocking=True)
+                o_cut.copy_(runner.layer.sel.cutoff_rank, non_blocking=True)
 
         with torch.cuda.stream(stream):
             e2e_step()
@@ -427,7 +552,7 @@ def run_ours(args):
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": ws * tokens_per_step / (ems / args.e2e_steps / 1e3), "unit": "tokens/s",
+        e2e = {"value": job_tokens * layers / (ems / args.e2e_steps / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d * layers, "d2h_bytes_per_step": d2h * layers,
                "steps": args.e2e_steps,
                "note": "per layer: H2D of q tail rows, K, V, hidden, positions, cu_seqlens from pinned "
@@ -445,16 +570,23 @@ def run_ours(args):
             cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": None, "sample": f"failed: {exc}"}
 
     if rank == 0:
+        if mode == "tp":
+            par = f"tp{runner.tp} head-sharded" + (" (emulated on 1 GPU: shards scored in turn)" if ws == 1 else "")
+        elif mode == "dp-split":
+            par = f"LPT request-sharded over {ws} GPU(s)"
+        else:
+            par = f"request-sharded dp{ws}"
         line = {
             "metric": "score+drop+compact tokens/s", "value": value, "unit": "tokens/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
             "config": {"workload": WORKLOAD_NAME[args.config], "model_shape": model, "requests": R,
                        "tokens_per_request": lengths[0] if len(set(lengths)) == 1 else lengths,
-                       "drop_layers": layers, "regime": args.regime, "retention_rho": rho,
-                       "activation_sets": n_sets, "l2": "inputs larger than L2 (distinct per-layer sets)",
-                       "cuda_graph": use_graph, "parallelism": f"request-sharded dp{ws}", **cfgd},
+                       "tokens_per_rank": T, "drop_layers": layers, "regime": args.regime,
+                       "retention_rho": rho, "activation_sets": n_sets,
+                       "l2": "inputs larger than L2 (distinct per-layer sets, each >> 126 MB)",
+                       "cuda_graph": use_graph, "parallelism": par, **cfgd},
             "roofline": roofline, "stages": stage_info, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk, "gpu_launches": launches_per_layer * layers * args.steps,
         }

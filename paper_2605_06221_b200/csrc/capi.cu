@@ -26,7 +26,9 @@ cudaError_t launch_score_tc4(int D, const CUtensorMap& qm, const CUtensorMap& km
 cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int G, int32_t* cu_blocks,
                                uint32_t* err, cudaStream_t stream);
 struct BlockCombineParams;
+struct PairWeightsParams;
 cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int num_sms,
                               cudaStream_t stream);
 cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request, int num_sms,
@@ -82,7 +84,7 @@ unsigned long long* select_debug_buffer() {
 
 // ---- workspace layout --------------------------------------------------------------
 struct Layout {
-    size_t err, cu_units, pair_counters, unit_sid, P, stat_m, stat_l, stat_w, simt_m, simt_l,
+    size_t err, cu_units, unit_sid, P, stat_m, stat_l, stat_w, simt_m, simt_l,
         simt_tok, tile_counts, ret_idx, blk_keep, total;
     int64_t max_blocks, max_units;
     int32_t simt_n;
@@ -110,7 +112,6 @@ Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c
     };
     L.err = take(256);
     L.cu_units = take(sizeof(int32_t) * (R + 1));
-    L.pair_counters = take(sizeof(int32_t) * R * (H > 0 ? H : 1));
     L.unit_sid = take(sizeof(int32_t) * L.max_units);
     L.P = take(sizeof(float) * H * L.max_blocks * kRows);
     L.stat_m = take(sizeof(float) * L.max_units * kRows);
@@ -286,7 +287,6 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
         p.cu_blocks = cu_blocks;
         p.cu_units_out = at<int32_t>(ws, L.cu_units);
         p.unit_sid = at<int32_t>(ws, L.unit_sid);
-        p.pair_counters = at<int32_t>(ws, L.pair_counters);
         p.err = err;
         p.P = at<float>(ws, L.P);
         p.stat_m = at<float>(ws, L.stat_m);
@@ -319,6 +319,21 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
                             ? launch_score_tc4(D, qm, km, p, grid, stream)
                             : launch_score_tc(D, hpc, qm, km, p, grid, stream);
         if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
+        PairWeightsParams wp{};
+        wp.cu_seqlens = b->cu_seqlens;
+        wp.cu_units = p.cu_units_out;
+        wp.stat_m = p.stat_m;
+        wp.stat_l = p.stat_l;
+        wp.stat_w = p.stat_w;
+        wp.err = err;
+        wp.num_requests = R;
+        wp.num_hgroups = nhg;
+        wp.hpc = hpc;
+        wp.score_grid = grid;
+        wp.query_window_n = c->query_window_n;
+        const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
+        const int wgrid = static_cast<int>(wtasks < num_sms() * 8 ? wtasks : num_sms() * 8);
+        if ((e = launch_pair_weights(wp, wgrid, stream)) != cudaSuccess) return UP_ERR_CUDA;
         BlockCombineParams bp{};
         bp.cu_seqlens = b->cu_seqlens;
         bp.cu_blocks = cu_blocks;
@@ -334,7 +349,7 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
         bp.block_size_g = G;
         bp.unit_keys = p.unit_keys;
         if ((e = launch_block_combine(bp, num_sms() * 8, stream)) != cudaSuccess) return UP_ERR_CUDA;
-        g_launches = 2;
+        g_launches = 3;
         return UP_OK;
     }
 

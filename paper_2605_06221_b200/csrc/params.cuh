@@ -13,7 +13,6 @@ struct ScoreTcParams {
     int32_t* cu_blocks;       // out [R+1] (written by CTA 0)
     int32_t* cu_units_out;    // out [R+1] (written by CTA 0, read by the combine)
     int32_t* unit_sid;        // out [total units]: item id (stats row) of every unit
-    int32_t* pair_counters;   // [R * num_hgroups], zero between launches (self-cleaning)
     uint32_t* err;
     float* P;                 // [Hq][max_blocks][128]
     float* stat_m;            // [units * HPC][128]
@@ -31,6 +30,20 @@ struct ScoreTcParams {
     int32_t gqa_group;
     float scale_log2;         // log2(e) / sqrt(D)
     unsigned long long* dbg;  // optional per-CTA timing [grid][4] (UP_SCORE_DEBUG), else null
+};
+
+struct PairWeightsParams {
+    const int32_t* cu_seqlens;
+    const int32_t* cu_units;  // [R+1] from the scorer
+    const float* stat_m;
+    const float* stat_l;
+    float* stat_w;
+    uint32_t* err;
+    int32_t num_requests;
+    int32_t num_hgroups;
+    int32_t hpc;
+    int32_t score_grid;       // the scorer's gridDim.x (defines the item ranges)
+    int32_t query_window_n;
 };
 
 struct BlockCombineParams {

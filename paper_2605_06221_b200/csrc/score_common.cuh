@@ -6,7 +6,6 @@
 
 namespace up {
 
-constexpr int kMaxPairItems = 256;  // item starts of one (request, head-group) pair kept in smem
 
 // ---------------------------------------------------------------- partition
 struct Part {
@@ -56,22 +55,24 @@ __device__ __forceinline__ Item make_item(const Part& P, int64_t pos, int64_t en
     return it;
 }
 
+// Of the 16 element pairs of a 32-column group, NP evaluate 2^x with the FMA-pipe
+// polynomial (exp2_poly2) instead of MUFU.EX2.  Measured on B200 (4x32K LLaMA layer):
+// the four-warpgroup scorer gains ~5% at NP = 3..4 (score_tc4.cu, kTc4PolyPairs); the
+// two-warpgroup kernel is latency- rather than MUFU-limited and uses NP = 0.
 #ifndef UP_POLY_PAIRS
 #define UP_POLY_PAIRS 0
 #endif
-// Of the 16 element pairs of a 32-column group, this many evaluate 2^x with the FMA-pipe
-// polynomial (exp2_poly2) instead of MUFU.EX2 (0 measured fastest on B200: the epilogue
-// is issue/latency-limited, not MUFU-limited, at two epilogue warps per SMSP).
 constexpr int kPolyPairs = UP_POLY_PAIRS;
 
 // Σ_k 2^(v_k * sc - m) over 32 TMEM values: packed FFMA2 for the exponent argument, MUFU
-// ex2 (or the FMA-pipe polynomial for the last kPolyPairs pairs), two FADD2 chains.
+// ex2 (or the FMA-pipe polynomial for the last NP pairs), two FADD2 chains.
+template <int NP = kPolyPairs>
 __device__ __forceinline__ float group_sum_pk(const uint32_t* v, uint64_t sc2, uint64_t m2) {
     uint64_t a0 = 0, a1 = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         const uint64_t x = fma2(static_cast<uint64_t>(v[2 * i]) | (static_cast<uint64_t>(v[2 * i + 1]) << 32), sc2, m2);
-        const uint64_t e = i < 16 - kPolyPairs ? pk(ex2_approx(lo_f(x)), ex2_approx(hi_f(x))) : exp2_poly2(x);
+        const uint64_t e = i < 16 - NP ? pk(ex2_approx(lo_f(x)), ex2_approx(hi_f(x))) : exp2_poly2(x);
         if (i & 1) a1 = add2(a1, e); else a0 = add2(a0, e);
     }
     const uint64_t a = add2(a0, a1);

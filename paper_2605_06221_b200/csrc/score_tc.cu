@@ -43,10 +43,9 @@ struct TcCfg {
     static constexpr int NBAR = 2 + 2 * KST + 2 * NREG;
     static constexpr int FIXED = Q_BYTES + KST * K_STAGE + NBAR * 8 + 64 + 1024;
     static constexpr int THREADS = 320;
-    static int smem(int R) { return FIXED + 5 * NSLOT * 256 * 4 + 2 * (R + 1) * 4 + kMaxPairItems * 4; }
+    static int smem(int R) { return FIXED + 5 * NSLOT * 256 * 4 + 2 * (R + 1) * 4; }
 };
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 template <int D, int HPC>
 __global__ void __launch_bounds__(320, 1)
@@ -69,7 +68,6 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
     float* s_state = reinterpret_cast<float*>(misc + 16);  // [5][NSLOT][256] epilogue state
     int32_t* s_cu_units = reinterpret_cast<int32_t*>(s_state + 5 * C::NSLOT * 256);
     int32_t* s_cu_blocks = s_cu_units + (p.num_requests + 1);
-    int32_t* s_items = s_cu_blocks + (p.num_requests + 1);  // [kMaxPairItems]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -364,58 +362,6 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
             }
             for (int u = it.u0 + etid; u < it.u1; u += 256) p.unit_sid[it.seg_start + u] = static_cast<int32_t>(it.sid);
 
-            // The last CTA to finish an item of this (request, head-group) pair turns the
-            // pair's item statistics into row weights.
-            const int64_t seg_end = it.seg_start + it.units_r;
-            epi_bar();
-            if (etid == 0) {
-                // Item starts of this pair (contiguous ranges of consecutive CTAs).
-                int n_items = 0;
-                for (int64_t s = it.seg_start; s < seg_end; ++n_items) {
-                    if (n_items < kMaxPairItems) s_items[n_items] = static_cast<int32_t>(s);
-                    const int64_t e = range_begin(P, cta_of(P, s) + 1);
-                    s = e < seg_end ? e : seg_end;
-                }
-                int32_t* ctr = p.pair_counters + it.r * P.nhg + it.hg;
-                __threadfence();
-                const int old = atomicAdd(ctr, 1);
-                const bool is_last = old == n_items - 1;
-                if (is_last) *ctr = 0;  // self-cleaning for the next launch
-                misc[2] = is_last ? 1u : 0u;
-                misc[3] = static_cast<uint32_t>(n_items);
-            }
-            epi_bar();
-            if (misc[2]) {
-                __threadfence();
-                const int n_items = static_cast<int>(misc[3]);
-                for (int x = etid; x < HPC * kRows; x += 256) {
-                    const int hh = x / kRows, jj = x - (x / kRows) * kRows;
-                    const bool valid = jj < neff;
-                    auto item_at = [&](int k, int64_t& s) {  // k-th item start of the pair
-                        if (k < kMaxPairItems) { s = s_items[k]; return; }
-                        s = range_begin(P, cta_of(P, s) + 1);  // continue from item k-1
-                    };
-                    float M = -INFINITY;
-                    int64_t s = 0;
-                    for (int k = 0; k < n_items; ++k) {
-                        item_at(k, s);
-                        M = fmaxf(M, __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]));
-                    }
-                    float L = 0.f;
-                    for (int k = 0; k < n_items; ++k) {
-                        item_at(k, s);
-                        const float mc = __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]);
-                        if (mc != -INFINITY) L += __ldcg(&p.stat_l[(s * HPC + hh) * kRows + jj]) * ex2_approx(mc - M);
-                    }
-                    if (valid && !(L > 0.f)) raise_error(p.err, kErrMaskedRow);
-                    const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
-                    for (int k = 0; k < n_items; ++k) {
-                        item_at(k, s);
-                        const float mc = __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]);
-                        p.stat_w[(s * HPC + hh) * kRows + jj] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
-                    }
-                }
-            }
         }
     }
 
@@ -435,6 +381,89 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
         asm volatile("mov.u32 %0, %%smid;" : "=r"(nsm));
         p.dbg[blockIdx.x * 4 + 3] = nsm;
     }
+}
+
+// Row weights of every (request, head-group) pair, from the per-item statistics the
+// scorer wrote: w[item][hh][j] = 2^(m_item - M) / (L n_eff), M = max_items m,
+// L = Σ_items l 2^(m - M) -- the softmax denominator over the full key range
+// (online_softmax_reduce pass 1, importance.cpp:41-58) assembled from the items' partial
+// denominators.  One CTA per (pair, head, 32-row chunk): warp w folds items w, w+8, ...
+// (lane = row, coalesced), the eight partial (M, L) are merged in warp order
+// (deterministic), then the warps write the weights.
+__global__ void __launch_bounds__(256)
+pair_weights_kernel(const PairWeightsParams p) {
+    __shared__ float sM[8][32], sL[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int R = p.num_requests, hpc = p.hpc, nhg = p.num_hgroups;
+    Part P;
+    P.cu_units = p.cu_units;
+    P.R = R;
+    P.nhg = nhg;
+    P.U = static_cast<int64_t>(p.cu_units[R]) * nhg;
+    P.grid = p.score_grid;
+    if (P.U == 0) return;
+    const int64_t tasks = static_cast<int64_t>(R) * nhg * hpc * 4;
+    for (int64_t t = blockIdx.x; t < tasks; t += gridDim.x) {
+        const int chunk = static_cast<int>(t & 3);
+        const int hh = static_cast<int>((t >> 2) % hpc);
+        const int64_t pair = (t >> 2) / hpc;
+        const int r = static_cast<int>(pair / nhg), hg = static_cast<int>(pair - static_cast<int64_t>(r) * nhg);
+        const int units_r = p.cu_units[r + 1] - p.cu_units[r];
+        if (units_r == 0) continue;  // block-uniform
+        const int N = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+        const int neff = min(p.query_window_n, N);
+        const int64_t seg_start = static_cast<int64_t>(p.cu_units[r]) * nhg + static_cast<int64_t>(hg) * units_r;
+        const int64_t seg_end = seg_start + units_r;
+        const int c_first = cta_of(P, seg_start);
+        const int n_items = cta_of(P, seg_end - 1) - c_first + 1;  // CTAs spanned
+        const int j = chunk * 32 + lane;
+        // Item k = the part of the pair in CTA c_first + k; CTAs with empty ranges (more
+        // CTAs than units) hold no item.
+        auto sid_of = [&](int k) -> int64_t {
+            const int64_t b = range_begin(P, c_first + k);
+            if (k > 0 && b == range_begin(P, c_first + k + 1)) return -1;
+            return b > seg_start ? b : seg_start;
+        };
+        float M = -INFINITY, L = 0.f;
+        for (int k = warp; k < n_items; k += 8) {
+            const int64_t sid = sid_of(k);
+            if (sid < 0) continue;
+            const int64_t x = (sid * hpc + hh) * kRows + j;
+            const float mc = __ldcg(&p.stat_m[x]);
+            const float lc = __ldcg(&p.stat_l[x]);
+            if (mc == -INFINITY) continue;
+            if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
+            else L += lc * ex2_approx(mc - M);
+        }
+        sM[warp][lane] = M;
+        sL[warp][lane] = L;
+        __syncthreads();
+        M = -INFINITY;
+        L = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const float mc = sM[w][lane], lc = sL[w][lane];
+            if (mc == -INFINITY) continue;
+            if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
+            else L += lc * ex2_approx(mc - M);
+        }
+        __syncthreads();
+        const bool valid = j < neff;
+        if (valid && !(L > 0.f) && warp == 0) raise_error(p.err, kErrMaskedRow);
+        const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
+        for (int k = warp; k < n_items; k += 8) {
+            const int64_t sid = sid_of(k);
+            if (sid < 0) continue;
+            const int64_t x = (sid * hpc + hh) * kRows + j;
+            const float mc = __ldcg(&p.stat_m[x]);
+            p.stat_w[x] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
+        }
+    }
+}
+
+cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, cudaStream_t stream) {
+    pair_weights_kernel<<<grid, 256, 0, stream>>>(p);
+    return cudaGetLastError();
 }
 
 // Warp per block: b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][hh][j].

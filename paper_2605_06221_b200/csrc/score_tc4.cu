@@ -14,6 +14,20 @@
 
 namespace up {
 
+#ifndef UP_SCORE_DIAG
+#define UP_SCORE_DIAG 0  // dev only: 1 = skip the epilogue math, 2 = skip the MMAs,
+#endif                   // 3 = one K-step MMA per subtile, 5 = 1 without K reloads
+#ifndef UP_TC4_POLY_PAIRS
+#define UP_TC4_POLY_PAIRS 4
+#endif
+constexpr int kTc4PolyPairs = UP_TC4_POLY_PAIRS;
+#ifndef UP_TC4_PREFETCH
+#define UP_TC4_PREFETCH 0
+#endif
+#ifndef UP_TC4_KST
+#define UP_TC4_KST 2
+#endif
+
 template <int D>
 struct Tc4Cfg {
     static constexpr int HPC = 4;
@@ -21,16 +35,15 @@ struct Tc4Cfg {
     static constexpr int SUB = 128 * 128;
     static constexpr int Q_BYTES = HPC * KC * SUB;
     static constexpr int K_STAGE = KC * SUB;
-    static constexpr int KST = 2;
+    static constexpr int KST = UP_TC4_KST;
     static constexpr int SUBN = 64;                // keys per MMA / TMEM region width
     static constexpr int NREG = HPC * 2;           // (head, buffer) regions
     static constexpr int NBAR = 2 + 2 * KST + 2 * NREG;
     static constexpr int THREADS = 64 + 512;
     static constexpr int FIXED = Q_BYTES + KST * K_STAGE + NBAR * 8 + 64 + 1024;
-    static int smem(int R) { return FIXED + 2 * (R + 1) * 4 + kMaxPairItems * 4; }
+    static int smem(int R) { return FIXED + 2 * (R + 1) * 4; }
 };
 
-__device__ __forceinline__ void epi_bar512() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 
 template <int D>
 __global__ void __launch_bounds__(576, 1)
@@ -53,7 +66,6 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
     uint32_t* misc = reinterpret_cast<uint32_t*>(bars + C::NBAR);  // [0] tmem base, [1] ok, [2] last, [3] n
     int32_t* s_cu_units = reinterpret_cast<int32_t*>(misc + 16);
     int32_t* s_cu_blocks = s_cu_units + (p.num_requests + 1);
-    int32_t* s_items = s_cu_blocks + (p.num_requests + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -159,6 +171,11 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 }
                 for (int t = 0; t < ntiles; ++t) {
                     mbar_wait(&k_empty[stage], phase ^ 1);
+                    if (UP_SCORE_DIAG == 5 && t >= C::KST) {
+                        mbar_arrive(&k_full[stage]);
+                        if (++stage == C::KST) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&k_full[stage], C::K_STAGE);
                     const int krow = seg0 + key0 + t * kTileKeys;
 #pragma unroll
@@ -206,7 +223,8 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                                 const uint64_t a = smem_desc_sw128(sq_addr + hh * C::KC * C::SUB + off);
                                 // rows s*64.. of the K tile: 8 swizzle atoms (8 KB) further
                                 const uint64_t b = smem_desc_sw128(sk_addr + stage * C::K_STAGE + off + s * 8192);
-                                mma_bf16_ss(d_tmem, a, b, kIdesc, kk > 0 ? 1u : 0u);
+                                if (UP_SCORE_DIAG != 2 && (UP_SCORE_DIAG != 3 || kk == 0))
+                                    mma_bf16_ss(d_tmem, a, b, kIdesc, kk > 0 ? 1u : 0u);
                             }
                             mma_commit(&t_full[reg]);
                         }
@@ -237,7 +255,7 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             const int key1 = min(it.u1 * unit_keys, N);
             const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
             const bool row_valid = j < neff;
-            const int qpos = N - neff + j;
+            const int qpos = N - neff + j;  // row j's causal limit (importance.cpp:27)
             const int64_t gb_seg = s_cu_blocks[it.r];
             const int blk0 = key0 / G;
             float* Prow = p.P + (static_cast<int64_t>(it.hg * HPC + w) * p.max_blocks + gb_seg) * kRows + j;
@@ -247,60 +265,92 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
 #pragma unroll 1
             for (int t2 = 0; t2 < 2 * ntiles; ++t2, ++u) {
                 const int cbase = key0 + t2 * C::SUBN;
-                const bool tail = cbase + C::SUBN - 1 > N - neff;  // warp-uniform
                 const uint32_t reg = w * 2 + (u & 1);
                 mbar_wait(&t_full[reg], (u >> 1) & 1);
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + lane_base + reg * C::SUBN;
-#pragma unroll 1
-                for (int q2 = 0; q2 < C::SUBN / 32; ++q2) {
-                    const int c0 = cbase + q2 * 32;
-                    uint32_t v[32];
-                    tmem_ld32(taddr + q2 * 32, v);
+                // Fast path (warp-uniform): all 64 keys inside the segment and left of every
+                // row's causal limit -> two packed group sums and one overflow check.  The
+                // region is handed back to the MMA warp only after the check, so the
+                // generic path can re-read it.  (96 registers at 18 warps: one 32-column
+                // half in registers at a time.)
+                const bool fast = cbase + C::SUBN <= N - neff + 1 && UP_SCORE_DIAG != 1 && UP_SCORE_DIAG != 5;
+                float gs0 = 0.f, gs1 = 0.f;
+                bool redo = !fast && cbase < N && UP_SCORE_DIAG != 1 && UP_SCORE_DIAG != 5;
+                if (fast) {
+#if UP_TC4_PREFETCH
+                    uint32_t v[32], w2[32];
+                    tmem_ld32(taddr, v);
                     tmem_ld_wait();
-                    if (q2 == C::SUBN / 32 - 1) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&t_empty[reg]);
-                    }
-                    if (c0 >= N) continue;  // warp-uniform
-                    float gs;
-                    if (!tail) {
-                        gs = group_sum_pk(v, pk(sc, sc), pk(-m, -m));
-                    } else {
-                        const int lim = qpos - c0;
-                        float a0 = 0.f, a1 = 0.f;
+                    tmem_ld32(taddr + 32, w2);  // in flight while half 0 is reduced
+                    gs0 = group_sum_pk<kTc4PolyPairs>(v, pk(sc, sc), pk(-m, -m));
+                    tmem_ld_wait();
+                    gs1 = group_sum_pk<kTc4PolyPairs>(w2, pk(sc, sc), pk(-m, -m));
+#else
+                    uint32_t v[32];
+                    tmem_ld32(taddr, v);
+                    tmem_ld_wait();
+                    gs0 = group_sum_pk<kTc4PolyPairs>(v, pk(sc, sc), pk(-m, -m));
+                    tmem_ld32(taddr + 32, v);
+                    tmem_ld_wait();
+                    gs1 = group_sum_pk<kTc4PolyPairs>(v, pk(sc, sc), pk(-m, -m));
+#endif
+                    redo = !(gs0 + gs1 <= 0x1p40f);
+                }
+                if (redo) {
+                    // Generic path: causal tail, ragged segment end, or a rebase of m.
+#pragma unroll 1
+                    for (int q2 = 0; q2 < 2; ++q2) {
+                        const int c0 = cbase + q2 * 32;
+                        const int lim = min(qpos - c0, min(31, N - 1 - c0));  // last valid column
+                        uint32_t v[32];
+                        tmem_ld32(taddr + q2 * 32, v);
+                        tmem_ld_wait();
+                        float gs = 0.f;
+                        if (lim >= 0) {
+                            float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-                        for (int k = 0; k < 32; k += 2) {
-                            const float e0 = ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, -m));
-                            const float e1 = ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, -m));
-                            a0 += (k + 0 <= lim) ? e0 : 0.f;
-                            a1 += (k + 1 <= lim) ? e1 : 0.f;
+                            for (int k = 0; k < 32; k += 2) {
+                                const float e0 = ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, -m));
+                                const float e1 = ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, -m));
+                                a0 += (k + 0 <= lim) ? e0 : 0.f;
+                                a1 += (k + 1 <= lim) ? e1 : 0.f;
+                            }
+                            gs = a0 + a1;
                         }
-                        gs = a0 + a1;
-                    }
-                    if (!(gs <= 0x1p40f)) {  // rebase (see score_tc.cu)
-                        const int lim = tail ? qpos - c0 : 31;
-                        float gmax = -INFINITY;
+                        if (!(gs <= 0x1p40f)) {  // rebase (see score_tc.cu)
+                            float gmax = -INFINITY;
 #pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            if (k <= lim) gmax = fmaxf(gmax, __uint_as_float(v[k]));
-                        const float mnew = fmaxf(m, gmax * sc);
-                        if (m != -INFINITY) {
-                            const float f = ex2_approx(m - mnew);
-                            l *= f;
-                            bsum *= f;
-                            rescale_rows(Prow, blk0, blk, f);
-                        }
-                        m = mnew;
-                        gs = 0.f;
+                            for (int k = 0; k < 32; ++k)
+                                if (k <= lim) gmax = fmaxf(gmax, __uint_as_float(v[k]));
+                            const float mnew = fmaxf(m, gmax * sc);
+                            if (m != -INFINITY) {
+                                const float f = ex2_approx(m - mnew);
+                                l *= f;
+                                bsum *= f;
+                                gs0 *= f;  // q2 == 1: half 0 is not yet folded into bsum
+                                rescale_rows(Prow, blk0, blk, f);
+                            }
+                            m = mnew;
+                            gs = 0.f;
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) {
-                            const float e = ex2_approx(fmaf(__uint_as_float(v[k]), sc, -mnew));
-                            gs += (k <= lim) ? e : 0.f;
+                            for (int k = 0; k < 32; ++k) {
+                                const float e = ex2_approx(fmaf(__uint_as_float(v[k]), sc, -mnew));
+                                gs += (k <= lim) ? e : 0.f;
+                            }
                         }
+                        if (q2 == 0) gs0 = gs; else gs1 = gs;
                     }
-                    bsum += gs;
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&t_empty[reg]);
+                if (cbase >= N) continue;  // warp-uniform: padding subtile past the segment end
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const int c0 = cbase + q2 * 32;
+                    if (c0 >= N) break;  // warp-uniform
+                    bsum += q2 == 0 ? gs0 : gs1;
                     if (++gib == gpb || c0 + 32 >= N) {
                         Prow[static_cast<int64_t>(blk) * kRows] = row_valid ? bsum : 0.f;
                         l += bsum;
@@ -317,55 +367,6 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             }
             for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
 
-            const int64_t seg_end = it.seg_start + it.units_r;
-            epi_bar512();
-            if (etid == 0) {
-                int n_items = 0;
-                for (int64_t s = it.seg_start; s < seg_end; ++n_items) {
-                    if (n_items < kMaxPairItems) s_items[n_items] = static_cast<int32_t>(s);
-                    const int64_t e = range_begin(P, cta_of(P, s) + 1);
-                    s = e < seg_end ? e : seg_end;
-                }
-                int32_t* ctr = p.pair_counters + it.r * P.nhg + it.hg;
-                __threadfence();
-                const int old = atomicAdd(ctr, 1);
-                const bool is_last = old == n_items - 1;
-                if (is_last) *ctr = 0;
-                misc[2] = is_last ? 1u : 0u;
-                misc[3] = static_cast<uint32_t>(n_items);
-            }
-            epi_bar512();
-            if (misc[2]) {
-                __threadfence();
-                const int n_items = static_cast<int>(misc[3]);
-                for (int x = etid; x < HPC * kRows; x += 512) {
-                    const int hh = x / kRows, jj = x - (x / kRows) * kRows;
-                    const bool valid = jj < neff;
-                    auto item_at = [&](int k, int64_t& s) {
-                        if (k < kMaxPairItems) { s = s_items[k]; return; }
-                        s = range_begin(P, cta_of(P, s) + 1);
-                    };
-                    float M = -INFINITY;
-                    int64_t s = 0;
-                    for (int k = 0; k < n_items; ++k) {
-                        item_at(k, s);
-                        M = fmaxf(M, __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]));
-                    }
-                    float L = 0.f;
-                    for (int k = 0; k < n_items; ++k) {
-                        item_at(k, s);
-                        const float mc = __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]);
-                        if (mc != -INFINITY) L += __ldcg(&p.stat_l[(s * HPC + hh) * kRows + jj]) * ex2_approx(mc - M);
-                    }
-                    if (valid && !(L > 0.f)) raise_error(p.err, kErrMaskedRow);
-                    const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
-                    for (int k = 0; k < n_items; ++k) {
-                        item_at(k, s);
-                        const float mc = __ldcg(&p.stat_m[(s * HPC + hh) * kRows + jj]);
-                        p.stat_w[(s * HPC + hh) * kRows + jj] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
-                    }
-                }
-            }
         }
     }
 

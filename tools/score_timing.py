@@ -1,10 +1,10 @@
 import os, sys, torch, ctypes, numpy as np
-sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_06221_b200 as up
 from paper_2605_06221_b200.synthetic import make_batch
 sb = make_batch([32768]*4, 32, 8, 128, 64, regime=os.environ.get("REGIME","planted"), seed=1, device="cuda", with_v=False)
 cfg = up.ScoreConfig(); h = up.HeadLayout(32, 8, 128)
-out = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, cfg, h, check=True)
+out = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, cfg, h, check=not os.environ.get("NOCHECK"))
 for _ in range(3): up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, cfg, h, out=out)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -1,5 +1,5 @@
 import os, sys, torch, numpy as np
-sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_06221_b200 as up
 def run(lengths, p, reps=20):
     G = 64
