@@ -293,8 +293,10 @@ class LayerRunner:
         plane_dtypes = [torch.bfloat16, torch.bfloat16, torch.bfloat16, torch.int64]
         self.layer = up.DropLayer(cfg, up.HeadLayout(Hq, Hkv, D), self.T, self.R, plane_shapes, plane_dtypes,
                                   device=dev)
-        self.partials = [torch.empty(self.layer.scores.block_scores.numel(), dtype=torch.float32, device=dev)
-                         for _ in range(len(self.shards) if mode == "tp" and world == 1 else 0)]
+        if mode == "tp" and world == 1:
+            nbmax = self.layer.scores.block_scores.numel()
+            self.sharded = up.ShardedBlockScores(torch.empty(self.tp, nbmax, dtype=torch.float32, device=dev),
+                                                 self.layer.scores.block_scores, self.layer.scores.cu_blocks)
 
     def localize(self, sb):
         """TP rank at N>1: keep only this rank's q-heads and kv-heads (what a rank holds)."""
@@ -317,14 +319,12 @@ class LayerRunner:
             up.score_blocks_varlen(sb.q, sb.k, cu, self.cfg, L.heads, max_tokens=self.T, workspace=L.ws,
                                    out=L.scores)
             return up.lib.up_last_launch_count()
-        n = 0
         if self.world == 1:
-            for ((qb, qe), (kb, ke), h), part in zip(self.heads, self.partials):
-                up.score_blocks_varlen(sb.q[:, qb:qe], sb.k[:, kb:ke], cu, self.cfg, h, max_tokens=self.T,
-                                       workspace=L.ws, out=up.BlockScores(part, L.scores.cu_blocks))
-                n += up.lib.up_last_launch_count()
-            up.reduce_block_scores([p_[:self.nb] for p_ in self.partials], out=L.scores.block_scores[:self.nb])
-            return n + up.lib.up_last_launch_count()
+            # the whole TP group on one device: per-shard partials + ascending-shard sum in
+            # one up_score_blocks_tp call (sharded_block_scores + allreduce_scores)
+            up.score_blocks_tp(sb.q, sb.k, cu, self.cfg, self.tp, L.heads, max_tokens=self.T, workspace=L.ws,
+                               out=self.sharded)
+            return up.lib.up_last_launch_count()
         from paper_2605_06221_b200.distributed import allreduce_block_scores
         (qb, qe), (kb, ke), h = self.heads[0]
         up.score_blocks_varlen(sb.q[:, qb:qe], sb.k[:, kb:ke], cu, self.cfg, h, max_tokens=self.T,
@@ -571,7 +571,8 @@ def run_ours(args):
 
     if rank == 0:
         if mode == "tp":
-            par = f"tp{runner.tp} head-sharded" + (" (emulated on 1 GPU: shards scored in turn)" if ws == 1 else "")
+            par = f"tp{runner.tp} head-sharded" + (" (whole TP group on 1 GPU: per-shard partials + ordered "
+                                                   "shard sum in one up_score_blocks_tp call)" if ws == 1 else "")
         elif mode == "dp-split":
             par = f"LPT request-sharded over {ws} GPU(s)"
         else:

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define UP_ABI_VERSION 1
+#define UP_ABI_VERSION 2
 
 typedef enum {
     UP_OK = 0,
@@ -129,6 +129,16 @@ up_status up_score_blocks(void* stream, const up_batch* batch, const up_heads* h
                           const up_score_config* cfg, const void* q, const void* k,
                           float* block_scores, int32_t* cu_blocks, float* token_scores,
                           void* workspace, size_t workspace_bytes);
+
+/* Head-sharded importance scores in one call: the local q-heads form tp contiguous
+ * shards of Hq/tp heads (sharded_block_scores, tp_sim.cpp:12-27); writes every shard's
+ * partial block scores to shard_scores[t * shard_stride + g] (shard_stride >=
+ * up_max_blocks) and their elementwise sum in ascending shard order to block_scores
+ * (allreduce_scores, tp_sim.cpp:29-49).  UP_ERR_CONFIG when tp <= 0 or Hq % tp != 0. */
+up_status up_score_blocks_tp(void* stream, const up_batch* batch, const up_heads* heads,
+                             const up_score_config* cfg, const void* q, const void* k, int32_t tp,
+                             float* shard_scores, int64_t shard_stride, float* block_scores,
+                             int32_t* cu_blocks, void* workspace, size_t workspace_bytes);
 
 /* Elementwise sum of tp partial block-score vectors in ascending shard order
  * (allreduce_scores, tp_sim.cpp:43-47): out[g] = ((0 + s_0[g]) + s_1[g]) + ...

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libuniprefill_b200.so")
 # Symbols the header declares (checked by tests/test_capi_symbols.py).
 EXPORTED = (
     "up_abi_version", "up_status_string", "up_config_validate", "up_max_blocks",
-    "up_workspace_bytes", "up_score_blocks", "up_reduce_block_scores", "up_select",
+    "up_workspace_bytes", "up_score_blocks", "up_score_blocks_tp", "up_reduce_block_scores", "up_select",
     "up_compact", "up_drop_layer", "up_device_status", "up_scorer_kind", "up_last_launch_count",
 )
 
@@ -66,6 +66,8 @@ def _load():
         "up_workspace_bytes": ([P(BatchC), P(HeadsC), P(ScoreConfigC)], sz),
         "up_score_blocks": ([vp, P(BatchC), P(HeadsC), P(ScoreConfigC), vp, vp, vp, vp, vp, vp, sz],
                             ctypes.c_int),
+        "up_score_blocks_tp": ([vp, P(BatchC), P(HeadsC), P(ScoreConfigC), vp, vp, i32, vp, i64, vp, vp, vp,
+                                sz], ctypes.c_int),
         "up_reduce_block_scores": ([vp, P(vp), i32, i64, vp], ctypes.c_int),
         "up_select": ([vp, P(BatchC), P(ScoreConfigC), vp, vp, vp, vp, P(SelectionOutC), vp, sz],
                       ctypes.c_int),

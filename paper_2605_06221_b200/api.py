@@ -211,6 +211,57 @@ def score_blocks_varlen(q: torch.Tensor, k: torch.Tensor, cu_seqlens, config: Sc
 
 
 @dataclass
+class ShardedBlockScores:
+    shard_scores: torch.Tensor          # fp32 [tp, >= Σ ceil(N_r/G)] per-shard partials
+    block_scores: torch.Tensor          # fp32 ascending-shard sum (allreduce_scores)
+    cu_blocks: torch.Tensor             # int32 [R+1]
+
+
+def score_blocks_tp(q: torch.Tensor, k: torch.Tensor, cu_seqlens, config: ScoreConfig, tp_degree: int,
+                    heads: Optional[HeadLayout] = None, drop_enabled=None, max_tokens: Optional[int] = None,
+                    workspace: Optional[Workspace] = None, out: Optional[ShardedBlockScores] = None,
+                    check: bool = False) -> ShardedBlockScores:
+    """Head-sharded block scores in one call (up_score_blocks_tp): shard t scores q-heads
+    [t*H/T, (t+1)*H/T) (sharded_block_scores, tp_sim.cpp:12-27) and block_scores is their
+    ascending-shard fp32 sum (allreduce_scores, tp_sim.cpp:29-49) -- what a TP group of
+    tp_degree ranks computes, on one device."""
+    if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16:
+        raise ContractViolation("q and k must be bfloat16")
+    dev = q.device
+    cu = _as_i32_cuda(cu_seqlens, dev)
+    R = cu.numel() - 1
+    T = int(max_tokens if max_tokens is not None else q.shape[0])
+    if heads is None:
+        if q.dim() != 3 or k.dim() != 3:
+            raise ContractViolation("pass heads= for 2-D q/k")
+        heads = HeadLayout(q.shape[1], k.shape[1], q.shape[2])
+    qv, qs, D = _heads_view(q, heads.num_q_heads)
+    kv, ks, _ = _heads_view(k, heads.num_kv_heads)
+    if D != heads.head_dim:
+        raise ContractViolation("partial_scores: head dim mismatch")
+    en = None if drop_enabled is None else drop_enabled.to(device=dev, dtype=torch.uint8).contiguous()
+    b = _batch(cu, T, en)
+    hc = heads.c(qs, ks)
+    cfg = config.c()
+    ws = workspace or _ws(dev)
+    buf = ws.get(b, hc, cfg)
+    nbmax = int(lib.up_max_blocks(ctypes.byref(b), ctypes.byref(cfg)))
+    if out is None:
+        tpn = max(int(tp_degree), 1)
+        out = ShardedBlockScores(torch.empty(tpn, nbmax, dtype=torch.float32, device=dev),
+                                 torch.empty(nbmax, dtype=torch.float32, device=dev),
+                                 torch.empty(R + 1, dtype=torch.int32, device=dev))
+    st = lib.up_score_blocks_tp(_stream_ptr(dev), ctypes.byref(b), ctypes.byref(hc), ctypes.byref(cfg), _ptr(qv),
+                                _ptr(kv), int(tp_degree), _ptr(out.shard_scores), out.shard_scores.stride(0),
+                                _ptr(out.block_scores), _ptr(out.cu_blocks), ctypes.c_void_p(buf.data_ptr()),
+                                buf.numel())
+    _check(st, "score_blocks_tp")
+    if check:
+        ws.device_status()
+    return out
+
+
+@dataclass
 class VarlenSelection:
     keep: torch.Tensor             # uint8 [T]
     cutoff_rank: torch.Tensor      # int64 [R] (-1 for pass-through segments)

@@ -21,8 +21,10 @@ struct CompactParams;
 int tc_max_hpc(int D);
 cudaError_t launch_score_tc(int D, int HPC, const CUtensorMap& qm, const CUtensorMap& km,
                             const ScoreTcParams& p, int grid, cudaStream_t stream);
-cudaError_t launch_score_tc4(int D, const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p,
-                             int grid, cudaStream_t stream);
+cudaError_t launch_score_tcw(int D, int HPC, const CUtensorMap& qm, const CUtensorMap& km,
+                             const ScoreTcParams& p, int grid, cudaStream_t stream);
+bool tcw_supported(int D, int HPC, int G, int R);
+int tcw_stage_keys(int D);
 cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int G, int32_t* cu_blocks,
                                uint32_t* err, cudaStream_t stream);
 struct BlockCombineParams;
@@ -99,8 +101,10 @@ Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c
     const int64_t G = c->block_size_g > 0 ? c->block_size_g : 1;
     const int64_t H = h ? h->num_q_heads : 0;
     L.max_blocks = T / G + R + 1;
-    // Σ_r ceil(N_r / unit) * num_hgroups * HPC <= Hq * (T / 128 + R): bounds the item ids.
-    L.max_units = (H > 0 ? H : 1) * (T / kTileKeys + R + 1);
+    // Σ_r ceil(N_r / unit) * num_hgroups * HPC * npar <= Hq * npar * (T / 128 + R): bounds
+    // the item statistics rows (npar = 2 for the two-warpgroups-per-head scorer).
+    const int64_t npar = h ? 2 : 1;
+    L.max_units = (H > 0 ? H : 1) * npar * (T / kTileKeys + R + 1);
     const int64_t n = c->query_window_n < T ? c->query_window_n : T;
     L.simt_n = static_cast<int32_t>(n > 0 ? n : 1);
     size_t off = 0;
@@ -174,23 +178,44 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D bf16 view [rows, cols] with row stride `ld` elements, box 64 cols x 128 rows, 128B swizzle.
-bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows = 128) {
     EncodeTiledFn fn = encode_fn();
     if (fn == nullptr) return false;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-    const cuuint32_t box[2] = {64, 128};
+    const cuuint32_t box[2] = {64, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int pick_hpc(const up_heads* h) {
-    int hpc = tc_max_hpc(h->head_dim);
+// q-heads per CTA (sharing one kv-head's K tile): the largest power of two <= max_hpc
+// that divides the local head count, the head offset, the GQA group and the heads of
+// one TP shard.
+int pick_hpc(const up_heads* h, int max_hpc, int shard_heads) {
+    int hpc = max_hpc;
     if (hpc > h->gqa_group) hpc = h->gqa_group;
-    while (hpc > 1 && (h->num_q_heads % hpc || h->q_head_offset % hpc || h->gqa_group % hpc)) hpc >>= 1;
+    while (hpc > 1 && (h->num_q_heads % hpc || h->q_head_offset % hpc || h->gqa_group % hpc || shard_heads % hpc))
+        hpc >>= 1;
     return hpc < 1 ? 1 : hpc;
+}
+
+// Which tensor-core scorer serves this shape: the four-warpgroup kernel (score_tcw.cu,
+// wide = true) when it applies, else score_tc.cu.  npar = epilogue warpgroups per head.
+struct TcPlan {
+    bool wide;
+    int hpc, npar;
+};
+
+TcPlan tc_plan(const up_batch* b, const up_heads* h, const up_score_config* c, int shard_heads) {
+    const int D = h->head_dim;
+    TcPlan t{};
+    t.hpc = pick_hpc(h, D == 256 ? 2 : 4, shard_heads);
+    t.wide = (t.hpc == 4 || t.hpc == 2) && tcw_supported(D, t.hpc, c->block_size_g, b->num_requests);
+    if (!t.wide) t.hpc = pick_hpc(h, tc_max_hpc(D), shard_heads);
+    t.npar = t.wide ? 4 / t.hpc : 1;
+    return t;
 }
 
 bool tc_eligible(const up_heads* h, const up_score_config* c, int want_tokens) {
@@ -255,6 +280,96 @@ int up_scorer_kind(const up_heads* h, const up_score_config* c, int want_token_s
     return tc_eligible(h, c, want_token_scores) ? 1 : 2;
 }
 
+// Tensor-core path: scorer kernel -> pair_weights -> block_combine.  With tp > 1 the local
+// q-heads form tp contiguous shards; block_combine writes each shard's partial to
+// shard_scores[t * shard_stride + g] (when non-null) and their ascending-order fp32 sum to
+// block_scores (sharded_block_scores + allreduce_scores, tp_sim.cpp:12-49).
+static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_heads* h,
+                               const up_score_config* c, const void* q, const void* k, int tp,
+                               float* shard_scores, int64_t shard_stride, float* block_scores,
+                               int32_t* cu_blocks, const Layout& L, void* ws) {
+    const int D = h->head_dim;
+    const int R = b->num_requests;
+    const int G = c->block_size_g;
+    uint32_t* err = at<uint32_t>(ws, L.err);
+    const TcPlan plan = tc_plan(b, h, c, h->num_q_heads / tp);
+    const int hpc = plan.hpc;
+    const int nhg = h->num_q_heads / hpc;
+    CUtensorMap qm, km;
+    if (!make_map(&qm, q, b->max_tokens, static_cast<int64_t>(h->num_q_heads) * D, h->q_row_stride, 128) ||
+        !make_map(&km, k, b->max_tokens, static_cast<int64_t>(h->num_kv_heads) * D, h->k_row_stride,
+                  plan.wide ? tcw_stage_keys(D) : 128))
+        return UP_ERR_CUDA;
+    ScoreTcParams p{};
+    p.cu_seqlens = b->cu_seqlens;
+    p.drop_enabled = b->drop_enabled;
+    p.cu_blocks = cu_blocks;
+    p.cu_units_out = at<int32_t>(ws, L.cu_units);
+    p.unit_sid = at<int32_t>(ws, L.unit_sid);
+    p.err = err;
+    p.P = at<float>(ws, L.P);
+    p.stat_m = at<float>(ws, L.stat_m);
+    p.stat_l = at<float>(ws, L.stat_l);
+    p.stat_w = at<float>(ws, L.stat_w);
+    p.max_tokens = b->max_tokens;
+    p.max_blocks = L.max_blocks;
+    p.num_requests = R;
+    p.query_window_n = c->query_window_n;
+    p.block_size_g = G;
+    p.unit_keys = static_cast<int32_t>(lcm64(G, kTileKeys));
+    p.num_hgroups = nhg;
+    p.q_head_offset = h->q_head_offset;
+    p.kv_head_offset = h->kv_head_offset;
+    p.gqa_group = h->gqa_group;
+    p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
+    static const int grid_override = [] {
+        const char* s = std::getenv("UP_SCORE_GRID");
+        return s ? std::atoi(s) : 0;
+    }();
+    const int grid = grid_override > 0 ? grid_override : num_sms();
+    p.dbg = score_debug_buffer();
+    cudaError_t e = plan.wide ? launch_score_tcw(D, hpc, qm, km, p, grid, stream)
+                              : launch_score_tc(D, hpc, qm, km, p, grid, stream);
+    if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
+    PairWeightsParams wp{};
+    wp.cu_seqlens = b->cu_seqlens;
+    wp.cu_units = p.cu_units_out;
+    wp.stat_m = p.stat_m;
+    wp.stat_l = p.stat_l;
+    wp.stat_w = p.stat_w;
+    wp.err = err;
+    wp.num_requests = R;
+    wp.num_hgroups = nhg;
+    wp.hpc = hpc;
+    wp.npar = plan.npar;
+    wp.score_grid = grid;
+    wp.query_window_n = c->query_window_n;
+    const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
+    const int wgrid = static_cast<int>(wtasks < num_sms() * 8 ? wtasks : num_sms() * 8);
+    if ((e = launch_pair_weights(wp, wgrid, stream)) != cudaSuccess) return UP_ERR_CUDA;
+    BlockCombineParams bp{};
+    bp.cu_seqlens = b->cu_seqlens;
+    bp.cu_blocks = cu_blocks;
+    bp.cu_units = p.cu_units_out;
+    bp.unit_sid = p.unit_sid;
+    bp.P = p.P;
+    bp.stat_w = p.stat_w;
+    bp.block_scores = block_scores;
+    bp.shard_scores = shard_scores;
+    bp.shard_stride = shard_stride;
+    bp.max_blocks = L.max_blocks;
+    bp.num_requests = R;
+    bp.num_heads = h->num_q_heads;
+    bp.num_shards = tp;
+    bp.hpc = hpc;
+    bp.npar = plan.npar;
+    bp.block_size_g = G;
+    bp.unit_keys = p.unit_keys;
+    if ((e = launch_block_combine(bp, num_sms() * 8, stream)) != cudaSuccess) return UP_ERR_CUDA;
+    g_launches = 3;
+    return UP_OK;
+}
+
 up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
                           const up_score_config* c, const void* q, const void* k,
                           float* block_scores, int32_t* cu_blocks, float* token_scores, void* ws,
@@ -273,85 +388,8 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
     const int G = c->block_size_g;
     uint32_t* err = at<uint32_t>(ws, L.err);
 
-    if (tc_eligible(h, c, token_scores != nullptr)) {
-        const int D = h->head_dim;
-        const int hpc = pick_hpc(h);
-        const int nhg = h->num_q_heads / hpc;
-        CUtensorMap qm, km;
-        if (!make_map(&qm, q, b->max_tokens, static_cast<int64_t>(h->num_q_heads) * D, h->q_row_stride) ||
-            !make_map(&km, k, b->max_tokens, static_cast<int64_t>(h->num_kv_heads) * D, h->k_row_stride))
-            return UP_ERR_CUDA;
-        ScoreTcParams p{};
-        p.cu_seqlens = b->cu_seqlens;
-        p.drop_enabled = b->drop_enabled;
-        p.cu_blocks = cu_blocks;
-        p.cu_units_out = at<int32_t>(ws, L.cu_units);
-        p.unit_sid = at<int32_t>(ws, L.unit_sid);
-        p.err = err;
-        p.P = at<float>(ws, L.P);
-        p.stat_m = at<float>(ws, L.stat_m);
-        p.stat_l = at<float>(ws, L.stat_l);
-        p.stat_w = at<float>(ws, L.stat_w);
-        p.max_tokens = b->max_tokens;
-        p.max_blocks = L.max_blocks;
-        p.num_requests = R;
-        p.query_window_n = c->query_window_n;
-        p.block_size_g = G;
-        p.unit_keys = static_cast<int32_t>(lcm64(G, kTileKeys));
-        p.num_hgroups = nhg;
-        p.q_head_offset = h->q_head_offset;
-        p.kv_head_offset = h->kv_head_offset;
-        p.gqa_group = h->gqa_group;
-        p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
-        static const int grid_override = [] {
-            const char* s = std::getenv("UP_SCORE_GRID");
-            return s ? std::atoi(s) : 0;
-        }();
-        const int grid = grid_override > 0 ? grid_override : num_sms();
-        p.dbg = score_debug_buffer();
-        // Four q-heads per kv-head: the four-warpgroup variant (score_tc4.cu); UP_SCORE_TC4=0
-        // selects the two-warpgroup kernel for comparison.
-        static const bool use_tc4 = [] {
-            const char* s = std::getenv("UP_SCORE_TC4");
-            return !(s && s[0] == '0');
-        }();
-        cudaError_t e = (use_tc4 && hpc == 4 && (D == 64 || D == 128))
-                            ? launch_score_tc4(D, qm, km, p, grid, stream)
-                            : launch_score_tc(D, hpc, qm, km, p, grid, stream);
-        if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
-        PairWeightsParams wp{};
-        wp.cu_seqlens = b->cu_seqlens;
-        wp.cu_units = p.cu_units_out;
-        wp.stat_m = p.stat_m;
-        wp.stat_l = p.stat_l;
-        wp.stat_w = p.stat_w;
-        wp.err = err;
-        wp.num_requests = R;
-        wp.num_hgroups = nhg;
-        wp.hpc = hpc;
-        wp.score_grid = grid;
-        wp.query_window_n = c->query_window_n;
-        const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
-        const int wgrid = static_cast<int>(wtasks < num_sms() * 8 ? wtasks : num_sms() * 8);
-        if ((e = launch_pair_weights(wp, wgrid, stream)) != cudaSuccess) return UP_ERR_CUDA;
-        BlockCombineParams bp{};
-        bp.cu_seqlens = b->cu_seqlens;
-        bp.cu_blocks = cu_blocks;
-        bp.cu_units = p.cu_units_out;
-        bp.unit_sid = p.unit_sid;
-        bp.P = p.P;
-        bp.stat_w = p.stat_w;
-        bp.block_scores = block_scores;
-        bp.max_blocks = L.max_blocks;
-        bp.num_requests = R;
-        bp.num_heads = h->num_q_heads;
-        bp.hpc = hpc;
-        bp.block_size_g = G;
-        bp.unit_keys = p.unit_keys;
-        if ((e = launch_block_combine(bp, num_sms() * 8, stream)) != cudaSuccess) return UP_ERR_CUDA;
-        g_launches = 3;
-        return UP_OK;
-    }
+    if (tc_eligible(h, c, token_scores != nullptr))
+        return score_tc_path(stream, b, h, c, q, k, 1, nullptr, 0, block_scores, cu_blocks, L, ws);
 
     // Generic SIMT path.
     cudaError_t e = launch_blocks_plan(b->cu_seqlens, R, b->max_tokens, G, cu_blocks, err, stream);
@@ -381,6 +419,46 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
     if ((e = launch_score_simt(p, b->max_tokens, num_sms(), stream)) != cudaSuccess) return UP_ERR_CUDA;
     g_launches = 4;
     return UP_OK;
+}
+
+up_status up_score_blocks_tp(void* stream_, const up_batch* b, const up_heads* h,
+                             const up_score_config* c, const void* q, const void* k, int32_t tp,
+                             float* shard_scores, int64_t shard_stride, float* block_scores,
+                             int32_t* cu_blocks, void* ws, size_t ws_bytes) {
+    g_launches = 0;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    if (tp <= 0) return UP_ERR_CONFIG;  // "tp_degree must be positive" (tp_sim.cpp:14)
+    up_status st = up_config_validate(c);
+    if (st != UP_OK) return st;
+    if ((st = check_batch(b)) != UP_OK) return st;
+    if ((st = check_heads(h)) != UP_OK) return st;
+    if (h->num_q_heads % tp != 0) return UP_ERR_CONFIG;  // tp_sim.cpp:15-17
+    if (q == nullptr || k == nullptr || block_scores == nullptr || cu_blocks == nullptr || shard_scores == nullptr)
+        return UP_ERR_INVALID_ARGUMENT;
+    if (shard_stride < up_max_blocks(b, c)) return UP_ERR_INVALID_ARGUMENT;
+    const Layout L = layout_for(b, h, c);
+    if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
+    if (tc_eligible(h, c, 0))
+        return score_tc_path(stream, b, h, c, q, k, tp, shard_scores, shard_stride, block_scores, cu_blocks, L, ws);
+    // Generic shapes: one SIMT scoring pass per shard, then the ordered shard sum.
+    if (tp > 16) return UP_ERR_UNSUPPORTED;
+    const int hps = h->num_q_heads / tp;
+    const float* shards[16];
+    int launches = 0;
+    for (int t = 0; t < tp; ++t) {
+        up_heads ht = *h;
+        ht.num_q_heads = hps;
+        ht.q_head_offset = h->q_head_offset + t * hps;
+        const void* qt = static_cast<const __nv_bfloat16*>(q) + static_cast<int64_t>(t) * hps * h->head_dim;
+        float* out_t = shard_scores + static_cast<int64_t>(t) * shard_stride;
+        if ((st = up_score_blocks(stream_, b, &ht, c, qt, k, out_t, cu_blocks, nullptr, ws, ws_bytes)) != UP_OK)
+            return st;
+        launches += g_launches;
+        shards[t] = out_t;
+    }
+    const cudaError_t e = launch_reduce_shards(shards, tp, up_max_blocks(b, c), block_scores, num_sms(), stream);
+    g_launches = launches + 1;
+    return cuda_status(e);
 }
 
 up_status up_reduce_block_scores(void* stream, const float* const* shards, int32_t tp,

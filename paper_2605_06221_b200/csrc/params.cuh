@@ -42,6 +42,7 @@ struct PairWeightsParams {
     int32_t num_requests;
     int32_t num_hgroups;
     int32_t hpc;
+    int32_t npar;             // statistics rows per head (parity warpgroups of score_tcw)
     int32_t score_grid;       // the scorer's gridDim.x (defines the item ranges)
     int32_t query_window_n;
 };
@@ -54,10 +55,14 @@ struct BlockCombineParams {
     const float* P;
     const float* stat_w;
     float* block_scores;
+    float* shard_scores;      // optional [num_shards][shard_stride] per-shard partials
+    int64_t shard_stride;
     int64_t max_blocks;
     int32_t num_requests;
     int32_t num_heads;
+    int32_t num_shards;       // 1, or T contiguous head shards summed in ascending order
     int32_t hpc;
+    int32_t npar;             // epilogue warpgroups per head (score_tcw): stats row hh*npar+par
     int32_t block_size_g;
     int32_t unit_keys;
 };

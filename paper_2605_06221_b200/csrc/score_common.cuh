@@ -7,6 +7,8 @@
 namespace up {
 
 
+constexpr int kTcwMaxRequests = 256;  // segments per launch of score_tcw (plan kept in smem)
+
 // ---------------------------------------------------------------- partition
 struct Part {
     const int32_t* cu_units;  // smem [R+1]

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(256)
 pair_weights_kernel(const PairWeightsParams p) {
     __shared__ float sM[8][32], sL[8][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int R = p.num_requests, hpc = p.hpc, nhg = p.num_hgroups;
+    const int R = p.num_requests, hpc = p.hpc, nhg = p.num_hgroups, npar = p.npar;
     Part P;
     P.cu_units = p.cu_units;
     P.R = R;
@@ -424,16 +424,20 @@ pair_weights_kernel(const PairWeightsParams p) {
             if (k > 0 && b == range_begin(P, c_first + k + 1)) return -1;
             return b > seg_start ? b : seg_start;
         };
+        // statistics rows of head hh: (sid * hpc + hh) * npar + par, par < npar (the
+        // parity warpgroups of score_tcw keep separate running (m, l) for one head)
         float M = -INFINITY, L = 0.f;
         for (int k = warp; k < n_items; k += 8) {
             const int64_t sid = sid_of(k);
             if (sid < 0) continue;
-            const int64_t x = (sid * hpc + hh) * kRows + j;
-            const float mc = __ldcg(&p.stat_m[x]);
-            const float lc = __ldcg(&p.stat_l[x]);
-            if (mc == -INFINITY) continue;
-            if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
-            else L += lc * ex2_approx(mc - M);
+            for (int q = 0; q < npar; ++q) {
+                const int64_t x = ((sid * hpc + hh) * npar + q) * kRows + j;
+                const float mc = __ldcg(&p.stat_m[x]);
+                const float lc = __ldcg(&p.stat_l[x]);
+                if (mc == -INFINITY) continue;
+                if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
+                else L += lc * ex2_approx(mc - M);
+            }
         }
         sM[warp][lane] = M;
         sL[warp][lane] = L;
@@ -454,9 +458,11 @@ pair_weights_kernel(const PairWeightsParams p) {
         for (int k = warp; k < n_items; k += 8) {
             const int64_t sid = sid_of(k);
             if (sid < 0) continue;
-            const int64_t x = (sid * hpc + hh) * kRows + j;
-            const float mc = __ldcg(&p.stat_m[x]);
-            p.stat_w[x] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
+            for (int q = 0; q < npar; ++q) {
+                const int64_t x = ((sid * hpc + hh) * npar + q) * kRows + j;
+                const float mc = __ldcg(&p.stat_m[x]);
+                p.stat_w[x] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
+            }
         }
     }
 }
@@ -467,17 +473,27 @@ cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, cudaStream
 }
 
 // Warp per block: b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][hh][j].
+// With num_shards = T > 1 the heads form T contiguous shards (sharded_block_scores,
+// tp_sim.cpp:12-27): each shard's partial b_g^t is formed on its own (written to
+// shard_scores[t] when non-null) and block_scores[g] = ((0 + b^0) + b^1) + ... in fp32,
+// ascending shard order (allreduce_scores, tp_sim.cpp:43-47).
 __global__ void __launch_bounds__(256)
 block_combine_kernel(const BlockCombineParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int R = p.num_requests;
     const int total = p.cu_blocks[R];
     const int nhg = p.num_heads / p.hpc;
+    const int T = p.num_shards;
+    const int hps = p.num_heads / T;  // heads per shard (a multiple of hpc)
     for (int gb = blockIdx.x * (blockDim.x >> 5) + warp; gb < total; gb += gridDim.x * (blockDim.x >> 5)) {
         const int r = find_segment(p.cu_blocks, R, gb);
         const int units_r = p.cu_units[r + 1] - p.cu_units[r];
         if (units_r == 0) {  // pass-through segment
-            if (lane == 0) p.block_scores[gb] = 0.f;
+            if (lane == 0) {
+                p.block_scores[gb] = 0.f;
+                if (p.shard_scores != nullptr)
+                    for (int t = 0; t < T; ++t) p.shard_scores[static_cast<int64_t>(t) * p.shard_stride + gb] = 0.f;
+            }
             continue;
         }
         const int g = gb - p.cu_blocks[r];
@@ -485,43 +501,53 @@ block_combine_kernel(const BlockCombineParams p) {
         const int size = min(p.block_size_g, N - g * p.block_size_g);
         const int u = (g * p.block_size_g) / p.unit_keys;
         const int64_t pair0 = static_cast<int64_t>(p.cu_units[r]) * nhg;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int hg0 = 0; hg0 < nhg; hg0 += 32) {
-            // Item ids of up to 32 head groups, one per lane, then broadcast.
-            const int my_hg = hg0 + lane;
-            const int my_sid = my_hg < nhg ? p.unit_sid[pair0 + static_cast<int64_t>(my_hg) * units_r + u] : 0;
-            const int h_end = min(p.num_heads, (hg0 + 32) * p.hpc);
-            int h = hg0 * p.hpc;
-            for (; h + 8 <= h_end; h += 8) {
-                float4 pv[8], wv[8];
+        // statistics row of head hh: hh * npar + (parity of the block's 64-key subtile)
+        const int par = p.npar > 1 ? ((g * p.block_size_g) >> 6) % p.npar : 0;
+        const int hpcv = p.hpc * p.npar;
+        float red = 0.f;
+        for (int t = 0; t < T; ++t) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            const int hg_begin = t * hps / p.hpc, hg_end = (t + 1) * hps / p.hpc;
+            for (int hg0 = hg_begin; hg0 < hg_end; hg0 += 32) {
+                // Item ids of up to 32 head groups, one per lane, then broadcast.
+                const int my_hg = hg0 + lane;
+                const int my_sid = my_hg < hg_end ? p.unit_sid[pair0 + static_cast<int64_t>(my_hg) * units_r + u] : 0;
+                const int h_end = min((t + 1) * hps, (hg0 + 32) * p.hpc);
+                int h = hg0 * p.hpc;
+                for (; h + 8 <= h_end; h += 8) {
+                    float4 pv[8], wv[8];
 #pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                    const int hx = h + x;
-                    const int hgx = hx / p.hpc;
-                    const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
-                    pv[x] = __ldcs(reinterpret_cast<const float4*>(
-                                p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
-                    wv[x] = __ldg(reinterpret_cast<const float4*>(
-                                p.stat_w + (sid * p.hpc + (hx - hgx * p.hpc)) * kRows) + lane);
+                    for (int x = 0; x < 8; ++x) {
+                        const int hx = h + x;
+                        const int hgx = hx / p.hpc;
+                        const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
+                        pv[x] = __ldcs(reinterpret_cast<const float4*>(
+                                    p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
+                        wv[x] = __ldg(reinterpret_cast<const float4*>(
+                                    p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);
+                    }
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        acc[x] = fmaf(pv[x].x, wv[x].x, fmaf(pv[x].y, wv[x].y, fmaf(pv[x].z, wv[x].z, fmaf(pv[x].w, wv[x].w, acc[x]))));
                 }
+                for (; h < h_end; ++h) {
+                    const int hgx = h / p.hpc;
+                    const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
+                    const float4 pv = __ldcs(reinterpret_cast<const float4*>(
+                        p.P + (static_cast<int64_t>(h) * p.max_blocks + gb) * kRows) + lane);
+                    const float4 wv = __ldg(reinterpret_cast<const float4*>(
+                        p.stat_w + (sid * hpcv + (h - hgx * p.hpc) * p.npar + par) * kRows) + lane);
+                    acc[0] = fmaf(pv.x, wv.x, fmaf(pv.y, wv.y, fmaf(pv.z, wv.z, fmaf(pv.w, wv.w, acc[0]))));
+                }
+            }
+            float a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 #pragma unroll
-                for (int x = 0; x < 8; ++x)
-                    acc[x] = fmaf(pv[x].x, wv[x].x, fmaf(pv[x].y, wv[x].y, fmaf(pv[x].z, wv[x].z, fmaf(pv[x].w, wv[x].w, acc[x]))));
-            }
-            for (; h < h_end; ++h) {
-                const int hgx = h / p.hpc;
-                const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
-                const float4 pv = __ldcs(reinterpret_cast<const float4*>(
-                    p.P + (static_cast<int64_t>(h) * p.max_blocks + gb) * kRows) + lane);
-                const float4 wv = __ldg(reinterpret_cast<const float4*>(
-                    p.stat_w + (sid * p.hpc + (h - hgx * p.hpc)) * kRows) + lane);
-                acc[0] = fmaf(pv.x, wv.x, fmaf(pv.y, wv.y, fmaf(pv.z, wv.z, fmaf(pv.w, wv.w, acc[0]))));
-            }
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            const float bt = a / static_cast<float>(size);
+            if (p.shard_scores != nullptr && lane == 0) p.shard_scores[static_cast<int64_t>(t) * p.shard_stride + gb] = bt;
+            red = T == 1 ? bt : red + bt;
         }
-        float a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0) p.block_scores[gb] = a / static_cast<float>(size);
+        if (lane == 0) p.block_scores[gb] = red;
     }
 }
 

@@ -1,56 +1,73 @@
-// score_tc4.cu -- tensor-core scorer variant for four q-heads per kv-head (HPC = 4, e.g.
-// LLaMA-3.1-8B: 32 q-heads / 8 kv-heads, D = 128) with four epilogue warpgroups.
+// score_tcw.cu -- tensor-core block scorer with four epilogue warpgroups for HPC = 4 or 2
+// q-heads per kv-head (LLaMA-3.1-8B: D = 128, HPC = 4; Gemma-3 / Qwen3-Next full-attention
+// layers: D = 256, HPC = 2).
 //
-// Same math, work partition, statistics and row-weight epilogue as score_tc.cu (see its
-// header: importance.cpp:17-132 restated as a single pass over K).  What differs is the
-// pipeline shape, chosen because the exp2 epilogue -- not the tensor core -- bounds the
-// scorer (MUFU 16 ex2/clk/SM vs 32 S elements/clk/SM from tcgen05 at D = 128):
-//  * 18 warps: warp 0 TMA, warp 1 MMA, warps 2..17 = four epilogue warpgroups, one per
-//    q-head of the group, so every SMSP runs four exp2 streams (vs two) and each thread
-//    keeps its row's running state (m, l, block partial) in registers;
-//  * every 128-key tile is issued as two N = 64 MMAs per head into eight 64-column TMEM
-//    regions = (head, buffer): a warpgroup drains one buffer while tcgen05 fills the other.
+// Same math, work partition and per-item statistics as score_tc.cu (its header restates
+// importance.cpp:17-132 as a single pass over K); pair_weights_kernel and
+// block_combine_kernel finish the job.  What this kernel changes is the pipeline shape,
+// because the exp2 epilogue (MUFU, 16/clk/SM) -- not the tensor core -- bounds the scorer:
+//  * 18 warps: warp 0 TMA, warp 1 MMA, warps 2..17 = four epilogue warpgroups, so every
+//    SMSP runs four exp2 streams.  Warpgroup wg drains head hh = wg / NPAR and, with
+//    HPC = 2 (NPAR = 2), only the 64-key subtiles whose parity is wg % NPAR: the two
+//    warpgroups of a head keep separate running statistics, recorded as separate
+//    "virtual heads" vh = hh * NPAR + par in the item statistics (requires G in {32, 64}
+//    so that every block lies inside one subtile);
+//  * K is streamed in stages of SK keys (128 x 2 stages at D <= 128, 64 x 3 at D = 256)
+//    next to the resident Q of the HPC heads (128 KB), so the kv-head's K tile is read
+//    from HBM once for all HPC heads;
+//  * every 64-key subtile is one N = 64 MMA per head into a ring of NB = 8 / HPC TMEM
+//    regions per head (512 columns in total).
 #include "score_common.cuh"
 
 namespace up {
 
-#ifndef UP_SCORE_DIAG
-#define UP_SCORE_DIAG 0  // dev only: 1 = skip the epilogue math, 2 = skip the MMAs,
-#endif                   // 3 = one K-step MMA per subtile, 5 = 1 without K reloads
-#ifndef UP_TC4_POLY_PAIRS
-#define UP_TC4_POLY_PAIRS 4
+#ifndef UP_TCW_POLY_PAIRS_D128
+#define UP_TCW_POLY_PAIRS_D128 4
 #endif
-constexpr int kTc4PolyPairs = UP_TC4_POLY_PAIRS;
-#ifndef UP_TC4_PREFETCH
-#define UP_TC4_PREFETCH 0
-#endif
-#ifndef UP_TC4_KST
-#define UP_TC4_KST 2
+#ifndef UP_TCW_POLY_PAIRS_D256
+#define UP_TCW_POLY_PAIRS_D256 0
 #endif
 
-template <int D>
-struct Tc4Cfg {
-    static constexpr int HPC = 4;
-    static constexpr int KC = D / 64;
-    static constexpr int SUB = 128 * 128;
-    static constexpr int Q_BYTES = HPC * KC * SUB;
-    static constexpr int K_STAGE = KC * SUB;
-    static constexpr int KST = UP_TC4_KST;
-    static constexpr int SUBN = 64;                // keys per MMA / TMEM region width
-    static constexpr int NREG = HPC * 2;           // (head, buffer) regions
+#ifndef UP_TCW_STAGE_KEYS_D128
+#define UP_TCW_STAGE_KEYS_D128 128
+#endif
+
+template <int D, int HPC>
+struct TcwCfg {
+    static constexpr int SK = D <= 128 ? UP_TCW_STAGE_KEYS_D128 : 64;  // keys per K stage
+    static constexpr int SPS = SK / 64;           // 64-key subtiles per stage
+    static constexpr int NPAR = 4 / HPC;          // epilogue warpgroups per head
+    static constexpr int NB = 8 / HPC;            // TMEM regions (64 columns) per head
+    static constexpr int KC = D / 64;             // 128-byte K-chunks per row
+    static constexpr int QSUB = 128 * 128;        // [128 rows x 64 bf16] Q tile
+    static constexpr int KSUB = SK * 128;         // [SK keys x 64 bf16] K tile
+    static constexpr int Q_BYTES = HPC * KC * QSUB;
+    static constexpr int K_STAGE = KC * KSUB;
+    static constexpr int R_RESERVE = 2 * (kTcwMaxRequests + 1) * 4;
+    static constexpr int BUDGET = 232448 - 1024 - 512 - R_RESERVE;
+    static constexpr int KST = (BUDGET - Q_BYTES) / K_STAGE > 8 ? 8 : (BUDGET - Q_BYTES) / K_STAGE;
+    static constexpr int NREG = HPC * NB;         // = 8
     static constexpr int NBAR = 2 + 2 * KST + 2 * NREG;
     static constexpr int THREADS = 64 + 512;
-    static constexpr int FIXED = Q_BYTES + KST * K_STAGE + NBAR * 8 + 64 + 1024;
-    static int smem(int R) { return FIXED + 2 * (R + 1) * 4; }
+    static constexpr int NP = D <= 128 ? UP_TCW_POLY_PAIRS_D128 : UP_TCW_POLY_PAIRS_D256;
+    static int smem(int R) { return Q_BYTES + KST * K_STAGE + NBAR * 8 + 64 + 1024 + 2 * (R + 1) * 4; }
+    static_assert(KST >= 2, "K ring too small");
 };
 
+// Rebase (cold): rescale the partials this thread already wrote for the item -- blocks
+// [g0, g1) that lie in subtiles of this warpgroup's parity.
+static __device__ __noinline__ void rescale_rows_par(float* prow, int g0, int g1, int G, int npar, int par,
+                                                     float f) {
+    for (int g = g0; g < g1; ++g)
+        if (((g * G) >> 6) % npar == par) prow[static_cast<int64_t>(g) * kRows] *= f;
+}
 
-template <int D>
+template <int D, int HPC>
 __global__ void __launch_bounds__(576, 1)
-score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                  const ScoreTcParams p) {
-    using C = Tc4Cfg<D>;
-    constexpr int HPC = C::HPC;
+    using C = TcwCfg<D, HPC>;
+    constexpr int NPAR = C::NPAR, NB = C::NB;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -63,7 +80,7 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
     uint64_t* k_empty = bars + 2 + C::KST;
     uint64_t* t_full = bars + 2 + 2 * C::KST;
     uint64_t* t_empty = bars + 2 + 2 * C::KST + C::NREG;
-    uint32_t* misc = reinterpret_cast<uint32_t*>(bars + C::NBAR);  // [0] tmem base, [1] ok, [2] last, [3] n
+    uint32_t* misc = reinterpret_cast<uint32_t*>(bars + C::NBAR);  // [0] tmem base, [1] plan ok
     int32_t* s_cu_units = reinterpret_cast<int32_t*>(misc + 16);
     int32_t* s_cu_blocks = s_cu_units + (p.num_requests + 1);
 
@@ -143,7 +160,7 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
     const int64_t my_end = P.U > 0 ? range_begin(P, blockIdx.x + 1) : 0;
 
     if (warp == 0) {
-        // ===== TMA producer (identical to score_tc.cu) =====
+        // ===== TMA producer: Q of the HPC heads once per item, K in 64-key stages =====
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
@@ -156,7 +173,7 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 const int neff = min(p.query_window_n, N);
                 const int key0 = it.u0 * unit_keys;
                 const int key1 = min(it.u1 * unit_keys, N);
-                const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
+                const int nst = (key1 - key0 + C::SK - 1) / C::SK;
                 const int kv_local = (p.q_head_offset + it.hg * HPC) / p.gqa_group - p.kv_head_offset;
                 mbar_wait(q_empty, (qiter & 1) ^ 1);
                 ++qiter;
@@ -166,34 +183,29 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 for (int hh = 0; hh < HPC; ++hh) {
 #pragma unroll
                     for (int kc = 0; kc < C::KC; ++kc)
-                        tma_load_2d(sq + (hh * C::KC + kc) * C::SUB, &qmap, q_full,
+                        tma_load_2d(sq + (hh * C::KC + kc) * C::QSUB, &qmap, q_full,
                                     (it.hg * HPC + hh) * D + kc * 64, qrow);
                 }
-                for (int t = 0; t < ntiles; ++t) {
+                for (int t = 0; t < nst; ++t) {
                     mbar_wait(&k_empty[stage], phase ^ 1);
-                    if (UP_SCORE_DIAG == 5 && t >= C::KST) {
-                        mbar_arrive(&k_full[stage]);
-                        if (++stage == C::KST) { stage = 0; phase ^= 1; }
-                        continue;
-                    }
                     mbar_arrive_expect_tx(&k_full[stage], C::K_STAGE);
-                    const int krow = seg0 + key0 + t * kTileKeys;
+                    const int krow = seg0 + key0 + t * C::SK;
 #pragma unroll
                     for (int kc = 0; kc < C::KC; ++kc)
-                        tma_load_2d(sk + stage * C::K_STAGE + kc * C::SUB, &kmap, &k_full[stage],
+                        tma_load_2d(sk + stage * C::K_STAGE + kc * C::KSUB, &kmap, &k_full[stage],
                                     kv_local * D + kc * 64, krow);
                     if (++stage == C::KST) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer: per tile, two 64-key halves x four heads, N = 64 =====
+        // ===== MMA issuer: per 64-key stage, one N = 64 MMA per head =====
         if (elect_one()) {
-            constexpr uint32_t kIdesc = idesc_bf16_f32(128, C::SUBN);
+            constexpr uint32_t kIdesc = idesc_bf16_f32(128, 64);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t qiter = 0;
-            uint32_t u = 0;  // 64-key sub-tile counter
+            uint32_t u = 0;  // 64-key subtile counter (selects the TMEM region of every head)
             const uint32_t sq_addr = smem_u32(sq);
             const uint32_t sk_addr = smem_u32(sk);
             for (int64_t pos = my_begin; pos < my_end;) {
@@ -202,29 +214,28 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 const int N = p.cu_seqlens[it.r + 1] - p.cu_seqlens[it.r];
                 const int key0 = it.u0 * unit_keys;
                 const int key1 = min(it.u1 * unit_keys, N);
-                const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
+                const int nst = (key1 - key0 + C::SK - 1) / C::SK;
                 mbar_wait(q_full, qiter & 1);
                 ++qiter;
                 tc_fence_after();
-                for (int t = 0; t < ntiles; ++t) {
+                for (int t = 0; t < nst; ++t) {
                     mbar_wait(&k_full[stage], phase);
                     tc_fence_after();
 #pragma unroll
-                    for (int s = 0; s < 2; ++s, ++u) {
+                    for (int s = 0; s < C::SPS; ++s, ++u) {
 #pragma unroll
                         for (int hh = 0; hh < HPC; ++hh) {
-                            const uint32_t reg = hh * 2 + (u & 1);
-                            mbar_wait(&t_empty[reg], ((u >> 1) & 1) ^ 1);
+                            const uint32_t reg = hh * NB + u % NB;
+                            mbar_wait(&t_empty[reg], ((u / NB) & 1) ^ 1);
                             tc_fence_after();
-                            const uint32_t d_tmem = tmem_base + reg * C::SUBN;
+                            const uint32_t d_tmem = tmem_base + reg * 64;
 #pragma unroll
                             for (int kk = 0; kk < D / 16; ++kk) {
-                                const uint32_t off = (kk >> 2) * C::SUB + (kk & 3) * 32;
-                                const uint64_t a = smem_desc_sw128(sq_addr + hh * C::KC * C::SUB + off);
-                                // rows s*64.. of the K tile: 8 swizzle atoms (8 KB) further
-                                const uint64_t b = smem_desc_sw128(sk_addr + stage * C::K_STAGE + off + s * 8192);
-                                if (UP_SCORE_DIAG != 2 && (UP_SCORE_DIAG != 3 || kk == 0))
-                                    mma_bf16_ss(d_tmem, a, b, kIdesc, kk > 0 ? 1u : 0u);
+                                const uint64_t a = smem_desc_sw128(sq_addr + (hh * C::KC + (kk >> 2)) * C::QSUB + (kk & 3) * 32);
+                                // subtile s = rows s*64.. of the stage: 8 swizzle atoms (8 KB) further
+                                const uint64_t b = smem_desc_sw128(sk_addr + stage * C::K_STAGE + (kk >> 2) * C::KSUB +
+                                                                   (kk & 3) * 32 + s * 8192);
+                                mma_bf16_ss(d_tmem, a, b, kIdesc, kk > 0 ? 1u : 0u);
                             }
                             mma_commit(&t_full[reg]);
                         }
@@ -236,14 +247,16 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             }
         }
     } else {
-        // ===== epilogue: warpgroup w drains head w; thread = query row =====
+        // ===== epilogue: warpgroup wg -> head hh, subtile parity par; thread = query row =====
         const int etid = threadIdx.x - 64;   // 0..511
-        const int w = (warp - 2) >> 2;       // head within the group
-        const int quarter = warp & 3;        // TMEM lane quarter
+        const int wg = (warp - 2) >> 2;
+        const int hh = wg / NPAR;
+        const int par = wg % NPAR;
+        const int vh = hh * NPAR + par;      // virtual head of the item statistics
+        const int quarter = warp & 3;        // TMEM lane quarter this warp may access
         const int j = quarter * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const float sc = p.scale_log2;
-        const int gpb = G / 32;
         uint32_t u = 0;
         for (int64_t pos = my_begin; pos < my_end;) {
             const Item it = make_item(P, pos, my_end);
@@ -253,48 +266,42 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             const int neff = min(p.query_window_n, N);
             const int key0 = it.u0 * unit_keys;
             const int key1 = min(it.u1 * unit_keys, N);
-            const int ntiles = (key1 - key0 + kTileKeys - 1) / kTileKeys;
+            const int nsub = (key1 - key0 + C::SK - 1) / C::SK * C::SPS;  // as issued by the MMA warp
             const bool row_valid = j < neff;
             const int qpos = N - neff + j;  // row j's causal limit (importance.cpp:27)
             const int64_t gb_seg = s_cu_blocks[it.r];
             const int blk0 = key0 / G;
-            float* Prow = p.P + (static_cast<int64_t>(it.hg * HPC + w) * p.max_blocks + gb_seg) * kRows + j;
+            float* Prow = p.P + (static_cast<int64_t>(it.hg * HPC + hh) * p.max_blocks + gb_seg) * kRows + j;
             float m = -INFINITY, l = 0.f, bsum = 0.f;
+            // block bookkeeping: NPAR = 1 walks every group in order (counters, any G that
+            // is a multiple of 32); NPAR = 2 sees every other subtile (G = 32 or 64: shifts)
+            const int gpb = G >> 5;
+            const int gshift = G == 64 ? 1 : 0;
             int gib = 0, blk = blk0;
 
 #pragma unroll 1
-            for (int t2 = 0; t2 < 2 * ntiles; ++t2, ++u) {
-                const int cbase = key0 + t2 * C::SUBN;
-                const uint32_t reg = w * 2 + (u & 1);
-                mbar_wait(&t_full[reg], (u >> 1) & 1);
+            for (int t = 0; t < nsub; ++t, ++u) {
+                if (NPAR > 1 && (t % NPAR) != par) continue;  // the other warpgroup's subtile
+                const int cbase = key0 + t * 64;
+                const uint32_t reg = hh * NB + u % NB;
+                mbar_wait(&t_full[reg], (u / NB) & 1);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + lane_base + reg * C::SUBN;
+                const uint32_t taddr = tmem_base + lane_base + reg * 64;
                 // Fast path (warp-uniform): all 64 keys inside the segment and left of every
                 // row's causal limit -> two packed group sums and one overflow check.  The
-                // region is handed back to the MMA warp only after the check, so the
-                // generic path can re-read it.  (96 registers at 18 warps: one 32-column
-                // half in registers at a time.)
-                const bool fast = cbase + C::SUBN <= N - neff + 1 && UP_SCORE_DIAG != 1 && UP_SCORE_DIAG != 5;
+                // region goes back to the MMA warp after the check, so the generic path can
+                // re-read it.
+                const bool fast = cbase + 64 <= N - neff + 1;
                 float gs0 = 0.f, gs1 = 0.f;
-                bool redo = !fast && cbase < N && UP_SCORE_DIAG != 1 && UP_SCORE_DIAG != 5;
+                bool redo = !fast && cbase < N;
                 if (fast) {
-#if UP_TC4_PREFETCH
-                    uint32_t v[32], w2[32];
-                    tmem_ld32(taddr, v);
-                    tmem_ld_wait();
-                    tmem_ld32(taddr + 32, w2);  // in flight while half 0 is reduced
-                    gs0 = group_sum_pk<kTc4PolyPairs>(v, pk(sc, sc), pk(-m, -m));
-                    tmem_ld_wait();
-                    gs1 = group_sum_pk<kTc4PolyPairs>(w2, pk(sc, sc), pk(-m, -m));
-#else
                     uint32_t v[32];
                     tmem_ld32(taddr, v);
                     tmem_ld_wait();
-                    gs0 = group_sum_pk<kTc4PolyPairs>(v, pk(sc, sc), pk(-m, -m));
+                    gs0 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
                     tmem_ld32(taddr + 32, v);
                     tmem_ld_wait();
-                    gs1 = group_sum_pk<kTc4PolyPairs>(v, pk(sc, sc), pk(-m, -m));
-#endif
+                    gs1 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
                     redo = !(gs0 + gs1 <= 0x1p40f);
                 }
                 if (redo) {
@@ -318,7 +325,8 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                             }
                             gs = a0 + a1;
                         }
-                        if (!(gs <= 0x1p40f)) {  // rebase (see score_tc.cu)
+                        if (!(gs <= 0x1p40f)) {
+                            // Rebase: move m to this group's maximum (see score_tc.cu).
                             float gmax = -INFINITY;
 #pragma unroll
                             for (int k = 0; k < 32; ++k)
@@ -329,7 +337,8 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                                 l *= f;
                                 bsum *= f;
                                 gs0 *= f;  // q2 == 1: half 0 is not yet folded into bsum
-                                rescale_rows(Prow, blk0, blk, f);
+                                rescale_rows_par(Prow, blk0, NPAR == 1 ? blk : cbase >> (5 + gshift), G, NPAR,
+                                                 par, f);
                             }
                             m = mnew;
                             gs = 0.f;
@@ -351,8 +360,18 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                     const int c0 = cbase + q2 * 32;
                     if (c0 >= N) break;  // warp-uniform
                     bsum += q2 == 0 ? gs0 : gs1;
-                    if (++gib == gpb || c0 + 32 >= N) {
-                        Prow[static_cast<int64_t>(blk) * kRows] = row_valid ? bsum : 0.f;
+                    bool done;
+                    int b;
+                    if (NPAR == 1) {
+                        done = ++gib == gpb || c0 + 32 >= N;
+                        b = blk;
+                    } else {
+                        const int gi = c0 >> 5;
+                        done = (gi & (gpb - 1)) == gpb - 1 || c0 + 32 >= N;
+                        b = gi >> gshift;
+                    }
+                    if (done) {  // block b complete
+                        Prow[static_cast<int64_t>(b) * kRows] = row_valid ? bsum : 0.f;
                         l += bsum;
                         bsum = 0.f;
                         gib = 0;
@@ -361,12 +380,11 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 }
             }
             {
-                const int64_t x = (it.sid * HPC + w) * kRows + j;
+                const int64_t x = (it.sid * (HPC * NPAR) + vh) * kRows + j;
                 p.stat_m[x] = row_valid ? m : -INFINITY;
                 p.stat_l[x] = row_valid ? l : 0.f;
             }
             for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
-
         }
     }
 
@@ -388,22 +406,37 @@ score_tc4_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
     }
 }
 
-template <int D>
-static cudaError_t launch_tc4(const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p, int grid,
-                             cudaStream_t stream) {
-    using C = Tc4Cfg<D>;
+template <int D, int HPC>
+static cudaError_t launch_tcw(const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p, int grid,
+                              cudaStream_t stream) {
+    using C = TcwCfg<D, HPC>;
     const int smem = C::smem(p.num_requests);
-    if (smem > 232448) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(score_tc4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (p.num_requests > kTcwMaxRequests || smem > 232448) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(score_tcw_kernel<D, HPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    score_tc4_kernel<D><<<grid, C::THREADS, smem, stream>>>(qm, km, p);
+    score_tcw_kernel<D, HPC><<<grid, C::THREADS, smem, stream>>>(qm, km, p);
     return cudaGetLastError();
 }
 
-cudaError_t launch_score_tc4(int D, const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p,
+// Keys per K stage (the K tensor map's box rows).
+int tcw_stage_keys(int D) { return D <= 128 ? TcwCfg<128, 4>::SK : TcwCfg<256, 2>::SK; }
+
+// Shapes this kernel serves: HPC = 4 at D in {64, 128}, HPC = 2 at D in {64, 128, 256}; with HPC = 2 the
+// block size must be 32 or 64 (blocks inside one 64-key subtile).
+bool tcw_supported(int D, int HPC, int G, int R) {
+    if (R > kTcwMaxRequests || G % 32 != 0) return false;
+    if (HPC == 4) return D == 64 || D == 128;
+    if (HPC == 2) return (D == 64 || D == 128 || D == 256) && (G == 32 || G == 64);
+    return false;
+}
+
+cudaError_t launch_score_tcw(int D, int HPC, const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p,
                              int grid, cudaStream_t stream) {
-    if (D == 64) return launch_tc4<64>(qm, km, p, grid, stream);
-    if (D == 128) return launch_tc4<128>(qm, km, p, grid, stream);
+    if (D == 64 && HPC == 4) return launch_tcw<64, 4>(qm, km, p, grid, stream);
+    if (D == 64 && HPC == 2) return launch_tcw<64, 2>(qm, km, p, grid, stream);
+    if (D == 128 && HPC == 4) return launch_tcw<128, 4>(qm, km, p, grid, stream);
+    if (D == 128 && HPC == 2) return launch_tcw<128, 2>(qm, km, p, grid, stream);
+    if (D == 256 && HPC == 2) return launch_tcw<256, 2>(qm, km, p, grid, stream);
     return cudaErrorInvalidValue;
 }
 

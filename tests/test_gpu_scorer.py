@@ -45,6 +45,13 @@ def _assert_blocks_close(got, want):
     (8, 2, 128, [1024, 513], 64, 32),      # n=64, G=32
     (8, 2, 128, [2048], 128, 128),         # G=128
     (8, 2, 128, [1300], 100, 96),          # n < 128, G not a power of two
+    (4, 2, 256, [700, 1200], 128, 32),     # D=256, G=32 (two warpgroups per head, 2 blocks/subtile)
+    (2, 1, 256, [5000], 128, 64),          # Qwen3-Next TP-rank slice: 2 q-heads on 1 kv-head
+    (4, 2, 256, [1000], 128, 128),         # D=256, G=128 -> two-warpgroup kernel, HPC 1
+    (8, 4, 128, [1500, 260], 128, 64),     # GQA 2 at D=128 (HPC 2, parity warpgroups)
+    (8, 2, 64, [900], 128, 64),            # D=64, HPC 4
+    (4, 2, 64, [650], 128, 32),            # D=64, HPC 2
+    (16, 8, 256, [3000, 64, 4100], 128, 64),  # Gemma-3 layout, varlen
 ])
 def test_tc_scorer_matches_oracle(up, port, Hq, Hkv, D, lengths, n, G):
     cfg = dict(query_window_n=n, block_size_g=G, sink_count_a=128, top_p=0.99)
@@ -123,3 +130,43 @@ def test_score_tokens_mirror_head_ranges_and_tp_sum(up, port):
         _assert_blocks_close(red, full.block_scores.cpu().numpy())
     with pytest.raises(up.ConfigError):
         up.sharded_block_scores(q, k, H, cfg, 3, num_kv_heads=Hkv)
+
+
+@pytest.mark.parametrize("Hq,Hkv,D,tp,lengths", [
+    (16, 2, 256, 8, [3000]),      # Qwen3-Next full-attention layer at TP=8 (2 heads per shard)
+    (32, 8, 128, 8, [1100, 700]),  # LLaMA layout at TP=8 (4 heads per shard)
+    (8, 2, 128, 2, [900]),
+    (4, 4, 32, 4, [300]),         # generic shape (SIMT shards + ordered reduce kernel)
+])
+def test_score_blocks_tp_matches_reference_sharding(up, port, ref, Hq, Hkv, D, tp, lengths):
+    """up_score_blocks_tp == sharded_block_scores + allreduce_scores (tp_sim.cpp:12-49):
+    every shard within rtol of the reference shard, the reduction bitwise equal to the
+    ascending-shard fp32 sum of the returned shard partials."""
+    cfg = dict(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99)
+    sb = make_batch(lengths, Hq, Hkv, D, 64, regime="planted", seed=len(lengths) * 31 + D)
+    res = up.score_blocks_tp(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), tp, up.HeadLayout(Hq, Hkv, D),
+                             check=True)
+    cub = res.cu_blocks.cpu().numpy()
+    cu = sb.cu_seqlens.cpu().numpy()
+    shards = res.shard_scores.cpu().numpy()
+    red = res.block_scores.cpu().numpy()
+    nb = int(cub[-1])
+    want_red = np.zeros(nb, np.float32)
+    for t in range(tp):
+        want_red = (want_red + shards[t, :nb]).astype(np.float32)
+    assert np.array_equal(red[:nb].view(np.uint32), want_red.view(np.uint32))
+    for r in range(len(lengths)):
+        s, e = int(cu[r]), int(cu[r + 1])
+        q = sb.q[s:e].float().reshape(e - s, -1).cpu().numpy()
+        k = sb.k[s:e].float().reshape(e - s, -1).cpu().numpy()
+        ref_shards, ref_red = ref.sharded_allreduce(q, k, Hq, Hkv, tp, **cfg)
+        for t in range(tp):
+            _assert_blocks_close(shards[t, cub[r]:cub[r + 1]], ref_shards[t])
+        _assert_blocks_close(red[cub[r]:cub[r + 1]], ref_red)
+
+
+def test_score_blocks_tp_rejects_bad_degree(up):
+    sb = make_batch([200], 8, 2, 128, 64, seed=1)
+    for tp in (0, 3):
+        with pytest.raises(up.ConfigError):
+            up.score_blocks_tp(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(), tp, up.HeadLayout(8, 2, 128))
