@@ -319,7 +319,8 @@ def compact_varlen(keep: torch.Tensor, cu_seqlens, planes: Sequence[torch.Tensor
                    max_tokens: Optional[int] = None, outs: Optional[Sequence[torch.Tensor]] = None,
                    workspace: Optional[Workspace] = None, result: Optional[Compacted] = None,
                    check: bool = False) -> Compacted:
-    """Segmented prefix sum + gather of retained rows (up_compact).  planes: [T, ...] tensors."""
+    """Segmented prefix sum + gather of retained rows (up_compact).  planes: [T, ...] tensors on
+    the device, or in pinned host memory (read in place: only retained rows cross PCIe)."""
     dev = keep.device
     cu = _as_i32_cuda(cu_seqlens, dev)
     R = cu.numel() - 1
@@ -338,6 +339,11 @@ def compact_varlen(keep: torch.Tensor, cu_seqlens, planes: Sequence[torch.Tensor
     for i, (src, dst) in enumerate(zip(planes, result.planes)):
         if not (src.is_contiguous() and dst.is_contiguous()):
             raise ContractViolation("compact planes must be contiguous")
+        if dst.device != dev or (src.device != dev and not (src.device.type == "cpu" and src.is_pinned())):
+            # A source plane may live in pinned host memory: under unified addressing the
+            # copy kernel reads it in place over PCIe, so only the retained rows cross the bus.
+            raise ContractViolation("compact planes: sources on the keep mask's device or pinned host, "
+                                    "destinations on the device")
         rb = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
         arr[i] = PlaneC(src.data_ptr(), dst.data_ptr(), rb, 0, 0)
     st = lib.up_compact(_stream_ptr(dev), ctypes.byref(b), _ptr(keep), arr, len(planes),

@@ -13,5 +13,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 520 --csv \
     --log-file "$OUT/launches.csv" $BENCH > "$OUT/launches_bench.log" 2>&1 || true
 
 ncu --set full --clock-control none --import-source on \
-    -k regex:'score_tc|compact_copy|select_radix|block_combine|expand_kernel' -s 7 -c 5 \
+    -k regex:'score_tcw|compact_copy|select_radix|block_combine|pair_weights|expand_kernel' -s 12 -c 6 \
     -o "$OUT/prof_full" -f $BENCH > "$OUT/prof_full.log" 2>&1 || true

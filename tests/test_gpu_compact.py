@@ -109,3 +109,29 @@ def test_compact_capacity_larger_than_batch(up, port):
     idx = np.flatnonzero(keep[:T])
     assert torch.equal(res.planes[0][:n], hid[torch.from_numpy(idx).cuda()])
     assert res.cu_seqlens.cpu().tolist() == [0, int(keep[:500].sum()), n]
+
+
+def test_compact_reads_pinned_host_planes_in_place(up):
+    """Source planes in pinned host memory are gathered in place (zero-copy over PCIe):
+    byte-identical to compacting the same planes from device memory."""
+    g = torch.Generator().manual_seed(9)
+    lengths = [3000, 1, 1700]
+    T = sum(lengths)
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(lengths)]), dtype=torch.int32, device="cuda")
+    keep = (torch.rand(T, generator=g) < 0.3).to(torch.uint8).cuda()
+    hid_h = torch.randn(T, 4096, generator=g).to(torch.bfloat16).pin_memory()
+    v_h = torch.randn(T, 2, 128, generator=g).to(torch.bfloat16).pin_memory()
+    pos_h = torch.arange(T, dtype=torch.int64).pin_memory()
+    k_d = torch.randn(T, 2, 128, generator=g).to(torch.bfloat16).cuda()
+    outs = [torch.empty(T, 4096, dtype=torch.bfloat16, device="cuda"), torch.empty_like(k_d),
+            torch.empty(T, 2, 128, dtype=torch.bfloat16, device="cuda"),
+            torch.empty(T, dtype=torch.int64, device="cuda")]
+    res = up.compact_varlen(keep, cu, [hid_h, k_d, v_h, pos_h], outs=outs, check=True)
+    want = up.compact_varlen(keep, cu, [hid_h.cuda(), k_d, v_h.cuda(), pos_h.cuda()], check=True)
+    n = int(res.num_out.item())
+    assert n == int(want.num_out.item()) == int(keep.sum().item())
+    assert torch.equal(res.cu_seqlens, want.cu_seqlens)
+    for a, b in zip(res.planes, want.planes):
+        assert torch.equal(a[:n], b[:n])
+    with pytest.raises(up.ContractViolation):  # pageable host memory is rejected
+        up.compact_varlen(keep, cu, [torch.zeros(T, 8)], outs=[torch.empty(T, 8, device="cuda")])
