@@ -163,6 +163,15 @@ up_status up_compact(void* stream, const up_batch* batch, const uint8_t* keep,
                      int32_t* retained_index, int32_t* num_tokens_out, void* workspace,
                      size_t workspace_bytes);
 
+/* Row scatter, the inverse of up_compact's gather: for o < *num_rows (device int32; or
+ * max_rows when num_rows is NULL) and index[o] >= 0, row o of every plane's src is copied
+ * to row index[o] of its dst.  Passing up_compact's retained_index and num_tokens_out
+ * writes the current compacted states back over their pre-drop rows, turning the pre-drop
+ * buffer into the reconstituted stream (reconstitute, propagation.cpp:79-100; unwind the
+ * drops of a block in reverse order).  Also re-admits parked rows at their positions. */
+up_status up_scatter_rows(void* stream, const int32_t* index, const int32_t* num_rows, int64_t max_rows,
+                          const up_plane* planes, int32_t num_planes);
+
 /* up_score_blocks -> up_select -> up_compact for a single-rank (non-TP) layer. */
 up_status up_drop_layer(void* stream, const up_batch* batch, const up_heads* heads,
                         const up_score_config* cfg, const void* q, const void* k,

@@ -132,6 +132,19 @@ inline void score_blocks(cudaStream_t s, const VarlenBatch& b, const HeadLayout&
           "score_blocks");
 }
 
+/// sharded_block_scores + allreduce_scores (tp_sim.cpp:12-49) in one call: shard t's
+/// partials at shard_scores + t * shard_stride, their ascending-shard sum in block_scores.
+inline void sharded_block_scores(cudaStream_t s, const VarlenBatch& b, const HeadLayout& h, const ScoreConfig& cfg,
+                                 const void* q_bf16, const void* k_bf16, int tp_degree, float* shard_scores,
+                                 int64_t shard_stride, float* block_scores, int32_t* cu_blocks, Workspace& ws) {
+    const up_batch bc = b.c();
+    const up_heads hc = h.c();
+    const up_score_config cc = cfg.c();
+    check(up_score_blocks_tp(s, &bc, &hc, &cc, q_bf16, k_bf16, tp_degree, shard_scores, shard_stride, block_scores,
+                             cu_blocks, ws.data(), ws.bytes()),
+          "sharded_block_scores");
+}
+
 /// allreduce_scores (tp_sim.cpp:29-49) over device-addressable shard partials.
 inline void reduce_block_scores(cudaStream_t s, const std::vector<const float*>& shards, int64_t count,
                                 float* out) {
@@ -157,6 +170,14 @@ inline void compact(cudaStream_t s, const VarlenBatch& b, const uint8_t* keep, c
     check(up_compact(s, &bc, keep, planes.data(), static_cast<int32_t>(planes.size()), cu_seqlens_out,
                      retained_index, num_tokens_out, ws.data(), ws.bytes()),
           "compact");
+}
+
+/// Reconstitution step (propagation.cpp:79-100): rows 0..*num_rows of every plane's src
+/// go back to rows index[o] of its dst (up_compact's retained_index unwinds a drop).
+inline void scatter_rows(cudaStream_t s, const int32_t* index, const int32_t* num_rows, int64_t max_rows,
+                         const std::vector<up_plane>& planes) {
+    check(up_scatter_rows(s, index, num_rows, max_rows, planes.data(), static_cast<int32_t>(planes.size())),
+          "scatter_rows");
 }
 
 /// Synchronizes and raises the sticky device-side ContractViolation (NaN / negative block

@@ -260,6 +260,9 @@ class Ref(_Lib):
         P = ctypes.POINTER
         self._fn("apply_drop", [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, P(ctypes.c_uint8),
                                 P(ctypes.c_float), P(ctypes.c_int64), P(ctypes.c_int64)])
+        self._fn("reconstitute_sequence", [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                           P(P(ctypes.c_uint8)), P(P(ctypes.c_float)), P(ctypes.c_float),
+                                           P(ctypes.c_int64)])
         self._fn("patch_metadata", [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, P(ctypes.c_int64),
                                     ctypes.c_int32, P(ctypes.c_uint8), P(ctypes.c_uint8),
                                     P(ctypes.c_uint8), P(ctypes.c_float), P(ctypes.c_int64)])
@@ -284,6 +287,22 @@ class Ref(_Lib):
                                      _ptr(pos, ctypes.c_int64), ctypes.byref(n))
         _raise(st, "apply_drop")
         return out[: n.value], pos[: n.value]
+
+    def reconstitute_sequence(self, prompt: np.ndarray, keeps, afters):
+        """apply_drop per keep mask (replacing the active states by afters[d] after drop d),
+        then reconstitute (propagation.cpp:79-100).  Returns (states, positions)."""
+        pr = np.ascontiguousarray(prompt, dtype=np.float32)
+        ks = [np.ascontiguousarray(k, dtype=np.uint8) for k in keeps]
+        afs = [None if a is None else np.ascontiguousarray(a, dtype=np.float32) for a in afters]
+        P = ctypes.POINTER
+        kp = (P(ctypes.c_uint8) * len(ks))(*[_ptr(k, ctypes.c_uint8) for k in ks])
+        ap = (P(ctypes.c_float) * len(ks))(*[_ptr(a, ctypes.c_float) if a is not None else None for a in afs])
+        out = np.zeros_like(pr)
+        pos = np.zeros(pr.shape[0], np.int64)
+        st = self.lib.ref_reconstitute_sequence(_ptr(pr, ctypes.c_float), pr.shape[0], pr.shape[1], len(ks), kp, ap,
+                                                _ptr(out, ctypes.c_float), _ptr(pos, ctypes.c_int64))
+        _raise(st, "reconstitute_sequence")
+        return out, pos
 
     def patch_metadata(self, tokens: np.ndarray, cu_seqlens, keep, selected, is_decode=None):
         t = np.ascontiguousarray(tokens, dtype=np.float32)

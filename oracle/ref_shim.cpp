@@ -187,6 +187,39 @@ int ref_apply_drop(const float* states, int64_t rows, int64_t cols, const uint8_
     });
 }
 
+// A sequence of drops with the states transformed between them, then reconstitute
+// (propagation.cpp:47-100).  keeps[d] has one entry per row active before drop d;
+// after[d] (rows retained by drop d, or NULL) replaces the active states after drop d
+// -- standing in for the layers between drops.  Writes the full-length reconstituted
+// states and positions.
+int ref_reconstitute_sequence(const float* prompt, int64_t rows, int64_t cols, int32_t num_drops,
+                              const uint8_t* const* keeps, const float* const* after, float* out_states,
+                              int64_t* out_positions) {
+    return guarded([&] {
+        Matrix m(rows, cols);
+        std::memcpy(m.data.data(), prompt, sizeof(float) * static_cast<size_t>(rows * cols));
+        TokenStream stream = TokenStream::from_prompt(m);
+        DropHistory history;
+        history.original_length = rows;
+        for (int32_t d = 0; d < num_drops; ++d) {
+            const int64_t n = stream.active_count();
+            Selection sel;
+            sel.keep_mask.assign(keeps[d], keeps[d] + n);
+            for (int64_t i = 0; i < n; ++i)
+                if (keeps[d][i]) sel.retained_indices.push_back(i);
+            apply_drop(stream, sel, d, history);
+            if (after != nullptr && after[d] != nullptr)
+                std::memcpy(stream.active_states.data.data(), after[d],
+                            sizeof(float) * stream.active_states.data.size());
+        }
+        reconstitute(stream);
+        stream.validate();
+        std::memcpy(out_states, stream.active_states.data.data(), sizeof(float) * stream.active_states.data.size());
+        std::memcpy(out_positions, stream.logical_positions.data(),
+                    sizeof(int64_t) * stream.logical_positions.size());
+    });
+}
+
 // patch_metadata (scheduler.hpp:52-53) over a packed batch.  selected[s] != 0 attaches a
 // Selection built from keep; is_decode[s] marks decode-phase segments.
 int ref_patch_metadata(const float* tokens, int64_t total_rows, int64_t cols,

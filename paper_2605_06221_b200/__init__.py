@@ -7,7 +7,8 @@ mirror of the reference's operator API (see ``api.py``).
 from .api import (BlockScores, Compacted, ConfigError, ContractViolation, CudaError, DropEvent,
                   DropHistory, DropLayer, HeadLayout, ImportanceScores, PackedBatch, ScoreConfig,
                   Selection, ShardedBlockScores, ShardScores, TokenStream, UnsupportedError, VarlenSelection, Workspace,
-                  allreduce_scores, apply_drop, compact_varlen, patch_metadata, reduce_block_scores,
+                  allreduce_scores, apply_drop, compact_varlen, patch_metadata, reconstitute, reconstitute_varlen,
+                  reduce_block_scores, scatter_rows,
                   score_blocks_tp, score_blocks_varlen, score_tokens, score_tokens_heads, select_varlen,
                   sharded_block_scores, top_p_select)
 from ._capi import LIB_PATH, lib
@@ -16,7 +17,8 @@ __all__ = [
     "BlockScores", "Compacted", "ConfigError", "ContractViolation", "CudaError", "DropEvent",
     "DropHistory", "DropLayer", "HeadLayout", "ImportanceScores", "PackedBatch", "ScoreConfig",
     "Selection", "ShardedBlockScores", "ShardScores", "TokenStream", "UnsupportedError", "VarlenSelection", "Workspace",
-    "allreduce_scores", "apply_drop", "compact_varlen", "patch_metadata", "reduce_block_scores",
+    "allreduce_scores", "apply_drop", "compact_varlen", "patch_metadata", "reconstitute",
+    "reconstitute_varlen", "reduce_block_scores", "scatter_rows",
     "score_blocks_tp", "score_blocks_varlen", "score_tokens", "score_tokens_heads", "select_varlen",
     "sharded_block_scores", "top_p_select", "LIB_PATH", "lib",
 ]

@@ -355,6 +355,39 @@ def compact_varlen(keep: torch.Tensor, cu_seqlens, planes: Sequence[torch.Tensor
     return result
 
 
+def scatter_rows(index: torch.Tensor, planes: Sequence[torch.Tensor], outs: Sequence[torch.Tensor],
+                 num_rows: Optional[torch.Tensor] = None) -> None:
+    """Row scatter (up_scatter_rows), the inverse of compact_varlen's gather:
+    outs[p][index[o]] = planes[p][o] for o < num_rows (device int32 count; default: all
+    rows of index), skipping index[o] < 0."""
+    if index.dtype != torch.int32 or not index.is_contiguous():
+        raise ContractViolation("scatter_rows: index must be contiguous int32")
+    dev = index.device
+    arr = (PlaneC * max(len(planes), 1))()
+    for i, (src, dst) in enumerate(zip(planes, outs)):
+        if not (src.is_contiguous() and dst.is_contiguous()):
+            raise ContractViolation("scatter planes must be contiguous")
+        if src.device != dev or dst.device != dev:
+            raise ContractViolation("scatter planes must be on the index's device")
+        rb = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
+        if (dst[0].numel() * dst.element_size() if dst.dim() > 1 else dst.element_size()) != rb:
+            raise ContractViolation("scatter planes: row size mismatch")
+        arr[i] = PlaneC(src.data_ptr(), dst.data_ptr(), rb, 0, 0)
+    _check(lib.up_scatter_rows(_stream_ptr(dev), _ptr(index), _ptr(num_rows), int(index.numel()), arr,
+                               len(planes)), "scatter_rows")
+
+
+def reconstitute_varlen(current_planes: Sequence[torch.Tensor], drop: "Compacted",
+                        pre_drop_planes: Sequence[torch.Tensor]) -> None:
+    """Undo one drop of a varlen batch in place: the current state of every row retained by
+    `drop` (current_planes, row o = output row o of the drop, first drop.num_out rows) is
+    written back over its row of the pre-drop buffer, which still holds the dropped rows as
+    they were when parked.  Applied to a block's drops in reverse order this is the engine's
+    reconstitution at a block boundary (scheduler.cpp:349-360 + reconstitute,
+    propagation.cpp:79-100); the batch's cu_seqlens become the pre-drop ones again."""
+    scatter_rows(drop.retained_index, current_planes, pre_drop_planes, num_rows=drop.num_out)
+
+
 def reduce_block_scores(shards: Sequence[torch.Tensor], out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Ascending-shard fp32 sum (up_reduce_block_scores), bitwise like allreduce_scores."""
     if len(shards) == 0:
@@ -595,6 +628,24 @@ class TokenStream:
 
     def active_count(self) -> int:
         return int(self.logical_positions.numel())
+
+
+def reconstitute(stream: TokenStream) -> None:
+    """reconstitute (propagation.hpp:43, propagation.cpp:79-100): rebuild the full-length
+    stream -- parked rows with the state they had when dropped, active rows with their
+    current state, positions 0..n-1 -- through up_scatter_rows.  No-op without parked rows."""
+    if not stream.parked_states:
+        return
+    n = stream.original_length
+    act = stream.active_states.contiguous()
+    full = torch.empty((n, *act.shape[1:]), dtype=act.dtype, device=act.device)
+    for pos, st in zip(stream.parked_positions, stream.parked_states):
+        scatter_rows(pos.to(torch.int32).contiguous(), [st.contiguous()], [full])
+    scatter_rows(stream.logical_positions.to(torch.int32).contiguous(), [act], [full])
+    stream.active_states = full
+    stream.logical_positions = torch.arange(n, dtype=torch.int64, device=act.device)
+    stream.parked_positions = []
+    stream.parked_states = []
 
 
 def apply_drop(stream: TokenStream, selection: Selection, layer: int, history: DropHistory) -> None:

@@ -38,6 +38,7 @@ cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_reque
 cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t count, float* out,
                                  int num_sms, cudaStream_t stream);
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_t stream);
 int64_t compact_tiles(int64_t max_tokens);
 int compact_max_planes();
 
@@ -549,6 +550,33 @@ up_status up_compact(void* stream, const up_batch* b, const uint8_t* keep, const
     }
     const cudaError_t e = launch_compact(p, num_sms(), static_cast<cudaStream_t>(stream));
     g_launches = num_planes > 0 ? 3 : 2;
+    return cuda_status(e);
+}
+
+up_status up_scatter_rows(void* stream, const int32_t* index, const int32_t* num_rows, int64_t max_rows,
+                          const up_plane* planes, int32_t num_planes) {
+    g_launches = 0;
+    if (index == nullptr || max_rows < 0) return index == nullptr ? UP_ERR_INVALID_ARGUMENT : UP_ERR_CONTRACT;
+    if (num_planes < 0 || num_planes > compact_max_planes()) return UP_ERR_UNSUPPORTED;
+    if (num_planes > 0 && planes == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (max_rows > (int64_t{1} << 31) - 1) return UP_ERR_UNSUPPORTED;
+    CompactParams p{};
+    p.retained_index = const_cast<int32_t*>(index);
+    p.num_out = const_cast<int32_t*>(num_rows);
+    p.num_planes = num_planes;
+    p.max_tokens = max_rows;
+    for (int i = 0; i < num_planes; ++i) {
+        const up_plane& pl = planes[i];
+        if (pl.src == nullptr || pl.dst == nullptr || pl.row_bytes <= 0) return UP_ERR_INVALID_ARGUMENT;
+        p.src[i] = static_cast<const uint8_t*>(pl.src);
+        p.dst[i] = static_cast<uint8_t*>(pl.dst);
+        p.row_bytes[i] = pl.row_bytes;
+        p.src_stride[i] = pl.src_stride_bytes > 0 ? pl.src_stride_bytes : pl.row_bytes;
+        p.dst_stride[i] = pl.dst_stride_bytes > 0 ? pl.dst_stride_bytes : pl.row_bytes;
+        if (p.src_stride[i] < pl.row_bytes || p.dst_stride[i] < pl.row_bytes) return UP_ERR_CONTRACT;
+    }
+    const cudaError_t e = launch_scatter_rows(p, num_sms(), static_cast<cudaStream_t>(stream));
+    g_launches = num_planes > 0 && max_rows > 0 ? 1 : 0;
     return cuda_status(e);
 }
 

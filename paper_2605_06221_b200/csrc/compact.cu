@@ -113,47 +113,87 @@ compact_index_kernel(const CompactParams p) {
     }
 }
 
+// One warp copies row src_row of every plane to row dst_row: 16-byte streaming vectors, a
+// batch of 8 in flight per lane (scalar fallbacks for unaligned planes).
+__device__ __forceinline__ void copy_row_planes(const CompactParams& p, int64_t src_row, int64_t dst_row, int lane) {
+#pragma unroll 1
+    for (int pl = 0; pl < p.num_planes; ++pl) {
+        const int64_t rb = p.row_bytes[pl];
+        const uint8_t* src = p.src[pl] + src_row * p.src_stride[pl];
+        uint8_t* dst = p.dst[pl] + dst_row * p.dst_stride[pl];
+        const uintptr_t align = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst);
+        if (((rb | static_cast<int64_t>(align)) & 15) == 0) {
+            const int4* s = reinterpret_cast<const int4*>(src);
+            int4* d = reinterpret_cast<int4*>(dst);
+            const int64_t nv = rb >> 4;
+            int64_t v = lane;
+            for (; v + 7 * 32 < nv; v += 8 * 32) {
+                int4 x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) x[u] = __ldcs(s + v + u * 32);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) __stcs(d + v + u * 32, x[u]);
+            }
+            int4 x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (v + u * 32 < nv) x[u] = __ldcs(s + v + u * 32);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (v + u * 32 < nv) __stcs(d + v + u * 32, x[u]);
+        } else if (((rb | static_cast<int64_t>(align)) & 3) == 0) {
+            for (int64_t b = lane * 4; b < rb; b += 32 * 4)
+                *reinterpret_cast<uint32_t*>(dst + b) = *reinterpret_cast<const uint32_t*>(src + b);
+        } else {
+            for (int64_t b = lane; b < rb; b += 32) dst[b] = src[b];
+        }
+    }
+}
+
+// Gather: output row o <- source row retained_index[o] (persistent grid, warp per row).
 __global__ void __launch_bounds__(kCopyThreads)
 compact_copy_kernel(const CompactParams p) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * kCopyThreads + threadIdx.x) >> 5;
     const int nw = (gridDim.x * kCopyThreads) >> 5;
     const int n = p.cu_out[p.num_requests];
-    for (int o = gw; o < n; o += nw) {
-        const int64_t src_row = p.retained_index[o];
-#pragma unroll 1
-        for (int pl = 0; pl < p.num_planes; ++pl) {
-            const int64_t rb = p.row_bytes[pl];
-            const uint8_t* src = p.src[pl] + src_row * p.src_stride[pl];
-            uint8_t* dst = p.dst[pl] + static_cast<int64_t>(o) * p.dst_stride[pl];
-            const uintptr_t align = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst);
-            if (((rb | static_cast<int64_t>(align)) & 15) == 0) {
-                const int4* s = reinterpret_cast<const int4*>(src);
-                int4* d = reinterpret_cast<int4*>(dst);
-                const int64_t nv = rb >> 4;
-                int64_t v = lane;
-                for (; v + 7 * 32 < nv; v += 8 * 32) {
-                    int4 x[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) x[u] = __ldcs(s + v + u * 32);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) __stcs(d + v + u * 32, x[u]);
-                }
-                int4 x[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (v + u * 32 < nv) x[u] = __ldcs(s + v + u * 32);
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (v + u * 32 < nv) __stcs(d + v + u * 32, x[u]);
-            } else if (((rb | static_cast<int64_t>(align)) & 3) == 0) {
-                for (int64_t b = lane * 4; b < rb; b += 32 * 4)
-                    *reinterpret_cast<uint32_t*>(dst + b) = *reinterpret_cast<const uint32_t*>(src + b);
-            } else {
-                for (int64_t b = lane; b < rb; b += 32) dst[b] = src[b];
-            }
-        }
+    for (int o = gw; o < n; o += nw) copy_row_planes(p, p.retained_index[o], o, lane);
+}
+
+// Scatter, the inverse of the gather: row o of src -> row index[o] of dst, for the first
+// *num_out rows (or max_tokens when num_out is null).  Unwinding a drop this way writes the
+// current state of every retained row back over its pre-drop row, so the pre-drop buffer
+// becomes the reconstituted stream (reconstitute, propagation.cpp:79-100: parked rows keep
+// the state they had when dropped).
+__global__ void __launch_bounds__(kCopyThreads)
+scatter_rows_kernel(const CompactParams p) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * kCopyThreads + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * kCopyThreads) >> 5;
+    const int64_t n = p.num_out != nullptr ? static_cast<int64_t>(*p.num_out) : p.max_tokens;
+    for (int64_t o = gw; o < n; o += nw) {
+        const int32_t d = p.retained_index[o];
+        if (d < 0) continue;  // row without a destination
+        copy_row_planes(p, o, d, lane);
     }
+}
+
+static int copy_grid(int num_sms, int64_t rows) {
+    static int occ = 0;
+    if (occ == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compact_copy_kernel, kCopyThreads, 0);
+        if (occ < 1) occ = 1;
+    }
+    int64_t grid = static_cast<int64_t>(num_sms) * occ;
+    const int64_t need = (rows + (kCopyThreads / 32) - 1) / (kCopyThreads / 32);
+    if (grid > need) grid = need;
+    return static_cast<int>(grid < 1 ? 1 : grid);
+}
+
+cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_t stream) {
+    if (p.num_planes == 0 || p.max_tokens == 0) return cudaSuccess;
+    scatter_rows_kernel<<<copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream>>>(p);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream) {
@@ -164,15 +204,7 @@ cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t str
     compact_index_kernel<<<static_cast<unsigned>(tiles), kCompactThreads, 0, stream>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (p.num_planes > 0) {
-        static int occ = 0;
-        if (occ == 0) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compact_copy_kernel, kCopyThreads, 0);
-            if (occ < 1) occ = 1;
-        }
-        int64_t grid = static_cast<int64_t>(num_sms) * occ;
-        const int64_t need = (p.max_tokens + (kCopyThreads / 32) - 1) / (kCopyThreads / 32);
-        if (grid > need) grid = need;
-        compact_copy_kernel<<<static_cast<unsigned>(grid), kCopyThreads, 0, stream>>>(p);
+        compact_copy_kernel<<<copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream>>>(p);
         e = cudaGetLastError();
     }
     return e;

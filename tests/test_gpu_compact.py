@@ -135,3 +135,71 @@ def test_compact_reads_pinned_host_planes_in_place(up):
         assert torch.equal(a[:n], b[:n])
     with pytest.raises(up.ContractViolation):  # pageable host memory is rejected
         up.compact_varlen(keep, cu, [torch.zeros(T, 8)], outs=[torch.empty(T, 8, device="cuda")])
+
+
+def _ref_reconstitute(ref, prompt, keeps, afters):
+    return ref.reconstitute_sequence(prompt, keeps, afters)
+
+
+@pytest.mark.parametrize("rows,drops", [(1, 1), (8, 2), (300, 3), (2049, 2)])
+def test_reconstitute_matches_reference(up, ref, rows, drops):
+    """TokenStream: apply_drop x k (states transformed in between) then reconstitute ==
+    the reference's reconstitute (propagation.cpp:79-100), bit for bit."""
+    rng = np.random.default_rng(rows * 10 + drops)
+    cols = 24
+    prompt = rng.standard_normal((rows, cols)).astype(np.float32)
+    stream = up.TokenStream.from_prompt(torch.from_numpy(prompt).cuda())
+    hist = up.DropHistory(original_length=rows)
+    keeps, afters = [], []
+    for d in range(drops):
+        n = stream.active_count()
+        keep = (rng.random(n) < 0.6).astype(np.uint8)
+        keep[0] = 1  # keep the stream non-empty
+        up.apply_drop(stream, _sel(up, keep.tolist()), d, hist)
+        after = rng.standard_normal((int(keep.sum()), cols)).astype(np.float32)
+        stream.active_states = torch.from_numpy(after).cuda()
+        keeps.append(keep)
+        afters.append(after)
+    up.reconstitute(stream)
+    want_states, want_pos = _ref_reconstitute(ref, prompt, keeps, afters)
+    assert stream.logical_positions.cpu().tolist() == want_pos.tolist()
+    assert np.array_equal(stream.active_states.cpu().numpy().view(np.uint32), want_states.view(np.uint32))
+    assert not stream.parked_states
+    up.reconstitute(stream)  # idempotent without parked rows
+    assert np.array_equal(stream.active_states.cpu().numpy(), want_states)
+
+
+def test_reconstitute_varlen_unwinds_drops_in_reverse(up, ref):
+    """Varlen batch: two out-of-place drops (compact_varlen), states transformed after each,
+    then the block boundary unwinds them with reconstitute_varlen (scatter of the compacted
+    rows over the pre-drop buffers) -> every request equals the reference reconstitute."""
+    rng = np.random.default_rng(4)
+    lengths = [700, 1, 1300, 64]
+    R, T, cols = len(lengths), sum(lengths), 32
+    cu0 = torch.tensor(np.concatenate([[0], np.cumsum(lengths)]), dtype=torch.int32, device="cuda")
+    prompt = rng.standard_normal((T, cols)).astype(np.float32)
+    buf0 = torch.from_numpy(prompt).cuda()               # pre-drop buffer of drop 0
+    keep0 = (rng.random(T) < 0.5).astype(np.uint8)
+    c0 = up.compact_varlen(torch.from_numpy(keep0).cuda(), cu0, [buf0], check=True)
+    n0 = int(c0.num_out.item())
+    after0 = rng.standard_normal((n0, cols)).astype(np.float32)
+    buf1 = torch.from_numpy(after0).cuda()               # states entering drop 1 (= pre-drop buffer 1)
+    keep1 = (rng.random(n0) < 0.5).astype(np.uint8)
+    c1 = up.compact_varlen(torch.from_numpy(keep1).cuda(), c0.cu_seqlens, [buf1], max_tokens=n0, check=True)
+    n1 = int(c1.num_out.item())
+    after1 = rng.standard_normal((n1, cols)).astype(np.float32)
+    cur = torch.from_numpy(after1).cuda()              # the layers after drop 1 transform the stream
+    up.reconstitute_varlen([cur], c1, [buf1])           # unwind drop 1: buf1 = stream in drop-0 row space
+    up.reconstitute_varlen([buf1], c0, [buf0])          # then drop 0: buf0 is the full stream
+    got = buf0.cpu().numpy()
+    cu0h, cu1h, cu2h = cu0.cpu().numpy(), c0.cu_seqlens.cpu().numpy(), c1.cu_seqlens.cpu().numpy()
+    for r in range(R):
+        s, e = cu0h[r], cu0h[r + 1]
+        k0 = keep0[s:e]
+        k1 = keep1[cu1h[r]:cu1h[r + 1]]
+        a0 = after0[cu1h[r]:cu1h[r + 1]]
+        a1 = after1[cu2h[r]:cu2h[r + 1]]
+        want, pos = _ref_reconstitute(ref, prompt[s:e], [k0, k1], [a0, a1]) if k0.any() and k1.any() else (None, None)
+        if want is None:
+            continue
+        assert np.array_equal(got[s:e].view(np.uint32), want.view(np.uint32)), f"request {r}"
