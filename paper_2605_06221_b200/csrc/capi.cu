@@ -30,7 +30,7 @@ cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int
 struct BlockCombineParams;
 struct PairWeightsParams;
 cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream);
-cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int num_sms,
                               cudaStream_t stream);
 cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request, int num_sms,
@@ -332,6 +332,11 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     cudaError_t e = plan.wide ? launch_score_tcw(D, hpc, qm, km, p, grid, stream)
                               : launch_score_tc(D, hpc, qm, km, p, grid, stream);
     if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
+    static const int skip_tail = [] {  // dev timing only: 1 = scorer only, 2 = + pair weights
+        const char* s = std::getenv("UP_SCORE_TAIL_SKIP");
+        return s ? std::atoi(s) : 0;
+    }();
+    if (skip_tail == 1) { g_launches = 1; return UP_OK; }
     PairWeightsParams wp{};
     wp.cu_seqlens = b->cu_seqlens;
     wp.cu_units = p.cu_units_out;
@@ -347,7 +352,10 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     wp.query_window_n = c->query_window_n;
     const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
     const int wgrid = static_cast<int>(wtasks < num_sms() * 8 ? wtasks : num_sms() * 8);
-    if ((e = launch_pair_weights(wp, wgrid, stream)) != cudaSuccess) return UP_ERR_CUDA;
+    // CTAs one (request, head-group) pair spans, for equal-length requests
+    const int items_est = grid / (R * nhg > 0 ? R * nhg : 1) + 2;
+    if ((e = launch_pair_weights(wp, wgrid, items_est, stream)) != cudaSuccess) return UP_ERR_CUDA;
+    if (skip_tail == 2) { g_launches = 2; return UP_OK; }
     BlockCombineParams bp{};
     bp.cu_seqlens = b->cu_seqlens;
     bp.cu_blocks = cu_blocks;
@@ -439,7 +447,7 @@ up_status up_score_blocks_tp(void* stream_, const up_batch* b, const up_heads* h
     if (shard_stride < up_max_blocks(b, c)) return UP_ERR_INVALID_ARGUMENT;
     const Layout L = layout_for(b, h, c);
     if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
-    if (tc_eligible(h, c, 0))
+    if (tc_eligible(h, c, 0) && tp <= 32)  // the combine holds one shard sum per lane
         return score_tc_path(stream, b, h, c, q, k, tp, shard_scores, shard_stride, block_scores, cu_blocks, L, ws);
     // Generic shapes: one SIMT scoring pass per shard, then the ordered shard sum.
     if (tp > 16) return UP_ERR_UNSUPPORTED;

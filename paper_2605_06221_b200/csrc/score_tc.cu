@@ -390,10 +390,19 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
 // denominators.  One CTA per (pair, head, 32-row chunk): warp w folds items w, w+8, ...
 // (lane = row, coalesced), the eight partial (M, L) are merged in warp order
 // (deterministic), then the warps write the weights.
-__global__ void __launch_bounds__(256)
+constexpr int kPwWarps = 16;
+
+__device__ __forceinline__ void lse_merge(float& M, float& L, float mc, float lc) {
+    if (mc == -INFINITY) return;
+    if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
+    else L += lc * ex2_approx(mc - M);
+}
+
+__global__ void __launch_bounds__(kPwWarps * 32)
 pair_weights_kernel(const PairWeightsParams p) {
-    __shared__ float sM[8][32], sL[8][32];
+    __shared__ float sM[kPwWarps][32], sL[kPwWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;  // <= kPwWarps, sized by the launcher to the item count
     const int R = p.num_requests, hpc = p.hpc, nhg = p.num_hgroups, npar = p.npar;
     Part P;
     P.cu_units = p.cu_units;
@@ -425,37 +434,40 @@ pair_weights_kernel(const PairWeightsParams p) {
             return b > seg_start ? b : seg_start;
         };
         // statistics rows of head hh: (sid * hpc + hh) * npar + par, par < npar (the
-        // parity warpgroups of score_tcw keep separate running (m, l) for one head)
+        // parity warpgroups of score_tcw keep separate running (m, l) for one head).
+        // Two items per warp iteration: their loads are issued before the merges.
         float M = -INFINITY, L = 0.f;
-        for (int k = warp; k < n_items; k += 8) {
-            const int64_t sid = sid_of(k);
-            if (sid < 0) continue;
-            for (int q = 0; q < npar; ++q) {
-                const int64_t x = ((sid * hpc + hh) * npar + q) * kRows + j;
-                const float mc = __ldcg(&p.stat_m[x]);
-                const float lc = __ldcg(&p.stat_l[x]);
-                if (mc == -INFINITY) continue;
-                if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
-                else L += lc * ex2_approx(mc - M);
+        for (int k = warp; k < n_items; k += 2 * nwarps) {
+            float mc[4], lc[4];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const int kk = k + x * nwarps;
+                const int64_t sid = kk < n_items ? sid_of(kk) : -1;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    mc[x * 2 + q] = -INFINITY;
+                    lc[x * 2 + q] = 0.f;
+                    if (sid >= 0 && q < npar) {
+                        const int64_t xx = ((sid * hpc + hh) * npar + q) * kRows + j;
+                        mc[x * 2 + q] = __ldcg(&p.stat_m[xx]);
+                        lc[x * 2 + q] = __ldcg(&p.stat_l[xx]);
+                    }
+                }
             }
+#pragma unroll
+            for (int y = 0; y < 4; ++y) lse_merge(M, L, mc[y], lc[y]);
         }
         sM[warp][lane] = M;
         sL[warp][lane] = L;
         __syncthreads();
         M = -INFINITY;
         L = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const float mc = sM[w][lane], lc = sL[w][lane];
-            if (mc == -INFINITY) continue;
-            if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
-            else L += lc * ex2_approx(mc - M);
-        }
+        for (int w = 0; w < nwarps; ++w) lse_merge(M, L, sM[w][lane], sL[w][lane]);
         __syncthreads();
         const bool valid = j < neff;
         if (valid && !(L > 0.f) && warp == 0) raise_error(p.err, kErrMaskedRow);
         const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
-        for (int k = warp; k < n_items; k += 8) {
+        for (int k = warp; k < n_items; k += nwarps) {
             const int64_t sid = sid_of(k);
             if (sid < 0) continue;
             for (int q = 0; q < npar; ++q) {
@@ -467,8 +479,11 @@ pair_weights_kernel(const PairWeightsParams p) {
     }
 }
 
-cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, cudaStream_t stream) {
-    pair_weights_kernel<<<grid, 256, 0, stream>>>(p);
+// items_per_pair: the launcher's estimate of the CTAs one pair spans (sizes the CTA).
+cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream) {
+    int warps = 2;
+    while (warps < kPwWarps && 2 * warps < items_per_pair) warps *= 2;
+    pair_weights_kernel<<<grid, warps * 32, 0, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -504,6 +519,45 @@ block_combine_kernel(const BlockCombineParams p) {
         // statistics row of head hh: hh * npar + (parity of the block's 64-key subtile)
         const int par = p.npar > 1 ? ((g * p.block_size_g) >> 6) % p.npar : 0;
         const int hpcv = p.hpc * p.npar;
+        if (T > 1) {
+            // Sharded: every head's dot product is reduced across the warp and added, in
+            // head order, to its shard's sum held by lane t = h / hps; loads of 8 heads
+            // are in flight together.
+            float shard_acc = 0.f;
+            for (int hg0 = 0; hg0 < nhg; hg0 += 32) {
+                const int my_hg = hg0 + lane;
+                const int my_sid = my_hg < nhg ? p.unit_sid[pair0 + static_cast<int64_t>(my_hg) * units_r + u] : 0;
+                const int h_end = min(p.num_heads, (hg0 + 32) * p.hpc);
+                for (int h = hg0 * p.hpc; h < h_end; h += 8) {
+                    float d[8];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        const int hx = min(h + x, h_end - 1);
+                        const int hgx = hx / p.hpc;
+                        const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
+                        const float4 pv = __ldcs(reinterpret_cast<const float4*>(
+                            p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
+                        const float4 wv = __ldg(reinterpret_cast<const float4*>(
+                            p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);
+                        d[x] = fmaf(pv.x, wv.x, fmaf(pv.y, wv.y, fmaf(pv.z, wv.z, pv.w * wv.w)));
+                    }
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        if (h + x >= h_end) break;
+                        float v = d[x];
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                        if (lane == (h + x) / hps) shard_acc += v;
+                    }
+                }
+            }
+            const float bt = shard_acc / static_cast<float>(size);
+            if (p.shard_scores != nullptr && lane < T) p.shard_scores[static_cast<int64_t>(lane) * p.shard_stride + gb] = bt;
+            float red = 0.f;
+            for (int t = 0; t < T; ++t) red += __shfl_sync(0xffffffffu, bt, t);  // ascending shard order
+            if (lane == 0) p.block_scores[gb] = red;
+            continue;
+        }
         float red = 0.f;
         for (int t = 0; t < T; ++t) {
             float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};

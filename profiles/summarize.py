@@ -1,6 +1,6 @@
 """Summarise the ncu outputs of profiles/run_profile.sh into committed files.
 
-    python profiles/summarize.py gpurun_out r01
+    python profiles/summarize.py gpurun_out r01 [SUFFIX CONFIG]   (e.g. _c3 c3: the Qwen3-Next capture)
 
 writes profiles/launches_<tag>.csv (per-kernel share of the step from the launch list),
 profiles/ncu_summary_<tag>.md (key metrics of the `--set full` captures) and
@@ -80,15 +80,19 @@ def to_bytes(v, unit):
 def main():
     src = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
     tag = sys.argv[2] if len(sys.argv) > 2 else "r01"
-    shares = launch_shares(os.path.join(src, "launches.csv"))
-    with open(os.path.join(HERE, f"launches_{tag}.csv"), "w") as f:
+    suffix = sys.argv[3] if len(sys.argv) > 3 else ""
+    config = sys.argv[4] if len(sys.argv) > 4 else "c2"
+    workload = {"c2": "LLaMA-3.1-8B layer shape, 4x32K", "c3": "Qwen3-Next-80B-A3B full-attn layer, 1x128K, TP=8 sharded",
+                "c4": "Gemma-3-12B layer shape, 16x64K"}.get(config, config)
+    shares = launch_shares(os.path.join(src, f"launches{suffix}.csv"))
+    with open(os.path.join(HERE, f"launches_{tag}{suffix}.csv"), "w") as f:
         f.write("kernel,launches,avg_ns,share_of_our_kernels\n")
         for k, n, avg, sh in shares:
             f.write(f"{k},{n},{avg:.0f},{sh:.4f}\n")
-    full = full_metrics(os.path.join(src, "prof_full.ncu-rep"))
+    full = full_metrics(os.path.join(src, f"prof_full{suffix}.ncu-rep"))
     traffic = {}
     lines = [f"# ncu summary ({tag})", "",
-             "Command: `profiles/run_profile.sh` (bench.py --config c2, LLaMA-3.1-8B layer shape, 4x32K, "
+             f"Command: `CONFIG={config} profiles/run_profile.sh` (bench.py --config {config}, {workload}, "
              "--no-graph, 2 activation sets); ncu --clock-control none.", "",
              "## Launch list (gpu__time_duration, cold-cache, serialised: compare shares)", "",
              "| kernel | launches | avg us | share of our kernels |", "|---|---|---|---|"]
@@ -105,10 +109,11 @@ def main():
             wr = to_bytes(*d["dram__bytes_write.sum"])
             traffic.setdefault(d["kernel"], rd + wr)
         lines.append("")
-    with open(os.path.join(HERE, f"ncu_summary_{tag}.md"), "w") as f:
+    with open(os.path.join(HERE, f"ncu_summary_{tag}{suffix}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    with open(os.path.join(HERE, "ncu_traffic.json"), "w") as f:
-        json.dump(traffic, f, indent=1)
+    if config == "c2":  # bench.py's roofline.traffic is quoted for the default workload
+        with open(os.path.join(HERE, "ncu_traffic.json"), "w") as f:
+            json.dump(traffic, f, indent=1)
     print("\n".join(lines))
 
 
