@@ -52,7 +52,8 @@ typedef enum {
     UP_ERR_UNSUPPORTED = 3,    /* valid input outside the implemented envelope */
     UP_ERR_WORKSPACE = 4,      /* workspace missing or too small */
     UP_ERR_CUDA = 5,           /* CUDA runtime / driver failure */
-    UP_ERR_INVALID_ARGUMENT = 6
+    UP_ERR_INVALID_ARGUMENT = 6,
+    UP_ERR_ALLOCATION_MISS = 7  /* AllocationMissError (errors.hpp:33-36) */
 } up_status;
 
 /* ScoreConfig (config.hpp:53-63).  Defaults: n=128, G=64, A=128, p=0.99. */
@@ -179,6 +180,26 @@ up_status up_drop_layer(void* stream, const up_batch* batch, const up_heads* hea
                         uint8_t* keep, const up_selection_out* sel, const up_plane* planes,
                         int32_t num_planes, int32_t* cu_seqlens_out, int32_t* retained_index,
                         int32_t* num_tokens_out, void* workspace, size_t workspace_bytes);
+
+/* Eq. 16 slot mapping for downstream layers (recompute_slots_after_drop, kvcache.cpp:147-158;
+ * slot_for, kvcache.cpp:67-80): for each row i < *num_rows (device; or max_rows when NULL)
+ * of the compacted batch (segments from cu_seqlens, R of them) and each of num_layers layers,
+ *   slots[l * slot_stride + i] = block_tables[(l * R + r_i) * max_pages + p_i / B] * B + p_i % B
+ * with p_i = positions[i].  A page the table does not hold writes -1 and raises the sticky
+ * UP_ERR_ALLOCATION_MISS flag (read by up_device_status). */
+up_status up_slot_mapping(void* stream, const int32_t* cu_seqlens, int32_t num_requests, const int32_t* num_rows,
+                          int64_t max_rows, const int64_t* positions, const int32_t* block_tables,
+                          int32_t num_layers, int32_t max_pages, int32_t block_size, int64_t* slots,
+                          int64_t slot_stride, void* workspace, size_t workspace_bytes);
+
+/* Eq. 17 per-layer decode KV length (decode_seqused, kvcache.cpp:182-186):
+ *   seqused[l * R + r] = len_k(r) + decode_appended[r]
+ * where len_k is segment r's length in cu_after[k] (device cu_seqlens after drop event k,
+ * HOST array of num_drops pointers) for the last drop with drop_layers[k] < l, else its
+ * length in cu_orig.  drop_layers (HOST) strictly increasing; decode_appended may be NULL. */
+up_status up_decode_seqused(void* stream, int32_t num_layers, int32_t num_requests, const int32_t* cu_orig,
+                            int32_t num_drops, const int32_t* drop_layers, const int32_t* const* cu_after,
+                            const int32_t* decode_appended, int32_t* seqused);
 
 /* Synchronizes `stream`, returns the sticky device-side status raised since the last call
  * (UP_OK if none) and clears it. */

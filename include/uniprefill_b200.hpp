@@ -45,6 +45,10 @@ class CudaError : public std::runtime_error {
 public:
     using std::runtime_error::runtime_error;
 };
+class AllocationMissError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
 
 inline void check(up_status s, const char* what) {
     if (s == UP_OK) return;
@@ -54,6 +58,7 @@ inline void check(up_status s, const char* what) {
     case UP_ERR_CONTRACT: throw ContractViolation(msg);
     case UP_ERR_UNSUPPORTED: throw UnsupportedError(msg);
     case UP_ERR_CUDA: throw CudaError(msg);
+    case UP_ERR_ALLOCATION_MISS: throw AllocationMissError(msg);
     default: throw std::runtime_error(msg);
     }
 }
@@ -178,6 +183,26 @@ inline void scatter_rows(cudaStream_t s, const int32_t* index, const int32_t* nu
                          const std::vector<up_plane>& planes) {
     check(up_scatter_rows(s, index, num_rows, max_rows, planes.data(), static_cast<int32_t>(planes.size())),
           "scatter_rows");
+}
+
+/// recompute_slots_after_drop (kvcache.cpp:147-158), Eq. 16: KV slots of the retained rows
+/// for num_layers downstream layers from their block tables [L][R][max_pages].
+inline void slot_mapping(cudaStream_t s, const VarlenBatch& compacted, const int32_t* num_rows, const int64_t* positions,
+                         const int32_t* block_tables, int32_t num_layers, int32_t max_pages, int32_t block_size,
+                         int64_t* slots, int64_t slot_stride, Workspace& ws) {
+    check(up_slot_mapping(s, compacted.cu_seqlens, compacted.num_requests, num_rows, compacted.max_tokens, positions,
+                          block_tables, num_layers, max_pages, block_size, slots, slot_stride, ws.data(), ws.bytes()),
+          "slot_mapping");
+}
+
+/// decode_seqused (kvcache.cpp:182-186), Eq. 17, for every (layer, request).
+inline void decode_seqused(cudaStream_t s, int32_t num_layers, int32_t num_requests, const int32_t* cu_orig,
+                           const std::vector<int32_t>& drop_layers, const std::vector<const int32_t*>& cu_after,
+                           const int32_t* decode_appended, int32_t* seqused) {
+    if (drop_layers.size() != cu_after.size()) throw ContractViolation("decode_seqused: one cu_seqlens per drop");
+    check(up_decode_seqused(s, num_layers, num_requests, cu_orig, static_cast<int32_t>(drop_layers.size()),
+                            drop_layers.data(), cu_after.data(), decode_appended, seqused),
+          "decode_seqused");
 }
 
 /// Synchronizes and raises the sticky device-side ContractViolation (NaN / negative block

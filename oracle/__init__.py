@@ -263,6 +263,10 @@ class Ref(_Lib):
         self._fn("reconstitute_sequence", [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                            P(P(ctypes.c_uint8)), P(P(ctypes.c_float)), P(ctypes.c_float),
                                            P(ctypes.c_int64)])
+        self._fn("recompute_slots", [ctypes.c_int, ctypes.c_int, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_int64,
+                                     ctypes.c_int64, P(ctypes.c_int32), P(ctypes.c_int64)])
+        self._fn("decode_seqused", [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, P(ctypes.c_int32),
+                                    P(ctypes.c_int64), ctypes.c_int32, P(ctypes.c_int64)])
         self._fn("patch_metadata", [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, P(ctypes.c_int64),
                                     ctypes.c_int32, P(ctypes.c_uint8), P(ctypes.c_uint8),
                                     P(ctypes.c_uint8), P(ctypes.c_float), P(ctypes.c_int64)])
@@ -303,6 +307,25 @@ class Ref(_Lib):
                                                 _ptr(out, ctypes.c_float), _ptr(pos, ctypes.c_int64))
         _raise(st, "reconstitute_sequence")
         return out, pos
+
+    def recompute_slots(self, num_layers: int, block_size: int, prealloc_len: int, retained, max_pages: int):
+        """PagedKVCache::recompute_slots_after_drop for one request -> (tables [L, max_pages], slots [L, n])."""
+        ret = np.ascontiguousarray(retained, dtype=np.int64)
+        tables = np.zeros((num_layers, max_pages), np.int32)
+        slots = np.zeros((num_layers, max(ret.size, 1)), np.int64)
+        st = self.lib.ref_recompute_slots(num_layers, block_size, prealloc_len, _ptr(ret, ctypes.c_int64), ret.size,
+                                          max_pages, _ptr(tables, ctypes.c_int32), _ptr(slots, ctypes.c_int64))
+        _raise(st, "recompute_slots")
+        return tables, slots[:, :ret.size]
+
+    def decode_seqused(self, original_length: int, decode_appended: int, event_layers, retained_lengths, layer: int):
+        el = np.ascontiguousarray(event_layers, dtype=np.int32)
+        rl = np.ascontiguousarray(retained_lengths, dtype=np.int64)
+        out = ctypes.c_int64(0)
+        st = self.lib.ref_decode_seqused(original_length, decode_appended, el.size, _ptr(el, ctypes.c_int32),
+                                         _ptr(rl, ctypes.c_int64), layer, ctypes.byref(out))
+        _raise(st, "decode_seqused")
+        return int(out.value)
 
     def patch_metadata(self, tokens: np.ndarray, cu_seqlens, keep, selected, is_decode=None):
         t = np.ascontiguousarray(tokens, dtype=np.float32)

@@ -9,6 +9,7 @@
 #include "uniprefill/errors.hpp"
 #include "uniprefill/importance.hpp"
 #include "uniprefill/propagation.hpp"
+#include "uniprefill/kvcache.hpp"
 #include "uniprefill/scheduler.hpp"
 #include "uniprefill/selection.hpp"
 #include "uniprefill/tp_sim.hpp"
@@ -217,6 +218,47 @@ int ref_reconstitute_sequence(const float* prompt, int64_t rows, int64_t cols, i
         std::memcpy(out_states, stream.active_states.data.data(), sizeof(float) * stream.active_states.data.size());
         std::memcpy(out_positions, stream.logical_positions.data(),
                     sizeof(int64_t) * stream.logical_positions.size());
+    });
+}
+
+// PagedKVCache::recompute_slots_after_drop (kvcache.cpp:147-158) for one request: pages
+// for positions [0, prealloc_len) are first allocated layer-interleaved (so physical ids
+// differ per layer), then the slots of the retained positions are recomputed (allocating
+// any missing page on demand).  Exports the resulting block tables [num_layers][max_pages]
+// (-1 = no page) and the slots [num_layers][n_ret].
+int ref_recompute_slots(int num_layers, int block_size, int64_t prealloc_len, const int64_t* retained,
+                        int64_t n_ret, int64_t max_pages, int32_t* tables, int64_t* slots) {
+    return guarded([&] {
+        PagedKVCache cache(num_layers, 8, block_size);
+        for (int64_t pos = 0; pos < prealloc_len; pos += block_size)
+            for (int l = num_layers - 1; l >= 0; --l) cache.ensure_slot(l, 0, pos);
+        std::vector<int> layers(static_cast<size_t>(num_layers));
+        for (int l = 0; l < num_layers; ++l) layers[static_cast<size_t>(l)] = l;
+        const auto out = cache.recompute_slots_after_drop(layers, 0, std::span<const int64_t>(retained, n_ret));
+        for (int l = 0; l < num_layers; ++l) {
+            for (int64_t i = 0; i < n_ret; ++i) slots[l * n_ret + i] = out[static_cast<size_t>(l)][static_cast<size_t>(i)];
+            for (int64_t pg = 0; pg < max_pages; ++pg)
+                tables[l * max_pages + pg] = cache.page_allocated(l, 0, pg * block_size)
+                                                 ? static_cast<int32_t>(cache.slot_for(l, 0, pg * block_size) / block_size)
+                                                 : -1;
+        }
+    });
+}
+
+// decode_seqused (kvcache.cpp:182-186) for one request's drop history.
+int ref_decode_seqused(int64_t original_length, int64_t decode_appended, int32_t num_events,
+                       const int32_t* event_layers, const int64_t* retained_lengths, int32_t layer, int64_t* out) {
+    return guarded([&] {
+        DropHistory h;
+        h.original_length = original_length;
+        h.decode_appended = decode_appended;
+        for (int32_t e = 0; e < num_events; ++e) {
+            DropEvent ev;
+            ev.layer = event_layers[e];
+            ev.retained_length = retained_lengths[e];
+            h.events.push_back(ev);
+        }
+        *out = decode_seqused(h, layer);
     });
 }
 

@@ -4,21 +4,21 @@ The compute lives in hand-written sm_100a kernels behind the C ABI in
 ``include/uniprefill_b200.h`` (``_lib/libuniprefill_b200.so``); this package is the host-side
 mirror of the reference's operator API (see ``api.py``).
 """
-from .api import (BlockScores, Compacted, ConfigError, ContractViolation, CudaError, DropEvent,
+from .api import (AllocationMissError, BlockScores, Compacted, ConfigError, ContractViolation, CudaError, DropEvent,
                   DropHistory, DropLayer, HeadLayout, ImportanceScores, PackedBatch, ScoreConfig,
                   Selection, ShardedBlockScores, ShardScores, TokenStream, UnsupportedError, VarlenSelection, Workspace,
                   allreduce_scores, apply_drop, compact_varlen, patch_metadata, reconstitute, reconstitute_varlen,
-                  reduce_block_scores, scatter_rows,
+                  reduce_block_scores, scatter_rows, slot_mapping, decode_seqused,
                   score_blocks_tp, score_blocks_varlen, score_tokens, score_tokens_heads, select_varlen,
                   sharded_block_scores, top_p_select)
 from ._capi import LIB_PATH, lib
 
 __all__ = [
-    "BlockScores", "Compacted", "ConfigError", "ContractViolation", "CudaError", "DropEvent",
+    "AllocationMissError", "BlockScores", "Compacted", "ConfigError", "ContractViolation", "CudaError", "DropEvent",
     "DropHistory", "DropLayer", "HeadLayout", "ImportanceScores", "PackedBatch", "ScoreConfig",
     "Selection", "ShardedBlockScores", "ShardScores", "TokenStream", "UnsupportedError", "VarlenSelection", "Workspace",
     "allreduce_scores", "apply_drop", "compact_varlen", "patch_metadata", "reconstitute",
-    "reconstitute_varlen", "reduce_block_scores", "scatter_rows",
+    "reconstitute_varlen", "reduce_block_scores", "scatter_rows", "slot_mapping", "decode_seqused",
     "score_blocks_tp", "score_blocks_varlen", "score_tokens", "score_tokens_heads", "select_varlen",
     "sharded_block_scores", "top_p_select", "LIB_PATH", "lib",
 ]

@@ -16,11 +16,11 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libuniprefill_b200.so")
 EXPORTED = (
     "up_abi_version", "up_status_string", "up_config_validate", "up_max_blocks",
     "up_workspace_bytes", "up_score_blocks", "up_score_blocks_tp", "up_reduce_block_scores", "up_select",
-    "up_compact", "up_scatter_rows", "up_drop_layer", "up_device_status", "up_scorer_kind", "up_last_launch_count",
+    "up_compact", "up_scatter_rows", "up_slot_mapping", "up_decode_seqused", "up_drop_layer", "up_device_status", "up_scorer_kind", "up_last_launch_count",
 )
 
 UP_OK, UP_ERR_CONFIG, UP_ERR_CONTRACT, UP_ERR_UNSUPPORTED, UP_ERR_WORKSPACE, UP_ERR_CUDA, \
-    UP_ERR_INVALID_ARGUMENT = range(7)
+    UP_ERR_INVALID_ARGUMENT, UP_ERR_ALLOCATION_MISS = range(8)
 
 
 class ScoreConfigC(ctypes.Structure):
@@ -73,6 +73,8 @@ def _load():
                       ctypes.c_int),
         "up_compact": ([vp, P(BatchC), vp, P(PlaneC), i32, vp, vp, vp, vp, sz], ctypes.c_int),
         "up_scatter_rows": ([vp, vp, vp, i64, P(PlaneC), i32], ctypes.c_int),
+        "up_slot_mapping": ([vp, vp, i32, vp, i64, vp, vp, i32, i32, i32, vp, i64, vp, sz], ctypes.c_int),
+        "up_decode_seqused": ([vp, i32, i32, vp, i32, P(i32), P(vp), vp, vp], ctypes.c_int),
         "up_drop_layer": ([vp, P(BatchC), P(HeadsC), P(ScoreConfigC), vp, vp, vp, vp, vp, vp,
                            P(SelectionOutC), P(PlaneC), i32, vp, vp, vp, vp, sz], ctypes.c_int),
         "up_device_status": ([vp, vp], ctypes.c_int),

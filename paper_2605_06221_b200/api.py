@@ -39,6 +39,10 @@ class UnsupportedError(RuntimeError):
     """Valid input outside the implemented envelope."""
 
 
+class AllocationMissError(RuntimeError):
+    """Reference AllocationMissError (errors.hpp:33-36): a KV slot whose page is absent."""
+
+
 class CudaError(RuntimeError):
     """CUDA runtime / driver failure."""
 
@@ -55,6 +59,8 @@ def _check(status: int, what: str) -> None:
         raise UnsupportedError(msg)
     if status == _capi.UP_ERR_CUDA:
         raise CudaError(msg)
+    if status == _capi.UP_ERR_ALLOCATION_MISS:
+        raise AllocationMissError(msg)
     raise RuntimeError(msg)
 
 
@@ -386,6 +392,53 @@ def reconstitute_varlen(current_planes: Sequence[torch.Tensor], drop: "Compacted
     reconstitution at a block boundary (scheduler.cpp:349-360 + reconstitute,
     propagation.cpp:79-100); the batch's cu_seqlens become the pre-drop ones again."""
     scatter_rows(drop.retained_index, current_planes, pre_drop_planes, num_rows=drop.num_out)
+
+
+def slot_mapping(cu_seqlens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor, block_size: int,
+                 num_rows: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                 workspace: Optional[Workspace] = None, check: bool = False) -> torch.Tensor:
+    """Eq. 16 KV slot mapping of the retained rows for downstream layers (up_slot_mapping;
+    recompute_slots_after_drop, kvcache.cpp:147-158).  cu_seqlens int32 [R+1] and positions
+    int64 [rows] of the compacted batch, block_tables int32 [L, R, max_pages] (-1 = no
+    page).  Returns int64 [L, rows]."""
+    dev = positions.device
+    cu = _as_i32_cuda(cu_seqlens, dev)
+    R = cu.numel() - 1
+    if block_tables.dim() != 3 or block_tables.shape[1] != R or block_tables.dtype != torch.int32:
+        raise ContractViolation("slot_mapping: block_tables must be int32 [layers, R, max_pages]")
+    L, _, max_pages = block_tables.shape
+    rows = positions.numel()
+    if out is None:
+        out = torch.empty(L, rows, dtype=torch.int64, device=dev)
+    ws = workspace or _ws(dev)
+    b = _batch(cu, max(rows, 1), None)
+    buf = ws.get(b, None, ScoreConfig(1, 1, 0, 1.0).c())
+    _check(lib.up_slot_mapping(_stream_ptr(dev), _ptr(cu), R, _ptr(num_rows), rows,
+                               _ptr(positions.contiguous()), _ptr(block_tables.contiguous()), L, max_pages,
+                               int(block_size), _ptr(out), out.stride(0), ctypes.c_void_p(buf.data_ptr()),
+                               buf.numel()), "slot_mapping")
+    if check:
+        ws.device_status()
+    return out
+
+
+def decode_seqused(num_layers: int, cu_orig: torch.Tensor, drop_layers: Sequence[int],
+                   cu_after: Sequence[torch.Tensor], decode_appended: Optional[torch.Tensor] = None,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Eq. 17 per-layer decode KV lengths (up_decode_seqused; decode_seqused,
+    kvcache.cpp:182-186) for every request: int32 [num_layers, R]."""
+    dev = cu_orig.device
+    cu0 = _as_i32_cuda(cu_orig, dev)
+    R = cu0.numel() - 1
+    cus = [_as_i32_cuda(c, dev) for c in cu_after]
+    if out is None:
+        out = torch.empty(num_layers, R, dtype=torch.int32, device=dev)
+    dl = (ctypes.c_int32 * max(len(drop_layers), 1))(*[int(x) for x in drop_layers])
+    ptrs = (ctypes.c_void_p * max(len(cus), 1))(*[c.data_ptr() for c in cus])
+    app = None if decode_appended is None else decode_appended.to(device=dev, dtype=torch.int32).contiguous()
+    _check(lib.up_decode_seqused(_stream_ptr(dev), int(num_layers), R, _ptr(cu0), len(cus), dl, ptrs,
+                                 _ptr(app), _ptr(out)), "decode_seqused")
+    return out
 
 
 def reduce_block_scores(shards: Sequence[torch.Tensor], out: Optional[torch.Tensor] = None) -> torch.Tensor:

@@ -29,6 +29,8 @@ cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int
                                uint32_t* err, cudaStream_t stream);
 struct BlockCombineParams;
 struct PairWeightsParams;
+struct SlotMapParams;
+struct SequsedParams;
 cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int num_sms,
@@ -39,6 +41,8 @@ cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t cou
                                  int num_sms, cudaStream_t stream);
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_slot_mapping(const SlotMapParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_decode_seqused(const SequsedParams& p, cudaStream_t stream);
 int64_t compact_tiles(int64_t max_tokens);
 int compact_max_planes();
 
@@ -251,6 +255,7 @@ const char* up_status_string(up_status s) {
     case UP_ERR_WORKSPACE: return "workspace missing or too small";
     case UP_ERR_CUDA: return "CUDA error";
     case UP_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case UP_ERR_ALLOCATION_MISS: return "AllocationMissError: KV page not allocated";
     }
     return "unknown status";
 }
@@ -605,6 +610,64 @@ up_status up_drop_layer(void* stream, const up_batch* b, const up_heads* h,
     return st;
 }
 
+up_status up_slot_mapping(void* stream, const int32_t* cu_seqlens, int32_t num_requests, const int32_t* num_rows,
+                          int64_t max_rows, const int64_t* positions, const int32_t* block_tables,
+                          int32_t num_layers, int32_t max_pages, int32_t block_size, int64_t* slots,
+                          int64_t slot_stride, void* ws, size_t ws_bytes) {
+    g_launches = 0;
+    if (cu_seqlens == nullptr || positions == nullptr || block_tables == nullptr || slots == nullptr || ws == nullptr)
+        return UP_ERR_INVALID_ARGUMENT;
+    if (num_requests < 1 || num_layers < 0 || max_pages < 1 || max_rows < 0) return UP_ERR_CONTRACT;
+    if (block_size <= 0) return UP_ERR_CONFIG;  // PagedKVCache: kv_block_size must be positive
+    if (slot_stride < max_rows) return UP_ERR_INVALID_ARGUMENT;
+    if (ws_bytes < 256) return UP_ERR_WORKSPACE;
+    if (num_layers == 0 || max_rows == 0) return UP_OK;
+    SlotMapParams p{};
+    p.cu_seqlens = cu_seqlens;
+    p.num_rows = num_rows;
+    p.positions = positions;
+    p.block_tables = block_tables;
+    p.slots = slots;
+    p.err = static_cast<uint32_t*>(ws);  // the sticky flags word at the workspace start
+    p.max_rows = max_rows;
+    p.slot_stride = slot_stride;
+    p.num_requests = num_requests;
+    p.num_layers = num_layers;
+    p.max_pages = max_pages;
+    p.block_size = block_size;
+    const cudaError_t e = launch_slot_mapping(p, num_sms(), static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return cuda_status(e);
+}
+
+up_status up_decode_seqused(void* stream, int32_t num_layers, int32_t num_requests, const int32_t* cu_orig,
+                            int32_t num_drops, const int32_t* drop_layers, const int32_t* const* cu_after,
+                            const int32_t* decode_appended, int32_t* seqused) {
+    g_launches = 0;
+    if (cu_orig == nullptr || seqused == nullptr || (num_drops > 0 && (drop_layers == nullptr || cu_after == nullptr)))
+        return UP_ERR_INVALID_ARGUMENT;
+    if (num_layers < 0 || num_requests < 1 || num_drops < 0) return UP_ERR_CONTRACT;
+    if (num_drops > kMaxDrops) return UP_ERR_UNSUPPORTED;
+    SequsedParams p{};
+    for (int d = 0; d < num_drops; ++d) {
+        // DropHistory::validate: layers strictly increasing (drop_history.hpp:27-29)
+        if (d > 0 && drop_layers[d] <= drop_layers[d - 1]) return UP_ERR_CONTRACT;
+        if (cu_after[d] == nullptr) return UP_ERR_INVALID_ARGUMENT;
+        p.drop_layers[d] = drop_layers[d];
+        p.cu_after[d] = cu_after[d];
+    }
+    if (num_layers == 0) return UP_OK;
+    p.cu_orig = cu_orig;
+    p.decode_appended = decode_appended;
+    p.seqused = seqused;
+    p.num_drops = num_drops;
+    p.num_layers = num_layers;
+    p.num_requests = num_requests;
+    const cudaError_t e = launch_decode_seqused(p, static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return cuda_status(e);
+}
+
 up_status up_device_status(void* stream, void* ws) {
     if (ws == nullptr) return UP_ERR_INVALID_ARGUMENT;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -617,6 +680,7 @@ up_status up_device_status(void* stream, void* ws) {
         if (cudaStreamSynchronize(s) != cudaSuccess) return UP_ERR_CUDA;
     }
     if (flags & kErrTooManyBlocks) return UP_ERR_UNSUPPORTED;
+    if (flags & kErrAllocationMiss) return UP_ERR_ALLOCATION_MISS;
     if (flags & (kErrBadScore | kErrBadSeqlens | kErrMaskedRow)) return UP_ERR_CONTRACT;
     return UP_OK;
 }

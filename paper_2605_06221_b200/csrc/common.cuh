@@ -18,6 +18,7 @@ enum : uint32_t {
     kErrBadSeqlens = 2u,    // cu_seqlens not 0-based / strictly increasing / over capacity
     kErrTooManyBlocks = 4u, // a request has more blocks than the on-chip sort holds
     kErrMaskedRow = 8u,     // fully masked query row (importance.cpp:57-59)
+    kErrAllocationMiss = 16u,  // slot for a page the block table does not hold (kvcache.cpp:71-78)
 };
 
 constexpr int kMaxSortBlocks = 16384;  // per-request blocks the select kernel sorts on chip

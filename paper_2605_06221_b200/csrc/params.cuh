@@ -132,4 +132,32 @@ struct CompactParams {
     int64_t dst_stride[kMaxPlanes];
 };
 
+struct SlotMapParams {
+    const int32_t* cu_seqlens;    // [R+1] of the compacted batch
+    const int32_t* num_rows;      // device row count (or null: max_rows)
+    const int64_t* positions;     // [rows] logical positions
+    const int32_t* block_tables;  // [num_layers][R][max_pages] physical page ids (-1 = none)
+    int64_t* slots;               // [num_layers][slot_stride]
+    uint32_t* err;
+    int64_t max_rows;
+    int64_t slot_stride;
+    int32_t num_requests;
+    int32_t num_layers;
+    int32_t max_pages;
+    int32_t block_size;
+};
+
+constexpr int kMaxDrops = 64;
+
+struct SequsedParams {
+    const int32_t* cu_orig;              // [R+1] prompt lengths (original cu_seqlens)
+    const int32_t* cu_after[kMaxDrops];  // cu_seqlens after each drop event
+    int32_t drop_layers[kMaxDrops];      // strictly increasing
+    const int32_t* decode_appended;      // [R] or null
+    int32_t* seqused;                    // [num_layers][R]
+    int32_t num_drops;
+    int32_t num_layers;
+    int32_t num_requests;
+};
+
 }  // namespace up
