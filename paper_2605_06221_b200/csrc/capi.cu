@@ -216,7 +216,11 @@ struct TcPlan {
 TcPlan tc_plan(const up_batch* b, const up_heads* h, const up_score_config* c, int shard_heads) {
     const int D = h->head_dim;
     TcPlan t{};
-    t.hpc = pick_hpc(h, D == 256 ? 2 : 4, shard_heads);
+    static const int max_hpc_env = [] {  // dev sweeps only
+        const char* s = std::getenv("UP_MAX_HPC");
+        return s ? std::atoi(s) : 0;
+    }();
+    t.hpc = pick_hpc(h, max_hpc_env > 0 ? max_hpc_env : (D == 256 ? 2 : 4), shard_heads);
     t.wide = (t.hpc == 4 || t.hpc == 2) && tcw_supported(D, t.hpc, c->block_size_g, b->num_requests);
     if (!t.wide) t.hpc = pick_hpc(h, tc_max_hpc(D), shard_heads);
     t.npar = t.wide ? 4 / t.hpc : 1;
@@ -307,6 +311,8 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
                   plan.wide ? tcw_stage_keys(D) : 128))
         return UP_ERR_CUDA;
     ScoreTcParams p{};
+    p.q = static_cast<const __nv_bfloat16*>(q);
+    p.q_row_stride = h->q_row_stride;
     p.cu_seqlens = b->cu_seqlens;
     p.drop_enabled = b->drop_enabled;
     p.cu_blocks = cu_blocks;

@@ -8,6 +8,8 @@
 namespace up {
 
 struct ScoreTcParams {
+    const __nv_bfloat16* q;   // [max_tokens, q_row_stride] (score_tcw TS variant loads Q rows itself)
+    int64_t q_row_stride;
     const int32_t* cu_seqlens;
     const uint8_t* drop_enabled;
     int32_t* cu_blocks;       // out [R+1] (written by CTA 0)

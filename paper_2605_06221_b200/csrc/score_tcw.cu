@@ -28,25 +28,33 @@ namespace up {
 #define UP_TCW_POLY_PAIRS_D256 0
 #endif
 
+#ifndef UP_TCW_DIAG
+#define UP_TCW_DIAG 0  // dev timing only: 1 = skip the epilogue math, 3 = one K-step MMA per subtile
+#endif
 #ifndef UP_TCW_STAGE_KEYS_D128
 #define UP_TCW_STAGE_KEYS_D128 128
 #endif
 
 template <int D, int HPC>
 struct TcwCfg {
-    static constexpr int SK = D <= 128 ? UP_TCW_STAGE_KEYS_D128 : 64;  // keys per K stage
+    // TS: with two q-heads per CTA, Q lives in TMEM (tcgen05.mma A operand from tensor
+    // memory): the MMA then reads only K from shared memory, which keeps the D = 256
+    // MMA math-bound instead of shared-memory-bound, and frees the 128 KB Q tile.
+    static constexpr bool TS = HPC == 2 && D >= 128;
+    static constexpr int SK = TS ? 128 : (D <= 128 ? UP_TCW_STAGE_KEYS_D128 : 64);  // keys per K stage
     static constexpr int SPS = SK / 64;           // 64-key subtiles per stage
     static constexpr int NPAR = 4 / HPC;          // epilogue warpgroups per head
-    static constexpr int NB = 8 / HPC;            // TMEM regions (64 columns) per head
+    static constexpr int NB = (512 - (TS ? HPC * D / 2 : 0)) / (HPC * 64);  // TMEM regions (64 cols) per head
     static constexpr int KC = D / 64;             // 128-byte K-chunks per row
     static constexpr int QSUB = 128 * 128;        // [128 rows x 64 bf16] Q tile
     static constexpr int KSUB = SK * 128;         // [SK keys x 64 bf16] K tile
-    static constexpr int Q_BYTES = HPC * KC * QSUB;
+    static constexpr int Q_BYTES = TS ? 0 : HPC * KC * QSUB;
+    static constexpr int Q_COLS = TS ? HPC * D / 2 : 0;   // TMEM columns of the resident Q
     static constexpr int K_STAGE = KC * KSUB;
     static constexpr int R_RESERVE = 2 * (kTcwMaxRequests + 1) * 4;
     static constexpr int BUDGET = 232448 - 1024 - 512 - R_RESERVE;
     static constexpr int KST = (BUDGET - Q_BYTES) / K_STAGE > 8 ? 8 : (BUDGET - Q_BYTES) / K_STAGE;
-    static constexpr int NREG = HPC * NB;         // = 8
+    static constexpr int NREG = HPC * NB;
     static constexpr int NBAR = 2 + 2 * KST + 2 * NREG;
     static constexpr int THREADS = 64 + 512;
     static constexpr int NP = D <= 128 ? UP_TCW_POLY_PAIRS_D128 : UP_TCW_POLY_PAIRS_D256;
@@ -93,7 +101,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
     if (p.dbg != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     if (warp == 0 && lane == 0) {
-        mbar_init(q_full, 1);
+        mbar_init(q_full, C::TS ? 16 : 1);  // TS: every epilogue warp stores its Q slice
         mbar_init(q_empty, 1);
         for (int s = 0; s < C::KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
         for (int s = 0; s < C::NREG; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 4); }
@@ -175,16 +183,18 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 const int key1 = min(it.u1 * unit_keys, N);
                 const int nst = (key1 - key0 + C::SK - 1) / C::SK;
                 const int kv_local = (p.q_head_offset + it.hg * HPC) / p.gqa_group - p.kv_head_offset;
-                mbar_wait(q_empty, (qiter & 1) ^ 1);
-                ++qiter;
-                mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-                const int qrow = seg0 + N - neff;
+                if (!C::TS) {
+                    mbar_wait(q_empty, (qiter & 1) ^ 1);
+                    ++qiter;
+                    mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+                    const int qrow = seg0 + N - neff;
 #pragma unroll
-                for (int hh = 0; hh < HPC; ++hh) {
+                    for (int hh = 0; hh < HPC; ++hh) {
 #pragma unroll
-                    for (int kc = 0; kc < C::KC; ++kc)
-                        tma_load_2d(sq + (hh * C::KC + kc) * C::QSUB, &qmap, q_full,
-                                    (it.hg * HPC + hh) * D + kc * 64, qrow);
+                        for (int kc = 0; kc < C::KC; ++kc)
+                            tma_load_2d(sq + (hh * C::KC + kc) * C::QSUB, &qmap, q_full,
+                                        (it.hg * HPC + hh) * D + kc * 64, qrow);
+                    }
                 }
                 for (int t = 0; t < nst; ++t) {
                     mbar_wait(&k_empty[stage], phase ^ 1);
@@ -199,15 +209,17 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer: per 64-key stage, one N = 64 MMA per head =====
+        // ===== MMA issuer (one thread): per 64-key subtile, one N = 64 MMA per head =====
+        // Descriptors = a per-CTA base plus compile-time offsets (the 14-bit address field
+        // cannot carry into the other fields).
         if (elect_one()) {
             constexpr uint32_t kIdesc = idesc_bf16_f32(128, 64);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t qiter = 0;
             uint32_t u = 0;  // 64-key subtile counter (selects the TMEM region of every head)
-            const uint32_t sq_addr = smem_u32(sq);
-            const uint32_t sk_addr = smem_u32(sk);
+            const uint64_t a_base = smem_desc_sw128(smem_u32(sq));
+            const uint64_t b_base = smem_desc_sw128(smem_u32(sk));
             for (int64_t pos = my_begin; pos < my_end;) {
                 const Item it = make_item(P, pos, my_end);
                 pos += it.u1 - it.u0;
@@ -221,6 +233,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 for (int t = 0; t < nst; ++t) {
                     mbar_wait(&k_full[stage], phase);
                     tc_fence_after();
+                    const uint64_t b_stage = b_base + static_cast<uint32_t>((stage * C::K_STAGE) >> 4);
 #pragma unroll
                     for (int s = 0; s < C::SPS; ++s, ++u) {
 #pragma unroll
@@ -228,14 +241,19 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                             const uint32_t reg = hh * NB + u % NB;
                             mbar_wait(&t_empty[reg], ((u / NB) & 1) ^ 1);
                             tc_fence_after();
-                            const uint32_t d_tmem = tmem_base + reg * 64;
+                            const uint32_t d_tmem = tmem_base + C::Q_COLS + reg * 64;
 #pragma unroll
                             for (int kk = 0; kk < D / 16; ++kk) {
-                                const uint64_t a = smem_desc_sw128(sq_addr + (hh * C::KC + (kk >> 2)) * C::QSUB + (kk & 3) * 32);
+                                const uint32_t aoff = ((hh * C::KC + (kk >> 2)) * C::QSUB + (kk & 3) * 32) >> 4;
                                 // subtile s = rows s*64.. of the stage: 8 swizzle atoms (8 KB) further
-                                const uint64_t b = smem_desc_sw128(sk_addr + stage * C::K_STAGE + (kk >> 2) * C::KSUB +
-                                                                   (kk & 3) * 32 + s * 8192);
-                                mma_bf16_ss(d_tmem, a, b, kIdesc, kk > 0 ? 1u : 0u);
+                                const uint32_t boff = ((kk >> 2) * C::KSUB + (kk & 3) * 32 + s * 8192) >> 4;
+                                if (UP_TCW_DIAG != 3 || kk == 0) {
+                                    if (C::TS)  // A = head hh's Q columns [kk*8, kk*8+8) in TMEM
+                                        mma_bf16_ts(d_tmem, tmem_base + hh * (D / 2) + kk * 8, b_stage + boff, kIdesc,
+                                                    kk > 0 ? 1u : 0u);
+                                    else
+                                        mma_bf16_ss(d_tmem, a_base + aoff, b_stage + boff, kIdesc, kk > 0 ? 1u : 0u);
+                                }
                             }
                             mma_commit(&t_full[reg]);
                         }
@@ -258,6 +276,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const float sc = p.scale_log2;
         uint32_t u = 0;
+        uint32_t qiter = 0;
         for (int64_t pos = my_begin; pos < my_end;) {
             const Item it = make_item(P, pos, my_end);
             pos += it.u1 - it.u0;
@@ -272,6 +291,32 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             const int64_t gb_seg = s_cu_blocks[it.r];
             const int blk0 = key0 / G;
             float* Prow = p.P + (static_cast<int64_t>(it.hg * HPC + hh) * p.max_blocks + gb_seg) * kRows + j;
+            if (C::TS) {
+                // Q of this item into TMEM: warpgroup (hh, par) stores its half of head hh's
+                // D/2 columns (column c = bf16 elements 2c, 2c+1 of row j; zero rows past
+                // n_eff), once the previous item's MMAs have completed (q_empty).
+                mbar_wait(q_empty, (qiter & 1) ^ 1);
+                ++qiter;
+                tc_fence_after();
+                constexpr int COLS = D / 2 / NPAR;  // 64 at D = 256, 32 at D = 128
+                const __nv_bfloat16* qsrc = p.q + static_cast<int64_t>(seg0 + N - neff + j) * p.q_row_stride +
+                                            static_cast<int64_t>(it.hg * HPC + hh) * D + par * COLS * 2;
+#pragma unroll
+                for (int c0 = 0; c0 < COLS; c0 += 32) {
+                    uint32_t v[32];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                        if (row_valid) w = __ldg(reinterpret_cast<const uint4*>(qsrc + c0 * 2) + x);
+                        v[4 * x + 0] = w.x; v[4 * x + 1] = w.y; v[4 * x + 2] = w.z; v[4 * x + 3] = w.w;
+                    }
+                    tmem_st32(tmem_base + lane_base + hh * (D / 2) + par * COLS + c0, v);
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(q_full);
+            }
             float m = -INFINITY, l = 0.f, bsum = 0.f;
             // block bookkeeping: NPAR = 1 walks every group in order (counters, any G that
             // is a multiple of 32); NPAR = 2 sees every other subtile (G = 32 or 64: shifts)
@@ -286,14 +331,14 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 const uint32_t reg = hh * NB + u % NB;
                 mbar_wait(&t_full[reg], (u / NB) & 1);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + lane_base + reg * 64;
+                const uint32_t taddr = tmem_base + lane_base + C::Q_COLS + reg * 64;
                 // Fast path (warp-uniform): all 64 keys inside the segment and left of every
                 // row's causal limit -> two packed group sums and one overflow check.  The
                 // region goes back to the MMA warp after the check, so the generic path can
                 // re-read it.
-                const bool fast = cbase + 64 <= N - neff + 1;
+                const bool fast = cbase + 64 <= N - neff + 1 && UP_TCW_DIAG != 1;
                 float gs0 = 0.f, gs1 = 0.f;
-                bool redo = !fast && cbase < N;
+                bool redo = !fast && cbase < N && UP_TCW_DIAG != 1;
                 if (fast) {
                     uint32_t v[32];
                     tmem_ld32(taddr, v);
