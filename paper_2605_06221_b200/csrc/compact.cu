@@ -31,6 +31,8 @@ __device__ __forceinline__ bool row_kept(const CompactParams& p, int64_t i, int 
 
 __global__ void __launch_bounds__(kCompactThreads)
 compact_count_kernel(const CompactParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     constexpr int PER = kCompactTile / kCompactThreads;
     __shared__ int red[kCompactThreads / 32];
     const int T = p.cu_seqlens[p.num_requests];
@@ -54,6 +56,8 @@ compact_count_kernel(const CompactParams p) {
 
 __global__ void __launch_bounds__(kCompactThreads)
 compact_index_kernel(const CompactParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     constexpr int PER = kCompactTile / kCompactThreads;
     __shared__ int red[kCompactThreads / 32];
     __shared__ int warp_tot[kCompactThreads / 32];
@@ -153,6 +157,8 @@ __device__ __forceinline__ void copy_row_planes(const CompactParams& p, int64_t 
 // Gather: output row o <- source row retained_index[o] (persistent grid, warp per row).
 __global__ void __launch_bounds__(kCopyThreads)
 compact_copy_kernel(const CompactParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * kCopyThreads + threadIdx.x) >> 5;
     const int nw = (gridDim.x * kCopyThreads) >> 5;
@@ -167,6 +173,8 @@ compact_copy_kernel(const CompactParams p) {
 // the state they had when dropped).
 __global__ void __launch_bounds__(kCopyThreads)
 scatter_rows_kernel(const CompactParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * kCopyThreads + threadIdx.x) >> 5;
     const int nw = (gridDim.x * kCopyThreads) >> 5;
@@ -192,20 +200,17 @@ static int copy_grid(int num_sms, int64_t rows) {
 
 cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_t stream) {
     if (p.num_planes == 0 || p.max_tokens == 0) return cudaSuccess;
-    scatter_rows_kernel<<<copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream>>>(p);
-    return cudaGetLastError();
+    return launch_k(scatter_rows_kernel, copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream, p);
 }
 
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream) {
     const int64_t tiles = (p.max_tokens + kCompactTile - 1) / kCompactTile;
-    compact_count_kernel<<<static_cast<unsigned>(tiles), kCompactThreads, 0, stream>>>(p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_k(compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p);
     if (e != cudaSuccess) return e;
-    compact_index_kernel<<<static_cast<unsigned>(tiles), kCompactThreads, 0, stream>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_k(compact_index_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) != cudaSuccess)
+        return e;
     if (p.num_planes > 0) {
-        compact_copy_kernel<<<copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream>>>(p);
-        e = cudaGetLastError();
+        e = launch_k(compact_copy_kernel, copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream, p);
     }
     return e;
 }

@@ -17,6 +17,8 @@ namespace up {
 
 __global__ void __launch_bounds__(256)
 slot_mapping_kernel(const SlotMapParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int64_t n = p.num_rows != nullptr ? static_cast<int64_t>(*p.num_rows) : p.max_rows;
     const int64_t total = n * p.num_layers;
     for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < total;
@@ -38,6 +40,8 @@ slot_mapping_kernel(const SlotMapParams p) {
 
 __global__ void __launch_bounds__(256)
 decode_seqused_kernel(const SequsedParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int total = p.num_layers * p.num_requests;
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
         const int l = x / p.num_requests;
@@ -59,15 +63,13 @@ cudaError_t launch_slot_mapping(const SlotMapParams& p, int num_sms, cudaStream_
     int64_t grid = (work + 255) / 256;
     if (grid > num_sms * 8) grid = num_sms * 8;
     if (grid < 1) grid = 1;
-    slot_mapping_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(p);
-    return cudaGetLastError();
+    return launch_k(slot_mapping_kernel, static_cast<unsigned>(grid), 256, 0, stream, p);
 }
 
 cudaError_t launch_decode_seqused(const SequsedParams& p, cudaStream_t stream) {
     const int total = p.num_layers * p.num_requests;
     const int grid = total > 0 ? (total + 255) / 256 : 1;
-    decode_seqused_kernel<<<grid, 256, 0, stream>>>(p);
-    return cudaGetLastError();
+    return launch_k(decode_seqused_kernel, grid, 256, 0, stream, p);
 }
 
 }  // namespace up

@@ -26,6 +26,8 @@ __device__ __forceinline__ int kv_of(const ScoreSimtParams& p, int h) {
 }
 
 __global__ void simt_row_stats_kernel(const ScoreSimtParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.x * (blockDim.x >> 5) + warp;
     const int r = blockIdx.y / p.num_heads;
@@ -63,6 +65,8 @@ __global__ void simt_row_stats_kernel(const ScoreSimtParams p) {
 
 // Warp per global token index; lanes stride over (head, query row) pairs.
 __global__ void simt_token_kernel(const ScoreSimtParams p, int64_t total_tokens_cap) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
     const int T = p.cu_seqlens[p.num_requests];
@@ -96,6 +100,8 @@ __global__ void simt_token_kernel(const ScoreSimtParams p, int64_t total_tokens_
 }
 
 __global__ void simt_block_kernel(const ScoreSimtParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int R = p.num_requests;
     const int total = p.cu_blocks[R];
     for (int gb = blockIdx.x * blockDim.x + threadIdx.x; gb < total; gb += gridDim.x * blockDim.x) {
@@ -119,15 +125,12 @@ cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int 
                               cudaStream_t stream) {
     const int rows_per_cta = 8;
     dim3 g1((p.simt_n + rows_per_cta - 1) / rows_per_cta, p.num_requests * p.num_heads);
-    simt_row_stats_kernel<<<g1, rows_per_cta * 32, 0, stream>>>(p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_k(simt_row_stats_kernel, g1, rows_per_cta * 32, 0, stream, p);
     if (e != cudaSuccess) return e;
     const int64_t g2 = (max_tokens + 7) / 8;
-    simt_token_kernel<<<static_cast<unsigned>(g2), 256, 0, stream>>>(p, max_tokens);
-    e = cudaGetLastError();
+    e = launch_k(simt_token_kernel, static_cast<unsigned>(g2), 256, 0, stream, p, max_tokens);
     if (e != cudaSuccess) return e;
-    simt_block_kernel<<<num_sms * 2, 256, 0, stream>>>(p);
-    return cudaGetLastError();
+    return launch_k(simt_block_kernel, num_sms * 2, 256, 0, stream, p);
 }
 
 }  // namespace up

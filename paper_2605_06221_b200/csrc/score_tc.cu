@@ -51,6 +51,8 @@ template <int D, int HPC>
 __global__ void __launch_bounds__(320, 1)
 score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                 const ScoreTcParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     using C = TcCfg<D, HPC>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -400,6 +402,8 @@ __device__ __forceinline__ void lse_merge(float& M, float& L, float mc, float lc
 
 __global__ void __launch_bounds__(kPwWarps * 32)
 pair_weights_kernel(const PairWeightsParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     __shared__ float sM[kPwWarps][32], sL[kPwWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;  // <= kPwWarps, sized by the launcher to the item count
@@ -483,8 +487,7 @@ pair_weights_kernel(const PairWeightsParams p) {
 cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream) {
     int warps = 2;
     while (warps < kPwWarps && 2 * warps < items_per_pair) warps *= 2;
-    pair_weights_kernel<<<grid, warps * 32, 0, stream>>>(p);
-    return cudaGetLastError();
+    return launch_k(pair_weights_kernel, grid, warps * 32, 0, stream, p);
 }
 
 // Warp per block: b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][hh][j].
@@ -494,6 +497,8 @@ cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_
 // ascending shard order (allreduce_scores, tp_sim.cpp:43-47).
 __global__ void __launch_bounds__(256)
 block_combine_kernel(const BlockCombineParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int R = p.num_requests;
     const int total = p.cu_blocks[R];
@@ -608,6 +613,8 @@ block_combine_kernel(const BlockCombineParams p) {
 // SIMT-path plan: validates cu_seqlens and writes cu_blocks (one warp).
 __global__ void blocks_plan_kernel(const int32_t* __restrict__ cu, int R, int64_t max_tokens, int G,
                                    int32_t* __restrict__ cu_blocks, uint32_t* __restrict__ err) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int lane = threadIdx.x;
     bool ok = cu[0] == 0;
     int carry = 0;
@@ -645,8 +652,7 @@ static cudaError_t launch_tc(const CUtensorMap& qm, const CUtensorMap& km, const
     cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<D, HPC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    score_tc_kernel<D, HPC><<<grid, C::THREADS, smem, stream>>>(qm, km, p);
-    return cudaGetLastError();
+    return launch_k(score_tc_kernel<D, HPC>, grid, C::THREADS, smem, stream, qm, km, p);
 }
 
 int tc_max_hpc(int D) { return D == 64 ? 8 : (D == 128 ? 4 : 1); }
@@ -664,13 +670,11 @@ cudaError_t launch_score_tc(int D, int HPC, const CUtensorMap& qm, const CUtenso
 
 cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int G, int32_t* cu_blocks,
                                uint32_t* err, cudaStream_t stream) {
-    blocks_plan_kernel<<<1, 32, 0, stream>>>(cu, R, max_tokens, G, cu_blocks, err);
-    return cudaGetLastError();
+    return launch_k(blocks_plan_kernel, 1, 32, 0, stream, cu, R, max_tokens, G, cu_blocks, err);
 }
 
 cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream) {
-    block_combine_kernel<<<grid, 256, 0, stream>>>(p);
-    return cudaGetLastError();
+    return launch_k(block_combine_kernel, grid, 256, 0, stream, p);
 }
 
 }  // namespace up

@@ -74,6 +74,8 @@ template <int D, int HPC>
 __global__ void __launch_bounds__(576, 1)
 score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                  const ScoreTcParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     using C = TcwCfg<D, HPC>;
     constexpr int NPAR = C::NPAR, NB = C::NB;
     extern __shared__ uint8_t smem_raw[];
@@ -459,8 +461,7 @@ static cudaError_t launch_tcw(const CUtensorMap& qm, const CUtensorMap& km, cons
     if (p.num_requests > kTcwMaxRequests || smem > 232448) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(score_tcw_kernel<D, HPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    score_tcw_kernel<D, HPC><<<grid, C::THREADS, smem, stream>>>(qm, km, p);
-    return cudaGetLastError();
+    return launch_k(score_tcw_kernel<D, HPC>, grid, C::THREADS, smem, stream, qm, km, p);
 }
 
 // Keys per K stage (the K tensor map's box rows).

@@ -191,6 +191,8 @@ __device__ __forceinline__ bool crossing_certain(bool reached, int rc, double ra
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
 select_radix_kernel(const SelectParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, int32_t>;
     constexpr int CAP = THREADS * ITEMS;
     __shared__ union {
@@ -321,6 +323,8 @@ select_radix_kernel(const SelectParams p) {
 // ---- bitonic variant for large requests (<= kMaxSortBlocks blocks) ------------------
 __global__ void __launch_bounds__(kSelThreads)
 select_kernel(const SelectParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ double red_d[32];
     __shared__ int red_i[32];
@@ -440,6 +444,8 @@ select_kernel(const SelectParams p) {
 // pass-through segments keep everything.  16 tokens per thread, one 16-byte store.
 __global__ void __launch_bounds__(256)
 expand_kernel(const SelectParams p, int R) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     const int T = p.cu_seqlens[R];
     const int64_t A = p.sink_count_a;
     const int G = p.block_size_g;
@@ -483,23 +489,22 @@ cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_reque
                           cudaStream_t stream) {
     cudaError_t e;
     if (max_blocks_per_request <= 512) {
-        select_radix_kernel<128, 4><<<R, 128, 0, stream>>>(p);
+        e = launch_k(select_radix_kernel<128, 4>, R, 128, 0, stream, p);
     } else if (max_blocks_per_request <= 2048) {
-        select_radix_kernel<512, 4><<<R, 512, 0, stream>>>(p);
+        e = launch_k(select_radix_kernel<512, 4>, R, 512, 0, stream, p);
     } else {
         const int cap = max_blocks_per_request < kMaxSortBlocks ? max_blocks_per_request : kMaxSortBlocks;
         const size_t smem = select_smem_bytes(cap);
         e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        select_kernel<<<R, kSelThreads, smem, stream>>>(p);
+        e = launch_k(select_kernel, R, kSelThreads, smem, stream, p);
     }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (e != cudaSuccess) return e;
     const int64_t chunks = (p.max_tokens + 15) / 16;
     int64_t grid = (chunks + 255) / 256;
     if (grid > num_sms * 8) grid = num_sms * 8;
     if (grid < 1) grid = 1;
-    expand_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(p, R);
-    return cudaGetLastError();
+    return launch_k(expand_kernel, static_cast<unsigned>(grid), 256, 0, stream, p, R);
 }
 
 // allreduce_scores (tp_sim.cpp:43-47): fp32 sum in ascending shard order from 0.0f.
@@ -511,6 +516,8 @@ struct ReduceParams {
 };
 
 __global__ void reduce_shards_kernel(const ReduceParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < p.count;
          g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         float acc = 0.0f;
@@ -529,8 +536,7 @@ cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t cou
     int64_t grid = (count + 255) / 256;
     if (grid > num_sms * 4) grid = num_sms * 4;
     if (grid < 1) grid = 1;
-    reduce_shards_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(p);
-    return cudaGetLastError();
+    return launch_k(reduce_shards_kernel, static_cast<unsigned>(grid), 256, 0, stream, p);
 }
 
 }  // namespace up
