@@ -571,7 +571,7 @@ def run_ours(args):
 
     # ---- CPU baseline (rank 0 only, N=1 semantics) ----
     cpu = None
-    if rank == 0 and not args.skip_cpu:
+    if rank == 0 and ws == 1 and not args.skip_cpu:  # reported at N=1 only
         try:
             sample = CpuReferenceSample(model, cfgd, args.regime)
             v = sample.run()

@@ -385,7 +385,10 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     bp.npar = plan.npar;
     bp.block_size_g = G;
     bp.unit_keys = p.unit_keys;
-    if ((e = launch_block_combine(bp, num_sms() * 8, stream)) != cudaSuccess) return UP_ERR_CUDA;
+    const int64_t cgrid = (L.max_blocks + 7) / 8;  // warp per block, 8 warps per CTA
+    if ((e = launch_block_combine(bp, static_cast<int>(cgrid < num_sms() * 8 ? cgrid : num_sms() * 8), stream)) !=
+        cudaSuccess)
+        return UP_ERR_CUDA;
     g_launches = 3;
     return UP_OK;
 }

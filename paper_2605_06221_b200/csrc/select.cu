@@ -449,15 +449,16 @@ expand_kernel(const SelectParams p, int R) {
     const int T = p.cu_seqlens[R];
     const int64_t A = p.sink_count_a;
     const int G = p.block_size_g;
-    const bool aligned = (reinterpret_cast<uintptr_t>(p.keep) & 15) == 0;
-    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c * 16 < T;
+    const bool aligned = (reinterpret_cast<uintptr_t>(p.keep) & 3) == 0;
+    // 4 tokens per thread (one 32-bit store): enough threads to cover the batch in one wave
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c * 4 < T;
          c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int i0 = static_cast<int>(c * 16);
+        const int i0 = static_cast<int>(c * 4);
         int r = find_segment(p.cu_seqlens, R, i0);
         int seg0 = p.cu_seqlens[r], seg1 = p.cu_seqlens[r + 1];
-        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        uint32_t w = 0u;
 #pragma unroll
-        for (int x = 0; x < 16; ++x) {
+        for (int x = 0; x < 4; ++x) {
             const int i = i0 + x;
             if (i >= T) break;
             while (i >= seg1) { ++r; seg0 = seg1; seg1 = p.cu_seqlens[r + 1]; }
@@ -469,12 +470,12 @@ expand_kernel(const SelectParams p, int R) {
                 k = (p.blk_keep[p.cu_blocks[r] + li / G] != 0 || li < A || li >= N - neff) ? 1u : 0u;
                 if (k && p.veto != nullptr && p.veto[i]) k = 0;
             }
-            w[x >> 2] |= k << (8 * (x & 3));
+            w |= k << (8 * x);
         }
-        if (aligned && i0 + 16 <= T) {
-            *reinterpret_cast<uint4*>(p.keep + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (aligned && i0 + 4 <= T) {
+            *reinterpret_cast<uint32_t*>(p.keep + i0) = w;
         } else {
-            for (int x = 0; x < 16 && i0 + x < T; ++x) p.keep[i0 + x] = static_cast<uint8_t>(w[x >> 2] >> (8 * (x & 3)));
+            for (int x = 0; x < 4 && i0 + x < T; ++x) p.keep[i0 + x] = static_cast<uint8_t>(w >> (8 * x));
         }
     }
 }
@@ -500,7 +501,7 @@ cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_reque
         e = launch_k(select_kernel, R, kSelThreads, smem, stream, p);
     }
     if (e != cudaSuccess) return e;
-    const int64_t chunks = (p.max_tokens + 15) / 16;
+    const int64_t chunks = (p.max_tokens + 3) / 4;
     int64_t grid = (chunks + 255) / 256;
     if (grid > num_sms * 8) grid = num_sms * 8;
     if (grid < 1) grid = 1;

@@ -7,6 +7,7 @@ from paper_2605_06221_b200.synthetic import make_batch
 
 SHAPES = {  # Hq, Hkv, D, lengths, tp
     "llama": (32, 8, 128, [32768] * 4, 1),
+    "llama4k": (32, 8, 128, [4096], 1),
     "gemma": (16, 8, 256, [65536] * 4, 1),
     "qwen": (16, 2, 256, [131072], 1),
     "qwen-tp8": (16, 2, 256, [131072], 8),
