@@ -1,0 +1,227 @@
+// score_tail.cuh -- the scorer's tail, shared by the standalone kernels (score_tc.cu) and
+// the fused cooperative path of score_tcw.cu: per-pair row weights from the per-item
+// softmax statistics, then the per-block combine over heads (and TP shards).
+#pragma once
+
+#include "score_common.cuh"
+
+namespace up {
+
+// Row weights of every (request, head-group) pair, from the per-item statistics the
+// scorer wrote: w[item][hh][j] = 2^(m_item - M) / (L n_eff), M = max_items m,
+// L = Σ_items l 2^(m - M) -- the softmax denominator over the full key range
+// (online_softmax_reduce pass 1, importance.cpp:41-58) assembled from the items' partial
+// denominators.  One CTA per (pair, head, 32-row chunk): warp w folds items w, w+8, ...
+// (lane = row, coalesced), the eight partial (M, L) are merged in warp order
+// (deterministic), then the warps write the weights.
+constexpr int kPwWarps = 16;
+
+__device__ __forceinline__ void lse_merge(float& M, float& L, float mc, float lc) {
+    if (mc == -INFINITY) return;
+    if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
+    else L += lc * ex2_approx(mc - M);
+}
+
+// Pair weights for tasks t0, t0 + tstep, ... (task = (pair, head, 32-row chunk)); every
+// thread of the CTA calls it (CTA barriers inside); warps >= nwarps only join the barriers.
+__device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int64_t t0, int64_t tstep, int nwarps,
+                                                 float (*sM)[32], float (*sL)[32]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int R = p.num_requests, hpc = p.hpc, nhg = p.num_hgroups, npar = p.npar;
+    Part P;
+    P.cu_units = p.cu_units;
+    P.R = R;
+    P.nhg = nhg;
+    P.U = static_cast<int64_t>(p.cu_units[R]) * nhg;
+    P.grid = p.score_grid;
+    if (P.U == 0) return;  // uniform across the CTA
+    const int64_t tasks = static_cast<int64_t>(R) * nhg * hpc * 4;
+    for (int64_t t = t0; t < tasks; t += tstep) {
+        const int chunk = static_cast<int>(t & 3);
+        const int hh = static_cast<int>((t >> 2) % hpc);
+        const int64_t pair = (t >> 2) / hpc;
+        const int r = static_cast<int>(pair / nhg), hg = static_cast<int>(pair - static_cast<int64_t>(r) * nhg);
+        const int units_r = p.cu_units[r + 1] - p.cu_units[r];
+        if (units_r == 0) continue;  // block-uniform
+        const int N = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+        const int neff = min(p.query_window_n, N);
+        const int64_t seg_start = static_cast<int64_t>(p.cu_units[r]) * nhg + static_cast<int64_t>(hg) * units_r;
+        const int64_t seg_end = seg_start + units_r;
+        const int c_first = cta_of(P, seg_start);
+        const int n_items = cta_of(P, seg_end - 1) - c_first + 1;  // CTAs spanned
+        const int j = chunk * 32 + lane;
+        // Item k = the part of the pair in CTA c_first + k; CTAs with empty ranges (more
+        // CTAs than units) hold no item.
+        auto sid_of = [&](int k) -> int64_t {
+            const int64_t b = range_begin(P, c_first + k);
+            if (k > 0 && b == range_begin(P, c_first + k + 1)) return -1;
+            return b > seg_start ? b : seg_start;
+        };
+        // statistics rows of head hh: (sid * hpc + hh) * npar + par, par < npar (the
+        // parity warpgroups of score_tcw keep separate running (m, l) for one head).
+        // Two items per warp iteration: their loads are issued before the merges.
+        float M = -INFINITY, L = 0.f;
+        for (int k = warp; warp < nwarps && k < n_items; k += 2 * nwarps) {
+            float mc[4], lc[4];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const int kk = k + x * nwarps;
+                const int64_t sid = kk < n_items ? sid_of(kk) : -1;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    mc[x * 2 + q] = -INFINITY;
+                    lc[x * 2 + q] = 0.f;
+                    if (sid >= 0 && q < npar) {
+                        const int64_t xx = ((sid * hpc + hh) * npar + q) * kRows + j;
+                        mc[x * 2 + q] = __ldcg(&p.stat_m[xx]);
+                        lc[x * 2 + q] = __ldcg(&p.stat_l[xx]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int y = 0; y < 4; ++y) lse_merge(M, L, mc[y], lc[y]);
+        }
+        if (warp < nwarps) {
+            sM[warp][lane] = M;
+            sL[warp][lane] = L;
+        }
+        __syncthreads();
+        M = -INFINITY;
+        L = 0.f;
+        for (int w = 0; w < nwarps; ++w) lse_merge(M, L, sM[w][lane], sL[w][lane]);
+        __syncthreads();
+        const bool valid = j < neff;
+        if (valid && !(L > 0.f) && warp == 0) raise_error(p.err, kErrMaskedRow);
+        const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
+        for (int k = warp; warp < nwarps && k < n_items; k += nwarps) {
+            const int64_t sid = sid_of(k);
+            if (sid < 0) continue;
+            for (int q = 0; q < npar; ++q) {
+                const int64_t x = ((sid * hpc + hh) * npar + q) * kRows + j;
+                const float mc = __ldcg(&p.stat_m[x]);
+                p.stat_w[x] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
+            }
+        }
+    }
+}
+
+// Warp per block: b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][hh][j].
+// With num_shards = T > 1 the heads form T contiguous shards (sharded_block_scores,
+// tp_sim.cpp:12-27): each shard's partial b_g^t is formed on its own (written to
+// shard_scores[t] when non-null) and block_scores[g] = ((0 + b^0) + b^1) + ... in fp32,
+// ascending shard order (allreduce_scores, tp_sim.cpp:43-47).
+// Global warps gw0, gw0 + gwstep, ... each take one block.
+__device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, int64_t gw0, int64_t gwstep) {
+    const int lane = threadIdx.x & 31;
+    const int R = p.num_requests;
+    const int total = p.cu_blocks[R];
+    const int nhg = p.num_heads / p.hpc;
+    const int T = p.num_shards;
+    const int hps = p.num_heads / T;  // heads per shard (a multiple of hpc)
+    for (int64_t gbl = gw0; gbl < total; gbl += gwstep) {
+        const int gb = static_cast<int>(gbl);
+        const int r = find_segment(p.cu_blocks, R, gb);
+        const int units_r = p.cu_units[r + 1] - p.cu_units[r];
+        if (units_r == 0) {  // pass-through segment
+            if (lane == 0) {
+                p.block_scores[gb] = 0.f;
+                if (p.shard_scores != nullptr)
+                    for (int t = 0; t < T; ++t) p.shard_scores[static_cast<int64_t>(t) * p.shard_stride + gb] = 0.f;
+            }
+            continue;
+        }
+        const int g = gb - p.cu_blocks[r];
+        const int N = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+        const int size = min(p.block_size_g, N - g * p.block_size_g);
+        const int u = (g * p.block_size_g) / p.unit_keys;
+        const int64_t pair0 = static_cast<int64_t>(p.cu_units[r]) * nhg;
+        // statistics row of head hh: hh * npar + (parity of the block's 64-key subtile)
+        const int par = p.npar > 1 ? ((g * p.block_size_g) >> 6) % p.npar : 0;
+        const int hpcv = p.hpc * p.npar;
+        if (T > 1) {
+            // Sharded: every head's dot product is reduced across the warp and added, in
+            // head order, to its shard's sum held by lane t = h / hps; loads of 8 heads
+            // are in flight together.
+            float shard_acc = 0.f;
+            for (int hg0 = 0; hg0 < nhg; hg0 += 32) {
+                const int my_hg = hg0 + lane;
+                const int my_sid = my_hg < nhg ? p.unit_sid[pair0 + static_cast<int64_t>(my_hg) * units_r + u] : 0;
+                const int h_end = min(p.num_heads, (hg0 + 32) * p.hpc);
+                for (int h = hg0 * p.hpc; h < h_end; h += 8) {
+                    float d[8];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        const int hx = min(h + x, h_end - 1);
+                        const int hgx = hx / p.hpc;
+                        const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
+                        const float4 pv = __ldcs(reinterpret_cast<const float4*>(
+                            p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
+                        const float4 wv = __ldg(reinterpret_cast<const float4*>(
+                            p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);
+                        d[x] = fmaf(pv.x, wv.x, fmaf(pv.y, wv.y, fmaf(pv.z, wv.z, pv.w * wv.w)));
+                    }
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        if (h + x >= h_end) break;
+                        float v = d[x];
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                        if (lane == (h + x) / hps) shard_acc += v;
+                    }
+                }
+            }
+            const float bt = shard_acc / static_cast<float>(size);
+            if (p.shard_scores != nullptr && lane < T) p.shard_scores[static_cast<int64_t>(lane) * p.shard_stride + gb] = bt;
+            float red = 0.f;
+            for (int t = 0; t < T; ++t) red += __shfl_sync(0xffffffffu, bt, t);  // ascending shard order
+            if (lane == 0) p.block_scores[gb] = red;
+            continue;
+        }
+        float red = 0.f;
+        for (int t = 0; t < T; ++t) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            const int hg_begin = t * hps / p.hpc, hg_end = (t + 1) * hps / p.hpc;
+            for (int hg0 = hg_begin; hg0 < hg_end; hg0 += 32) {
+                // Item ids of up to 32 head groups, one per lane, then broadcast.
+                const int my_hg = hg0 + lane;
+                const int my_sid = my_hg < hg_end ? p.unit_sid[pair0 + static_cast<int64_t>(my_hg) * units_r + u] : 0;
+                const int h_end = min((t + 1) * hps, (hg0 + 32) * p.hpc);
+                int h = hg0 * p.hpc;
+                for (; h + 8 <= h_end; h += 8) {
+                    float4 pv[8], wv[8];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        const int hx = h + x;
+                        const int hgx = hx / p.hpc;
+                        const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
+                        pv[x] = __ldcs(reinterpret_cast<const float4*>(
+                                    p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
+                        wv[x] = __ldg(reinterpret_cast<const float4*>(
+                                    p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);
+                    }
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        acc[x] = fmaf(pv[x].x, wv[x].x, fmaf(pv[x].y, wv[x].y, fmaf(pv[x].z, wv[x].z, fmaf(pv[x].w, wv[x].w, acc[x]))));
+                }
+                for (; h < h_end; ++h) {
+                    const int hgx = h / p.hpc;
+                    const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
+                    const float4 pv = __ldcs(reinterpret_cast<const float4*>(
+                        p.P + (static_cast<int64_t>(h) * p.max_blocks + gb) * kRows) + lane);
+                    const float4 wv = __ldg(reinterpret_cast<const float4*>(
+                        p.stat_w + (sid * hpcv + (h - hgx * p.hpc) * p.npar + par) * kRows) + lane);
+                    acc[0] = fmaf(pv.x, wv.x, fmaf(pv.y, wv.y, fmaf(pv.z, wv.z, fmaf(pv.w, wv.w, acc[0]))));
+                }
+            }
+            float a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            const float bt = a / static_cast<float>(size);
+            if (p.shard_scores != nullptr && lane == 0) p.shard_scores[static_cast<int64_t>(t) * p.shard_stride + gb] = bt;
+            red = T == 1 ? bt : red + bt;
+        }
+        if (lane == 0) p.block_scores[gb] = red;
+    }
+}
+
+}  // namespace up
