@@ -491,7 +491,7 @@ def run_ours(args):
             "score": {"bound": "tensor", "achieved": score_ach, "peak": tf_peak, "unit": "TFLOP/s",
                       "frac": score_ach / tf_peak, "ms_per_layer": stages["score"],
                       "algorithmic_flops_per_layer": runner.flops,
-                      "traffic": prof_traffic("score_tc4" if D <= 128 and Hq // Hkv >= 4 else "score_tc_kernel")},
+                      "traffic": prof_traffic("score_tcw")},
             "select": {"bound": "latency", "us_per_event": stages["select"] * 1e3, "requests": R},
             "compact": {"bound": "hbm", "achieved": comp_ach, "peak": hbm_peak, "unit": "GB/s",
                         "frac": comp_ach / hbm_peak, "ms_per_layer": stages["compact"],
