@@ -533,7 +533,7 @@ up_status up_select(void* stream, const up_batch* b, const up_score_config* c,
     const int64_t per_req = (b->max_tokens + c->block_size_g - 1) / c->block_size_g;
     const cudaError_t e = launch_select(p, b->num_requests, static_cast<int>(per_req < kMaxSortBlocks ? per_req : kMaxSortBlocks),
                                         num_sms(), static_cast<cudaStream_t>(stream));
-    g_launches = 2;
+    g_launches = 2 + (per_req > 512 ? 1 : 0) + (per_req > 2048 ? 1 : 0);  // size classes + expand
     return cuda_status(e);
 }
 

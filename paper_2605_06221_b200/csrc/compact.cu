@@ -200,17 +200,17 @@ static int copy_grid(int num_sms, int64_t rows) {
 
 cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_t stream) {
     if (p.num_planes == 0 || p.max_tokens == 0) return cudaSuccess;
-    return launch_k(scatter_rows_kernel, copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream, p);
+    return launch_k(kPdlCompact, scatter_rows_kernel, copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream, p);
 }
 
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream) {
     const int64_t tiles = (p.max_tokens + kCompactTile - 1) / kCompactTile;
-    cudaError_t e = launch_k(compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p);
+    cudaError_t e = launch_k(kPdlCompact, compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p);
     if (e != cudaSuccess) return e;
-    if ((e = launch_k(compact_index_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) != cudaSuccess)
+    if ((e = launch_k(kPdlCompact, compact_index_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) != cudaSuccess)
         return e;
     if (p.num_planes > 0) {
-        e = launch_k(compact_copy_kernel, copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream, p);
+        e = launch_k(kPdlCompact, compact_copy_kernel, copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream, p);
     }
     return e;
 }

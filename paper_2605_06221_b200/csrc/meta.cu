@@ -63,13 +63,13 @@ cudaError_t launch_slot_mapping(const SlotMapParams& p, int num_sms, cudaStream_
     int64_t grid = (work + 255) / 256;
     if (grid > num_sms * 8) grid = num_sms * 8;
     if (grid < 1) grid = 1;
-    return launch_k(slot_mapping_kernel, static_cast<unsigned>(grid), 256, 0, stream, p);
+    return launch_k(kPdlMeta, slot_mapping_kernel, static_cast<unsigned>(grid), 256, 0, stream, p);
 }
 
 cudaError_t launch_decode_seqused(const SequsedParams& p, cudaStream_t stream) {
     const int total = p.num_layers * p.num_requests;
     const int grid = total > 0 ? (total + 255) / 256 : 1;
-    return launch_k(decode_seqused_kernel, grid, 256, 0, stream, p);
+    return launch_k(kPdlMeta, decode_seqused_kernel, grid, 256, 0, stream, p);
 }
 
 }  // namespace up

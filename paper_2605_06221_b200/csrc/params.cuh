@@ -112,6 +112,7 @@ struct SelectParams {
     uint8_t* blk_keep;        // workspace [max_blocks]: per-block decisions for the expand kernel
     int64_t max_tokens;
     unsigned long long* dbg;  // optional phase clocks of CTA 0 (UP_SELECT_DEBUG), else null
+    int32_t nb_lo, nb_hi;     // this launch handles the requests with nb_lo < blocks <= nb_hi
 };
 
 constexpr int kMaxPlanes = 8;

@@ -125,12 +125,12 @@ cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int 
                               cudaStream_t stream) {
     const int rows_per_cta = 8;
     dim3 g1((p.simt_n + rows_per_cta - 1) / rows_per_cta, p.num_requests * p.num_heads);
-    cudaError_t e = launch_k(simt_row_stats_kernel, g1, rows_per_cta * 32, 0, stream, p);
+    cudaError_t e = launch_k(kPdlScore, simt_row_stats_kernel, g1, rows_per_cta * 32, 0, stream, p);
     if (e != cudaSuccess) return e;
     const int64_t g2 = (max_tokens + 7) / 8;
-    e = launch_k(simt_token_kernel, static_cast<unsigned>(g2), 256, 0, stream, p, max_tokens);
+    e = launch_k(kPdlScore, simt_token_kernel, static_cast<unsigned>(g2), 256, 0, stream, p, max_tokens);
     if (e != cudaSuccess) return e;
-    return launch_k(simt_block_kernel, num_sms * 2, 256, 0, stream, p);
+    return launch_k(kPdlScore, simt_block_kernel, num_sms * 2, 256, 0, stream, p);
 }
 
 }  // namespace up

@@ -397,7 +397,7 @@ pair_weights_kernel(const PairWeightsParams p) {
 cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream) {
     int warps = 2;
     while (warps < kPwWarps && 2 * warps < items_per_pair) warps *= 2;
-    return launch_k(pair_weights_kernel, grid, warps * 32, 0, stream, p);
+    return launch_k(kPdlScore, pair_weights_kernel, grid, warps * 32, 0, stream, p);
 }
 
 __global__ void __launch_bounds__(256)
@@ -450,7 +450,7 @@ static cudaError_t launch_tc(const CUtensorMap& qm, const CUtensorMap& km, const
     cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<D, HPC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return launch_k(score_tc_kernel<D, HPC>, grid, C::THREADS, smem, stream, qm, km, p);
+    return launch_k(kPdlScore, score_tc_kernel<D, HPC>, grid, C::THREADS, smem, stream, qm, km, p);
 }
 
 int tc_max_hpc(int D) { return D == 64 ? 8 : (D == 128 ? 4 : 1); }
@@ -468,11 +468,11 @@ cudaError_t launch_score_tc(int D, int HPC, const CUtensorMap& qm, const CUtenso
 
 cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int G, int32_t* cu_blocks,
                                uint32_t* err, cudaStream_t stream) {
-    return launch_k(blocks_plan_kernel, 1, 32, 0, stream, cu, R, max_tokens, G, cu_blocks, err);
+    return launch_k(kPdlScore, blocks_plan_kernel, 1, 32, 0, stream, cu, R, max_tokens, G, cu_blocks, err);
 }
 
 cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream) {
-    return launch_k(block_combine_kernel, grid, 256, 0, stream, p);
+    return launch_k(kPdlScore, block_combine_kernel, grid, 256, 0, stream, p);
 }
 
 }  // namespace up

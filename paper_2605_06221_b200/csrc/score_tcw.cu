@@ -461,7 +461,7 @@ static cudaError_t launch_tcw(const CUtensorMap& qm, const CUtensorMap& km, cons
     if (p.num_requests > kTcwMaxRequests || smem > 232448) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(score_tcw_kernel<D, HPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return launch_k(score_tcw_kernel<D, HPC>, grid, C::THREADS, smem, stream, qm, km, p);
+    return launch_k(kPdlScore, score_tcw_kernel<D, HPC>, grid, C::THREADS, smem, stream, qm, km, p);
 }
 
 // Keys per K stage (the K tensor map's box rows).

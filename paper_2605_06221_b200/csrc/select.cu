@@ -23,6 +23,9 @@
 namespace up {
 
 constexpr int kSelThreads = 512;
+#ifndef UP_SELECT_RADIX_BITS
+#define UP_SELECT_RADIX_BITS 4  // bits per radix-sort pass
+#endif
 
 __device__ __forceinline__ uint32_t phi_encode_dev(float x) {
     if (x == 0.0f) x = 0.0f;  // -0 -> +0
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(THREADS)
 select_radix_kernel(const SelectParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
-    using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, int32_t>;
+    using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, int32_t, UP_SELECT_RADIX_BITS>;
     constexpr int CAP = THREADS * ITEMS;
     __shared__ union {
         typename Sort::TempStorage sort;
@@ -213,6 +216,7 @@ select_radix_kernel(const SelectParams p) {
     const int N = p.cu_seqlens[r + 1] - seg0;
     const int G = p.block_size_g;
     const int nb = (N + G - 1) / G;
+    if (nb <= p.nb_lo || nb > p.nb_hi) return;  // another size class's launch owns it
     const int neff = min(p.query_window_n, N);
     const bool enabled = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
     if (!enabled) { keep_all_request(p, r, N, nb, -1); return; }
@@ -337,6 +341,7 @@ select_kernel(const SelectParams p) {
     const int N = p.cu_seqlens[r + 1] - seg0;
     const int G = p.block_size_g;
     const int nb = (N + G - 1) / G;
+    if (nb <= p.nb_lo || nb > p.nb_hi) return;  // another size class's launch owns it
     const int neff = min(p.query_window_n, N);
     const bool enabled = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
     if (!enabled) { keep_all_request(p, r, N, nb, -1); return; }
@@ -488,24 +493,34 @@ size_t select_smem_bytes(int max_blocks_per_request) {
 
 cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request, int num_sms,
                           cudaStream_t stream) {
+    // One launch per request size class present under the capacity (the sort's cost
+    // grows with the CTA's capacity, so small requests must not pay for a large one):
+    // <= 512 blocks: 128 x 4 radix sort; <= 2048: 512 x 4; larger: the bitonic kernel.
     cudaError_t e;
-    if (max_blocks_per_request <= 512) {
-        e = launch_k(select_radix_kernel<128, 4>, R, 128, 0, stream, p);
-    } else if (max_blocks_per_request <= 2048) {
-        e = launch_k(select_radix_kernel<512, 4>, R, 512, 0, stream, p);
-    } else {
+    SelectParams q = p;
+    q.nb_lo = 0;
+    q.nb_hi = 512;
+    if ((e = launch_k(kPdlSelect, select_radix_kernel<128, 4>, R, 128, 0, stream, q)) != cudaSuccess) return e;
+    if (max_blocks_per_request > 512) {
+        q.nb_lo = 512;
+        q.nb_hi = 2048;
+        if ((e = launch_k(kPdlSelect, select_radix_kernel<512, 4>, R, 512, 0, stream, q)) != cudaSuccess) return e;
+    }
+    if (max_blocks_per_request > 2048) {
         const int cap = max_blocks_per_request < kMaxSortBlocks ? max_blocks_per_request : kMaxSortBlocks;
         const size_t smem = select_smem_bytes(cap);
         e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        e = launch_k(select_kernel, R, kSelThreads, smem, stream, p);
+        q.nb_lo = 2048;
+        q.nb_hi = 0x7fffffff;
+        e = launch_k(kPdlSelect, select_kernel, R, kSelThreads, smem, stream, q);
     }
     if (e != cudaSuccess) return e;
     const int64_t chunks = (p.max_tokens + 3) / 4;
     int64_t grid = (chunks + 255) / 256;
     if (grid > num_sms * 8) grid = num_sms * 8;
     if (grid < 1) grid = 1;
-    return launch_k(expand_kernel, static_cast<unsigned>(grid), 256, 0, stream, p, R);
+    return launch_k(kPdlSelect, expand_kernel, static_cast<unsigned>(grid), 256, 0, stream, q, R);
 }
 
 // allreduce_scores (tp_sim.cpp:43-47): fp32 sum in ascending shard order from 0.0f.
@@ -537,7 +552,7 @@ cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t cou
     int64_t grid = (count + 255) / 256;
     if (grid > num_sms * 4) grid = num_sms * 4;
     if (grid < 1) grid = 1;
-    return launch_k(reduce_shards_kernel, static_cast<unsigned>(grid), 256, 0, stream, p);
+    return launch_k(kPdlSelect, reduce_shards_kernel, static_cast<unsigned>(grid), 256, 0, stream, p);
 }
 
 }  // namespace up
