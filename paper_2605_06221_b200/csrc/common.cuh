@@ -308,8 +308,14 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
                       pk(0.2426111716750347f, 0.2426111716750347f));
     p = fma2(p, f, pk(0.693260997791971f, 0.693260997791971f));
     p = fma2(p, f, pk(0.9999280708313836f, 0.9999280708313836f));
-    const uint32_t r0 = static_cast<uint32_t>(p) + (static_cast<uint32_t>(t) << 23);
-    const uint32_t r1 = static_cast<uint32_t>(p >> 32) + (static_cast<uint32_t>(t >> 32) << 23);
+    // exponent insert per lane (32-bit shift-adds; kept out of a fused 64-bit add with carry)
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 s;\n\t"
+        "shl.b32 s, %2, 23;\n\tadd.u32 %0, s, %3;\n\t"
+        "shl.b32 s, %4, 23;\n\tadd.u32 %1, s, %5;\n\t}"
+        : "=r"(r0), "=r"(r1)
+        : "r"(static_cast<uint32_t>(t)), "r"(static_cast<uint32_t>(p)), "r"(static_cast<uint32_t>(t >> 32)),
+          "r"(static_cast<uint32_t>(p >> 32)));
     return static_cast<uint64_t>(r0) | (static_cast<uint64_t>(r1) << 32);
 }
 

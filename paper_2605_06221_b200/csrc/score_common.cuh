@@ -75,7 +75,10 @@ __device__ __forceinline__ float group_sum_pk(const uint32_t* v, uint64_t sc2, u
     for (int i = 0; i < 16; ++i) {
         const uint64_t x = fma2(static_cast<uint64_t>(v[2 * i]) | (static_cast<uint64_t>(v[2 * i + 1]) << 32), sc2, m2);
         const uint64_t e = i < 16 - NP ? pk(ex2_approx(lo_f(x)), ex2_approx(hi_f(x))) : exp2_poly2(x);
-        if (i & 1) a1 = add2(a1, e); else a0 = add2(a0, e);
+        if (i == 0) a0 = e;
+        else if (i == 1) a1 = e;
+        else if (i & 1) a1 = add2(a1, e);
+        else a0 = add2(a0, e);
     }
     const uint64_t a = add2(a0, a1);
     return lo_f(a) + hi_f(a);

@@ -74,11 +74,53 @@ void run(const char* name, K kern, int per_thread_results, int threads) {
     cudaFree(out); cudaFree(clk);
 }
 
-int main() {
+int main_group();
+int main(int argc, char**) {
+    if (argc > 1) return main_group();
     for (int t : {256, 512, 1024}) {
         run("ex2.f32", k_f32, 1, t);
         run("ex2.f16x2", k_h2, 2, t);
         run("ex2.bf16x2", k_b2, 2, t);
     }
+    return 0;
+}
+
+// ---- epilogue mix probe: the scorer's group sum (score_common.cuh) on register data ----
+#include "../paper_2605_06221_b200/csrc/score_common.cuh"
+template <int NP>
+__global__ void __launch_bounds__(512) k_group(float* out, float seed, long long* clk, int iters) {
+    uint32_t v[32];
+    for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(seed * (threadIdx.x + c) * 1e-3f - 2.0f);
+    const uint64_t sc2 = up::pk(1.0f, 1.0f);
+    float acc = 0.f;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        const float mm = -0.5f - static_cast<float>(i) * 1e-6f;  // varies per iteration: no hoisting
+        acc += up::group_sum_pk<NP>(v, sc2, up::pk(mm, mm));
+    }
+    long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+    if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+}
+
+template <int NP>
+void run_group(int threads) {
+    float* out; long long* clk;
+    const int blocks = 148, iters = 2048;
+    cudaMalloc(&out, blocks * threads * 4); cudaMalloc(&clk, blocks * 8);
+    k_group<NP><<<blocks, threads>>>(out, 1.f, clk, iters);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    k_group<NP><<<blocks, threads>>>(out, 1.f, clk, iters);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double elems = double(blocks) * threads * iters * 32;
+    printf("group_sum_pk<%d> threads=%d: %.2f elements/clk/SM (%.3f ms)\n", NP, threads,
+           elems / (ms * 1e-3 * 1.965e9) / blocks, ms);
+    cudaFree(out); cudaFree(clk);
+}
+
+int main_group() {
+    for (int t : {256, 512}) { run_group<0>(t); run_group<2>(t); run_group<4>(t); run_group<6>(t); }
     return 0;
 }
