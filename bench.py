@@ -564,6 +564,7 @@ def run_ours(args):
         e2e = {"value": job_tokens * layers / (ems / args.e2e_steps / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d * layers, "d2h_bytes_per_step": d2h * layers,
                "steps": args.e2e_steps,
+               "pcie_gbs": (h2d + d2h) * layers / (ems / args.e2e_steps / 1e3) / 1e9,
                "note": "per layer: H2D copies of the query-window rows, K and cu_seqlens from pinned host "
                        "memory; hidden, V and positions read in place from pinned host memory by the "
                        "compaction kernel (retained rows only); D2H of keep mask, new cu_seqlens, cutoff "

@@ -53,7 +53,7 @@ typedef enum {
     UP_ERR_WORKSPACE = 4,      /* workspace missing or too small */
     UP_ERR_CUDA = 5,           /* CUDA runtime / driver failure */
     UP_ERR_INVALID_ARGUMENT = 6,
-    UP_ERR_ALLOCATION_MISS = 7  /* AllocationMissError (errors.hpp:33-36) */
+    UP_ERR_ALLOCATION_MISS = 7  /* AllocationMissError (errors.hpp:32-35) */
 } up_status;
 
 /* ScoreConfig (config.hpp:53-63).  Defaults: n=128, G=64, A=128, p=0.99. */

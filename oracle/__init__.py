@@ -26,7 +26,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "liboracle_port.so")
 REF_SO = os.path.join(HERE, "_ref", "libuniprefill_ref.so")
 
-OK, ERR_CONFIG, ERR_CONTRACT = 0, 1, 2
+OK, ERR_CONFIG, ERR_CONTRACT, ERR_ALLOCATION_MISS = 0, 1, 2, 3
 
 
 class OracleConfigError(Exception):
@@ -37,6 +37,10 @@ class OracleContractViolation(Exception):
     """Reference ContractViolation (errors.hpp:22-25)."""
 
 
+class OracleAllocationMiss(Exception):
+    """Reference AllocationMissError (errors.hpp:32-35)."""
+
+
 def _raise(status: int, what: str) -> None:
     if status == OK:
         return
@@ -44,6 +48,8 @@ def _raise(status: int, what: str) -> None:
         raise OracleConfigError(what)
     if status == ERR_CONTRACT:
         raise OracleContractViolation(what)
+    if status == ERR_ALLOCATION_MISS:
+        raise OracleAllocationMiss(what)
     raise RuntimeError(f"{what}: oracle status {status}")
 
 
@@ -203,6 +209,40 @@ class Port(_Lib):
         self._fn("rng_normal", [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double], ctypes.c_float)
         self._fn("scoring_flops", [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int],
                  ctypes.c_uint64)
+        self._fn("reconstitute", [ctypes.c_void_p, P(ctypes.c_int64), ctypes.c_int64, ctypes.c_void_p,
+                                  P(ctypes.c_int64), ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                  ctypes.c_void_p])
+        self._fn("slot_for", [P(ctypes.c_int64), ctypes.c_int64, ctypes.c_int, ctypes.c_int64, P(ctypes.c_int64)])
+        self._fn("decode_seqused", [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, P(ctypes.c_int32),
+                                    P(ctypes.c_int64), ctypes.c_int32], ctypes.c_int64)
+
+    def reconstitute(self, active: np.ndarray, active_pos, parked: np.ndarray, parked_pos) -> np.ndarray:
+        """reconstitute (propagation.cpp:79-100) of one stream."""
+        a = np.ascontiguousarray(active)
+        pk = np.ascontiguousarray(parked, dtype=a.dtype).reshape(-1, *a.shape[1:])
+        ap = np.ascontiguousarray(active_pos, dtype=np.int64)
+        pp = np.ascontiguousarray(parked_pos, dtype=np.int64)
+        n = ap.size + pp.size
+        out = np.zeros((n, *a.shape[1:]), a.dtype)
+        rb = a[0].nbytes if a.shape[0] else pk[0].nbytes
+        st = self.lib.orc_reconstitute(a.ctypes.data, _ptr(ap, ctypes.c_int64), ap.size, pk.ctypes.data,
+                                       _ptr(pp, ctypes.c_int64), pp.size, rb, n, out.ctypes.data)
+        _raise(st, "reconstitute")
+        return out
+
+    def slot_for(self, table, block_size: int, pos: int) -> int:
+        t = np.ascontiguousarray(table, dtype=np.int64)
+        out = ctypes.c_int64(0)
+        _raise(self.lib.orc_slot_for(_ptr(t, ctypes.c_int64), t.size, block_size, pos, ctypes.byref(out)),
+               "slot_for")
+        return int(out.value)
+
+    def decode_seqused(self, original_length: int, decode_appended: int, event_layers, retained_lengths,
+                       layer: int) -> int:
+        el = np.ascontiguousarray(event_layers, dtype=np.int32)
+        rl = np.ascontiguousarray(retained_lengths, dtype=np.int64)
+        return int(self.lib.orc_decode_seqused(original_length, decode_appended, el.size, _ptr(el, ctypes.c_int32),
+                                               _ptr(rl, ctypes.c_int64), layer))
 
     def restrict_selection(self, sel: OracleSelection, veto, block_scores, block_size) -> OracleSelection:
         keep = sel.keep_mask.astype(np.uint8).copy()

@@ -270,7 +270,8 @@ int orc_top_p_select(const float* block_scores, int64_t num_blocks, const orc_sc
         total += s;
     }
     const int64_t n_eff = cfg->query_window_n < num_tokens ? cfg->query_window_n : num_tokens;
-    uint8_t* block_mask = (uint8_t*)calloc((size_t)nb, 1);
+    if (nb < 0) return ORC_ERR_CONTRACT;
+    uint8_t* block_mask = (uint8_t*)calloc((size_t)nb + 1, 1);
     int degenerate = 0;
     int64_t k_star = 0;
     if (total <= 0.0) {
@@ -365,6 +366,52 @@ int orc_compact(const uint8_t* keep, const int64_t* cu_seqlens, int32_t num_requ
     }
     *num_out = out;
     return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ reconstitution & KV metadata */
+
+/* reconstitute (propagation.cpp:79-100): walk positions 0..n-1; a parked position takes
+ * its parked row, any other position the next active row (active rows are in position
+ * order). */
+int orc_reconstitute(const void* active, const int64_t* active_pos, int64_t n_active, const void* parked,
+                     const int64_t* parked_pos, int64_t n_parked, int64_t row_bytes, int64_t n_orig,
+                     void* out) {
+    if (n_active + n_parked != n_orig) return ORC_ERR_CONTRACT;
+    int64_t a = 0;
+    for (int64_t pos = 0; pos < n_orig; ++pos) {
+        int64_t k = -1;
+        for (int64_t q = 0; q < n_parked; ++q)
+            if (parked_pos[q] == pos) { k = q; break; }
+        if (k >= 0) {
+            memcpy((char*)out + pos * row_bytes, (const char*)parked + k * row_bytes, (size_t)row_bytes);
+        } else {
+            if (a >= n_active || active_pos[a] != pos) return ORC_ERR_CONTRACT;
+            memcpy((char*)out + pos * row_bytes, (const char*)active + a * row_bytes, (size_t)row_bytes);
+            ++a;
+        }
+    }
+    return ORC_OK;
+}
+
+/* PagedKVCache::slot_for (kvcache.cpp:67-80). */
+int orc_slot_for(const int64_t* table, int64_t table_len, int block_size, int64_t pos, int64_t* slot) {
+    if (pos < 0 || block_size <= 0) return ORC_ERR_CONTRACT;
+    const int64_t page = pos / block_size;
+    if (page >= table_len || table[page] < 0) return ORC_ERR_ALLOCATION_MISS;
+    *slot = table[page] * block_size + pos % block_size;
+    return ORC_OK;
+}
+
+/* decode_seqused (kvcache.cpp:182-186) with DropHistory::last_event_before (:32-39). */
+int64_t orc_decode_seqused(int64_t original_length, int64_t decode_appended, int32_t num_events,
+                           const int32_t* event_layers, const int64_t* retained_lengths, int32_t layer) {
+    int32_t found = -1;
+    for (int32_t e = 0; e < num_events; ++e) {
+        if (event_layers[e] < layer) found = e;
+        else break;
+    }
+    const int64_t base = found >= 0 ? retained_lengths[found] : original_length;
+    return base + decode_appended;
 }
 
 /* scoring_flops (flops.cpp:35-39). */

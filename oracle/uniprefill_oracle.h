@@ -31,6 +31,7 @@ enum {
     ORC_OK = 0,
     ORC_ERR_CONFIG = 1,   /* ConfigError */
     ORC_ERR_CONTRACT = 2, /* ContractViolation */
+    ORC_ERR_ALLOCATION_MISS = 3, /* AllocationMissError */
 };
 
 /* ScoreConfig (config.hpp:53-63). */
@@ -106,6 +107,20 @@ int orc_compact(const uint8_t* keep, const int64_t* cu_seqlens, int32_t num_requ
                 const uint8_t* selected, int32_t n_planes, const void* const* src,
                 void* const* dst, const int64_t* row_bytes, int64_t* cu_out,
                 int64_t* retained_index, int64_t* num_out);
+
+/* reconstitute (propagation.cpp:79-100): the full-length stream of n_orig rows (row_bytes
+ * each) -- row p = parked[k] for p = parked_pos[k], else the next active row in order. */
+int orc_reconstitute(const void* active, const int64_t* active_pos, int64_t n_active, const void* parked,
+                     const int64_t* parked_pos, int64_t n_parked, int64_t row_bytes, int64_t n_orig,
+                     void* out);
+
+/* PagedKVCache::slot_for (kvcache.cpp:67-80), Eq. 16: table[pos / B] * B + pos % B;
+ * ORC_ERR_ALLOCATION_MISS when the page is absent (negative entry or past the table). */
+int orc_slot_for(const int64_t* table, int64_t table_len, int block_size, int64_t pos, int64_t* slot);
+
+/* decode_seqused (kvcache.cpp:182-186) / DropHistory::last_event_before (:32-39), Eq. 17. */
+int64_t orc_decode_seqused(int64_t original_length, int64_t decode_appended, int32_t num_events,
+                           const int32_t* event_layers, const int64_t* retained_lengths, int32_t layer);
 
 /* Scoring FLOPs (flops.cpp:35-39): 2 * n_eff * N * D * H. */
 uint64_t orc_scoring_flops(int64_t effective_n, int64_t num_keys, int head_dim, int num_heads);

@@ -40,7 +40,7 @@ class UnsupportedError(RuntimeError):
 
 
 class AllocationMissError(RuntimeError):
-    """Reference AllocationMissError (errors.hpp:33-36): a KV slot whose page is absent."""
+    """Reference AllocationMissError (errors.hpp:32-35): a KV slot whose page is absent."""
 
 
 class CudaError(RuntimeError):

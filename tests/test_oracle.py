@@ -205,3 +205,40 @@ def test_port_matches_reference_compaction(port, ref):
     want, cu_want = ref.patch_metadata(toks, cu, keep, sel)
     (got,), cu_got, _ = port.compact(keep, cu, [toks], selected=sel)
     assert np.array_equal(got, want) and cu_got.tolist() == cu_want.tolist()
+
+
+def test_port_reconstitute_matches_reference(port, ref):
+    """orc_reconstitute restates propagation.cpp:79-100: drop sequences through the
+    reference (apply_drop x2 + reconstitute) vs the port fed the same active/parked rows."""
+    rng = np.random.default_rng(3)
+    for rows in (1, 9, 257):
+        prompt = rng.standard_normal((rows, 6)).astype(np.float32)
+        keep0 = (rng.random(rows) < 0.5).astype(np.uint8)
+        keep0[0] = 1
+        after0 = rng.standard_normal((int(keep0.sum()), 6)).astype(np.float32)
+        keep1 = (rng.random(int(keep0.sum())) < 0.5).astype(np.uint8)
+        keep1[0] = 1
+        after1 = rng.standard_normal((int(keep1.sum()), 6)).astype(np.float32)
+        want, pos = ref.reconstitute_sequence(prompt, [keep0, keep1], [after0, after1])
+        pos0 = np.flatnonzero(keep0)
+        parked_pos = list(np.flatnonzero(keep0 == 0)) + list(pos0[keep1 == 0])
+        parked = np.concatenate([prompt[keep0 == 0], after0[keep1 == 0]])
+        got = port.reconstitute(after1, pos0[keep1 == 1], parked, parked_pos)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+        assert pos.tolist() == list(range(rows))
+
+
+def test_port_slot_for_and_seqused_match_reference(port, ref):
+    """Eq. 16 / Eq. 17 restatements vs PagedKVCache::recompute_slots_after_drop and
+    decode_seqused of the reference (kvcache.cpp:67-80, :147-158, :182-186)."""
+    import oracle
+    retained = [0, 3, 17, 40, 41, 99]
+    tables, slots = ref.recompute_slots(2, 16, 50, retained, 8)
+    for l in range(2):
+        for i, p in enumerate(retained):
+            assert port.slot_for(tables[l], 16, p) == slots[l, i]
+    with pytest.raises(oracle.OracleAllocationMiss):
+        port.slot_for([5, -1], 16, 20)
+    for layer in range(12):
+        assert port.decode_seqused(100, 7, [2, 5, 9], [80, 50, 20], layer) == \
+            ref.decode_seqused(100, 7, [2, 5, 9], [80, 50, 20], layer)
