@@ -18,3 +18,18 @@ def test_cpp_parity_suite(up):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+def test_cpp_host_driver_runs_the_layer_loop(up):
+    """examples/drop_layer_bench: score -> select -> compact driven from C++ only (the host
+    mirror over the C ABI), graph-captured; it must run and drop tokens in the planted regime."""
+    import json
+    exe = os.path.join(ROOT, "examples", "_build", "drop_layer_bench")
+    if not os.path.exists(exe):
+        pytest.skip("examples/_build/drop_layer_bench not built")
+    r = subprocess.run([exe, "--requests", "2", "--len", "8192", "--layers", "3", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["tokens_per_s"] > 0 and 0.05 < line["retention_rho"] < 0.8
+    assert line["launches_per_layer"] >= 6
