@@ -175,6 +175,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             int stage = 0;
             uint32_t phase = 0;
             uint32_t qiter = 0;
+            const uint64_t k_policy = l2_policy_evict_first();
             for (int64_t pos = my_begin; pos < my_end;) {
                 const Item it = make_item(P, pos, my_end);
                 pos += it.u1 - it.u0;
@@ -204,8 +205,8 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                     const int krow = seg0 + key0 + t * C::SK;
 #pragma unroll
                     for (int kc = 0; kc < C::KC; ++kc)
-                        tma_load_2d(sk + stage * C::K_STAGE + kc * C::KSUB, &kmap, &k_full[stage],
-                                    kv_local * D + kc * 64, krow);
+                        tma_load_2d_hint(sk + stage * C::K_STAGE + kc * C::KSUB, &kmap, &k_full[stage],
+                                         kv_local * D + kc * 64, krow, k_policy);
                     if (++stage == C::KST) { stage = 0; phase ^= 1; }
                 }
             }
