@@ -170,3 +170,19 @@ def test_score_blocks_tp_rejects_bad_degree(up):
     for tp in (0, 3):
         with pytest.raises(up.ConfigError):
             up.score_blocks_tp(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(), tp, up.HeadLayout(8, 2, 128))
+
+
+def test_many_requests_fallback_kernel(up, port):
+    """More segments than score_tcw plans in shared memory (R > 256): the two-warpgroup
+    kernel serves the batch; every segment still matches the oracle."""
+    rng = np.random.default_rng(8)
+    lengths = [int(x) for x in rng.integers(1, 400, size=300)]
+    cfg = dict(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99)
+    sb = make_batch(lengths, 8, 2, 128, 16, regime="planted", seed=8)
+    res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), up.HeadLayout(8, 2, 128),
+                                 check=True)
+    cub = res.cu_blocks.cpu().numpy()
+    bs = res.block_scores.cpu().numpy()
+    for r in range(0, len(lengths), 37):
+        _, want = _oracle_blocks(port, sb, r, 8, 2, cfg)
+        _assert_blocks_close(bs[cub[r]:cub[r + 1]], want)

@@ -165,3 +165,26 @@ def test_varlen_select_matches_per_request(up, port):
         want = port.top_p_select(scores[r], n, **_cfgd(cfg))
         assert np.array_equal(got, want.keep_mask)
         assert int(sel.cutoff_rank[r]) == want.cutoff_rank
+
+
+def test_request_beyond_2048_blocks_uses_bitonic_kernel(up, port):
+    """A 200K-token request (3125 blocks) goes to the large-request select kernel; the keep
+    mask and k* stay bit-exact with the reference; a small request in the same batch is
+    served by the small size class."""
+    rng = np.random.default_rng(21)
+    lengths = [200000, 3000]
+    G = 64
+    nbs = [(n + G - 1) // G for n in lengths]
+    scores = (rng.random(sum(nbs)) ** 6).astype(np.float32)
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(lengths)]), dtype=torch.int32, device="cuda")
+    cub = torch.tensor(np.concatenate([[0], np.cumsum(nbs)]), dtype=torch.int32, device="cuda")
+    cfg = dict(query_window_n=128, block_size_g=G, sink_count_a=128, top_p=0.99)
+    sel = up.select_varlen(torch.from_numpy(scores).cuda(), cub, cu, up.ScoreConfig(**cfg), check=True)
+    keep = sel.keep.cpu().numpy()
+    kst = sel.cutoff_rank.cpu().numpy()
+    off = 0
+    for r, n in enumerate(lengths):
+        want = port.top_p_select(scores[sum(nbs[:r]):sum(nbs[:r + 1])], n, **cfg)
+        assert np.array_equal(keep[off:off + n], want.keep_mask)
+        assert int(kst[r]) == want.cutoff_rank
+        off += n
