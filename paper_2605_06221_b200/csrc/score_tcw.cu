@@ -31,6 +31,9 @@ namespace up {
 #ifndef UP_TCW_DIAG
 #define UP_TCW_DIAG 0  // dev timing only: 1 = skip the epilogue math, 3 = one K-step MMA per subtile
 #endif
+#ifndef UP_TCW_SUBN_HPC4
+#define UP_TCW_SUBN_HPC4 128
+#endif
 #ifndef UP_TCW_STAGE_KEYS_D128
 #define UP_TCW_STAGE_KEYS_D128 128
 #endif
@@ -42,9 +45,12 @@ struct TcwCfg {
     // MMA math-bound instead of shared-memory-bound, and frees the 128 KB Q tile.
     static constexpr bool TS = HPC == 2 && D >= 128;
     static constexpr int SK = TS ? 128 : (D <= 128 ? UP_TCW_STAGE_KEYS_D128 : 64);  // keys per K stage
-    static constexpr int SPS = SK / 64;           // 64-key subtiles per stage
+    // keys per MMA / TMEM region (UP_TCW_SUBN_HPC4 = 128: one N = 128 region per head)
+    static constexpr int SUBN = HPC == 4 ? UP_TCW_SUBN_HPC4 : 64;
+    static constexpr int NG = SUBN / 32;          // 32-column groups per subtile
+    static constexpr int SPS = SK / SUBN;         // subtiles per K stage
     static constexpr int NPAR = 4 / HPC;          // epilogue warpgroups per head
-    static constexpr int NB = (512 - (TS ? HPC * D / 2 : 0)) / (HPC * 64);  // TMEM regions (64 cols) per head
+    static constexpr int NB = (512 - (TS ? HPC * D / 2 : 0)) / (HPC * SUBN);  // TMEM regions per head
     static constexpr int KC = D / 64;             // 128-byte K-chunks per row
     static constexpr int QSUB = 128 * 128;        // [128 rows x 64 bf16] Q tile
     static constexpr int KSUB = SK * 128;         // [SK keys x 64 bf16] K tile
@@ -216,7 +222,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         // Descriptors = a per-CTA base plus compile-time offsets (the 14-bit address field
         // cannot carry into the other fields).
         if (elect_one()) {
-            constexpr uint32_t kIdesc = idesc_bf16_f32(128, 64);
+            constexpr uint32_t kIdesc = idesc_bf16_f32(128, C::SUBN);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t qiter = 0;
@@ -244,12 +250,12 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                             const uint32_t reg = hh * NB + u % NB;
                             mbar_wait(&t_empty[reg], ((u / NB) & 1) ^ 1);
                             tc_fence_after();
-                            const uint32_t d_tmem = tmem_base + C::Q_COLS + reg * 64;
+                            const uint32_t d_tmem = tmem_base + C::Q_COLS + reg * C::SUBN;
 #pragma unroll
                             for (int kk = 0; kk < D / 16; ++kk) {
                                 const uint32_t aoff = ((hh * C::KC + (kk >> 2)) * C::QSUB + (kk & 3) * 32) >> 4;
-                                // subtile s = rows s*64.. of the stage: 8 swizzle atoms (8 KB) further
-                                const uint32_t boff = ((kk >> 2) * C::KSUB + (kk & 3) * 32 + s * 8192) >> 4;
+                                // subtile s = rows s*SUBN.. of the stage: SUBN/8 swizzle atoms further
+                                const uint32_t boff = ((kk >> 2) * C::KSUB + (kk & 3) * 32 + s * C::SUBN * 128) >> 4;
                                 if (UP_TCW_DIAG != 3 || kk == 0) {
                                     if (C::TS)  // A = head hh's Q columns [kk*8, kk*8+8) in TMEM
                                         mma_bf16_ts(d_tmem, tmem_base + hh * (D / 2) + kk * 8, b_stage + boff, kIdesc,
@@ -330,17 +336,17 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
 #pragma unroll 1
             for (int t = 0; t < nsub; ++t, ++u) {
                 if (NPAR > 1 && (t % NPAR) != par) continue;  // the other warpgroup's subtile
-                const int cbase = key0 + t * 64;
+                const int cbase = key0 + t * C::SUBN;
                 const uint32_t reg = hh * NB + u % NB;
                 mbar_wait(&t_full[reg], (u / NB) & 1);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + lane_base + C::Q_COLS + reg * 64;
+                const uint32_t taddr = tmem_base + lane_base + C::Q_COLS + reg * C::SUBN;
                 // Fast path (warp-uniform): all 64 keys inside the segment and left of every
                 // row's causal limit -> two packed group sums and one overflow check.  The
                 // region goes back to the MMA warp after the check, so the generic path can
                 // re-read it.
-                const bool fast = cbase + 64 <= N - neff + 1 && UP_TCW_DIAG != 1;
-                float gs0 = 0.f, gs1 = 0.f;
+                const bool fast = cbase + C::SUBN <= N - neff + 1 && UP_TCW_DIAG != 1;
+                float gs0 = 0.f, gs1 = 0.f, gs2 = 0.f, gs3 = 0.f;
                 bool redo = !fast && cbase < N && UP_TCW_DIAG != 1;
                 if (fast) {
                     uint32_t v[32];
@@ -350,12 +356,20 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                     tmem_ld32(taddr + 32, v);
                     tmem_ld_wait();
                     gs1 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
-                    redo = !(gs0 + gs1 <= 0x1p40f);
+                    if (C::NG == 4) {
+                        tmem_ld32(taddr + 64, v);
+                        tmem_ld_wait();
+                        gs2 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
+                        tmem_ld32(taddr + 96, v);
+                        tmem_ld_wait();
+                        gs3 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
+                    }
+                    redo = !((gs0 + gs1) + (gs2 + gs3) <= 0x1p40f);
                 }
                 if (redo) {
                     // Generic path: causal tail, ragged segment end, or a rebase of m.
 #pragma unroll 1
-                    for (int q2 = 0; q2 < 2; ++q2) {
+                    for (int q2 = 0; q2 < C::NG; ++q2) {
                         const int c0 = cbase + q2 * 32;
                         const int lim = min(qpos - c0, min(31, N - 1 - c0));  // last valid column
                         uint32_t v[32];
@@ -384,7 +398,10 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                                 const float f = ex2_approx(m - mnew);
                                 l *= f;
                                 bsum *= f;
-                                gs0 *= f;  // q2 == 1: half 0 is not yet folded into bsum
+                                // groups of this subtile before q2 are not yet folded into bsum
+                                gs0 *= f;
+                                gs1 *= f;
+                                gs2 *= f;
                                 rescale_rows_par(Prow, blk0, NPAR == 1 ? blk : cbase >> (5 + gshift), G, NPAR,
                                                  par, f);
                             }
@@ -396,7 +413,10 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                                 gs += (k <= lim) ? e : 0.f;
                             }
                         }
-                        if (q2 == 0) gs0 = gs; else gs1 = gs;
+                        if (q2 == 0) gs0 = gs;
+                        else if (q2 == 1) gs1 = gs;
+                        else if (q2 == 2) gs2 = gs;
+                        else gs3 = gs;
                     }
                 }
                 tc_fence_before();
@@ -404,10 +424,10 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 if (lane == 0) mbar_arrive(&t_empty[reg]);
                 if (cbase >= N) continue;  // warp-uniform: padding subtile past the segment end
 #pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2) {
+                for (int q2 = 0; q2 < C::NG; ++q2) {
                     const int c0 = cbase + q2 * 32;
                     if (c0 >= N) break;  // warp-uniform
-                    bsum += q2 == 0 ? gs0 : gs1;
+                    bsum += q2 == 0 ? gs0 : (q2 == 1 ? gs1 : (q2 == 2 ? gs2 : gs3));
                     bool done;
                     int b;
                     if (NPAR == 1) {
