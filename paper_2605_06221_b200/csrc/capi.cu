@@ -343,11 +343,6 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     cudaError_t e = plan.wide ? launch_score_tcw(D, hpc, qm, km, p, grid, stream)
                               : launch_score_tc(D, hpc, qm, km, p, grid, stream);
     if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
-    static const int skip_tail = [] {  // dev timing only: 1 = scorer only, 2 = + pair weights
-        const char* s = std::getenv("UP_SCORE_TAIL_SKIP");
-        return s ? std::atoi(s) : 0;
-    }();
-    if (skip_tail == 1) { g_launches = 1; return UP_OK; }
     PairWeightsParams wp{};
     wp.cu_seqlens = b->cu_seqlens;
     wp.cu_units = p.cu_units_out;
@@ -366,7 +361,6 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     // CTAs one (request, head-group) pair spans, for equal-length requests
     const int items_est = grid / (R * nhg > 0 ? R * nhg : 1) + 2;
     if ((e = launch_pair_weights(wp, wgrid, items_est, stream)) != cudaSuccess) return UP_ERR_CUDA;
-    if (skip_tail == 2) { g_launches = 2; return UP_OK; }
     BlockCombineParams bp{};
     bp.cu_seqlens = b->cu_seqlens;
     bp.cu_blocks = cu_blocks;
@@ -411,7 +405,9 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
     const int G = c->block_size_g;
     uint32_t* err = at<uint32_t>(ws, L.err);
 
-    if (tc_eligible(h, c, token_scores != nullptr))
+    // TMA needs 16-byte aligned bases (strides are checked by tc_eligible)
+    const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15) == 0;
+    if (aligned && tc_eligible(h, c, token_scores != nullptr))
         return score_tc_path(stream, b, h, c, q, k, 1, nullptr, 0, block_scores, cu_blocks, L, ws);
 
     // Generic SIMT path.
@@ -461,7 +457,8 @@ up_status up_score_blocks_tp(void* stream_, const up_batch* b, const up_heads* h
     if (shard_stride < up_max_blocks(b, c)) return UP_ERR_INVALID_ARGUMENT;
     const Layout L = layout_for(b, h, c);
     if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
-    if (tc_eligible(h, c, 0) && tp <= 32)  // the combine holds one shard sum per lane
+    const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15) == 0;
+    if (aligned && tc_eligible(h, c, 0) && tp <= 32)  // the combine holds one shard sum per lane
         return score_tc_path(stream, b, h, c, q, k, tp, shard_scores, shard_stride, block_scores, cu_blocks, L, ws);
     // Generic shapes: one SIMT scoring pass per shard, then the ordered shard sum.
     if (tp > 16) return UP_ERR_UNSUPPORTED;

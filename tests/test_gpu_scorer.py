@@ -186,3 +186,18 @@ def test_many_requests_fallback_kernel(up, port):
     for r in range(0, len(lengths), 37):
         _, want = _oracle_blocks(port, sb, r, 8, 2, cfg)
         _assert_blocks_close(bs[cub[r]:cub[r + 1]], want)
+
+
+def test_unaligned_q_takes_the_simt_path(up, port):
+    """A q view whose base is not 16-byte aligned cannot feed TMA: the scorer must still
+    answer (SIMT path) within rtol of the oracle."""
+    lengths = [500]
+    cfg = dict(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99)
+    sb = make_batch(lengths, 4, 1, 128, 16, regime="planted", seed=5)
+    buf = torch.empty(sb.q.numel() + 1, dtype=torch.bfloat16, device="cuda")
+    q = buf[1:].view(sb.q.shape)
+    q.copy_(sb.q)
+    assert q.data_ptr() % 16 != 0
+    res = up.score_blocks_varlen(q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), up.HeadLayout(4, 1, 128), check=True)
+    _, want = _oracle_blocks(port, sb, 0, 4, 1, cfg)
+    _assert_blocks_close(res.block_scores[:len(want)].cpu().numpy(), want)
