@@ -62,7 +62,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Kernel families for the PDL policy (UP_PDL_MASK bit per family; default all).
-enum PdlFamily : int { kPdlScore = 1, kPdlSelect = 2, kPdlCompact = 4, kPdlMeta = 8 };
+enum PdlFamily : int { kPdlScore = 1, kPdlSelect = 2, kPdlCompact = 4, kPdlMeta = 8, kPdlCompactScan = 16 };
 
 inline int pdl_mask() {
     static const int m = [] {

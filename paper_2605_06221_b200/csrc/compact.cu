@@ -205,9 +205,9 @@ cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_
 
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream) {
     const int64_t tiles = (p.max_tokens + kCompactTile - 1) / kCompactTile;
-    cudaError_t e = launch_k(kPdlCompact, compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p);
+    cudaError_t e = launch_k(kPdlCompactScan, compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p);
     if (e != cudaSuccess) return e;
-    if ((e = launch_k(kPdlCompact, compact_index_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) != cudaSuccess)
+    if ((e = launch_k(kPdlCompactScan, compact_index_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) != cudaSuccess)
         return e;
     if (p.num_planes > 0) {
         e = launch_k(kPdlCompact, compact_copy_kernel, copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream, p);

@@ -88,7 +88,7 @@ int main(int argc, char**) {
 // ---- epilogue mix probe: the scorer's group sum (score_common.cuh) on register data ----
 #include "../paper_2605_06221_b200/csrc/score_common.cuh"
 template <int NP>
-__global__ void __launch_bounds__(512) k_group(float* out, float seed, long long* clk, int iters) {
+__global__ void __launch_bounds__(1024) k_group(float* out, float seed, long long* clk, int iters) {
     uint32_t v[32];
     for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(seed * (threadIdx.x + c) * 1e-3f - 2.0f);
     const uint64_t sc2 = up::pk(1.0f, 1.0f);
@@ -121,6 +121,6 @@ void run_group(int threads) {
 }
 
 int main_group() {
-    for (int t : {256, 512}) { run_group<0>(t); run_group<2>(t); run_group<4>(t); run_group<6>(t); }
+    for (int t : {256, 512, 768, 1024}) { run_group<0>(t); run_group<4>(t); run_group<6>(t); run_group<8>(t); }
     return 0;
 }
