@@ -1,5 +1,5 @@
 // score_common.cuh -- pieces shared by the tcgen05 scorer kernels (score_tc.cu,
-// score_tc4.cu): the balanced work partition and the packed exp2 group sums.
+// score_tcw.cu): the balanced work partition and the packed exp2 group sums.
 #pragma once
 
 #include "params.cuh"
@@ -58,9 +58,9 @@ __device__ __forceinline__ Item make_item(const Part& P, int64_t pos, int64_t en
 }
 
 // Of the 16 element pairs of a 32-column group, NP evaluate 2^x with the FMA-pipe
-// polynomial (exp2_poly2) instead of MUFU.EX2.  Measured on B200 (4x32K LLaMA layer):
-// the four-warpgroup scorer gains ~5% at NP = 3..4 (score_tc4.cu, kTc4PolyPairs); the
-// two-warpgroup kernel is latency- rather than MUFU-limited and uses NP = 0.
+// polynomial (exp2_poly2) instead of MUFU.EX2.  Measured on B200: the four-warpgroup
+// scorer (score_tcw.cu) is fastest at NP = 3..5 for D = 128 (MUFU-bound) and NP = 0 for
+// D = 256; the two-warpgroup kernel is latency- rather than MUFU-limited and uses NP = 0.
 #ifndef UP_POLY_PAIRS
 #define UP_POLY_PAIRS 0
 #endif

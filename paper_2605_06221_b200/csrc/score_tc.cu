@@ -23,10 +23,12 @@
 //    e = 2^(s*log2e/sqrt(D) - m) against a per-(row, item) reference m that moves only
 //    when a value would exceed it by ~2^20 (rare; the item's already-written partials are
 //    rescaled then).  Per (row, block) Σ e goes to P, per (row, item) (m, l = Σ e) to the
-//    stats.  The last CTA to finish an item of a (request, head-group) pair (atomic
-//    counter) turns that pair's stats into per-item row weights
-//    w = 2^(m - M) / (L n_eff), M = max_items m, L = Σ_items l 2^(m - M).
-//  * block_combine_kernel -- b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][j].
+//    stats.  This kernel serves the shapes score_tcw.cu does not (HPC 1 or 8, block
+//    sizes other than 32/64 at two heads per CTA, more than 256 segments).
+//  * pair_weights_kernel (score_tail.cuh) -- per (request, head-group) pair, the items'
+//    statistics become row weights w = 2^(m - M) / (L n_eff), M = max_items m,
+//    L = Σ_items l 2^(m - M);
+//  * block_combine_kernel (score_tail.cuh) -- b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][j].
 #include "score_tail.cuh"
 
 namespace up {
