@@ -226,3 +226,65 @@ def test_cuda_graph_capture_of_drop_layer(up):
     torch.cuda.synchronize()
     assert torch.equal(layer.sel.keep, keep0)
     assert int(layer.out.num_out.item()) == n0
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(seed)
+    Hq, Hkv, D = [(8, 2, 128), (4, 2, 256), (4, 4, 64), (16, 8, 256), (32, 8, 128), (2, 1, 256)][seed % 6]
+    cfgd = dict(query_window_n=int(rng.choice([16, 64, 100, 128, 200])),
+                block_size_g=int(rng.choice([8, 32, 64, 96, 128])),
+                sink_count_a=int(rng.choice([0, 16, 128, 1000])),
+                top_p=float(rng.choice([0.5, 0.9, 0.99, 1.0])))
+    R = int(rng.integers(1, 6))
+    lengths = [int(x) for x in rng.choice([1, 5, 40, 130, 700, 1500, 2600], size=R)]
+    en = (rng.random(R) < 0.8).astype(np.uint8)
+    veto_frac = float(rng.choice([0.0, 0.0, 0.05]))
+    return (Hq, Hkv, D), cfgd, lengths, en, veto_frac
+
+
+@pytest.mark.parametrize("seed", list(range(24)))
+def test_drop_layer_random_configs_vs_oracle(up, port, seed):
+    """Seeded sweep over the knobs (n, G, A, p), head layouts (every scorer kernel), varlen
+    segments incl. single-token and n > N, drop-disabled segments and a no-readmission veto:
+    block scores within rtol of the oracle, the keep mask bit-exact with the reference's
+    top_p_select (+ restrict_selection for the veto) on the GPU's own scores, compaction
+    exact (SURVEY parity rules 1-3)."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    (Hq, Hkv, D), cfgd, lengths, en, veto_frac = _random_case(seed)
+    cfg = up.ScoreConfig(**cfgd)
+    T = sum(lengths)
+    sb = make_batch(lengths, Hq, Hkv, D, 32, regime="planted", block_size_g=cfgd["block_size_g"], seed=seed)
+    rng = np.random.default_rng(100 + seed)
+    veto = (rng.random(T) < veto_frac).astype(np.uint8) if veto_frac > 0 else None
+    en_t = torch.from_numpy(en).cuda()
+    veto_t = torch.from_numpy(veto).cuda() if veto is not None else None
+    layer = up.DropLayer(cfg, up.HeadLayout(Hq, Hkv, D), T, len(lengths), [(32,), ()],
+                         [torch.bfloat16, torch.int64])
+    out = layer(sb.q, sb.k, sb.cu_seqlens, [sb.hidden, sb.positions], drop_enabled=en_t, veto=veto_t)
+    layer.check()
+    cu = sb.cu_seqlens.cpu().numpy()
+    cub = layer.scores.cu_blocks.cpu().numpy()
+    bs = layer.scores.block_scores.cpu().numpy()
+    keep = layer.sel.keep.cpu().numpy()
+    kst = layer.sel.cutoff_rank.cpu().numpy()
+    for r in range(len(lengths)):
+        s, e = int(cu[r]), int(cu[r + 1])
+        got = bs[cub[r]:cub[r + 1]]
+        if not en[r]:  # pass-through segment: untouched, all kept
+            assert (keep[s:e] == 1).all() and int(kst[r]) == -1 and not got.any()
+            continue
+        q = sb.q[s:e].float().reshape(e - s, -1).cpu().numpy()
+        k = sb.k[s:e].float().reshape(e - s, -1).cpu().numpy()
+        _, want, _ = port.score_tokens(q, k, Hq, Hkv, want_tokens=False, **cfgd)
+        np.testing.assert_allclose(got, want, rtol=RTOL, atol=1e-6 * max(want.sum(), 1e-30) / len(want))
+        own = port.top_p_select(got, e - s, **cfgd)
+        if veto is not None:
+            own = port.restrict_selection(own, veto[s:e], got, cfgd["block_size_g"])
+        assert np.array_equal(keep[s:e], own.keep_mask), f"segment {r}"
+        assert int(kst[r]) == own.cutoff_rank
+    n = int(out.num_out.item())
+    idx = np.flatnonzero(keep[:T])
+    assert n == len(idx)
+    ii = torch.from_numpy(idx).cuda()
+    assert torch.equal(out.planes[0][:n], sb.hidden[ii])
+    assert torch.equal(out.planes[1][:n], sb.positions[ii])
