@@ -53,6 +53,21 @@ def _raise(status: int, what: str) -> None:
     raise RuntimeError(f"{what}: oracle status {status}")
 
 
+class _ModelCfg(ctypes.Structure):
+    _fields_ = [("num_blocks", ctypes.c_int32), ("sublayers_per_block", ctypes.c_int32),
+                ("hidden_dim", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("num_heads", ctypes.c_int32),
+                ("window_size", ctypes.c_int32), ("ffn_dim", ctypes.c_int32),
+                ("layer_pattern", ctypes.POINTER(ctypes.c_int32))]
+
+
+def _model_cfg(cfg):
+    """ctypes view of a paper_2605_06221_b200.ledger.ModelConfig (keeps the pattern alive)."""
+    pat = np.ascontiguousarray([int(k) for k in cfg.layer_pattern], dtype=np.int32)
+    c = _ModelCfg(cfg.num_blocks, cfg.sublayers_per_block, cfg.hidden_dim, cfg.head_dim, cfg.num_heads,
+                  cfg.window_size, cfg.ffn_dim, _ptr(pat, ctypes.c_int32))
+    return c, pat
+
+
 class _Cfg(ctypes.Structure):
     _fields_ = [("query_window_n", ctypes.c_int32), ("block_size_g", ctypes.c_int32),
                 ("sink_count_a", ctypes.c_int32), ("top_p", ctypes.c_float)]
@@ -314,6 +329,11 @@ class Ref(_Lib):
                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int, P(_Cfg), ctypes.c_int, P(ctypes.c_float),
                                        P(ctypes.c_float)])
+        self._fn("layer_flops", [ctypes.c_int32, ctypes.c_int64, P(_ModelCfg), P(ctypes.c_uint64)])
+        self._fn("scoring_flops", [ctypes.c_int64, ctypes.c_int64, P(_ModelCfg), P(ctypes.c_uint64)])
+        self._fn("validate_savings", [P(_ModelCfg), ctypes.c_int64, P(ctypes.c_int64), ctypes.c_int32,
+                                      P(ctypes.c_int32), P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_double),
+                                      ctypes.c_uint64, P(ctypes.c_uint64), P(ctypes.c_int32), P(ctypes.c_double)])
         self._fn("drop_layer_varlen", [P(ctypes.c_float), ctypes.c_int64, P(ctypes.c_float),
                                        ctypes.c_int64, P(ctypes.c_float), ctypes.c_int64,
                                        P(ctypes.c_int64), ctypes.c_int32, ctypes.c_int, ctypes.c_int,
@@ -366,6 +386,41 @@ class Ref(_Lib):
                                          _ptr(rl, ctypes.c_int64), layer, ctypes.byref(out))
         _raise(st, "decode_seqused")
         return int(out.value)
+
+    def layer_flops(self, kind: int, tokens: int, cfg) -> int:
+        c, _pat = _model_cfg(cfg)
+        out = ctypes.c_uint64(0)
+        _raise(self.lib.ref_layer_flops(int(kind), tokens, ctypes.byref(c), ctypes.byref(out)), "layer_flops")
+        return int(out.value)
+
+    def scoring_flops(self, effective_n: int, num_keys: int, cfg) -> int:
+        c, _pat = _model_cfg(cfg)
+        out = ctypes.c_uint64(0)
+        _raise(self.lib.ref_scoring_flops(effective_n, num_keys, ctypes.byref(c), ctypes.byref(out)), "scoring_flops")
+        return int(out.value)
+
+    def validate_savings(self, cfg, original: int, accel_tokens, drops, scoring: int) -> dict:
+        """validate_savings over a dense ledger at `original` tokens and an accelerated one
+        (accel_tokens per layer; drops = [(layer, before, after, retention_ratio)])."""
+        c, _pat = _model_cfg(cfg)
+        at = np.ascontiguousarray(accel_tokens, dtype=np.int64)
+        dl = np.ascontiguousarray([d[0] for d in drops] or [0], dtype=np.int32)
+        db = np.ascontiguousarray([d[1] for d in drops] or [0], dtype=np.int64)
+        da = np.ascontiguousarray([d[2] for d in drops] or [0], dtype=np.int64)
+        dr = np.ascontiguousarray([d[3] for d in drops] or [0.0], dtype=np.float64)
+        u = np.zeros(6, np.uint64)
+        i = np.zeros(5, np.int32)
+        f = np.zeros(2, np.float64)
+        st = self.lib.ref_validate_savings(ctypes.byref(c), original, _ptr(at, ctypes.c_int64), len(drops),
+                                           _ptr(dl, ctypes.c_int32), _ptr(db, ctypes.c_int64),
+                                           _ptr(da, ctypes.c_int64), _ptr(dr, ctypes.c_double), scoring,
+                                           _ptr(u, ctypes.c_uint64), _ptr(i, ctypes.c_int32), _ptr(f, ctypes.c_double))
+        _raise(st, "validate_savings")
+        return dict(dense_total=int(u[0]), accel_total=int(u[1]), scoring_overhead=int(u[2]),
+                    measured_delta=int(u[3]), formula_delta=int(u[4]), closed_linear_form=int(u[5]),
+                    exact_match=bool(i[0]), single_drop=bool(i[1]), drop_layer=int(i[2]),
+                    layers_after_drop=int(i[3]), linear_form_exact=bool(i[4]),
+                    retention_ratio=float(f[0]), attention_only_ratio=float(f[1]))
 
     def patch_metadata(self, tokens: np.ndarray, cu_seqlens, keep, selected, is_decode=None):
         t = np.ascontiguousarray(tokens, dtype=np.float32)

@@ -7,6 +7,7 @@
 // (core/include/uniprefill/*.hpp) and maps its exceptions to status codes:
 //   0 ok, 1 ConfigError, 2 ContractViolation, 9 any other exception.
 #include "uniprefill/errors.hpp"
+#include "uniprefill/flops.hpp"
 #include "uniprefill/importance.hpp"
 #include "uniprefill/propagation.hpp"
 #include "uniprefill/kvcache.hpp"
@@ -78,9 +79,83 @@ struct RefSelectionInfo {
     int32_t degenerate_keep_all;
 };
 
+struct RefModelCfg {
+    int32_t num_blocks;
+    int32_t sublayers_per_block;
+    int32_t hidden_dim;
+    int32_t head_dim;
+    int32_t num_heads;
+    int32_t window_size;
+    int32_t ffn_dim;
+    const int32_t* layer_pattern;  // pattern_length() SublayerKind values
+};
+
+ModelConfig to_model(const RefModelCfg* c) {
+    ModelConfig m;
+    m.num_blocks = c->num_blocks;
+    m.sublayers_per_block = c->sublayers_per_block;
+    m.hidden_dim = c->hidden_dim;
+    m.head_dim = c->head_dim;
+    m.num_heads = c->num_heads;
+    m.window_size = c->window_size;
+    m.ffn_dim = c->ffn_dim;
+    for (int i = 0; i < m.pattern_length(); ++i) m.layer_pattern.push_back(static_cast<SublayerKind>(c->layer_pattern[i]));
+    return m;
+}
+
 } // namespace
 
 extern "C" {
+
+// layer_flops / scoring_flops (flops.cpp:14-39).
+int ref_layer_flops(int32_t kind, int64_t tokens, const RefModelCfg* cfg, uint64_t* out) {
+    return guarded([&] { *out = layer_flops(static_cast<SublayerKind>(kind), tokens, to_model(cfg)); });
+}
+
+int ref_scoring_flops(int64_t effective_n, int64_t num_keys, const RefModelCfg* cfg, uint64_t* out) {
+    return guarded([&] { *out = scoring_flops(effective_n, num_keys, to_model(cfg)); });
+}
+
+// validate_savings (flops.cpp:58-144) over a dense ledger (every layer at `original`
+// tokens) and an accelerated ledger (accel_tokens[l] per layer, drops in order, scoring
+// overhead).  u64_out = {dense, accel, scoring, measured, formula, closed_linear_form};
+// i32_out = {exact, single_drop, drop_layer, layers_after_drop, linear_form_exact};
+// f64_out = {retention_ratio, attention_only_ratio}.
+int ref_validate_savings(const RefModelCfg* cfg, int64_t original, const int64_t* accel_tokens,
+                         int32_t num_drops, const int32_t* drop_layers, const int64_t* before,
+                         const int64_t* after, const double* retention, uint64_t scoring,
+                         uint64_t* u64_out, int32_t* i32_out, double* f64_out) {
+    return guarded([&] {
+        const ModelConfig m = to_model(cfg);
+        FlopsLedger dense, accel;
+        for (int l = 0; l < m.total_layers(); ++l) {
+            const SublayerKind kind = m.layer_pattern[static_cast<size_t>(l % m.pattern_length())];
+            dense.add_layer(l, kind, original, m);
+            accel.add_layer(l, kind, accel_tokens[l], m);
+        }
+        for (int32_t d = 0; d < num_drops; ++d) {
+            DropRecord r;
+            r.layer = drop_layers[d];
+            r.tokens_before = before[d];
+            r.tokens_after = after[d];
+            r.retention_ratio = retention[d];
+            accel.add_drop(r);
+        }
+        accel.add_scoring(scoring);
+        const SavingsReport rep = validate_savings(dense, accel, m);
+        const uint64_t u[6] = {rep.dense_total, rep.accel_total, rep.scoring_overhead, rep.measured_delta,
+                               rep.formula_delta, rep.closed_linear_form};
+        std::memcpy(u64_out, u, sizeof(u));
+        i32_out[0] = rep.exact_match;
+        i32_out[1] = rep.single_drop;
+        i32_out[2] = rep.drop_layer;
+        i32_out[3] = rep.layers_after_drop;
+        i32_out[4] = rep.linear_form_exact;
+        f64_out[0] = rep.retention_ratio;
+        f64_out[1] = rep.attention_only_ratio;
+    });
+}
+
 
 int ref_phi_encode(float x, uint32_t* out) {
     return guarded([&] { *out = phi_encode(x); });

@@ -12,6 +12,8 @@ from .api import (AllocationMissError, BlockScores, Compacted, ConfigError, Cont
                   score_blocks_tp, score_blocks_varlen, score_tokens, score_tokens_heads, select_varlen,
                   sharded_block_scores, top_p_select)
 from ._capi import LIB_PATH, lib
+from .ledger import (BatchLedger, DropRecord, FlopsLedger, LayerMeta, ModelConfig, SavingsReport, SublayerKind,
+                     layer_flops, layer_meta, scoring_flops, validate_savings)
 
 __all__ = [
     "AllocationMissError", "BlockScores", "Compacted", "ConfigError", "ContractViolation", "CudaError", "DropEvent",
@@ -21,4 +23,6 @@ __all__ = [
     "reconstitute_varlen", "reduce_block_scores", "scatter_rows", "slot_mapping", "decode_seqused",
     "score_blocks_tp", "score_blocks_varlen", "score_tokens", "score_tokens_heads", "select_varlen",
     "sharded_block_scores", "top_p_select", "LIB_PATH", "lib",
+    "BatchLedger", "DropRecord", "FlopsLedger", "LayerMeta", "ModelConfig", "SavingsReport", "SublayerKind",
+    "layer_flops", "layer_meta", "scoring_flops", "validate_savings",
 ]

@@ -73,3 +73,42 @@ def test_decode_seqused_matches_reference(up, ref):
     assert (got0 == np.array(lengths)[None, :]).all()
     with pytest.raises(up.ContractViolation):  # drop layers must increase (DropHistory::validate)
         up.decode_seqused(L, cu0, [9, 3], [res1.cu_seqlens, res2.cu_seqlens])
+
+
+def test_batch_ledger_over_device_drop_layers(up, ref):
+    """§8f row 4: LayerMeta snapshots and per-request FLOPs ledgers read off the device path's
+    own cu_seqlens through a 2-block hybrid model (drop at each block's full-attention layer,
+    reconstitution at the boundary), audited by the reference's validate_savings."""
+    from paper_2605_06221_b200.ledger import BatchLedger, FlopsLedger, ModelConfig, SublayerKind as K, validate_savings
+    from paper_2605_06221_b200.synthetic import make_batch
+    lengths = [3000, 129, 1500]
+    sb = make_batch(lengths, 32, 8, 128, 64, regime="planted", seed=11, device="cuda")
+    cfg = ModelConfig(2, 3, [K.FullAttention, K.SlidingWindowAttention, K.LinearAttention, K.FFN],
+                      hidden_dim=4096, head_dim=128, num_heads=32, window_size=4096, ffn_dim=14336)
+    layer = up.DropLayer(up.ScoreConfig(), up.HeadLayout(32, 8, 128), sum(lengths), len(lengths), [()],
+                         [torch.int64])
+    bl = BatchLedger(cfg)
+    for l in range(cfg.total_layers()):
+        if cfg.kind(l) == K.FullAttention:  # every block re-enters with the full prompt
+            out = layer(sb.q, sb.k, sb.cu_seqlens, [sb.positions])
+            layer.check()
+            meta = bl.record_layer(l, sb.cu_seqlens, out.cu_seqlens, layer.sel.covered_mass)
+            assert meta.seq_lens == lengths
+            cu_after = out.cu_seqlens
+        else:
+            meta = bl.record_layer(l, cu_after)
+    kept = np.diff(cu_after.cpu().numpy()).tolist()
+    assert bl.layer_meta[1].seq_lens == kept and bl.layer_meta[1].num_actual_tokens == sum(kept)
+    for r, n in enumerate(lengths):
+        dense = FlopsLedger()
+        for l in range(cfg.total_layers()):
+            dense.add_layer(l, cfg.kind(l), n, cfg)
+        acc = bl.ledgers[r]
+        rep = validate_savings(dense, acc, cfg)
+        want = ref.validate_savings(cfg, n, [e.tokens for e in acc.entries],
+                                    [(d.layer, d.tokens_before, d.tokens_after, d.retention_ratio) for d in acc.drops],
+                                    acc.scoring_overhead)
+        assert rep.exact_match and want["exact_match"]
+        for key in ("dense_total", "accel_total", "measured_delta", "formula_delta", "scoring_overhead"):
+            assert getattr(rep, key) == want[key], key
+        assert [d.tokens_after for d in acc.drops] == [kept[r]] * 2
