@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define UP_ABI_VERSION 2
+#define UP_ABI_VERSION 3
 
 typedef enum {
     UP_OK = 0,
@@ -200,6 +200,22 @@ up_status up_slot_mapping(void* stream, const int32_t* cu_seqlens, int32_t num_r
 up_status up_decode_seqused(void* stream, int32_t num_layers, int32_t num_requests, const int32_t* cu_orig,
                             int32_t num_drops, const int32_t* drop_layers, const int32_t* const* cu_after,
                             const int32_t* decode_appended, int32_t* seqused);
+
+/* Attention readout over the retained rows of a drop layer (attention_readout,
+ * model.cpp:215-263, as prefill_layer_step calls it after the selection,
+ * propagation.cpp:195-205).  For every segment r of batch (its cu_seqlens describe the
+ * COMPACTED rows, e.g. up_compact's cu_seqlens_out) and every local q-head, query row j
+ * attends to the segment's rows i with positions[i] in (positions[j] - window, positions[j]]
+ * (window <= 0: no lower bound):
+ *   out[j, h, :] = Σ_i softmax_i(q[j,h,:]·k[i,kvh,:] / sqrt(D)) v[i,kvh,:]
+ * q: bf16 [max_tokens, Hq_local, D] (heads->q_row_stride); k, v: bf16 [max_tokens,
+ * Hkv_local, D] (both heads->k_row_stride); positions: int64, strictly increasing within
+ * each segment; out: bf16 [max_tokens, Hq_local, D] (out_row_stride elements per row).
+ * D in {64, 128}.  A row with no visible key raises the sticky UP_ERR_CONTRACT
+ * (model.cpp:237; read by up_device_status). */
+up_status up_attention_varlen(void* stream, const up_batch* batch, const up_heads* heads, const void* q,
+                              const void* k, const void* v, const int64_t* positions, int64_t window,
+                              void* out, int64_t out_row_stride, void* workspace, size_t workspace_bytes);
 
 /* Synchronizes `stream`, returns the sticky device-side status raised since the last call
  * (UP_OK if none) and clears it. */

@@ -329,6 +329,9 @@ class Ref(_Lib):
                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int, P(_Cfg), ctypes.c_int, P(ctypes.c_float),
                                        P(ctypes.c_float)])
+        self._fn("attention_readout", [P(ctypes.c_float), P(ctypes.c_int64), ctypes.c_int64, P(ctypes.c_float),
+                                       P(ctypes.c_float), P(ctypes.c_int64), ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_int64, P(ctypes.c_float)])
         self._fn("layer_flops", [ctypes.c_int32, ctypes.c_int64, P(_ModelCfg), P(ctypes.c_uint64)])
         self._fn("scoring_flops", [ctypes.c_int64, ctypes.c_int64, P(_ModelCfg), P(ctypes.c_uint64)])
         self._fn("validate_savings", [P(_ModelCfg), ctypes.c_int64, P(ctypes.c_int64), ctypes.c_int32,
@@ -386,6 +389,22 @@ class Ref(_Lib):
                                          _ptr(rl, ctypes.c_int64), layer, ctypes.byref(out))
         _raise(st, "decode_seqused")
         return int(out.value)
+
+    def attention_readout(self, q, q_pos, k, v, kv_pos, num_heads: int, num_kv_heads: int, window: int = 0):
+        """attention_readout (model.cpp:215-263): q [rows, H*D], k/v [kv_rows, Hkv*D] fp32."""
+        qa = np.ascontiguousarray(q, dtype=np.float32)
+        ka = np.ascontiguousarray(k, dtype=np.float32)
+        va = np.ascontiguousarray(v, dtype=np.float32)
+        qp = np.ascontiguousarray(q_pos, dtype=np.int64)
+        kp = np.ascontiguousarray(kv_pos, dtype=np.int64)
+        D = qa.shape[1] // num_heads
+        out = np.zeros_like(qa)
+        st = self.lib.ref_attention_readout(_ptr(qa, ctypes.c_float), _ptr(qp, ctypes.c_int64), qa.shape[0],
+                                            _ptr(ka, ctypes.c_float), _ptr(va, ctypes.c_float),
+                                            _ptr(kp, ctypes.c_int64), ka.shape[0], num_heads, num_kv_heads, D,
+                                            int(window), _ptr(out, ctypes.c_float))
+        _raise(st, "attention_readout")
+        return out
 
     def layer_flops(self, kind: int, tokens: int, cfg) -> int:
         c, _pat = _model_cfg(cfg)

@@ -8,6 +8,7 @@
 //   0 ok, 1 ConfigError, 2 ContractViolation, 9 any other exception.
 #include "uniprefill/errors.hpp"
 #include "uniprefill/flops.hpp"
+#include "uniprefill/model.hpp"
 #include "uniprefill/importance.hpp"
 #include "uniprefill/propagation.hpp"
 #include "uniprefill/kvcache.hpp"
@@ -106,6 +107,24 @@ ModelConfig to_model(const RefModelCfg* c) {
 } // namespace
 
 extern "C" {
+
+// attention_readout (model.cpp:215-263) over one segment; GQA k/v ([rows, kv_heads*D]) are
+// expanded to the reference's MHA view.  window <= 0: no window.
+int ref_attention_readout(const float* q, const int64_t* q_pos, int64_t q_rows, const float* k, const float* v,
+                          const int64_t* kv_pos, int64_t kv_rows, int heads, int kv_heads, int head_dim,
+                          int64_t window, float* out) {
+    return guarded([&] {
+        Matrix qm(q_rows, static_cast<int64_t>(heads) * head_dim);
+        std::memcpy(qm.data.data(), q, sizeof(float) * qm.data.size());
+        const int64_t kld = static_cast<int64_t>(kv_heads) * head_dim;
+        const Matrix km = expand_heads(k, kld, kv_rows, kv_heads, heads, head_dim);
+        const Matrix vm = expand_heads(v, kld, kv_rows, kv_heads, heads, head_dim);
+        const Matrix o = attention_readout(qm, std::span<const int64_t>(q_pos, q_rows), km, vm,
+                                           std::span<const int64_t>(kv_pos, kv_rows), heads,
+                                           window > 0 ? std::optional<int64_t>(window) : std::nullopt);
+        std::memcpy(out, o.data.data(), sizeof(float) * o.data.size());
+    });
+}
 
 // layer_flops / scoring_flops (flops.cpp:14-39).
 int ref_layer_flops(int32_t kind, int64_t tokens, const RefModelCfg* cfg, uint64_t* out) {

@@ -4,7 +4,7 @@ The compute lives in hand-written sm_100a kernels behind the C ABI in
 ``include/uniprefill_b200.h`` (``_lib/libuniprefill_b200.so``); this package is the host-side
 mirror of the reference's operator API (see ``api.py``).
 """
-from .api import (AllocationMissError, BlockScores, Compacted, ConfigError, ContractViolation, CudaError, DropEvent,
+from .api import (AllocationMissError, attention_varlen, BlockScores, Compacted, ConfigError, ContractViolation, CudaError, DropEvent,
                   DropHistory, DropLayer, HeadLayout, ImportanceScores, PackedBatch, ScoreConfig,
                   Selection, ShardedBlockScores, ShardScores, TokenStream, UnsupportedError, VarlenSelection, Workspace,
                   allreduce_scores, apply_drop, compact_varlen, patch_metadata, reconstitute, reconstitute_varlen,
@@ -16,7 +16,7 @@ from .ledger import (BatchLedger, DropRecord, FlopsLedger, LayerMeta, ModelConfi
                      layer_flops, layer_meta, scoring_flops, validate_savings)
 
 __all__ = [
-    "AllocationMissError", "BlockScores", "Compacted", "ConfigError", "ContractViolation", "CudaError", "DropEvent",
+    "AllocationMissError", "attention_varlen", "BlockScores", "Compacted", "ConfigError", "ContractViolation", "CudaError", "DropEvent",
     "DropHistory", "DropLayer", "HeadLayout", "ImportanceScores", "PackedBatch", "ScoreConfig",
     "Selection", "ShardedBlockScores", "ShardScores", "TokenStream", "UnsupportedError", "VarlenSelection", "Workspace",
     "allreduce_scores", "apply_drop", "compact_varlen", "patch_metadata", "reconstitute",

@@ -422,6 +422,49 @@ def slot_mapping(cu_seqlens: torch.Tensor, positions: torch.Tensor, block_tables
     return out
 
 
+def attention_varlen(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, cu_seqlens, positions: torch.Tensor,
+                     heads: Optional[HeadLayout] = None, window: Optional[int] = None,
+                     max_tokens: Optional[int] = None, out: Optional[torch.Tensor] = None,
+                     workspace: Optional[Workspace] = None, check: bool = False) -> torch.Tensor:
+    """Attention readout over the retained rows (up_attention_varlen; attention_readout,
+    model.cpp:215-263, as prefill_layer_step calls it at a drop layer, propagation.cpp:195-205).
+
+    q bf16 [T, Hq, D], k / v bf16 [T, Hkv, D] (or 2-D with heads=), cu_seqlens int32 [R+1]
+    and positions int64 [T] of the compacted batch (``Compacted.cu_seqlens`` and its
+    positions plane).  Row j of a segment attends to the segment's rows with position in
+    (pos_j - window, pos_j].  Returns bf16 [T, Hq, D] (rows past cu_seqlens[-1] untouched)."""
+    for t in (q, k, v):
+        if t.dtype != torch.bfloat16:
+            raise ContractViolation("attention_varlen: q, k, v must be bfloat16")
+    if positions.dtype != torch.int64:
+        raise ContractViolation("attention_varlen: positions must be int64")
+    dev = q.device
+    cu = _as_i32_cuda(cu_seqlens, dev)
+    T = int(max_tokens if max_tokens is not None else q.shape[0])
+    if heads is None:
+        if q.dim() != 3 or k.dim() != 3:
+            raise ContractViolation("pass heads= for 2-D q/k/v")
+        heads = HeadLayout(q.shape[1], k.shape[1], q.shape[2])
+    qv, qs, D = _heads_view(q, heads.num_q_heads)
+    kv, ks, _ = _heads_view(k, heads.num_kv_heads)
+    vv, vs, _ = _heads_view(v, heads.num_kv_heads)
+    if D != heads.head_dim or vs != ks:
+        raise ContractViolation("attention_varlen: head dim / k-v row stride mismatch")
+    if out is None:
+        out = torch.empty(T, heads.num_q_heads, D, dtype=torch.bfloat16, device=dev)
+    ov, os_, _ = _heads_view(out, heads.num_q_heads)
+    b = _batch(cu, T, None)
+    hc = heads.c(qs, ks)
+    ws = workspace or _ws(dev)
+    buf = ws.get(b, hc, ScoreConfig().c())
+    _check(lib.up_attention_varlen(_stream_ptr(dev), ctypes.byref(b), ctypes.byref(hc), _ptr(qv), _ptr(kv), _ptr(vv),
+                                   _ptr(positions.contiguous()), int(window or 0), _ptr(ov), os_,
+                                   ctypes.c_void_p(buf.data_ptr()), buf.numel()), "attention_varlen")
+    if check:
+        ws.device_status()
+    return out
+
+
 def decode_seqused(num_layers: int, cu_orig: torch.Tensor, drop_layers: Sequence[int],
                    cu_after: Sequence[torch.Tensor], decode_appended: Optional[torch.Tensor] = None,
                    out: Optional[torch.Tensor] = None) -> torch.Tensor:

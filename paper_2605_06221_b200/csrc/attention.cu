@@ -1,0 +1,347 @@
+// attention.cu -- the drop layer's attention readout over the retained rows (SURVEY §8f
+// row 1): attention_readout (model.cpp:215-263) as prefill_layer_step calls it after the
+// selection (propagation.cpp:195-205) -- every retained query row attends to the retained
+// keys of its segment whose logical position lies in (pos_q - window, pos_q], softmax of
+// q·k/sqrt(D) over v.  The compacted rows come straight from up_compact (positions strictly
+// increasing per segment), so the visible keys of a row are one contiguous index range
+// [lo, hi) found by binary search over the positions.
+//
+// One CTA per (128-row query tile, q-head), six warps:
+//   warp 0     TMA producer: Q tile once, then K tiles (3-stage ring) and V tiles (2-stage)
+//   warp 1     MMA issuer (one elected thread): S_j = Q·K_j^T (ss, into TMEM S[j&1]);
+//              O += P_j·V_j (ts: P from TMEM, V as an MN-major smem operand)
+//   warps 2-5  softmax: one TMEM lane = one query row per thread; online softmax with a lazy
+//              reference (O and l are rescaled only when the row max grows by > 2^8), P
+//              written to TMEM as bf16 pairs, final O / l stored as bf16
+// TMEM (512 columns): S0 [0,128), S1 [128,256), O [256, 256+D), P0, P1 (64 columns each).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "params.cuh"
+
+namespace up {
+
+template <int D>
+struct AttnCfg {
+    static constexpr int BM = 128, BN = 128;
+    static constexpr int NCH = D / 64;                    // 64-element (128-byte) column boxes
+    static constexpr int BOX = BN * 128;                  // one box of 128 rows: 16 KB
+    static constexpr int Q_BYTES = NCH * BOX;
+    static constexpr int KV_STAGE = NCH * BOX;
+    static constexpr int KST = 3, VST = 2;
+    static constexpr int NBAR = 1 + 2 * KST + 2 * VST + 2 + 2 + 2;
+    static constexpr int THREADS = 192;
+    static constexpr uint32_t S_COL = 0, O_COL = 256, P_COL = 256 + D;
+    static constexpr int smem() { return 1024 + Q_BYTES + (KST + VST) * KV_STAGE + NBAR * 8 + 64; }
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// first index i in [b, e) with pos[i] > x (upper_bound) / >= x (lower_bound)
+__device__ __forceinline__ int64_t upper_pos(const int64_t* pos, int64_t b, int64_t e, int64_t x) {
+    while (b < e) {
+        const int64_t m = (b + e) >> 1;
+        if (pos[m] <= x) b = m + 1; else e = m;
+    }
+    return b;
+}
+__device__ __forceinline__ int64_t lower_pos(const int64_t* pos, int64_t b, int64_t e, int64_t x) {
+    while (b < e) {
+        const int64_t m = (b + e) >> 1;
+        if (pos[m] < x) b = m + 1; else e = m;
+    }
+    return b;
+}
+
+template <int D>
+__global__ void __launch_bounds__(192, 1)
+attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                 const __grid_constant__ CUtensorMap vmap, const AttnParams p) {
+    using C = AttnCfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sq = smem;
+    uint8_t* sk = sq + C::Q_BYTES;
+    uint8_t* sv = sk + C::KST * C::KV_STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sv + C::VST * C::KV_STAGE);
+    uint64_t* q_full = bars;
+    uint64_t* k_full = bars + 1;
+    uint64_t* k_empty = k_full + C::KST;
+    uint64_t* v_full = k_empty + C::KST;
+    uint64_t* v_empty = v_full + C::VST;
+    uint64_t* s_full = v_empty + C::VST;
+    uint64_t* p_full = s_full + 2;
+    uint64_t* pv_done = p_full + 2;
+    int64_t* plan = reinterpret_cast<int64_t*>(bars + C::NBAR);  // q0, seg_begin, seg_end, k_begin, k_end
+    uint32_t* misc = reinterpret_cast<uint32_t*>(plan + 5);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int H = p.num_q_heads;
+    const int h = blockIdx.x % H;
+    const int trev = blockIdx.x / H;
+
+    if (threadIdx.x == 0) {
+        // Tile of this CTA: tiles are numbered over the segments, last tile first (the causal
+        // tail tiles carry the most keys; scheduling them first evens out the wave).
+        const int R = p.num_requests;
+        int total = 0;
+        for (int r = 0; r < R; ++r) total += (p.cu_seqlens[r + 1] - p.cu_seqlens[r] + C::BM - 1) / C::BM;
+        int64_t q0 = -1, sb = 0, se = 0, kb = 0, ke = 0;
+        if (trev < total) {
+            int t = total - 1 - trev;
+            for (int r = 0; r < R; ++r) {
+                const int n = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+                const int nt = (n + C::BM - 1) / C::BM;
+                if (t < nt) {
+                    sb = p.cu_seqlens[r];
+                    se = p.cu_seqlens[r + 1];
+                    q0 = sb + static_cast<int64_t>(t) * C::BM;
+                    break;
+                }
+                t -= nt;
+            }
+            const int64_t qlast = (q0 + C::BM < se ? q0 + C::BM : se) - 1;
+            ke = upper_pos(p.positions, sb, se, p.positions[qlast]);
+            kb = p.window > 0 ? lower_pos(p.positions, sb, se, p.positions[q0] - p.window + 1) : sb;
+        }
+        plan[0] = q0;
+        plan[1] = sb;
+        plan[2] = se;
+        plan[3] = kb;
+        plan[4] = ke;
+        mbar_init(q_full, 1);
+        for (int s = 0; s < C::KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
+        for (int s = 0; s < C::VST; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&p_full[s], 4); mbar_init(&pv_done[s], 1); }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int64_t q0 = plan[0];
+    if (q0 < 0) return;  // beyond the batch's tiles (the grid is sized for the capacity)
+    const int64_t seg_begin = plan[1], seg_end = plan[2], k_begin = plan[3], k_end = plan[4];
+    const int nt = static_cast<int>((k_end - k_begin + C::BN - 1) / C::BN);
+    const int qh = p.q_head_offset + h;
+    const int kvh = qh / p.gqa_group - p.kv_head_offset;
+
+    if (warp == 1) tmem_alloc(misc, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = misc[0];
+
+    if (warp == 0) {
+        if (lane == 0) {
+            prefetch_tensormap(&qmap);
+            prefetch_tensormap(&kmap);
+            prefetch_tensormap(&vmap);
+            mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+            for (int c = 0; c < C::NCH; ++c)
+                tma_load_2d(sq + c * C::BOX, &qmap, q_full, h * D + c * 64, static_cast<int32_t>(q0));
+            for (int j = 0; j < nt; ++j) {
+                const int32_t row = static_cast<int32_t>(k_begin + static_cast<int64_t>(j) * C::BN);
+                const int ks = j % C::KST;
+                if (j >= C::KST) mbar_wait(&k_empty[ks], ((j / C::KST) - 1) & 1);
+                mbar_arrive_expect_tx(&k_full[ks], C::KV_STAGE);
+                for (int c = 0; c < C::NCH; ++c)
+                    tma_load_2d(sk + ks * C::KV_STAGE + c * C::BOX, &kmap, &k_full[ks], kvh * D + c * 64, row);
+                const int vs = j % C::VST;
+                if (j >= C::VST) mbar_wait(&v_empty[vs], ((j / C::VST) - 1) & 1);
+                mbar_arrive_expect_tx(&v_full[vs], C::KV_STAGE);
+                for (int c = 0; c < C::NCH; ++c)
+                    tma_load_2d(sv + vs * C::KV_STAGE + c * C::BOX, &vmap, &v_full[vs], kvh * D + c * 64, row);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t kIdescS = idesc_bf16_f32(128, C::BN);
+            constexpr uint32_t kIdescO = idesc_bf16_f32(128, D) | (1u << 16);  // B (V) MN-major
+            const uint64_t a_base = smem_desc_sw128(smem_u32(sq));
+            const uint64_t k_base = smem_desc_sw128(smem_u32(sk));
+            const uint64_t v_base = smem_desc_sw128_mn(smem_u32(sv), C::BOX, 1024);
+            mbar_wait(q_full, 0);
+            tc_fence_after();
+            auto issue_s = [&](int j) {
+                const int ks = j % C::KST;
+                mbar_wait(&k_full[ks], (j / C::KST) & 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + C::S_COL + (j & 1) * C::BN;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t off = ((kk >> 2) * C::BOX + (kk & 3) * 32) >> 4;
+                    mma_bf16_ss(d_tmem, a_base + off, k_base + ((ks * C::KV_STAGE) >> 4) + off, kIdescS,
+                                kk > 0 ? 1u : 0u);
+                }
+                mma_commit(&k_empty[ks]);
+                mma_commit(&s_full[j & 1]);
+            };
+            issue_s(0);
+            if (nt > 1) issue_s(1);
+            for (int j = 0; j < nt; ++j) {
+                mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+                const int vs = j % C::VST;
+                mbar_wait(&v_full[vs], (j / C::VST) & 1);
+                tc_fence_after();
+                const uint32_t a_tmem = tmem + C::P_COL + (j & 1) * (C::BN / 2);
+#pragma unroll
+                for (int kk = 0; kk < C::BN / 16; ++kk)  // 16 keys = two 8-row swizzle atoms
+                    mma_bf16_ts(tmem + C::O_COL, a_tmem + kk * 8,
+                                v_base + ((vs * C::KV_STAGE + kk * 2048) >> 4), kIdescO,
+                                (j > 0 || kk > 0) ? 1u : 0u);
+                mma_commit(&v_empty[vs]);
+                mma_commit(&pv_done[j & 1]);
+                if (j + 2 < nt) issue_s(j + 2);
+            }
+        }
+    } else {
+        // softmax warps: TMEM lane quarter = warp % 4
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+        const int64_t qi = q0 + r;
+        const bool valid = qi < seg_end;
+        int64_t lo = 0, hi = 0;
+        if (valid) {
+            const int64_t qp = p.positions[qi];
+            hi = upper_pos(p.positions, seg_begin, seg_end, qp);
+            lo = p.window > 0 ? lower_pos(p.positions, seg_begin, seg_end, qp - p.window + 1) : seg_begin;
+            if (lo >= hi) raise_error(p.err, kErrNoVisibleKey);
+        }
+        const float c = p.scale_log2;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int j = 0; j < nt; ++j) {
+            const int64_t kb = k_begin + static_cast<int64_t>(j) * C::BN;
+            const int vis0 = static_cast<int>(lo - kb < 0 ? 0 : (lo - kb > C::BN ? C::BN : lo - kb));
+            const int vis1 = static_cast<int>(hi - kb < 0 ? 0 : (hi - kb > C::BN ? C::BN : hi - kb));
+            const bool full = vis0 == 0 && vis1 == C::BN;
+            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            tc_fence_after();
+            const uint32_t s_addr = tmem + lane_base + C::S_COL + (j & 1) * C::BN;
+            uint32_t s[C::BN];
+#pragma unroll
+            for (int q = 0; q < C::BN / 32; ++q)
+                tmem_ld32(s_addr + q * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[q * 32]));
+            tmem_ld_wait();
+            float mx = -INFINITY;
+            if (full) {
+#pragma unroll
+                for (int i = 0; i < C::BN; ++i) mx = fmaxf(mx, __uint_as_float(s[i]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < C::BN; ++i)
+                    if (i >= vis0 && i < vis1) mx = fmaxf(mx, __uint_as_float(s[i]));
+            }
+            mx *= c;
+            // lazy rescale: keep the reference unless the max grew by more than 2^8.  The
+            // decision is per row, the O rescale warp-wide (tcgen05.ld/st are .sync.aligned).
+            const bool grow = mx > m_run + 8.f;
+            float alpha = 1.f;
+            if (grow) {
+                alpha = m_run == -INFINITY ? 0.f : ex2_approx(m_run - mx);
+                l_run *= alpha;
+                m_run = mx;
+            }
+            if (j > 0 && __any_sync(0xffffffffu, grow)) {
+                // O holds PV_0..PV_{j-1}: wait for the last one, then scale
+                mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int q = 0; q < D / 32; ++q) {
+                    uint32_t o[32];
+                    tmem_ld32(tmem + lane_base + C::O_COL + q * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tmem_st32(tmem + lane_base + C::O_COL + q * 32, o);
+                }
+            }
+            // P_j goes to P[j&1], last read by PV_{j-2}
+            if (j >= 2) {
+                mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
+                tc_fence_after();
+            }
+            const float mref = m_run == -INFINITY ? 0.f : m_run;
+            float lsum = 0.f;
+            const uint32_t p_addr = tmem + lane_base + C::P_COL + (j & 1) * (C::BN / 2);
+#pragma unroll
+            for (int q = 0; q < C::BN / 32; ++q) {
+                uint32_t pk16[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int e0 = q * 32 + 2 * i, e1 = e0 + 1;
+                    float p0 = ex2_approx(fmaf(__uint_as_float(s[e0]), c, -mref));
+                    float p1 = ex2_approx(fmaf(__uint_as_float(s[e1]), c, -mref));
+                    if (!full) {
+                        if (e0 < vis0 || e0 >= vis1) p0 = 0.f;
+                        if (e1 < vis0 || e1 >= vis1) p1 = 0.f;
+                    }
+                    lsum += p0 + p1;
+                    pk16[i] = pack_bf16(p0, p1);
+                }
+                tmem_st16(p_addr + q * 16, pk16);
+            }
+            l_run += lsum;
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[j & 1]);
+        }
+        // epilogue: O / l -> bf16
+        if (nt > 0) {
+            mbar_wait(&pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
+            tc_fence_after();
+        }
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        __nv_bfloat16* orow = p.out + qi * p.out_row_stride + static_cast<int64_t>(h) * D;
+#pragma unroll
+        for (int q = 0; q < D / 32; ++q) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_base + C::O_COL + q * 32, o);
+            tmem_ld_wait();
+            if (valid) {
+                uint4 w[4];
+                uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    wp[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+                uint4* dst = reinterpret_cast<uint4*>(orow + q * 32);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dst[i] = w[i];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int D>
+static cudaError_t launch_attn(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
+                               const AttnParams& p, int grid, cudaStream_t stream) {
+    using C = AttnCfg<D>;
+    const int smem = C::smem();
+    cudaError_t e = cudaFuncSetAttribute(attention_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    return launch_k(0, attention_kernel<D>, grid, C::THREADS, smem, stream, qm, km, vm, p);
+}
+
+bool attention_supported(int D) { return D == 64 || D == 128; }
+
+cudaError_t launch_attention(int D, const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
+                             const AttnParams& p, int grid, cudaStream_t stream) {
+    if (D == 64) return launch_attn<64>(qm, km, vm, p, grid, stream);
+    if (D == 128) return launch_attn<128>(qm, km, vm, p, grid, stream);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace up

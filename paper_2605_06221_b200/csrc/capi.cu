@@ -43,6 +43,10 @@ cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t str
 cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_slot_mapping(const SlotMapParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_decode_seqused(const SequsedParams& p, cudaStream_t stream);
+struct AttnParams;
+bool attention_supported(int D);
+cudaError_t launch_attention(int D, const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
+                             const AttnParams& p, int grid, cudaStream_t stream);
 int64_t compact_tiles(int64_t max_tokens);
 int compact_max_planes();
 
@@ -674,6 +678,56 @@ up_status up_decode_seqused(void* stream, int32_t num_layers, int32_t num_reques
     return cuda_status(e);
 }
 
+up_status up_attention_varlen(void* stream, const up_batch* b, const up_heads* h, const void* q, const void* k,
+                              const void* v, const int64_t* positions, int64_t window, void* out,
+                              int64_t out_row_stride, void* ws, size_t ws_bytes) {
+    g_launches = 0;
+    if (b == nullptr || h == nullptr || q == nullptr || k == nullptr || v == nullptr || positions == nullptr ||
+        out == nullptr || ws == nullptr || b->cu_seqlens == nullptr)
+        return UP_ERR_INVALID_ARGUMENT;
+    if (b->num_requests < 1 || b->max_tokens < 0 || h->num_q_heads < 1 || h->num_kv_heads < 1 || h->gqa_group < 1)
+        return UP_ERR_CONTRACT;
+    if (ws_bytes < 256) return UP_ERR_WORKSPACE;
+    const int D = h->head_dim;
+    if (!attention_supported(D)) return UP_ERR_UNSUPPORTED;
+    // every local q-head must read a local kv-head
+    const int kv_lo = h->q_head_offset / h->gqa_group - h->kv_head_offset;
+    const int kv_hi = (h->q_head_offset + h->num_q_heads - 1) / h->gqa_group - h->kv_head_offset;
+    if (kv_lo < 0 || kv_hi >= h->num_kv_heads) return UP_ERR_CONTRACT;
+    const int64_t qcols = static_cast<int64_t>(h->num_q_heads) * D, kcols = static_cast<int64_t>(h->num_kv_heads) * D;
+    if (h->q_row_stride < qcols || h->k_row_stride < kcols || out_row_stride < qcols) return UP_ERR_INVALID_ARGUMENT;
+    // TMA: 16-byte aligned bases and row strides
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+         reinterpret_cast<uintptr_t>(out)) & 15 || (h->q_row_stride | h->k_row_stride | out_row_stride) & 7)
+        return UP_ERR_UNSUPPORTED;
+    if (b->max_tokens == 0) return UP_OK;
+    CUtensorMap qm, km, vm;
+    if (!make_map(&qm, q, b->max_tokens, qcols, h->q_row_stride) ||
+        !make_map(&km, k, b->max_tokens, kcols, h->k_row_stride) ||
+        !make_map(&vm, v, b->max_tokens, kcols, h->k_row_stride))
+        return UP_ERR_CUDA;
+    AttnParams p{};
+    p.cu_seqlens = b->cu_seqlens;
+    p.positions = positions;
+    p.out = static_cast<__nv_bfloat16*>(out);
+    p.err = static_cast<uint32_t*>(ws);
+    p.max_tokens = b->max_tokens;
+    p.out_row_stride = out_row_stride;
+    p.window = window;
+    p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
+    p.num_requests = b->num_requests;
+    p.num_q_heads = h->num_q_heads;
+    p.gqa_group = h->gqa_group;
+    p.q_head_offset = h->q_head_offset;
+    p.kv_head_offset = h->kv_head_offset;
+    const int64_t tiles = (b->max_tokens + 127) / 128 + b->num_requests;
+    const int64_t grid = tiles * h->num_q_heads;
+    if (grid > 0x7fffffff) return UP_ERR_UNSUPPORTED;
+    const cudaError_t e = launch_attention(D, qm, km, vm, p, static_cast<int>(grid), static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return cuda_status(e);
+}
+
 up_status up_device_status(void* stream, void* ws) {
     if (ws == nullptr) return UP_ERR_INVALID_ARGUMENT;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -687,7 +741,7 @@ up_status up_device_status(void* stream, void* ws) {
     }
     if (flags & kErrTooManyBlocks) return UP_ERR_UNSUPPORTED;
     if (flags & kErrAllocationMiss) return UP_ERR_ALLOCATION_MISS;
-    if (flags & (kErrBadScore | kErrBadSeqlens | kErrMaskedRow)) return UP_ERR_CONTRACT;
+    if (flags & (kErrBadScore | kErrBadSeqlens | kErrMaskedRow | kErrNoVisibleKey)) return UP_ERR_CONTRACT;
     return UP_OK;
 }
 

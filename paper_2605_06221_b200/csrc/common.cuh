@@ -22,6 +22,7 @@ enum : uint32_t {
     kErrTooManyBlocks = 4u, // a request has more blocks than the on-chip sort holds
     kErrMaskedRow = 8u,     // fully masked query row (importance.cpp:57-59)
     kErrAllocationMiss = 16u,  // slot for a page the block table does not hold (kvcache.cpp:71-78)
+    kErrNoVisibleKey = 32u,    // attention row with no visible key (model.cpp:237)
 };
 
 constexpr int kMaxSortBlocks = 16384;  // per-request blocks the select kernel sorts on chip
@@ -256,6 +257,17 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         : "memory");
 }
 
+// 16 registers per thread -> 32 lanes x 16 consecutive 32-bit TMEM columns.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
+        : "memory");
+}
+
 __device__ __forceinline__ void tmem_st_wait() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -274,6 +286,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr) {
     d |= static_cast<uint64_t>(1024 >> 4) << 32;               // SBO
     d |= static_cast<uint64_t>(1) << 46;                       // descriptor version (sm_100)
     d |= static_cast<uint64_t>(2) << 61;                       // SWIZZLE_128B
+    return d;
+}
+
+// Same for an MN-major operand (N contiguous, e.g. V [keys][D] as the B of P·V) in the
+// SWIZZLE_128B layout TMA writes for 64-element-wide boxes: 64 N-elements per 128-byte
+// row, K rows 128 bytes apart, 8-row atoms SBO bytes apart, 64-wide N chunks LBO apart.
+__device__ __forceinline__ uint64_t smem_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
     return d;
 }
 

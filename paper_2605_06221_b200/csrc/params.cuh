@@ -163,4 +163,21 @@ struct SequsedParams {
     int32_t num_requests;
 };
 
+// Attention readout over the retained rows (attention.cu).
+struct AttnParams {
+    const int32_t* cu_seqlens;   // [R+1] segments of the (compacted) batch
+    const int64_t* positions;    // [rows] logical positions, strictly increasing per segment
+    __nv_bfloat16* out;          // [rows][out_row_stride], head h at column h*D
+    uint32_t* err;
+    int64_t max_tokens;
+    int64_t out_row_stride;
+    int64_t window;              // > 0: keys with pos > q_pos - window only
+    float scale_log2;            // log2(e) / sqrt(D)
+    int32_t num_requests;
+    int32_t num_q_heads;
+    int32_t gqa_group;
+    int32_t q_head_offset;
+    int32_t kv_head_offset;
+};
+
 }  // namespace up

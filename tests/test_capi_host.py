@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     from paper_2605_06221_b200._capi import lib, status_string
-    assert lib.up_abi_version() == 2
+    assert lib.up_abi_version() == 3
     assert status_string(0) == "ok"
     assert "ConfigError" in status_string(1)
     assert "ContractViolation" in status_string(2)
