@@ -249,6 +249,46 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
+def attention_stage(up, runner, sb, cu, Hq, D, stream, dev, tf_peak, reps=5):
+    """The drop layer's own attention over the retained rows (up_attention_varlen, SURVEY
+    §8f row 1; propagation.cpp:195-205): run one drop layer on `sb`, gather the retained
+    query rows (setup, untimed), then time the attention kernel over the compacted K, V and
+    positions.  Reported beside the path, not part of `value`.  Algorithmic FLOPs: 4·D·Hq
+    per (query row, visible key) -- QK^T and PV; causal, so row j of a segment of m
+    retained rows sees j+1 keys."""
+    torch = runner.torch
+    with torch.cuda.stream(stream):
+        runner(sb, cu)
+        torch.cuda.synchronize(dev)
+        L = runner.layer
+        rows = int(L.out.num_out.item())
+        idx = L.out.retained_index[:rows].long()
+        q = torch.zeros(runner.T, Hq, D, dtype=torch.bfloat16, device=dev)
+        q[:rows] = sb.q[idx]
+        _, kc, vc, pc = L.out.planes
+        heads = up.HeadLayout(Hq, runner.Hkv_local, D, gqa_group=runner.heads[0][2].gqa_group)
+        out = torch.empty_like(q)
+        cu_out = L.out.cu_seqlens
+        lens = (cu_out[1:] - cu_out[:-1]).double()
+        flops = float((4.0 * D * Hq * lens * (lens + 1) / 2).sum())
+
+        def run():
+            up.attention_varlen(q, kc, vc, cu_out, pc, heads=heads, max_tokens=runner.T, out=out)
+        run()
+        L.check()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            run()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / reps
+    ach = flops / (ms / 1e3) / 1e12
+    return {"bound": "tensor", "achieved": ach, "peak": tf_peak, "unit": "TFLOP/s", "frac": ach / tf_peak,
+            "ms_per_layer": ms, "algorithmic_flops_per_layer": flops, "rows": rows, "in_value": False,
+            "note": "drop-layer attention over the retained rows (SURVEY 8f row 1), not part of value"}
+
+
 class LayerRunner:
     """One drop layer (score -> [shard reduce] -> select -> compact) of the configured
     workload on this rank, through the public API (paper_2605_06221_b200.api)."""
@@ -358,10 +398,18 @@ def run_ours(args):
     from paper_2605_06221_b200.synthetic import MODEL_SHAPES, make_batch
 
     ws, rank, local = dist_env()
+    # one rank per GPU; UP_BENCH_BACKEND=gloo lets several ranks share one device (a
+    # functional check of the multi-rank path on a single-GPU box, never a bench number)
+    backend = os.environ.get("UP_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     model, lspec, layers, cfgd, mode = CONFIGS[args.config]
     shp = MODEL_SHAPES[model]
@@ -503,6 +551,8 @@ def run_ours(args):
         roofline = {"kernel": dominant, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                     "unit": d["unit"], "frac": d["frac"], "traffic": d["traffic"],
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json burst)"}
+        if not runner.local:
+            stage_info["attention"] = attention_stage(up, runner, sets[0], cu, Hq, D, stream, dev, tf_peak)
 
     # ---- e2e through the public API with host buffers ----
     # Inputs start in pinned host memory every step.  The scorer needs the query-window rows

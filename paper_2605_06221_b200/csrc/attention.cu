@@ -13,7 +13,8 @@
 //   warps 2-5  softmax: one TMEM lane = one query row per thread; online softmax with a lazy
 //              reference (O and l are rescaled only when the row max grows by > 2^8), P
 //              written to TMEM as bf16 pairs, final O / l stored as bf16
-// TMEM (512 columns): S0 [0,128), S1 [128,256), O [256, 256+D), P0, P1 (64 columns each).
+// TMEM (512 columns): S0, S1 (BN columns each), O (D columns), P0, P1 (BN/2 columns each);
+// BN = 128 keys per tile for D <= 128, 64 for D = 256.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -25,16 +26,21 @@ namespace up {
 
 template <int D>
 struct AttnCfg {
-    static constexpr int BM = 128, BN = 128;
+    // D=256: 64-key tiles so that Q (64 KB) + 3 K + 2 V stages fit in 227 KB of smem and
+    // S0, S1, O, P0, P1 fit in the 512 TMEM columns (64 + 64 + 256 + 32 + 32).
+    static constexpr int BM = 128, BN = D > 128 ? 64 : 128;
     static constexpr int NCH = D / 64;                    // 64-element (128-byte) column boxes
-    static constexpr int BOX = BN * 128;                  // one box of 128 rows: 16 KB
-    static constexpr int Q_BYTES = NCH * BOX;
-    static constexpr int KV_STAGE = NCH * BOX;
+    static constexpr int QBOX = BM * 128;                 // one box of the Q tile: 16 KB
+    static constexpr int KBOX = BN * 128;                 // one box of a K/V tile
+    static constexpr int Q_BYTES = NCH * QBOX;
+    static constexpr int KV_STAGE = NCH * KBOX;
     static constexpr int KST = 3, VST = 2;
     static constexpr int NBAR = 1 + 2 * KST + 2 * VST + 2 + 2 + 2;
     static constexpr int THREADS = 192;
-    static constexpr uint32_t S_COL = 0, O_COL = 256, P_COL = 256 + D;
+    static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, P_COL = 2 * BN + D;
+    static_assert(P_COL + BN <= 512, "TMEM columns");
     static constexpr int smem() { return 1024 + Q_BYTES + (KST + VST) * KV_STAGE + NBAR * 8 + 64; }
+    static_assert(smem() <= 232448, "shared memory");
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -144,19 +150,19 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             prefetch_tensormap(&vmap);
             mbar_arrive_expect_tx(q_full, C::Q_BYTES);
             for (int c = 0; c < C::NCH; ++c)
-                tma_load_2d(sq + c * C::BOX, &qmap, q_full, h * D + c * 64, static_cast<int32_t>(q0));
+                tma_load_2d(sq + c * C::QBOX, &qmap, q_full, h * D + c * 64, static_cast<int32_t>(q0));
             for (int j = 0; j < nt; ++j) {
                 const int32_t row = static_cast<int32_t>(k_begin + static_cast<int64_t>(j) * C::BN);
                 const int ks = j % C::KST;
                 if (j >= C::KST) mbar_wait(&k_empty[ks], ((j / C::KST) - 1) & 1);
                 mbar_arrive_expect_tx(&k_full[ks], C::KV_STAGE);
                 for (int c = 0; c < C::NCH; ++c)
-                    tma_load_2d(sk + ks * C::KV_STAGE + c * C::BOX, &kmap, &k_full[ks], kvh * D + c * 64, row);
+                    tma_load_2d(sk + ks * C::KV_STAGE + c * C::KBOX, &kmap, &k_full[ks], kvh * D + c * 64, row);
                 const int vs = j % C::VST;
                 if (j >= C::VST) mbar_wait(&v_empty[vs], ((j / C::VST) - 1) & 1);
                 mbar_arrive_expect_tx(&v_full[vs], C::KV_STAGE);
                 for (int c = 0; c < C::NCH; ++c)
-                    tma_load_2d(sv + vs * C::KV_STAGE + c * C::BOX, &vmap, &v_full[vs], kvh * D + c * 64, row);
+                    tma_load_2d(sv + vs * C::KV_STAGE + c * C::KBOX, &vmap, &v_full[vs], kvh * D + c * 64, row);
             }
         }
     } else if (warp == 1) {
@@ -165,7 +171,7 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             constexpr uint32_t kIdescO = idesc_bf16_f32(128, D) | (1u << 16);  // B (V) MN-major
             const uint64_t a_base = smem_desc_sw128(smem_u32(sq));
             const uint64_t k_base = smem_desc_sw128(smem_u32(sk));
-            const uint64_t v_base = smem_desc_sw128_mn(smem_u32(sv), C::BOX, 1024);
+            const uint64_t v_base = smem_desc_sw128_mn(smem_u32(sv), C::KBOX, 1024);
             mbar_wait(q_full, 0);
             tc_fence_after();
             auto issue_s = [&](int j) {
@@ -175,8 +181,9 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 const uint32_t d_tmem = tmem + C::S_COL + (j & 1) * C::BN;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = ((kk >> 2) * C::BOX + (kk & 3) * 32) >> 4;
-                    mma_bf16_ss(d_tmem, a_base + off, k_base + ((ks * C::KV_STAGE) >> 4) + off, kIdescS,
+                    const uint32_t koff = (kk & 3) * 32;
+                    mma_bf16_ss(d_tmem, a_base + (((kk >> 2) * C::QBOX + koff) >> 4),
+                                k_base + ((ks * C::KV_STAGE + (kk >> 2) * C::KBOX + koff) >> 4), kIdescS,
                                 kk > 0 ? 1u : 0u);
                 }
                 mma_commit(&k_empty[ks]);
@@ -335,12 +342,15 @@ static cudaError_t launch_attn(const CUtensorMap& qm, const CUtensorMap& km, con
     return launch_k(0, attention_kernel<D>, grid, C::THREADS, smem, stream, qm, km, vm, p);
 }
 
-bool attention_supported(int D) { return D == 64 || D == 128; }
+int attention_kv_box_rows(int D) { return D > 128 ? AttnCfg<256>::BN : AttnCfg<128>::BN; }
+
+bool attention_supported(int D) { return D == 64 || D == 128 || D == 256; }
 
 cudaError_t launch_attention(int D, const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
                              const AttnParams& p, int grid, cudaStream_t stream) {
     if (D == 64) return launch_attn<64>(qm, km, vm, p, grid, stream);
     if (D == 128) return launch_attn<128>(qm, km, vm, p, grid, stream);
+    if (D == 256) return launch_attn<256>(qm, km, vm, p, grid, stream);
     return cudaErrorInvalidValue;
 }
 

@@ -45,6 +45,7 @@ cudaError_t launch_slot_mapping(const SlotMapParams& p, int num_sms, cudaStream_
 cudaError_t launch_decode_seqused(const SequsedParams& p, cudaStream_t stream);
 struct AttnParams;
 bool attention_supported(int D);
+int attention_kv_box_rows(int D);
 cudaError_t launch_attention(int D, const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
                              const AttnParams& p, int grid, cudaStream_t stream);
 int64_t compact_tiles(int64_t max_tokens);
@@ -703,8 +704,8 @@ up_status up_attention_varlen(void* stream, const up_batch* b, const up_heads* h
     if (b->max_tokens == 0) return UP_OK;
     CUtensorMap qm, km, vm;
     if (!make_map(&qm, q, b->max_tokens, qcols, h->q_row_stride) ||
-        !make_map(&km, k, b->max_tokens, kcols, h->k_row_stride) ||
-        !make_map(&vm, v, b->max_tokens, kcols, h->k_row_stride))
+        !make_map(&km, k, b->max_tokens, kcols, h->k_row_stride, attention_kv_box_rows(D)) ||
+        !make_map(&vm, v, b->max_tokens, kcols, h->k_row_stride, attention_kv_box_rows(D)))
         return UP_ERR_CUDA;
     AttnParams p{};
     p.cu_seqlens = b->cu_seqlens;

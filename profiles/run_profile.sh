@@ -19,3 +19,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 520 --csv \
 ncu --set full --clock-control none --import-source on \
     -k regex:'score_tcw|compact_copy|select_radix|block_combine|pair_weights|expand_kernel' -s 12 -c 6 \
     -o "$OUT/prof_full$TAG" -f $BENCH > "$OUT/prof_full$TAG.log" 2>&1 || true
+
+# the drop layer's attention over the retained rows (bench.py attention stage, §8f row 1)
+ncu --set full --clock-control none --import-source on -k regex:attention_kernel -c 1 \
+    -o "$OUT/prof_attn$TAG" -f $BENCH > "$OUT/prof_attn$TAG.log" 2>&1 || true

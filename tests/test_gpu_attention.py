@@ -61,6 +61,8 @@ def _close(got, want):
     ([500, 70], 2, 2, 64, 0),
     ([400], 4, 2, 128, 40),
     ([256, 130], 8, 2, 64, 200),
+    ([300, 65, 1], 4, 2, 256, 0),
+    ([200], 2, 1, 256, 50),
 ])
 def test_attention_matches_reference(up, ref, lengths, Hq, Hkv, D, window):
     q, k, v, pos, cu = _inputs(lengths, Hq, Hkv, D, seed=sum(lengths) + D + window)
@@ -78,6 +80,8 @@ def test_attention_matches_reference(up, ref, lengths, Hq, Hkv, D, window):
     ([8192], 32, 8, 128, 0),
     ([3000, 5000, 1, 777], 8, 8, 128, 0),
     ([6000, 2048], 16, 4, 64, 1024),
+    ([4096, 1000], 16, 2, 256, 0),     # Qwen3-Next full-attention head layout
+    ([3000, 64], 16, 8, 256, 1024),    # Gemma-3 head layout, sliding window
 ])
 def test_attention_large_vs_torch(up, lengths, Hq, Hkv, D, window):
     q, k, v, pos, cu = _inputs(lengths, Hq, Hkv, D, seed=7 + D)
