@@ -46,6 +46,7 @@ cudaError_t launch_decode_seqused(const SequsedParams& p, cudaStream_t stream);
 struct AttnParams;
 bool attention_supported(int D);
 int attention_kv_box_rows(int D);
+int attention_rows_per_cta(int D);
 cudaError_t launch_attention(int D, const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
                              const AttnParams& p, int grid, cudaStream_t stream);
 int64_t compact_tiles(int64_t max_tokens);
@@ -721,7 +722,8 @@ up_status up_attention_varlen(void* stream, const up_batch* b, const up_heads* h
     p.gqa_group = h->gqa_group;
     p.q_head_offset = h->q_head_offset;
     p.kv_head_offset = h->kv_head_offset;
-    const int64_t tiles = (b->max_tokens + 127) / 128 + b->num_requests;
+    const int rows = attention_rows_per_cta(D);  // Σ_r ⌈n_r/rows⌉ <= ⌈max_tokens/rows⌉ + R
+    const int64_t tiles = (b->max_tokens + rows - 1) / rows + b->num_requests;
     const int64_t grid = tiles * h->num_q_heads;
     if (grid > 0x7fffffff) return UP_ERR_UNSUPPORTED;
     const cudaError_t e = launch_attention(D, qm, km, vm, p, static_cast<int>(grid), static_cast<cudaStream_t>(stream));
