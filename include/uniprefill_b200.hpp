@@ -205,6 +205,20 @@ inline void decode_seqused(cudaStream_t s, int32_t num_layers, int32_t num_reque
           "decode_seqused");
 }
 
+/// attention_readout (model.cpp:215-263) at a drop layer (propagation.cpp:195-205): every
+/// retained row of `compacted` attends to its segment's retained keys with position in
+/// (pos - window, pos]; out bf16 [max_tokens][out_row_stride].
+inline void attention_readout(cudaStream_t s, const VarlenBatch& compacted, const HeadLayout& h, const void* q,
+                              const void* k, const void* v, const int64_t* positions, int64_t window, void* out,
+                              int64_t out_row_stride, Workspace& ws) {
+    const up_batch b = compacted.c();
+    const up_heads hc = h.c();
+    check(up_attention_varlen(s, &b, &hc, q, k, v, positions, window, out,
+                              out_row_stride ? out_row_stride : int64_t(h.num_q_heads) * h.head_dim, ws.data(),
+                              ws.bytes()),
+          "attention_readout");
+}
+
 /// Synchronizes and raises the sticky device-side ContractViolation (NaN / negative block
 /// scores, malformed cu_seqlens) like the reference's exceptions.
 inline void check_device(cudaStream_t s, Workspace& ws) { check(up_device_status(s, ws.data()), "device"); }

@@ -21,5 +21,5 @@ ncu --set full --clock-control none --import-source on \
     -o "$OUT/prof_full$TAG" -f $BENCH > "$OUT/prof_full$TAG.log" 2>&1 || true
 
 # the drop layer's attention over the retained rows (bench.py attention stage, §8f row 1)
-ncu --set full --clock-control none --import-source on -k regex:attention_kernel -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:attention -c 1 \
     -o "$OUT/prof_attn$TAG" -f $BENCH > "$OUT/prof_attn$TAG.log" 2>&1 || true

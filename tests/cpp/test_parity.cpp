@@ -21,6 +21,8 @@ struct RefSelectionInfo { int64_t cutoff_rank, retained_count; double retention_
 int ref_top_p_select(const float*, int64_t, const RefScoreConfig*, int64_t, uint8_t*, RefSelectionInfo*);
 int ref_score_tokens_heads(const float*, int64_t, const float*, int64_t, int64_t, int, int, int, int, int,
                            const RefScoreConfig*, float*, float*, int32_t*);
+int ref_attention_readout(const float*, const int64_t*, int64_t, const float*, const float*, const int64_t*, int64_t,
+                          int, int, int, int64_t, float*);
 }
 
 namespace b2 = uniprefill::b200;
@@ -193,6 +195,44 @@ TEST_CASE(compaction_keeps_rows_in_position_order) {  // test_propagation.cpp:97
     CHECK(std::memcmp(&out[2 * cols], &st[6 * cols], cols * 4) == 0);
 }
 
+TEST_CASE(attention_readout_matches_reference) {  // model.cpp:215-263 over retained rows
+    const int H = 4, Hkv = 2, D = 128;
+    const std::vector<int32_t> lens{300, 1, 129};
+    std::vector<int32_t> cuv{0};
+    for (int32_t n : lens) cuv.push_back(cuv.back() + n);
+    const int T = cuv.back();
+    std::mt19937_64 rng(11);
+    std::normal_distribution<float> nd(0.f, 1.f);
+    std::vector<__nv_bfloat16> q(static_cast<size_t>(T) * H * D), k(static_cast<size_t>(T) * Hkv * D), v(k.size());
+    std::vector<float> qf(q.size()), kf(k.size()), vf(v.size());
+    for (size_t i = 0; i < q.size(); ++i) { q[i] = __float2bfloat16(nd(rng)); qf[i] = __bfloat162float(q[i]); }
+    for (size_t i = 0; i < k.size(); ++i) { k[i] = __float2bfloat16(nd(rng)); kf[i] = __bfloat162float(k[i]); }
+    for (size_t i = 0; i < v.size(); ++i) { v[i] = __float2bfloat16(nd(rng)); vf[i] = __bfloat162float(v[i]); }
+    std::vector<int64_t> pos(T);  // retained positions: strictly increasing with gaps
+    for (size_t r = 0; r < lens.size(); ++r)
+        for (int i = cuv[r]; i < cuv[r + 1]; ++i) pos[i] = 3 * (i - cuv[r]) + static_cast<int64_t>(r);
+    Dev<__nv_bfloat16> dq(q), dk(k), dv(v), dout(q.size());
+    Dev<int64_t> dpos(pos);
+    Dev<int32_t> cu(cuv);
+    b2::VarlenBatch b{static_cast<int32_t>(lens.size()), T, cu.p, nullptr};
+    b2::HeadLayout h{H, Hkv, D, H / Hkv};
+    b2::ScoreConfig cfg;
+    b2::Workspace ws(b, h, cfg);
+    b2::attention_readout(nullptr, b, h, dq.p, dk.p, dv.p, dpos.p, 0, dout.p, 0, ws);
+    b2::check_device(nullptr, ws);
+    const std::vector<__nv_bfloat16> got = dout.get(q.size());
+    for (size_t r = 0; r < lens.size(); ++r) {
+        const int b0 = cuv[r], n = lens[r];
+        std::vector<float> want(static_cast<size_t>(n) * H * D);
+        ref_attention_readout(&qf[static_cast<size_t>(b0) * H * D], &pos[b0], n, &kf[static_cast<size_t>(b0) * Hkv * D],
+                              &vf[static_cast<size_t>(b0) * Hkv * D], &pos[b0], n, H, Hkv, D, 0, want.data());
+        for (size_t i = 0; i < want.size(); ++i) {  // bf16 P and output: 2e-2 relative
+            const float g = __bfloat162float(got[static_cast<size_t>(b0) * H * D + i]);
+            CHECK(std::fabs(g - want[i]) <= 2e-2f * (1.f + std::fabs(want[i])));
+        }
+    }
+}
+
 int main() {
     struct { const char* name; void (*fn)(); } cases[] = {
         {"top_p_select worked example", top_p_select_worked_example},
@@ -201,6 +241,7 @@ int main() {
         {"negative block scores are contract violations", negative_block_scores_are_contract_violations},
         {"score_blocks within rtol 1e-3 of the reference", score_blocks_within_rtol_of_reference},
         {"compaction keeps rows in position order", compaction_keeps_rows_in_position_order},
+        {"attention_readout matches the reference", attention_readout_matches_reference},
     };
     for (auto& c : cases) {
         const int before = g_failed;
