@@ -553,6 +553,7 @@ def run_ours(args):
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json burst)"}
         if not runner.local:
             stage_info["attention"] = attention_stage(up, runner, sets[0], cu, Hq, D, stream, dev, tf_peak)
+            stage_info["attention"]["traffic"] = prof_traffic("attention")
 
     # ---- e2e through the public API with host buffers ----
     # Inputs start in pinned host memory every step.  The scorer needs the query-window rows

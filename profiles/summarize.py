@@ -90,6 +90,9 @@ def main():
         for k, n, avg, sh in shares:
             f.write(f"{k},{n},{avg:.0f},{sh:.4f}\n")
     full = full_metrics(os.path.join(src, f"prof_full{suffix}.ncu-rep"))
+    attn = os.path.join(src, f"prof_attn{suffix}.ncu-rep")  # the drop-layer attention stage
+    if os.path.exists(attn):
+        full += full_metrics(attn)
     traffic = {}
     lines = [f"# ncu summary ({tag})", "",
              f"Command: `CONFIG={config} profiles/run_profile.sh` (bench.py --config {config}, {workload}, "
