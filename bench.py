@@ -333,6 +333,10 @@ class LayerRunner:
         plane_dtypes = [torch.bfloat16, torch.bfloat16, torch.bfloat16, torch.int64]
         self.layer = up.DropLayer(cfg, up.HeadLayout(Hq, Hkv, D), self.T, self.R, plane_shapes, plane_dtypes,
                                   device=dev)
+        self.peer = None
+        if mode == "tp" and world > 1 and os.environ.get("UP_TP_REDUCE", "peer") == "peer":
+            from paper_2605_06221_b200.distributed import PeerScoreReducer
+            self.peer = PeerScoreReducer(self.nb, device=dev)
         if mode == "tp" and world == 1:
             nbmax = self.layer.scores.block_scores.numel()
             self.sharded = up.ShardedBlockScores(torch.empty(self.tp, nbmax, dtype=torch.float32, device=dev),
@@ -370,7 +374,9 @@ class LayerRunner:
         up.score_blocks_varlen(sb.q[:, qb:qe], sb.k[:, kb:ke], cu, self.cfg, h, max_tokens=self.T,
                                workspace=L.ws, out=L.scores)
         n = up.lib.up_last_launch_count()
-        allreduce_block_scores(L.scores.block_scores[:self.nb], deterministic=True)
+        # one-kernel peer-memory reduction (bitwise allreduce_scores); UP_TP_REDUCE=nccl:
+        # NCCL all-gather + the ordered reduce kernel
+        allreduce_block_scores(L.scores.block_scores[:self.nb], deterministic=True, peer=self.peer)
         return n + up.lib.up_last_launch_count()
 
     def select(self, cu):
@@ -656,6 +662,10 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
+        if runner.peer is not None:
+            runner.layer.check()
+            runner.peer.check()
+            runner.peer.close()
         dist.destroy_process_group()
 
 

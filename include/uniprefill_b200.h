@@ -10,6 +10,7 @@
  *                          (importance.hpp:42-47, importance.cpp:17-132) and, through the
  *                          head range, sharded_block_scores (tp_sim.hpp:25-26)
  *   up_reduce_block_scores replaces allreduce_scores (tp_sim.hpp:31, tp_sim.cpp:29-49)
+ *   up_peer_allreduce_scores  the same across a TP group of GPUs, over peer memory
  *                          for shard partials that are device-addressable from one GPU
  *   up_select              replaces top_p_select + expand_mask (selection.hpp:46-54,
  *                          selection.cpp:36-122) and the no-readmission veto
@@ -216,6 +217,29 @@ up_status up_decode_seqused(void* stream, int32_t num_layers, int32_t num_reques
 up_status up_attention_varlen(void* stream, const up_batch* batch, const up_heads* heads, const void* q,
                               const void* k, const void* v, const int64_t* positions, int64_t window,
                               void* out, int64_t out_row_stride, void* workspace, size_t workspace_bytes);
+
+/* ---- TP score all-reduce over peer memory (NVLink P2P / NVSwitch) ----------------------
+ * allreduce_scores (tp_sim.cpp:29-49) for a TP group of one process per GPU, as one kernel:
+ * every rank stores its partial into row `rank` of every peer's exchange buffer, raises a
+ * flag per peer, waits for the tp rows of its own buffer and sums them in ascending rank
+ * order from 0.0f -- bitwise the reference's reduction on every rank (an NCCL sum is not).
+ * Exchange buffers: one per rank from up_peer_buffer_alloc(tp, capacity) (zeroed), shared
+ * with up_ipc_get_handle / up_ipc_open_handle (UP_IPC_HANDLE_BYTES opaque bytes, exchanged
+ * by the host, e.g. over torch.distributed).  peer_buffers: HOST array of tp device
+ * pointers valid in this process, [rank] = this rank's own buffer.  Every rank must issue
+ * the same sequence of calls with the same count (<= capacity, the blocks of the batch);
+ * CUDA-graph capturable (the rendezvous state lives on the device).  A peer that never
+ * arrives raises the sticky UP_ERR_CUDA after ~2 s (read by up_device_status). */
+#define UP_IPC_HANDLE_BYTES 64
+size_t up_peer_buffer_bytes(int32_t tp, int64_t capacity);
+up_status up_peer_buffer_alloc(int32_t tp, int64_t capacity, void** buffer);
+up_status up_peer_buffer_free(void* buffer);
+up_status up_ipc_get_handle(const void* buffer, void* handle);
+up_status up_ipc_open_handle(const void* handle, void** buffer);
+up_status up_ipc_close_handle(void* buffer);
+up_status up_peer_allreduce_scores(void* stream, const float* partial, int64_t count, int32_t rank, int32_t tp,
+                                   void* const* peer_buffers, int64_t capacity, float* out, void* workspace,
+                                   size_t workspace_bytes);
 
 /* Synchronizes `stream`, returns the sticky device-side status raised since the last call
  * (UP_OK if none) and clears it. */

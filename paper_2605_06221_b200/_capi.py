@@ -16,7 +16,9 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libuniprefill_b200.so")
 EXPORTED = (
     "up_abi_version", "up_status_string", "up_config_validate", "up_max_blocks",
     "up_workspace_bytes", "up_score_blocks", "up_score_blocks_tp", "up_reduce_block_scores", "up_select",
-    "up_compact", "up_scatter_rows", "up_slot_mapping", "up_decode_seqused", "up_drop_layer", "up_attention_varlen", "up_device_status", "up_scorer_kind", "up_last_launch_count",
+    "up_compact", "up_scatter_rows", "up_slot_mapping", "up_decode_seqused", "up_drop_layer", "up_attention_varlen", "up_peer_buffer_bytes", "up_peer_buffer_alloc",
+    "up_peer_buffer_free", "up_ipc_get_handle", "up_ipc_open_handle", "up_ipc_close_handle",
+    "up_peer_allreduce_scores", "up_device_status", "up_scorer_kind", "up_last_launch_count",
 )
 
 UP_OK, UP_ERR_CONFIG, UP_ERR_CONTRACT, UP_ERR_UNSUPPORTED, UP_ERR_WORKSPACE, UP_ERR_CUDA, \
@@ -78,6 +80,13 @@ def _load():
         "up_drop_layer": ([vp, P(BatchC), P(HeadsC), P(ScoreConfigC), vp, vp, vp, vp, vp, vp,
                            P(SelectionOutC), P(PlaneC), i32, vp, vp, vp, vp, sz], ctypes.c_int),
         "up_attention_varlen": ([vp, P(BatchC), P(HeadsC), vp, vp, vp, vp, i64, vp, i64, vp, sz], ctypes.c_int),
+        "up_peer_buffer_bytes": ([i32, i64], sz),
+        "up_peer_buffer_alloc": ([i32, i64, P(vp)], ctypes.c_int),
+        "up_peer_buffer_free": ([vp], ctypes.c_int),
+        "up_ipc_get_handle": ([vp, vp], ctypes.c_int),
+        "up_ipc_open_handle": ([vp, P(vp)], ctypes.c_int),
+        "up_ipc_close_handle": ([vp], ctypes.c_int),
+        "up_peer_allreduce_scores": ([vp, vp, i64, i32, i32, P(vp), i64, vp, vp, sz], ctypes.c_int),
         "up_device_status": ([vp, vp], ctypes.c_int),
         "up_scorer_kind": ([P(HeadsC), P(ScoreConfigC), ctypes.c_int], ctypes.c_int),
         "up_last_launch_count": ([], ctypes.c_int),

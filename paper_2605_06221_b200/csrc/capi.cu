@@ -47,6 +47,8 @@ struct AttnParams;
 bool attention_supported(int D);
 int attention_kv_box_rows(int D);
 int attention_rows_per_cta(int D);
+struct PeerReduceParams;
+cudaError_t launch_peer_allreduce(const PeerReduceParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_attention(int D, const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
                              const AttnParams& p, int grid, cudaStream_t stream);
 int64_t compact_tiles(int64_t max_tokens);
@@ -731,6 +733,85 @@ up_status up_attention_varlen(void* stream, const up_batch* b, const up_heads* h
     return cuda_status(e);
 }
 
+size_t up_peer_buffer_bytes(int32_t tp, int64_t capacity) {
+    if (tp < 1 || tp > kPeerMaxRanks || capacity < 0) return 0;
+    return static_cast<size_t>(kPeerSlotsOffset) + static_cast<size_t>(tp) * static_cast<size_t>(capacity) * 4;
+}
+
+up_status up_peer_buffer_alloc(int32_t tp, int64_t capacity, void** buffer) {
+    if (buffer == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    const size_t bytes = up_peer_buffer_bytes(tp, capacity);
+    if (bytes == 0) return tp < 1 || capacity < 0 ? UP_ERR_CONTRACT : UP_ERR_UNSUPPORTED;
+    if (cudaMalloc(buffer, bytes) != cudaSuccess) return UP_ERR_CUDA;
+    if (cudaMemset(*buffer, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return UP_ERR_CUDA;
+    return UP_OK;
+}
+
+up_status up_peer_buffer_free(void* buffer) {
+    return cudaFree(buffer) == cudaSuccess ? UP_OK : UP_ERR_CUDA;
+}
+
+up_status up_ipc_get_handle(const void* buffer, void* handle) {
+    if (buffer == nullptr || handle == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    static_assert(sizeof(cudaIpcMemHandle_t) == UP_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, const_cast<void*>(buffer)) != cudaSuccess) return UP_ERR_CUDA;
+    std::memcpy(handle, &h, sizeof(h));
+    return UP_OK;
+}
+
+up_status up_ipc_open_handle(const void* handle, void** buffer) {
+    if (buffer == nullptr || handle == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    return cudaIpcOpenMemHandle(buffer, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? UP_OK : UP_ERR_CUDA;
+}
+
+up_status up_ipc_close_handle(void* buffer) {
+    return cudaIpcCloseMemHandle(buffer) == cudaSuccess ? UP_OK : UP_ERR_CUDA;
+}
+
+up_status up_peer_allreduce_scores(void* stream, const float* partial, int64_t count, int32_t rank, int32_t tp,
+                                   void* const* peer_buffers, int64_t capacity, float* out, void* ws,
+                                   size_t ws_bytes) {
+    g_launches = 0;
+    if (partial == nullptr || out == nullptr || peer_buffers == nullptr || ws == nullptr)
+        return UP_ERR_INVALID_ARGUMENT;
+    if (tp < 1 || rank < 0 || rank >= tp || count < 0 || count > capacity) return UP_ERR_CONTRACT;
+    if (tp > kPeerMaxRanks) return UP_ERR_UNSUPPORTED;
+    if (ws_bytes < 256) return UP_ERR_WORKSPACE;
+    for (int t = 0; t < tp; ++t)
+        if (peer_buffers[t] == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (count == 0) return UP_OK;
+    PeerReduceParams p{};
+    for (int t = 0; t < tp; ++t) {
+        uint8_t* b = static_cast<uint8_t*>(peer_buffers[t]);
+        p.peer_slots[t] = reinterpret_cast<float*>(b + kPeerSlotsOffset);
+        p.peer_flags[t] = reinterpret_cast<uint32_t*>(b + kPeerFlagsOffset);
+    }
+    uint8_t* own = static_cast<uint8_t*>(peer_buffers[rank]);
+    p.partial = partial;
+    p.slots = reinterpret_cast<const float*>(own + kPeerSlotsOffset);
+    p.flags = reinterpret_cast<const uint32_t*>(own + kPeerFlagsOffset);
+    p.epoch = reinterpret_cast<uint32_t*>(own);
+    p.out = out;
+    p.err = static_cast<uint32_t*>(ws);
+    p.count = count;
+    p.capacity = capacity;
+    p.rank = rank;
+    p.tp = tp;
+    // A fixed grid of one CTA per SM whatever the count (every chunk's CTA is resident
+    // while it waits for its peers, and every flag advances by tp per call, which the
+    // epoch-based targets rely on); trailing CTAs may own an empty chunk.
+    int grid = num_sms();
+    if (grid > kPeerMaxChunks) grid = kPeerMaxChunks;
+    int64_t chunk = (count + grid - 1) / grid;
+    p.chunk = (chunk + 63) / 64 * 64;
+    const cudaError_t e = launch_peer_allreduce(p, grid, static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return cuda_status(e);
+}
+
 up_status up_device_status(void* stream, void* ws) {
     if (ws == nullptr) return UP_ERR_INVALID_ARGUMENT;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -744,6 +825,7 @@ up_status up_device_status(void* stream, void* ws) {
     }
     if (flags & kErrTooManyBlocks) return UP_ERR_UNSUPPORTED;
     if (flags & kErrAllocationMiss) return UP_ERR_ALLOCATION_MISS;
+    if (flags & kErrPeerTimeout) return UP_ERR_CUDA;
     if (flags & (kErrBadScore | kErrBadSeqlens | kErrMaskedRow | kErrNoVisibleKey)) return UP_ERR_CONTRACT;
     return UP_OK;
 }

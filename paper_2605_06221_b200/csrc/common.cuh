@@ -23,6 +23,7 @@ enum : uint32_t {
     kErrMaskedRow = 8u,     // fully masked query row (importance.cpp:57-59)
     kErrAllocationMiss = 16u,  // slot for a page the block table does not hold (kvcache.cpp:71-78)
     kErrNoVisibleKey = 32u,    // attention row with no visible key (model.cpp:237)
+    kErrPeerTimeout = 64u,     // a TP peer's partial scores never arrived (peer.cu)
 };
 
 constexpr int kMaxSortBlocks = 16384;  // per-request blocks the select kernel sorts on chip

@@ -180,4 +180,25 @@ struct AttnParams {
     int32_t kv_head_offset;
 };
 
+// One-shot TP all-reduce of partial block scores over peer memory (peer.cu).
+constexpr int kPeerMaxRanks = 16;
+constexpr int kPeerMaxChunks = 256;
+constexpr int64_t kPeerFlagsOffset = 256;   // bytes: epoch[2] at 0, flags[kPeerMaxChunks] here,
+constexpr int64_t kPeerSlotsOffset = 2048;  // slots[tp][capacity] here
+struct PeerReduceParams {
+    const float* partial;                 // [count] this rank's partial
+    float* peer_slots[kPeerMaxRanks];     // rank t's slots (mapped), row-major [tp][capacity]
+    uint32_t* peer_flags[kPeerMaxRanks];  // rank t's flags (mapped)
+    const float* slots;                   // own slots
+    const uint32_t* flags;                // own flags
+    uint32_t* epoch;                      // own epoch[2]
+    float* out;
+    uint32_t* err;
+    int64_t count;
+    int64_t capacity;
+    int64_t chunk;
+    int32_t rank;
+    int32_t tp;
+};
+
 }  // namespace up

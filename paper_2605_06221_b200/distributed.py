@@ -11,16 +11,21 @@ Two ways the path shards:
   ranks before selection (Eq. 15).  ``allreduce_block_scores`` uses one
   NCCL all-reduce (sum) over NVLink; ``deterministic=True`` instead all-gathers the
   partials and sums them in ascending rank order with the sm_100a reduce kernel, which
-  reproduces allreduce_scores (tp_sim.cpp:43-47) bit for bit.
+  reproduces allreduce_scores (tp_sim.cpp:43-47) bit for bit.  ``PeerScoreReducer`` does
+  the same bitwise reduction as ONE sm_100a kernel over peer memory (CUDA IPC-mapped
+  exchange buffers on every rank, P2P stores over NVLink / NVSwitch + device flags):
+  no NCCL call and no separate gather on the data path.
 """
 from __future__ import annotations
 
+import ctypes
 from typing import Callable, List, Optional, Sequence
 
 import torch
 import torch.distributed as dist
 
-from .api import ContractViolation, ConfigError, reduce_block_scores
+from . import _capi
+from .api import ContractViolation, ConfigError, _check, _stream_ptr, reduce_block_scores
 
 
 def lpt_partition(lengths: Sequence[int], parts: int) -> List[List[int]]:
@@ -61,14 +66,86 @@ def head_slice(num_q_heads: int, num_kv_heads: int, tp_rank: int, tp_size: int):
     return (qb, qe), (kb, ke)
 
 
+class PeerScoreReducer:
+    """TP all-reduce of partial block scores over peer memory (up_peer_allreduce_scores).
+
+    Collective constructor: every rank of `group` allocates an exchange buffer for up to
+    `capacity` block scores, the CUDA IPC handles are all-gathered over `group` (any
+    backend) and the peers' buffers are mapped into this process.  A call then runs one
+    kernel: P2P stores of this rank's partial into every peer, device flags, and the
+    ascending-rank fp32 sum (bitwise allreduce_scores, tp_sim.cpp:43-47) on every rank.
+    Every rank must make the same sequence of calls with the same element counts."""
+
+    def __init__(self, capacity: int, group=None, device=None):
+        if not dist.is_initialized():
+            raise ContractViolation("PeerScoreReducer: torch.distributed is not initialized")
+        self.lib = _capi.lib
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.tp = dist.get_world_size(group)
+        self.capacity = int(capacity)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        own = ctypes.c_void_p()
+        _check(self.lib.up_peer_buffer_alloc(self.tp, self.capacity, ctypes.byref(own)), "peer_buffer_alloc")
+        self._own = own
+        handle = (ctypes.c_char * 64)()
+        _check(self.lib.up_ipc_get_handle(own, handle), "ipc_get_handle")
+        handles: list = [None] * self.tp
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        ptrs, self._opened = [], []
+        for t, h in enumerate(handles):
+            if t == self.rank:
+                ptrs.append(own.value)
+                continue
+            p = ctypes.c_void_p()
+            _check(self.lib.up_ipc_open_handle(ctypes.create_string_buffer(h, 64), ctypes.byref(p)),
+                   "ipc_open_handle")
+            self._opened.append(p)
+            ptrs.append(p.value)
+        self.buffers = (ctypes.c_void_p * self.tp)(*ptrs)
+        self.err = torch.zeros(64, dtype=torch.int32, device=self.device)
+        dist.barrier(group)
+
+    def __call__(self, partial: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Reduced scores of `partial` (fp32, contiguous, numel <= capacity) into `out`
+        (default: in place)."""
+        if partial.dtype != torch.float32 or not partial.is_contiguous():
+            raise ContractViolation("PeerScoreReducer: partial must be contiguous float32")
+        out = partial if out is None else out
+        _check(self.lib.up_peer_allreduce_scores(
+            _stream_ptr(partial.device), ctypes.c_void_p(partial.data_ptr()), partial.numel(), self.rank, self.tp,
+            self.buffers, self.capacity, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(self.err.data_ptr()),
+            self.err.numel() * 4), "peer_allreduce_scores")
+        return out
+
+    def check(self) -> None:
+        """Raise if a peer's partial never arrived (sticky device flag)."""
+        _check(self.lib.up_device_status(_stream_ptr(self.device), ctypes.c_void_p(self.err.data_ptr())),
+               "peer_allreduce_scores")
+
+    def close(self) -> None:
+        torch.cuda.synchronize(self.device)
+        dist.barrier(self.group)  # no peer still writes into a buffer about to go away
+        for p in self._opened:
+            self.lib.up_ipc_close_handle(p)
+        self._opened = []
+        dist.barrier(self.group)
+        if self._own is not None:
+            self.lib.up_peer_buffer_free(self._own)
+            self._own = None
+
+
 def allreduce_block_scores(partial: torch.Tensor, group=None, deterministic: bool = False,
-                           reducer: Optional[Callable[[List[torch.Tensor]], torch.Tensor]] = None
-                           ) -> torch.Tensor:
+                           reducer: Optional[Callable[[List[torch.Tensor]], torch.Tensor]] = None,
+                           peer: Optional[PeerScoreReducer] = None) -> torch.Tensor:
     """Sum per-rank partial block scores across the TP group, in place (returns `partial`).
 
     deterministic=False: one all-reduce (NCCL sum over NVLink).
     deterministic=True : all-gather + ascending-rank fp32 sum (bitwise allreduce_scores).
-    `reducer` overrides the ordered summation (tests pass the CPU oracle on gloo)."""
+    `reducer` overrides the ordered summation (tests pass the CPU oracle on gloo).
+    `peer`: the one-kernel peer-memory reduction (bitwise, like deterministic=True)."""
+    if peer is not None:
+        return peer(partial)
     if not dist.is_initialized():
         raise ContractViolation("allreduce_block_scores: torch.distributed is not initialized")
     if not deterministic:

@@ -1,0 +1,100 @@
+"""GPU: the TP score all-reduce over peer memory (up_peer_allreduce_scores,
+distributed.PeerScoreReducer) against allreduce_scores' ascending-rank fp32 sum
+(tp_sim.cpp:43-47), bit for bit.
+
+The GPU pool gives one GPU per call, so the TP group here is two processes sharing cuda:0:
+the exchange buffers are mapped across the processes with CUDA IPC exactly as across GPUs
+(the kernels of the two processes time-slice on the device, so this checks the protocol --
+stores, flags, epochs, graph replay -- not NVLink speed)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+COUNTS = [1, 300, 8192, 40000, 777]
+
+
+def _partial(rank, step, n):
+    g = torch.Generator().manual_seed(1000 * step + rank)
+    return torch.rand(n, generator=g, dtype=torch.float64).mul(10).float()
+
+
+def _expected(tp, step, n):
+    acc = np.zeros(n, dtype=np.float32)
+    for t in range(tp):  # ((0.0f + s_0) + s_1) + ... in fp32
+        acc = (acc + _partial(t, step, n).numpy()).astype(np.float32)
+    return acc
+
+
+def _worker(rank, tp, port, q):
+    import torch.distributed as dist
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=tp)
+        from paper_2605_06221_b200.distributed import PeerScoreReducer, allreduce_block_scores
+        red = PeerScoreReducer(max(COUNTS), device="cuda:0")
+        bad = []
+        for step, n in enumerate(COUNTS):
+            part = _partial(rank, step, n).cuda()
+            out = torch.empty_like(part)
+            red(part, out)
+            if step % 2:  # in place through the allreduce_block_scores entry point
+                allreduce_block_scores(part, peer=red)
+                if not torch.equal(part, out):
+                    bad.append(f"in-place step {step}")
+            torch.cuda.synchronize()
+            red.check()
+            if not np.array_equal(out.cpu().numpy().view(np.uint32), _expected(tp, step, n).view(np.uint32)):
+                bad.append(f"step {step} n={n}")
+        # CUDA graph: the rendezvous state (flags, epoch) lives on the device
+        n = 5000
+        part = torch.empty(n, device="cuda:0")
+        out = torch.empty_like(part)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            part.copy_(_partial(rank, 50, n))
+            red(part, out)  # warm-up outside capture
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                red(part, out)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for step in (51, 52):
+            part.copy_(_partial(rank, step, n))
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            if not np.array_equal(out.cpu().numpy().view(np.uint32), _expected(tp, step, n).view(np.uint32)):
+                bad.append(f"graph replay {step}")
+        red.check()
+        red.close()
+        dist.destroy_process_group()
+        q.put((rank, bad))
+    except Exception:  # report instead of hanging the parent
+        import traceback
+        tb = traceback.format_exc()
+        os.makedirs("gpurun_out", exist_ok=True)
+        with open(f"gpurun_out/peer_rank{rank}.txt", "w") as f:
+            f.write(tb)
+        q.put((rank, [tb.strip().splitlines()[-1]]))
+
+
+@pytest.mark.timeout(240)
+def test_peer_allreduce_bitwise_two_ranks_one_device():
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=200) for _ in procs)
+    for p in procs:
+        p.join(timeout=30)
+    assert results == {0: [], 1: []}, results
