@@ -381,15 +381,20 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
 }
 
 // ---------------------------------------------------------------------------------------
-// D <= 128: two query tiles per CTA (256 rows of one segment, one q-head), twelve warps:
-//   warp 0       TMA producer: Q0, Q1 once, then K_j / V_j (2-stage rings) shared by both tiles
+// D <= 128: persistent, one CTA per SM; each CTA takes work items = (pair of 128-row query
+// tiles of one segment, q-head), heaviest first.  Twelve warps:
+//   warp 0       TMA producer: Q0, Q1 per item (after the item before released them), then
+//                K_j / V_j (128 keys, 2-stage rings running across items) shared by both tiles
 //   warp 1       MMA issuer: S_i,j = Q_i·K_j^T into TMEM S_i; O_i += P_i,j·V_j with P_i,j read
 //                from the S_i columns it overwrote (ts).  Issue order S0,0 S1,0 | PV0,j S0,j+1
 //                PV1,j S1,j+1 | ...: tcgen05.mma of one thread execute in issue order, so
 //                S_i,j+1 overwrites S_i only after PV_i,j consumed P_i,j, and while one
 //                softmax warpgroup works on its tile the tensor pipe runs the other tile's
-//                PV and S (two softmax warps per SMSP hide each other's latency)
-//   warps 2-3    idle
+//                PV and S (two softmax warps per SMSP hide each other's latency).  The next
+//                item's first S MMAs overlap this item's epilogue.
+//   warp 2       scheduler: takes items from a global counter (heaviest first), plans them
+//                into a 2-deep smem ring
+//   warp 3       idle
 //   warps 4-7    softmax of tile 0, warps 8-11 softmax of tile 1 (TMEM lane = query row)
 // TMEM: S0 [0,128), S1 [128,256), O0 [256, 256+D), O1 [256+D, 256+2D).
 template <int D>
@@ -400,13 +405,54 @@ struct Attn2Cfg {
     static constexpr int Q_BYTES = NCH * BOX;             // one query tile
     static constexpr int KV_STAGE = NCH * BOX;
     static constexpr int KST = 2, VST = 2;
-    static constexpr int NBAR = 1 + 2 * KST + 2 * VST + 2 + 2 + 2;
+    static constexpr int PLANS = 2;                       // work-item ring depth
+    static constexpr int NBAR = 2 + 2 * KST + 2 * VST + 2 + 2 + 2 + 2 * PLANS;
     static constexpr int THREADS = 384;
     static constexpr uint32_t S_COL = 0, O_COL = 2 * BN;
     static_assert(O_COL + 2 * D <= 512, "TMEM columns");
-    static constexpr int smem() { return 1024 + 2 * Q_BYTES + (KST + VST) * KV_STAGE + NBAR * 8 + 64; }
+    static constexpr int smem() { return 1024 + 2 * Q_BYTES + (KST + VST) * KV_STAGE + NBAR * 8 + 64 + PLANS * 48; }
     static_assert(smem() <= 232448 - 1024, "shared memory");
 };
+
+// Work item = (pair of 128-row query tiles of one segment, q-head).  Pairs are numbered
+// over the segments with the last pair of the last segment first (the causal tail pairs
+// carry the most keys), the heads of one pair consecutive (they share K/V in L2); CTAs
+// take items from a global counter, so the heavy ones go first and the tail balances.
+struct PairPlan {
+    int64_t q0, seg_begin, seg_end, k_begin;
+    int32_t nt;  // 128-key tiles; -1 = no more work
+    int32_t h;   // local q-head
+};
+
+__device__ __forceinline__ int total_pairs(const AttnParams& p) {
+    int total = 0;
+    for (int r = 0; r < p.num_requests; ++r) total += (p.cu_seqlens[r + 1] - p.cu_seqlens[r] + 255) / 256;
+    return total;
+}
+
+__device__ PairPlan pair_plan(const AttnParams& p, int trev, int total) {
+    PairPlan pl{0, 0, 0, 0, 0, 0};
+    int t = total - 1 - trev;
+    for (int r = 0; r < p.num_requests; ++r) {
+        const int n = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+        const int np = (n + 255) / 256;
+        if (t < np) {
+            pl.seg_begin = p.cu_seqlens[r];
+            pl.seg_end = p.cu_seqlens[r + 1];
+            pl.q0 = pl.seg_begin + static_cast<int64_t>(t) * 256;
+            break;
+        }
+        t -= np;
+    }
+    const int64_t qlast = (pl.q0 + 256 < pl.seg_end ? pl.q0 + 256 : pl.seg_end) - 1;
+    // positions strictly increase within a segment, so without a window the visible keys
+    // of row i are exactly [seg_begin, i]: no search
+    const int64_t ke = p.window > 0 ? upper_pos(p.positions, pl.seg_begin, pl.seg_end, p.positions[qlast]) : qlast + 1;
+    pl.k_begin = p.window > 0 ? lower_pos(p.positions, pl.seg_begin, pl.seg_end, p.positions[pl.q0] - p.window + 1)
+                              : pl.seg_begin;
+    pl.nt = static_cast<int32_t>((ke - pl.k_begin + 127) / 128);
+    return pl;
+}
 
 template <int D>
 __global__ void __launch_bounds__(384, 1)
@@ -421,148 +467,172 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     uint8_t* sv = sk + C::KST * C::KV_STAGE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sv + C::VST * C::KV_STAGE);
     uint64_t* q_full = bars;
-    uint64_t* k_full = bars + 1;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* k_full = bars + 2;
     uint64_t* k_empty = k_full + C::KST;
     uint64_t* v_full = k_empty + C::KST;
     uint64_t* v_empty = v_full + C::VST;
     uint64_t* s_full = v_empty + C::VST;                  // [tile]
     uint64_t* p_full = s_full + 2;                        // [tile]
     uint64_t* o_done = p_full + 2;                        // [tile]
-    int64_t* plan = reinterpret_cast<int64_t*>(bars + C::NBAR);  // q0, seg_begin, seg_end, k_begin, k_end
-    uint32_t* misc = reinterpret_cast<uint32_t*>(plan + 5);
+    uint64_t* plan_full = o_done + 2;                     // [PLANS]
+    uint64_t* plan_empty = plan_full + C::PLANS;          // [PLANS]
+    PairPlan* plans = reinterpret_cast<PairPlan*>(bars + C::NBAR);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(plans + C::PLANS);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int H = p.num_q_heads;
-    const int h = blockIdx.x % H;
-    const int trev = blockIdx.x / H;
 
     if (threadIdx.x == 0) {
-        // tile pairs numbered over the segments, last pair first (most keys first)
-        const int R = p.num_requests;
-        int total = 0;
-        for (int r = 0; r < R; ++r) total += (p.cu_seqlens[r + 1] - p.cu_seqlens[r] + 2 * C::BM - 1) / (2 * C::BM);
-        int64_t q0 = -1, sb = 0, se = 0, kb = 0, ke = 0;
-        if (trev < total) {
-            int t = total - 1 - trev;
-            for (int r = 0; r < R; ++r) {
-                const int n = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
-                const int nt = (n + 2 * C::BM - 1) / (2 * C::BM);
-                if (t < nt) {
-                    sb = p.cu_seqlens[r];
-                    se = p.cu_seqlens[r + 1];
-                    q0 = sb + static_cast<int64_t>(t) * 2 * C::BM;
-                    break;
-                }
-                t -= nt;
-            }
-            const int64_t qlast = (q0 + 2 * C::BM < se ? q0 + 2 * C::BM : se) - 1;
-            ke = upper_pos(p.positions, sb, se, p.positions[qlast]);
-            kb = p.window > 0 ? lower_pos(p.positions, sb, se, p.positions[q0] - p.window + 1) : sb;
-        }
-        plan[0] = q0;
-        plan[1] = sb;
-        plan[2] = se;
-        plan[3] = kb;
-        plan[4] = ke;
         mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
         for (int s = 0; s < C::KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
         for (int s = 0; s < C::VST; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
         for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&p_full[s], 4); mbar_init(&o_done[s], 1); }
+        // a plan is read by the TMA warp, the MMA warp and the eight softmax warps
+        for (int s = 0; s < C::PLANS; ++s) { mbar_init(&plan_full[s], 1); mbar_init(&plan_empty[s], 10); }
         fence_barrier_init();
     }
-    __syncthreads();
-    const int64_t q0 = plan[0];
-    if (q0 < 0) return;  // beyond the batch's tile pairs (the grid is sized for the capacity)
-    const int64_t seg_begin = plan[1], seg_end = plan[2], k_begin = plan[3], k_end = plan[4];
-    const int nt = static_cast<int>((k_end - k_begin + C::BN - 1) / C::BN);
-    const int qh = p.q_head_offset + h;
-    const int kvh = qh / p.gqa_group - p.kv_head_offset;
-
     if (warp == 1) tmem_alloc(misc, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = misc[0];
+    // next work item of this CTA (written by the scheduler warp), read by a whole warp
+    auto take_plan = [&](int it) {
+        const int slot = it % C::PLANS;
+        mbar_wait(&plan_full[slot], (it / C::PLANS) & 1);
+        const PairPlan pl = plans[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&plan_empty[slot]);
+        return pl;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
             prefetch_tensormap(&qmap);
             prefetch_tensormap(&kmap);
             prefetch_tensormap(&vmap);
-            mbar_arrive_expect_tx(q_full, 2 * C::Q_BYTES);
-            for (int t = 0; t < 2; ++t)
-                for (int c = 0; c < C::NCH; ++c)
-                    tma_load_2d(sq + t * C::Q_BYTES + c * C::BOX, &qmap, q_full, h * D + c * 64,
-                                static_cast<int32_t>(q0 + t * C::BM));
-            for (int j = 0; j < nt; ++j) {
-                const int32_t row = static_cast<int32_t>(k_begin + static_cast<int64_t>(j) * C::BN);
-                const int ks = j % C::KST;
-                if (j >= C::KST) mbar_wait(&k_empty[ks], ((j / C::KST) - 1) & 1);
-                mbar_arrive_expect_tx(&k_full[ks], C::KV_STAGE);
-                for (int c = 0; c < C::NCH; ++c)
-                    tma_load_2d(sk + ks * C::KV_STAGE + c * C::BOX, &kmap, &k_full[ks], kvh * D + c * 64, row);
-                const int vs = j % C::VST;
-                if (j >= C::VST) mbar_wait(&v_empty[vs], ((j / C::VST) - 1) & 1);
-                mbar_arrive_expect_tx(&v_full[vs], C::KV_STAGE);
-                for (int c = 0; c < C::NCH; ++c)
-                    tma_load_2d(sv + vs * C::KV_STAGE + c * C::BOX, &vmap, &v_full[vs], kvh * D + c * 64, row);
+        }
+        uint32_t kv = 0;  // K/V tiles loaded so far (ring position)
+        for (int it = 0;; ++it) {
+            const PairPlan pl = take_plan(it);
+            if (pl.nt < 0) break;
+            const int h = pl.h;
+            const int kvh = (p.q_head_offset + h) / p.gqa_group - p.kv_head_offset;
+            if (lane == 0) {
+                if (it > 0) mbar_wait(q_empty, (it - 1) & 1);  // last S MMAs of the previous item done
+                mbar_arrive_expect_tx(q_full, 2 * C::Q_BYTES);
+                for (int t = 0; t < 2; ++t)
+                    for (int c = 0; c < C::NCH; ++c)
+                        tma_load_2d(sq + t * C::Q_BYTES + c * C::BOX, &qmap, q_full, h * D + c * 64,
+                                    static_cast<int32_t>(pl.q0 + t * C::BM));
+                for (int j = 0; j < pl.nt; ++j, ++kv) {
+                    const int32_t row = static_cast<int32_t>(pl.k_begin + static_cast<int64_t>(j) * C::BN);
+                    const uint32_t ks = kv % C::KST;
+                    if (kv >= C::KST) mbar_wait(&k_empty[ks], ((kv / C::KST) - 1) & 1);
+                    mbar_arrive_expect_tx(&k_full[ks], C::KV_STAGE);
+                    for (int c = 0; c < C::NCH; ++c)
+                        tma_load_2d(sk + ks * C::KV_STAGE + c * C::BOX, &kmap, &k_full[ks], kvh * D + c * 64, row);
+                    const uint32_t vs = kv % C::VST;
+                    if (kv >= C::VST) mbar_wait(&v_empty[vs], ((kv / C::VST) - 1) & 1);
+                    mbar_arrive_expect_tx(&v_full[vs], C::KV_STAGE);
+                    for (int c = 0; c < C::NCH; ++c)
+                        tma_load_2d(sv + vs * C::KV_STAGE + c * C::BOX, &vmap, &v_full[vs], kvh * D + c * 64, row);
+                }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t kIdescS = idesc_bf16_f32(128, C::BN);
-            constexpr uint32_t kIdescO = idesc_bf16_f32(128, D) | (1u << 16);  // B (V) MN-major
-            const uint64_t q_base = smem_desc_sw128(smem_u32(sq));
-            const uint64_t k_base = smem_desc_sw128(smem_u32(sk));
-            const uint64_t v_base = smem_desc_sw128_mn(smem_u32(sv), C::BOX, 1024);
-            mbar_wait(q_full, 0);
-            tc_fence_after();
-            auto issue_s = [&](int t, int j) {  // S_t,j (K_j already waited for)
-                const int ks = j % C::KST;
+        constexpr uint32_t kIdescS = idesc_bf16_f32(128, C::BN);
+        constexpr uint32_t kIdescO = idesc_bf16_f32(128, D) | (1u << 16);  // B (V) MN-major
+        const uint64_t q_base = smem_desc_sw128(smem_u32(sq));
+        const uint64_t k_base = smem_desc_sw128(smem_u32(sk));
+        const uint64_t v_base = smem_desc_sw128_mn(smem_u32(sv), C::BOX, 1024);
+        auto issue_s = [&](int t, uint32_t kvi) {  // S_t = Q_t K^T from ring slot kvi
+            const uint32_t ks = kvi % C::KST;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = ((kk >> 2) * C::BOX + (kk & 3) * 32) >> 4;
-                    mma_bf16_ss(tmem + C::S_COL + t * C::BN, q_base + ((t * C::Q_BYTES) >> 4) + off,
-                                k_base + ((ks * C::KV_STAGE) >> 4) + off, kIdescS, kk > 0 ? 1u : 0u);
-                }
-                mma_commit(&s_full[t]);
-            };
-            auto issue_pv = [&](int t, int j) {  // O_t += P_t,j V_j (V_j already waited for)
-                const int vs = j % C::VST;
+            for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t off = ((kk >> 2) * C::BOX + (kk & 3) * 32) >> 4;
+                mma_bf16_ss(tmem + C::S_COL + t * C::BN, q_base + ((t * C::Q_BYTES) >> 4) + off,
+                            k_base + ((ks * C::KV_STAGE) >> 4) + off, kIdescS, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&s_full[t]);
+        };
+        auto issue_pv = [&](int t, uint32_t kvi, bool first) {  // O_t += P_t V (P over S_t)
+            const uint32_t vs = kvi % C::VST;
 #pragma unroll
-                for (int kk = 0; kk < C::BN / 16; ++kk)  // 16 keys = 8 bf16-pair columns of P
-                    mma_bf16_ts(tmem + C::O_COL + t * D, tmem + C::S_COL + t * C::BN + kk * 8,
-                                v_base + ((vs * C::KV_STAGE + kk * 2048) >> 4), kIdescO,
-                                (j > 0 || kk > 0) ? 1u : 0u);
-            };
-            mbar_wait(&k_full[0], 0);
-            tc_fence_after();
-            issue_s(0, 0);
-            issue_s(1, 0);
-            mma_commit(&k_empty[0]);
-            for (int j = 0; j < nt; ++j) {
-                const int vs = j % C::VST;
-                const bool more = j + 1 < nt;
-                mbar_wait(&v_full[vs], (j / C::VST) & 1);
-                mbar_wait(&p_full[0], j & 1);
+            for (int kk = 0; kk < C::BN / 16; ++kk)  // 16 keys = 8 bf16-pair columns of P
+                mma_bf16_ts(tmem + C::O_COL + t * D, tmem + C::S_COL + t * C::BN + kk * 8,
+                            v_base + ((vs * C::KV_STAGE + kk * 2048) >> 4), kIdescO,
+                            (!first || kk > 0) ? 1u : 0u);
+        };
+        uint32_t kv = 0, js = 0;  // K/V ring position, S/P phases (tiles so far, per query tile)
+        for (int it = 0;; ++it) {
+            const PairPlan pl = take_plan(it);
+            if (pl.nt < 0) break;
+            const int nt = pl.nt;
+            if (lane == 0) {
+                mbar_wait(q_full, it & 1);
+                mbar_wait(&k_full[kv % C::KST], (kv / C::KST) & 1);
                 tc_fence_after();
-                issue_pv(0, j);
-                if (!more) mma_commit(&o_done[0]);
-                if (more) {
-                    mbar_wait(&k_full[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
+                issue_s(0, kv);
+                issue_s(1, kv);
+                if (nt == 1) mma_commit(q_empty);
+                mma_commit(&k_empty[kv % C::KST]);
+                for (int j = 0; j < nt; ++j) {
+                    const uint32_t kj = kv + j;
+                    const bool more = j + 1 < nt;
+                    mbar_wait(&v_full[kj % C::VST], (kj / C::VST) & 1);
+                    mbar_wait(&p_full[0], (js + j) & 1);
                     tc_fence_after();
-                    issue_s(0, j + 1);
+                    issue_pv(0, kj, j == 0);
+                    if (!more) mma_commit(&o_done[0]);
+                    if (more) {
+                        mbar_wait(&k_full[(kj + 1) % C::KST], ((kj + 1) / C::KST) & 1);
+                        tc_fence_after();
+                        issue_s(0, kj + 1);
+                    }
+                    mbar_wait(&p_full[1], (js + j) & 1);
+                    tc_fence_after();
+                    issue_pv(1, kj, j == 0);
+                    mma_commit(&v_empty[kj % C::VST]);
+                    if (!more) mma_commit(&o_done[1]);
+                    if (more) {
+                        issue_s(1, kj + 1);
+                        if (j + 2 == nt) mma_commit(q_empty);  // the item's last S MMAs
+                        mma_commit(&k_empty[(kj + 1) % C::KST]);
+                    }
                 }
-                mbar_wait(&p_full[1], j & 1);
-                tc_fence_after();
-                issue_pv(1, j);
-                mma_commit(&v_empty[vs]);
-                if (!more) mma_commit(&o_done[1]);
-                if (more) {
-                    issue_s(1, j + 1);
-                    mma_commit(&k_empty[(j + 1) % C::KST]);
+            }
+            kv += nt;
+            js += nt;
+        }
+    } else if (warp == 2) {
+        // scheduler: items are handed out dynamically (global counter in the workspace's
+        // error region, bytes [128, 136), returned to 0 by the last CTA), planned one
+        // ahead of the consumers
+        if (lane == 0) {
+            uint32_t* ctr = p.err + 32;
+            const int total = total_pairs(p);
+            const int items = total * H;
+            for (int it = 0;; ++it) {
+                const int slot = it % C::PLANS;
+                if (it >= C::PLANS) mbar_wait(&plan_empty[slot], ((it / C::PLANS) - 1) & 1);
+                const int item = static_cast<int>(atomicAdd(ctr, 1u));
+                PairPlan pl{0, 0, 0, 0, -1, 0};
+                if (item < items) {
+                    pl = pair_plan(p, item / H, total);
+                    pl.h = item % H;
                 }
+                plans[slot] = pl;
+                mbar_arrive(&plan_full[slot]);
+                if (item >= items) break;
+            }
+            __threadfence();
+            if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every CTA has taken its last item
+                atomicExch(ctr, 0u);
+                atomicExch(ctr + 1, 0u);
             }
         }
     } else if (warp >= 4) {
@@ -570,147 +640,164 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const int quarter = warp & 3;        // TMEM lane quarter
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-        const int64_t qi = q0 + t * C::BM + r;
-        const bool valid = qi < seg_end;
-        int64_t lo = 0, hi = 0;
-        if (valid) {
-            const int64_t qp = p.positions[qi];
-            hi = upper_pos(p.positions, seg_begin, seg_end, qp);
-            lo = p.window > 0 ? lower_pos(p.positions, seg_begin, seg_end, qp - p.window + 1) : seg_begin;
-            if (lo >= hi) raise_error(p.err, kErrNoVisibleKey);
-        }
-        const float c = p.scale_log2;
         const uint32_t s_addr = tmem + lane_base + C::S_COL + t * C::BN;
         const uint32_t o_addr = tmem + lane_base + C::O_COL + t * D;
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int j = 0; j < nt; ++j) {
-            const int64_t kb = k_begin + static_cast<int64_t>(j) * C::BN;
-            const int vis0 = static_cast<int>(lo - kb < 0 ? 0 : (lo - kb > C::BN ? C::BN : lo - kb));
-            const int vis1 = static_cast<int>(hi - kb < 0 ? 0 : (hi - kb > C::BN ? C::BN : hi - kb));
-            // warp-uniform: the P stores below are tcgen05.st (.sync.aligned)
-            const bool full = __all_sync(0xffffffffu, vis0 == 0 && vis1 == C::BN);
-            mbar_wait(&s_full[t], j & 1);
-            tc_fence_after();
-            // two passes over S_t in 64-column halves (keeps the row out of registers: the
-            // 384-thread CTA has 168 registers per thread): max, then exp2 -> P.  P half q
-            // lands in columns [32q, 32q+32), which only half 0 occupies and which is
-            // already in registers when it is overwritten.
-            constexpr int HALF = 64;
-            float mx = -INFINITY;
-#pragma unroll
-            for (int hf = 0; hf < C::BN / HALF; ++hf) {
-                uint32_t s[HALF];
-#pragma unroll
-                for (int q = 0; q < HALF / 32; ++q)
-                    tmem_ld32(s_addr + hf * HALF + q * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[q * 32]));
-                tmem_ld_wait();
-                if (full) {
-                    float a[4] = {mx, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-                    for (int i = 0; i < HALF; i += 8)
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            a[u] = fmax3(a[u], __uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1]));
-                    mx = fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3]));
-                } else {
-#pragma unroll
-                    for (int i = 0; i < HALF; ++i) {
-                        const int e = hf * HALF + i;
-                        if (e >= vis0 && e < vis1) mx = fmaxf(mx, __uint_as_float(s[i]));
-                    }
+        const float c = p.scale_log2;
+        uint32_t js = 0;
+        for (int it = 0;; ++it) {
+            const PairPlan pl = take_plan(it);
+            if (pl.nt < 0) break;
+            const int h = pl.h;
+            const int nt = pl.nt;
+            const int64_t qi = pl.q0 + t * C::BM + r;
+            const bool valid = qi < pl.seg_end;
+            int64_t lo = 0, hi = 0;
+            if (valid) {
+                if (p.window > 0) {
+                    const int64_t qp = p.positions[qi];
+                    hi = upper_pos(p.positions, pl.seg_begin, pl.seg_end, qp);
+                    lo = lower_pos(p.positions, pl.seg_begin, pl.seg_end, qp - p.window + 1);
+                } else {  // strictly increasing positions: keys [seg_begin, qi]
+                    hi = qi + 1;
+                    lo = pl.seg_begin;
                 }
+                if (lo >= hi) raise_error(p.err, kErrNoVisibleKey);
             }
-            mx *= c;
-            // lazy rescale (reference moves only when the row max grows by > 2^8).  O_t is
-            // idle here: PV_t,j-1 completed before S_t,j (issue order) signalled s_full.
-            const bool grow = mx > m_run + 8.f;
-            float alpha = 1.f;
-            if (grow) {
-                alpha = m_run == -INFINITY ? 0.f : ex2_approx(m_run - mx);
-                l_run *= alpha;
-                m_run = mx;
-            }
-            if (j > 0 && __any_sync(0xffffffffu, grow)) {
+            float m_run = -INFINITY, l_run = 0.f;
+            for (int j = 0; j < nt; ++j) {
+                const int64_t kb = pl.k_begin + static_cast<int64_t>(j) * C::BN;
+                const int vis0 = static_cast<int>(lo - kb < 0 ? 0 : (lo - kb > C::BN ? C::BN : lo - kb));
+                const int vis1 = static_cast<int>(hi - kb < 0 ? 0 : (hi - kb > C::BN ? C::BN : hi - kb));
+                // warp-uniform: the P stores below are tcgen05.st (.sync.aligned)
+                const bool full = __all_sync(0xffffffffu, vis0 == 0 && vis1 == C::BN);
+                mbar_wait(&s_full[t], (js + j) & 1);
+                tc_fence_after();
+                // two passes over S_t in 64-column halves (keeps the row out of registers:
+                // the 384-thread CTA has 168 registers per thread): max, then exp2 -> P.
+                // P half hf lands in columns [32hf, 32hf+32), which only half 0 occupies and
+                // which is already in registers when it is overwritten.
+                constexpr int HALF = 64;
+                float mx = -INFINITY;
 #pragma unroll
-                for (int q = 0; q < D / 32; ++q) {
-                    uint32_t o[32];
-                    tmem_ld32(o_addr + q * 32, o);
+                for (int hf = 0; hf < C::BN / HALF; ++hf) {
+                    uint32_t s[HALF];
+#pragma unroll
+                    for (int q = 0; q < HALF / 32; ++q)
+                        tmem_ld32(s_addr + hf * HALF + q * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[q * 32]));
                     tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                    tmem_st32(o_addr + q * 32, o);
-                }
-            }
-            const float mref = m_run == -INFINITY ? 0.f : m_run;
-            float lsum = 0.f;
-            const uint64_t c2 = pk(c, c), m2 = pk(-mref, -mref);
-            uint64_t acc0 = 0, acc1 = 0;
-#pragma unroll
-            for (int hf = 0; hf < C::BN / HALF; ++hf) {
-                uint32_t s[HALF];
-#pragma unroll
-                for (int q = 0; q < HALF / 32; ++q)
-                    tmem_ld32(s_addr + hf * HALF + q * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[q * 32]));
-                tmem_ld_wait();
-#pragma unroll
-                for (int q = 0; q < HALF / 32; ++q) {
-                    uint32_t pk16[16];
                     if (full) {
+                        float a[4] = {mx, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int e0 = q * 32 + 2 * i;
-                            const uint64_t x = fma2(static_cast<uint64_t>(s[e0]) | (static_cast<uint64_t>(s[e0 + 1]) << 32),
-                                                    c2, m2);
-                            const uint64_t e = i < 16 - kAttnPolyPairs<D> ? pk(ex2_approx(lo_f(x)), ex2_approx(hi_f(x)))
-                                                                          : exp2_poly2(x);
-                            if (i & 1) acc1 = add2(acc1, e);
-                            else acc0 = add2(acc0, e);
-                            pk16[i] = pack_bf16(lo_f(e), hi_f(e));
-                        }
+                        for (int i = 0; i < HALF; i += 8)
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                a[u] = fmax3(a[u], __uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1]));
+                        mx = fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3]));
                     } else {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int e0 = hf * HALF + q * 32 + 2 * i, e1 = e0 + 1;
-                            float p0 = ex2_approx(fmaf(__uint_as_float(s[q * 32 + 2 * i]), c, -mref));
-                            float p1 = ex2_approx(fmaf(__uint_as_float(s[q * 32 + 2 * i + 1]), c, -mref));
-                            if (e0 < vis0 || e0 >= vis1) p0 = 0.f;
-                            if (e1 < vis0 || e1 >= vis1) p1 = 0.f;
-                            lsum += p0 + p1;
-                            pk16[i] = pack_bf16(p0, p1);
+                        for (int i = 0; i < HALF; ++i) {
+                            const int e = hf * HALF + i;
+                            if (e >= vis0 && e < vis1) mx = fmaxf(mx, __uint_as_float(s[i]));
                         }
                     }
-                    tmem_st16(s_addr + hf * 32 + q * 16, pk16);
+                }
+                mx *= c;
+                // lazy rescale (reference moves only when the row max grows by > 2^8).  O_t
+                // is idle here: PV_t,j-1 completed before S_t,j (issue order) signalled.
+                const bool grow = mx > m_run + 8.f;
+                float alpha = 1.f;
+                if (grow) {
+                    alpha = m_run == -INFINITY ? 0.f : ex2_approx(m_run - mx);
+                    l_run *= alpha;
+                    m_run = mx;
+                }
+                if (j > 0 && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+                    for (int q = 0; q < D / 32; ++q) {
+                        uint32_t o[32];
+                        tmem_ld32(o_addr + q * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                        tmem_st32(o_addr + q * 32, o);
+                    }
+                }
+                const float mref = m_run == -INFINITY ? 0.f : m_run;
+                float lsum = 0.f;
+                const uint64_t c2 = pk(c, c), m2 = pk(-mref, -mref);
+                uint64_t acc0 = 0, acc1 = 0;
+#pragma unroll
+                for (int hf = 0; hf < C::BN / HALF; ++hf) {
+                    uint32_t s[HALF];
+#pragma unroll
+                    for (int q = 0; q < HALF / 32; ++q)
+                        tmem_ld32(s_addr + hf * HALF + q * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[q * 32]));
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int q = 0; q < HALF / 32; ++q) {
+                        uint32_t pk16[16];
+                        if (full) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const int e0 = q * 32 + 2 * i;
+                                const uint64_t x = fma2(
+                                    static_cast<uint64_t>(s[e0]) | (static_cast<uint64_t>(s[e0 + 1]) << 32), c2, m2);
+                                const uint64_t e = i < 16 - kAttnPolyPairs<D>
+                                                       ? pk(ex2_approx(lo_f(x)), ex2_approx(hi_f(x)))
+                                                       : exp2_poly2(x);
+                                if (i & 1) acc1 = add2(acc1, e);
+                                else acc0 = add2(acc0, e);
+                                pk16[i] = pack_bf16(lo_f(e), hi_f(e));
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const int e0 = hf * HALF + q * 32 + 2 * i, e1 = e0 + 1;
+                                float p0 = ex2_approx(fmaf(__uint_as_float(s[q * 32 + 2 * i]), c, -mref));
+                                float p1 = ex2_approx(fmaf(__uint_as_float(s[q * 32 + 2 * i + 1]), c, -mref));
+                                if (e0 < vis0 || e0 >= vis1) p0 = 0.f;
+                                if (e1 < vis0 || e1 >= vis1) p1 = 0.f;
+                                lsum += p0 + p1;
+                                pk16[i] = pack_bf16(p0, p1);
+                            }
+                        }
+                        tmem_st16(s_addr + hf * 32 + q * 16, pk16);
+                    }
+                }
+                {
+                    const uint64_t a2 = add2(acc0, acc1);
+                    lsum += lo_f(a2) + hi_f(a2);
+                }
+                l_run += lsum;
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[t]);
+            }
+            // epilogue: O_t / l -> bf16.  The next item's PV_t,0 (which overwrites O_t) is
+            // issued only after this warpgroup's next p_full arrival, i.e. after these loads.
+            mbar_wait(&o_done[t], it & 1);
+            tc_fence_after();
+            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+            __nv_bfloat16* orow = p.out + qi * p.out_row_stride + static_cast<int64_t>(h) * D;
+#pragma unroll
+            for (int q = 0; q < D / 32; ++q) {
+                uint32_t o[32];
+                tmem_ld32(o_addr + q * 32, o);
+                tmem_ld_wait();
+                if (valid) {
+                    uint4 w[4];
+                    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        wp[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+                    uint4* dst = reinterpret_cast<uint4*>(orow + q * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) dst[i] = w[i];
                 }
             }
-            {
-                const uint64_t a2 = add2(acc0, acc1);
-                lsum += lo_f(a2) + hi_f(a2);
-            }
-            l_run += lsum;
-            tmem_st_wait();
             tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[t]);
-        }
-        mbar_wait(&o_done[t], 0);
-        tc_fence_after();
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        __nv_bfloat16* orow = p.out + qi * p.out_row_stride + static_cast<int64_t>(h) * D;
-#pragma unroll
-        for (int q = 0; q < D / 32; ++q) {
-            uint32_t o[32];
-            tmem_ld32(o_addr + q * 32, o);
-            tmem_ld_wait();
-            if (valid) {
-                uint4 w[4];
-                uint32_t* wp = reinterpret_cast<uint32_t*>(w);
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    wp[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-                uint4* dst = reinterpret_cast<uint4*>(orow + q * 32);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) dst[i] = w[i];
-            }
+            js += nt;
         }
     }
     tc_fence_before();

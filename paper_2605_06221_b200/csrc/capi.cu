@@ -726,7 +726,8 @@ up_status up_attention_varlen(void* stream, const up_batch* b, const up_heads* h
     p.kv_head_offset = h->kv_head_offset;
     const int rows = attention_rows_per_cta(D);  // Σ_r ⌈n_r/rows⌉ <= ⌈max_tokens/rows⌉ + R
     const int64_t tiles = (b->max_tokens + rows - 1) / rows + b->num_requests;
-    const int64_t grid = tiles * h->num_q_heads;
+    int64_t grid = tiles * h->num_q_heads;
+    if (rows == 256 && grid > num_sms()) grid = num_sms();  // persistent two-tile kernel
     if (grid > 0x7fffffff) return UP_ERR_UNSUPPORTED;
     const cudaError_t e = launch_attention(D, qm, km, vm, p, static_cast<int>(grid), static_cast<cudaStream_t>(stream));
     g_launches = 1;
