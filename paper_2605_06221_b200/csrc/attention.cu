@@ -129,7 +129,7 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 t -= nt;
             }
             const int64_t qlast = (q0 + C::BM < se ? q0 + C::BM : se) - 1;
-            ke = upper_pos(p.positions, sb, se, p.positions[qlast]);
+            ke = p.window > 0 ? upper_pos(p.positions, sb, se, p.positions[qlast]) : qlast + 1;
             kb = p.window > 0 ? lower_pos(p.positions, sb, se, p.positions[q0] - p.window + 1) : sb;
         }
         plan[0] = q0;
@@ -231,7 +231,8 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         int64_t lo = 0, hi = 0;
         if (valid) {
             const int64_t qp = p.positions[qi];
-            hi = upper_pos(p.positions, seg_begin, seg_end, qp);
+            // strictly increasing positions: without a window the keys are [seg_begin, qi]
+            hi = p.window > 0 ? upper_pos(p.positions, seg_begin, seg_end, qp) : qi + 1;
             lo = p.window > 0 ? lower_pos(p.positions, seg_begin, seg_end, qp - p.window + 1) : seg_begin;
             if (lo >= hi) raise_error(p.err, kErrNoVisibleKey);
         }
