@@ -336,7 +336,7 @@ class LayerRunner:
         self.peer = None
         if mode == "tp" and world > 1 and os.environ.get("UP_TP_REDUCE", "peer") == "peer":
             from paper_2605_06221_b200.distributed import PeerScoreReducer
-            self.peer = PeerScoreReducer(self.nb, device=dev)
+            self.peer = PeerScoreReducer(self.T // G + self.R + 1, device=dev)  # up_max_blocks
         if mode == "tp" and world == 1:
             nbmax = self.layer.scores.block_scores.numel()
             self.sharded = up.ShardedBlockScores(torch.empty(self.tp, nbmax, dtype=torch.float32, device=dev),
@@ -371,12 +371,17 @@ class LayerRunner:
             return up.lib.up_last_launch_count()
         from paper_2605_06221_b200.distributed import allreduce_block_scores
         (qb, qe), (kb, ke), h = self.heads[0]
+        if self.peer is not None:
+            # this rank's heads scored with the all-reduce fused into the combine kernel
+            # (partials stored straight into the peers' buffers, ascending-rank sum)
+            self.peer.score_blocks(sb.q[:, qb:qe], sb.k[:, kb:ke], cu, self.cfg, h, max_tokens=self.T,
+                                   workspace=L.ws, out=L.scores)
+            return up.lib.up_last_launch_count()
         up.score_blocks_varlen(sb.q[:, qb:qe], sb.k[:, kb:ke], cu, self.cfg, h, max_tokens=self.T,
                                workspace=L.ws, out=L.scores)
         n = up.lib.up_last_launch_count()
-        # one-kernel peer-memory reduction (bitwise allreduce_scores); UP_TP_REDUCE=nccl:
-        # NCCL all-gather + the ordered reduce kernel
-        allreduce_block_scores(L.scores.block_scores[:self.nb], deterministic=True, peer=self.peer)
+        # UP_TP_REDUCE=nccl: NCCL all-gather + the ordered reduce kernel (bitwise allreduce_scores)
+        allreduce_block_scores(L.scores.block_scores[:self.nb], deterministic=True)
         return n + up.lib.up_last_launch_count()
 
     def select(self, cu):

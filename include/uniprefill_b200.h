@@ -241,6 +241,18 @@ up_status up_peer_allreduce_scores(void* stream, const float* partial, int64_t c
                                    void* const* peer_buffers, int64_t capacity, float* out, void* workspace,
                                    size_t workspace_bytes);
 
+/* up_score_blocks over this rank's head slice (heads->q_head_offset / kv_head_offset) FUSED
+ * with the TP all-reduce over peer memory: the block-combine kernel stores every block's
+ * partial straight into the peers' exchange buffers and, after the rendezvous, writes the
+ * ascending-rank sum to block_scores -- sharded_block_scores + allreduce_scores
+ * (tp_sim.cpp:12-49) across GPUs in the scorer's own launches.  capacity >= the batch's
+ * blocks (up_max_blocks).  Off the tensor-core envelope: the SIMT scorer, then
+ * up_peer_allreduce_scores over up_max_blocks entries. */
+up_status up_score_blocks_peer(void* stream, const up_batch* batch, const up_heads* heads,
+                               const up_score_config* cfg, const void* q, const void* k, int32_t rank, int32_t tp,
+                               void* const* peer_buffers, int64_t capacity, float* block_scores,
+                               int32_t* cu_blocks, void* workspace, size_t workspace_bytes);
+
 /* Synchronizes `stream`, returns the sticky device-side status raised since the last call
  * (UP_OK if none) and clears it. */
 up_status up_device_status(void* stream, void* workspace);

@@ -18,7 +18,7 @@ EXPORTED = (
     "up_workspace_bytes", "up_score_blocks", "up_score_blocks_tp", "up_reduce_block_scores", "up_select",
     "up_compact", "up_scatter_rows", "up_slot_mapping", "up_decode_seqused", "up_drop_layer", "up_attention_varlen", "up_peer_buffer_bytes", "up_peer_buffer_alloc",
     "up_peer_buffer_free", "up_ipc_get_handle", "up_ipc_open_handle", "up_ipc_close_handle",
-    "up_peer_allreduce_scores", "up_device_status", "up_scorer_kind", "up_last_launch_count",
+    "up_peer_allreduce_scores", "up_score_blocks_peer", "up_device_status", "up_scorer_kind", "up_last_launch_count",
 )
 
 UP_OK, UP_ERR_CONFIG, UP_ERR_CONTRACT, UP_ERR_UNSUPPORTED, UP_ERR_WORKSPACE, UP_ERR_CUDA, \
@@ -87,6 +87,8 @@ def _load():
         "up_ipc_open_handle": ([vp, P(vp)], ctypes.c_int),
         "up_ipc_close_handle": ([vp], ctypes.c_int),
         "up_peer_allreduce_scores": ([vp, vp, i64, i32, i32, P(vp), i64, vp, vp, sz], ctypes.c_int),
+        "up_score_blocks_peer": ([vp, P(BatchC), P(HeadsC), P(ScoreConfigC), vp, vp, i32, i32, P(vp), i64, vp, vp,
+                                  vp, sz], ctypes.c_int),
         "up_device_status": ([vp, vp], ctypes.c_int),
         "up_scorer_kind": ([P(HeadsC), P(ScoreConfigC), ctypes.c_int], ctypes.c_int),
         "up_last_launch_count": ([], ctypes.c_int),

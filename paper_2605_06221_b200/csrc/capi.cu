@@ -31,7 +31,11 @@ struct BlockCombineParams;
 struct PairWeightsParams;
 struct SlotMapParams;
 struct SequsedParams;
+struct PeerReduceParams;
 cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_block_combine_peer(const BlockCombineParams& p, const PeerReduceParams& pr, int grid,
+                                      cudaStream_t stream);
+int peer_grid(int num_sms);
 cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int num_sms,
                               cudaStream_t stream);
@@ -47,7 +51,6 @@ struct AttnParams;
 bool attention_supported(int D);
 int attention_kv_box_rows(int D);
 int attention_rows_per_cta(int D);
-struct PeerReduceParams;
 cudaError_t launch_peer_allreduce(const PeerReduceParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_attention(int D, const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
                              const AttnParams& p, int grid, cudaStream_t stream);
@@ -305,7 +308,8 @@ int up_scorer_kind(const up_heads* h, const up_score_config* c, int want_token_s
 static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_heads* h,
                                const up_score_config* c, const void* q, const void* k, int tp,
                                float* shard_scores, int64_t shard_stride, float* block_scores,
-                               int32_t* cu_blocks, const Layout& L, void* ws) {
+                               int32_t* cu_blocks, const Layout& L, void* ws,
+                               const PeerReduceParams* peer = nullptr) {
     const int D = h->head_dim;
     const int R = b->num_requests;
     const int G = c->block_size_g;
@@ -387,6 +391,12 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     bp.npar = plan.npar;
     bp.block_size_g = G;
     bp.unit_keys = p.unit_keys;
+    if (peer != nullptr) {  // fused with the TP all-reduce over peer memory
+        if ((e = launch_block_combine_peer(bp, *peer, peer_grid(num_sms()), stream)) != cudaSuccess)
+            return UP_ERR_CUDA;
+        g_launches = 3;
+        return UP_OK;
+    }
     const int64_t cgrid = (L.max_blocks + 7) / 8;  // warp per block, 8 warps per CTA
     if ((e = launch_block_combine(bp, static_cast<int>(cgrid < num_sms() * 8 ? cgrid : num_sms() * 8), stream)) !=
         cudaSuccess)
@@ -772,45 +782,85 @@ up_status up_ipc_close_handle(void* buffer) {
     return cudaIpcCloseMemHandle(buffer) == cudaSuccess ? UP_OK : UP_ERR_CUDA;
 }
 
+static up_status peer_params(int32_t rank, int32_t tp, void* const* peer_buffers, int64_t capacity, float* out,
+                             uint32_t* err, PeerReduceParams* p) {
+    if (peer_buffers == nullptr || out == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (tp < 1 || rank < 0 || rank >= tp || capacity < 0) return UP_ERR_CONTRACT;
+    if (tp > kPeerMaxRanks) return UP_ERR_UNSUPPORTED;
+    for (int t = 0; t < tp; ++t)
+        if (peer_buffers[t] == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    *p = PeerReduceParams{};
+    for (int t = 0; t < tp; ++t) {
+        uint8_t* b = static_cast<uint8_t*>(peer_buffers[t]);
+        p->peer_slots[t] = reinterpret_cast<float*>(b + kPeerSlotsOffset);
+        p->peer_flags[t] = reinterpret_cast<uint32_t*>(b + kPeerFlagsOffset);
+    }
+    uint8_t* own = static_cast<uint8_t*>(peer_buffers[rank]);
+    p->slots = reinterpret_cast<const float*>(own + kPeerSlotsOffset);
+    p->flags = reinterpret_cast<const uint32_t*>(own + kPeerFlagsOffset);
+    p->epoch = reinterpret_cast<uint32_t*>(own);
+    p->out = out;
+    p->err = err;
+    p->capacity = capacity;
+    p->rank = rank;
+    p->tp = tp;
+    return UP_OK;
+}
+
 up_status up_peer_allreduce_scores(void* stream, const float* partial, int64_t count, int32_t rank, int32_t tp,
                                    void* const* peer_buffers, int64_t capacity, float* out, void* ws,
                                    size_t ws_bytes) {
     g_launches = 0;
-    if (partial == nullptr || out == nullptr || peer_buffers == nullptr || ws == nullptr)
-        return UP_ERR_INVALID_ARGUMENT;
-    if (tp < 1 || rank < 0 || rank >= tp || count < 0 || count > capacity) return UP_ERR_CONTRACT;
-    if (tp > kPeerMaxRanks) return UP_ERR_UNSUPPORTED;
+    if (partial == nullptr || ws == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    if (count < 0 || count > capacity) return UP_ERR_CONTRACT;
     if (ws_bytes < 256) return UP_ERR_WORKSPACE;
-    for (int t = 0; t < tp; ++t)
-        if (peer_buffers[t] == nullptr) return UP_ERR_INVALID_ARGUMENT;
+    PeerReduceParams p;
+    const up_status st = peer_params(rank, tp, peer_buffers, capacity, out, static_cast<uint32_t*>(ws), &p);
+    if (st != UP_OK) return st;
     if (count == 0) return UP_OK;
-    PeerReduceParams p{};
-    for (int t = 0; t < tp; ++t) {
-        uint8_t* b = static_cast<uint8_t*>(peer_buffers[t]);
-        p.peer_slots[t] = reinterpret_cast<float*>(b + kPeerSlotsOffset);
-        p.peer_flags[t] = reinterpret_cast<uint32_t*>(b + kPeerFlagsOffset);
-    }
-    uint8_t* own = static_cast<uint8_t*>(peer_buffers[rank]);
     p.partial = partial;
-    p.slots = reinterpret_cast<const float*>(own + kPeerSlotsOffset);
-    p.flags = reinterpret_cast<const uint32_t*>(own + kPeerFlagsOffset);
-    p.epoch = reinterpret_cast<uint32_t*>(own);
-    p.out = out;
-    p.err = static_cast<uint32_t*>(ws);
     p.count = count;
-    p.capacity = capacity;
-    p.rank = rank;
-    p.tp = tp;
     // A fixed grid of one CTA per SM whatever the count (every chunk's CTA is resident
     // while it waits for its peers, and every flag advances by tp per call, which the
     // epoch-based targets rely on); trailing CTAs may own an empty chunk.
-    int grid = num_sms();
-    if (grid > kPeerMaxChunks) grid = kPeerMaxChunks;
-    int64_t chunk = (count + grid - 1) / grid;
+    const int grid = peer_grid(num_sms());
+    const int64_t chunk = (count + grid - 1) / grid;
     p.chunk = (chunk + 63) / 64 * 64;
     const cudaError_t e = launch_peer_allreduce(p, grid, static_cast<cudaStream_t>(stream));
     g_launches = 1;
     return cuda_status(e);
+}
+
+up_status up_score_blocks_peer(void* stream_, const up_batch* b, const up_heads* h, const up_score_config* c,
+                               const void* q, const void* k, int32_t rank, int32_t tp, void* const* peer_buffers,
+                               int64_t capacity, float* block_scores, int32_t* cu_blocks, void* ws, size_t ws_bytes) {
+    g_launches = 0;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    up_status st = up_config_validate(c);
+    if (st != UP_OK) return st;
+    if ((st = check_batch(b)) != UP_OK) return st;
+    if ((st = check_heads(h)) != UP_OK) return st;
+    if (q == nullptr || k == nullptr || block_scores == nullptr || cu_blocks == nullptr)
+        return UP_ERR_INVALID_ARGUMENT;
+    const Layout L = layout_for(b, h, c);
+    if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
+    PeerReduceParams pr;
+    if ((st = peer_params(rank, tp, peer_buffers, capacity, block_scores, at<uint32_t>(ws, L.err), &pr)) != UP_OK)
+        return st;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15) == 0;
+    if (aligned && tc_eligible(h, c, 0))
+        return score_tc_path(stream, b, h, c, q, k, 1, nullptr, 0, block_scores, cu_blocks, L, ws, &pr);
+    // off the tensor-core envelope: SIMT scoring, then the stand-alone peer all-reduce over
+    // the capacity-sized vector (the same count on every rank)
+    if ((st = up_score_blocks(stream_, b, h, c, q, k, block_scores, cu_blocks, nullptr, ws, ws_bytes)) != UP_OK)
+        return st;
+    const int n = g_launches;
+    const int64_t count = up_max_blocks(b, c);
+    if (count > capacity) return UP_ERR_UNSUPPORTED;
+    st = up_peer_allreduce_scores(stream_, block_scores, count, rank, tp, peer_buffers, capacity, block_scores,
+                                  at<uint32_t>(ws, L.err), 256);
+    g_launches += n;
+    return st;
 }
 
 up_status up_device_status(void* stream, void* ws) {

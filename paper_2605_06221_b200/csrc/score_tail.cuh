@@ -2,6 +2,8 @@
 // the fused cooperative path of score_tcw.cu: per-pair row weights from the per-item
 // softmax statistics, then the per-block combine over heads (and TP shards).
 #pragma once
+#include <cstdint>
+#include <type_traits>
 
 #include "score_common.cuh"
 
@@ -110,11 +112,20 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
 // tp_sim.cpp:12-27): each shard's partial b_g^t is formed on its own (written to
 // shard_scores[t] when non-null) and block_scores[g] = ((0 + b^0) + b^1) + ... in fp32,
 // ascending shard order (allreduce_scores, tp_sim.cpp:43-47).
-// Global warps gw0, gw0 + gwstep, ... each take one block.
-__device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, int64_t gw0, int64_t gwstep) {
+// Global warps gw0, gw0 + gwstep, ... each take one block below min(limit, #blocks); the
+// block's score goes to out(gb, value) (lane 0) -- by default block_scores[gb].
+struct StoreBlockScore {
+    float* block_scores;
+    __device__ __forceinline__ void operator()(int gb, float v) const { block_scores[gb] = v; }
+};
+
+template <class Out = StoreBlockScore>
+__device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, int64_t gw0, int64_t gwstep,
+                                                  int64_t limit = INT64_MAX, Out out = Out{nullptr}) {
+    if constexpr (std::is_same_v<Out, StoreBlockScore>) out.block_scores = p.block_scores;
     const int lane = threadIdx.x & 31;
     const int R = p.num_requests;
-    const int total = p.cu_blocks[R];
+    const int total = p.cu_blocks[R] < limit ? p.cu_blocks[R] : static_cast<int>(limit);
     const int nhg = p.num_heads / p.hpc;
     const int T = p.num_shards;
     const int hps = p.num_heads / T;  // heads per shard (a multiple of hpc)
@@ -124,7 +135,7 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
         const int units_r = p.cu_units[r + 1] - p.cu_units[r];
         if (units_r == 0) {  // pass-through segment
             if (lane == 0) {
-                p.block_scores[gb] = 0.f;
+                out(gb, 0.f);
                 if (p.shard_scores != nullptr)
                     for (int t = 0; t < T; ++t) p.shard_scores[static_cast<int64_t>(t) * p.shard_stride + gb] = 0.f;
             }
@@ -174,7 +185,7 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
             if (p.shard_scores != nullptr && lane < T) p.shard_scores[static_cast<int64_t>(lane) * p.shard_stride + gb] = bt;
             float red = 0.f;
             for (int t = 0; t < T; ++t) red += __shfl_sync(0xffffffffu, bt, t);  // ascending shard order
-            if (lane == 0) p.block_scores[gb] = red;
+            if (lane == 0) out(gb, red);
             continue;
         }
         float red = 0.f;
@@ -220,7 +231,7 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
             if (p.shard_scores != nullptr && lane == 0) p.shard_scores[static_cast<int64_t>(t) * p.shard_stride + gb] = bt;
             red = T == 1 ? bt : red + bt;
         }
-        if (lane == 0) p.block_scores[gb] = red;
+        if (lane == 0) out(gb, red);
     }
 }
 

@@ -30,6 +30,7 @@
 //    L = Σ_items l 2^(m - M);
 //  * block_combine_kernel (score_tail.cuh) -- b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][j].
 #include "score_tail.cuh"
+#include "peer.cuh"
 
 namespace up {
 
@@ -410,6 +411,37 @@ block_combine_kernel(const BlockCombineParams p) {
     block_combine_run(p, static_cast<int64_t>(blockIdx.x) * nw + (threadIdx.x >> 5), static_cast<int64_t>(gridDim.x) * nw);
 }
 
+// Fused combine + TP all-reduce over peer memory (Eq. 15): CTA c forms
+// the scores of a contiguous chunk of blocks from this rank's heads and stores them straight
+// into row `rank` of every peer's exchange buffer (no local partial vector), then runs the
+// rendezvous of peer.cuh and writes the ascending-rank fp32 sum (allreduce_scores,
+// tp_sim.cpp:43-47) to block_scores.  Fixed grid peer_grid() on every rank.
+struct StorePeers {
+    const PeerReduceParams* pr;
+    __device__ __forceinline__ void operator()(int gb, float v) const {
+        for (int t = 0; t < pr->tp; ++t) pr->peer_slots[t][static_cast<int64_t>(pr->rank) * pr->capacity + gb] = v;
+    }
+};
+
+__global__ void __launch_bounds__(256)
+block_combine_peer_kernel(const __grid_constant__ BlockCombineParams p, const __grid_constant__ PeerReduceParams pr) {
+    pdl_wait();
+    __shared__ uint32_t s_epoch;
+    if (threadIdx.x == 0) s_epoch = peer_epoch(pr);
+    int64_t total = p.cu_blocks[p.num_requests];
+    if (total > pr.capacity) {  // more blocks than the exchange buffers hold
+        if (threadIdx.x == 0) raise_error(pr.err, kErrTooManyBlocks);
+        total = pr.capacity;
+    }
+    const int64_t chunk = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = min(static_cast<int64_t>(blockIdx.x) * chunk, total), c1 = min(c0 + chunk, total);
+    block_combine_run(p, c0 + (threadIdx.x >> 5), blockDim.x >> 5, c1, StorePeers{&pr});
+    peer_publish_and_wait(pr, blockIdx.x, s_epoch);
+    peer_sum_chunk(pr, c0, c1);
+    pdl_trigger();
+    peer_epoch_advance(pr);
+}
+
 // SIMT-path plan: validates cu_seqlens and writes cu_blocks (one warp).
 __global__ void blocks_plan_kernel(const int32_t* __restrict__ cu, int R, int64_t max_tokens, int G,
                                    int32_t* __restrict__ cu_blocks, uint32_t* __restrict__ err) {
@@ -475,6 +507,11 @@ cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int
 
 cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream) {
     return launch_k(kPdlScore, block_combine_kernel, grid, 256, 0, stream, p);
+}
+
+cudaError_t launch_block_combine_peer(const BlockCombineParams& p, const PeerReduceParams& pr, int grid,
+                                      cudaStream_t stream) {
+    return launch_k(kPdlScore, block_combine_peer_kernel, grid, 256, 0, stream, p, pr);
 }
 
 }  // namespace up

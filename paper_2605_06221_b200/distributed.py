@@ -118,6 +118,38 @@ class PeerScoreReducer:
             self.err.numel() * 4), "peer_allreduce_scores")
         return out
 
+    def score_blocks(self, q: torch.Tensor, k: torch.Tensor, cu_seqlens, config, heads, max_tokens=None,
+                     workspace=None, out=None):
+        """This rank's head slice scored and all-reduced across the group in the scorer's own
+        launches (up_score_blocks_peer): the combine kernel stores each block's partial into
+        the peers and writes the ascending-rank sum.  Returns api.BlockScores with the
+        REDUCED block scores (identical on every rank)."""
+        from . import api
+        dev = q.device
+        cu = api._as_i32_cuda(cu_seqlens, dev)
+        R = cu.numel() - 1
+        T = int(max_tokens if max_tokens is not None else q.shape[0])
+        qv, qs, D = api._heads_view(q, heads.num_q_heads)
+        kv, ks, _ = api._heads_view(k, heads.num_kv_heads)
+        if D != heads.head_dim:
+            raise ContractViolation("score_blocks: head dim mismatch")
+        b = api._batch(cu, T, None)
+        hc = heads.c(qs, ks)
+        cfg = config.c()
+        ws = workspace or api._ws(dev)
+        buf = ws.get(b, hc, cfg)
+        nbmax = int(self.lib.up_max_blocks(ctypes.byref(b), ctypes.byref(cfg)))
+        if nbmax > self.capacity:
+            raise ContractViolation(f"score_blocks: {nbmax} blocks exceed the reducer capacity {self.capacity}")
+        if out is None:
+            out = api.BlockScores(torch.empty(nbmax, dtype=torch.float32, device=dev),
+                                  torch.empty(R + 1, dtype=torch.int32, device=dev), None)
+        _check(self.lib.up_score_blocks_peer(
+            _stream_ptr(dev), ctypes.byref(b), ctypes.byref(hc), ctypes.byref(cfg), api._ptr(qv), api._ptr(kv),
+            self.rank, self.tp, self.buffers, self.capacity, api._ptr(out.block_scores), api._ptr(out.cu_blocks),
+            ctypes.c_void_p(buf.data_ptr()), buf.numel()), "score_blocks_peer")
+        return out
+
     def check(self) -> None:
         """Raise if a peer's partial never arrived (sticky device flag)."""
         _check(self.lib.up_device_status(_stream_ptr(self.device), ctypes.c_void_p(self.err.data_ptr())),

@@ -98,3 +98,70 @@ def test_peer_allreduce_bitwise_two_ranks_one_device():
     for p in procs:
         p.join(timeout=30)
     assert results == {0: [], 1: []}, results
+
+
+def _worker_fused(rank, tp, port, q):
+    import torch.distributed as dist
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=tp)
+        import paper_2605_06221_b200 as up
+        from paper_2605_06221_b200.distributed import PeerScoreReducer, head_slice
+        from paper_2605_06221_b200.synthetic import make_batch
+        bad = []
+        for case, (lengths, Hq, Hkv, D) in enumerate([([3000, 1500, 64], 8, 2, 128),     # GQA-4, HPC 4 slices
+                                                      ([5000], 4, 4, 256),             # MHA, D=256
+                                                      ([700, 2100], 8, 1, 64)]):       # kv-head shared by ranks
+            sb = make_batch(lengths, Hq, Hkv, D, 64, regime="planted", seed=7 + case, device="cuda:0")
+            cfg = up.ScoreConfig()
+            nb = sum((n + 63) // 64 for n in lengths)
+            red = PeerScoreReducer(nb + len(lengths) + 1, device="cuda:0")
+            slices = [head_slice(Hq, Hkv, t, tp) for t in range(tp)]
+
+            def layout(t):
+                (qb, qe), (kb, ke) = slices[t]
+                return up.HeadLayout(qe - qb, ke - kb, D, gqa_group=Hq // Hkv, q_head_offset=qb, kv_head_offset=kb)
+
+            (qb, qe), (kb, ke) = slices[rank]
+            ws = up.Workspace("cuda:0")
+            for rep in range(3):  # repeated calls: flags / epochs advance
+                got = red.score_blocks(sb.q[:, qb:qe], sb.k[:, kb:ke], sb.cu_seqlens, cfg, layout(rank),
+                                       workspace=ws)
+                torch.cuda.synchronize()
+                ws.device_status()
+            # the same partials through the plain scorer, summed in ascending rank order
+            parts = []
+            for t in range(tp):
+                (tqb, tqe), (tkb, tke) = slices[t]
+                parts.append(up.score_blocks_varlen(sb.q[:, tqb:tqe], sb.k[:, tkb:tke], sb.cu_seqlens, cfg,
+                                                    layout(t)).block_scores[:nb].cpu().numpy())
+            want = np.zeros(nb, dtype=np.float32)
+            for t in range(tp):
+                want = (want + parts[t]).astype(np.float32)
+            if not np.array_equal(got.block_scores[:nb].cpu().numpy().view(np.uint32), want.view(np.uint32)):
+                bad.append(f"case {case}: fused != ascending sum of the partials")
+            red.close()
+        dist.destroy_process_group()
+        q.put((rank, bad))
+    except Exception:
+        import traceback
+        q.put((rank, [traceback.format_exc().strip().splitlines()[-1]]))
+
+
+@pytest.mark.timeout(300)
+def test_fused_score_and_peer_allreduce_two_ranks_one_device():
+    """up_score_blocks_peer: each rank's head slice scored, the combine kernel storing its
+    partials straight into the peers, bitwise the ascending-rank sum of the per-rank
+    partials of the plain scorer."""
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_fused, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=280) for _ in procs)
+    for p in procs:
+        p.join(timeout=30)
+    assert results == {0: [], 1: []}, results
