@@ -38,6 +38,13 @@ namespace up {
 #define UP_TCW_STAGE_KEYS_D128 128
 #endif
 
+// HPC = 4 fast path: the next 32-column TMEM load is in flight while a group is summed
+// (tools/ldpipe_sweep.sh: LLaMA 4x32K scorer 159.9 -> 158.5 us; D = 256 unchanged, so the
+// two-group HPC = 2 path keeps the plain sequence).
+#ifndef UP_TCW_LD_PIPE
+#define UP_TCW_LD_PIPE 1
+#endif
+
 template <int D, int HPC>
 struct TcwCfg {
     // TS: with two q-heads per CTA, Q lives in TMEM (tcgen05.mma A operand from tensor
@@ -349,20 +356,37 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 float gs0 = 0.f, gs1 = 0.f, gs2 = 0.f, gs3 = 0.f;
                 bool redo = !fast && cbase < N && UP_TCW_DIAG != 1;
                 if (fast) {
-                    uint32_t v[32];
-                    tmem_ld32(taddr, v);
-                    tmem_ld_wait();
-                    gs0 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
-                    tmem_ld32(taddr + 32, v);
-                    tmem_ld_wait();
-                    gs1 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
-                    if (C::NG == 4) {
-                        tmem_ld32(taddr + 64, v);
+                    if constexpr (UP_TCW_LD_PIPE && C::NG == 4) {
+                        // the next group's TMEM load is in flight while this group is summed
+                        uint32_t va[32], vb[32];
+                        tmem_ld32(taddr, va);
                         tmem_ld_wait();
-                        gs2 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
-                        tmem_ld32(taddr + 96, v);
+                        tmem_ld32(taddr + 32, vb);
+                        gs0 = group_sum_pk<C::NP>(va, pk(sc, sc), pk(-m, -m));
                         tmem_ld_wait();
-                        gs3 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
+                        tmem_ld32(taddr + 64, va);
+                        gs1 = group_sum_pk<C::NP>(vb, pk(sc, sc), pk(-m, -m));
+                        tmem_ld_wait();
+                        tmem_ld32(taddr + 96, vb);
+                        gs2 = group_sum_pk<C::NP>(va, pk(sc, sc), pk(-m, -m));
+                        tmem_ld_wait();
+                        gs3 = group_sum_pk<C::NP>(vb, pk(sc, sc), pk(-m, -m));
+                    } else {
+                        uint32_t v[32];
+                        tmem_ld32(taddr, v);
+                        tmem_ld_wait();
+                        gs0 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
+                        tmem_ld32(taddr + 32, v);
+                        tmem_ld_wait();
+                        gs1 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
+                        if (C::NG == 4) {
+                            tmem_ld32(taddr + 64, v);
+                            tmem_ld_wait();
+                            gs2 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
+                            tmem_ld32(taddr + 96, v);
+                            tmem_ld_wait();
+                            gs3 = group_sum_pk<C::NP>(v, pk(sc, sc), pk(-m, -m));
+                        }
                     }
                     redo = !((gs0 + gs1) + (gs2 + gs3) <= 0x1p40f);
                 }
