@@ -138,3 +138,14 @@ def test_mixed_stream_64_requests(up, port):
                     regime="planted", seed=14)
     _check_layer(up, port, sb, shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"], lengths, CFG,
                  exact_requests=(0, 31))
+
+
+def test_one_million_token_request_tp_rank(up, port):
+    """Maximum request size: a 2^20-token (1M context) request at one Qwen3-Next TP=8 rank's
+    head slice (2 q-heads, 1 kv-head, D = 256) -- 16384 blocks, the most the on-chip select
+    sort holds -- through score (fp64 restatement), select (bit-exact), compaction and the
+    reconstitution round trip."""
+    lengths = [1 << 20]
+    sb = make_batch(lengths, 2, 1, 256, 512, regime="planted", seed=15)
+    rho = _check_layer(up, port, sb, 2, 1, 256, lengths, CFG)
+    assert 0.05 < rho < 0.8

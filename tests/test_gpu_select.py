@@ -188,3 +188,31 @@ def test_request_beyond_2048_blocks_uses_bitonic_kernel(up, port):
         assert np.array_equal(keep[off:off + n], want.keep_mask)
         assert int(kst[r]) == want.cutoff_rank
         off += n
+
+
+def test_maximum_request_size(up, port):
+    """The largest request the on-chip sort holds: 2^20 tokens = 16384 blocks of 64 (a 1M
+    context), bit-exact with the reference; one block more raises the sticky
+    UnsupportedError (and keeps the request whole rather than dropping anything)."""
+    rng = np.random.default_rng(5)
+    G = 64
+    cfg = dict(query_window_n=128, block_size_g=G, sink_count_a=128, top_p=0.99)
+    n = 1 << 20
+    nb = n // G
+    scores = (rng.random(nb) ** 8).astype(np.float32)
+    cu = torch.tensor([0, n], dtype=torch.int32, device="cuda")
+    cub = torch.tensor([0, nb], dtype=torch.int32, device="cuda")
+    sel = up.select_varlen(torch.from_numpy(scores).cuda(), cub, cu, up.ScoreConfig(**cfg), check=True)
+    want = port.top_p_select(scores, n, **cfg)
+    assert np.array_equal(sel.keep.cpu().numpy(), want.keep_mask)
+    assert int(sel.cutoff_rank[0]) == want.cutoff_rank
+
+    n2 = n + 1
+    scores2 = np.concatenate([scores, scores[:1]])
+    cu2 = torch.tensor([0, n2], dtype=torch.int32, device="cuda")
+    cub2 = torch.tensor([0, nb + 1], dtype=torch.int32, device="cuda")
+    ws = up.Workspace("cuda")
+    sel2 = up.select_varlen(torch.from_numpy(scores2).cuda(), cub2, cu2, up.ScoreConfig(**cfg), workspace=ws)
+    with pytest.raises(up.UnsupportedError):
+        ws.device_status()
+    assert bool(sel2.keep.bool().all())
