@@ -205,6 +205,29 @@ inline void decode_seqused(cudaStream_t s, int32_t num_layers, int32_t num_reque
           "decode_seqused");
 }
 
+/// TP all-reduce of partial block scores over peer memory (allreduce_scores,
+/// tp_sim.cpp:29-49): peer_buffers[t] = rank t's exchange buffer mapped here (up_ipc_*).
+inline void peer_allreduce_scores(cudaStream_t s, const float* partial, int64_t count, int32_t rank,
+                                  const std::vector<void*>& peer_buffers, int64_t capacity, float* out,
+                                  Workspace& ws) {
+    check(up_peer_allreduce_scores(s, partial, count, rank, static_cast<int32_t>(peer_buffers.size()),
+                                   peer_buffers.data(), capacity, out, ws.data(), ws.bytes()),
+          "peer_allreduce_scores");
+}
+
+/// This TP rank's heads scored with the all-reduce fused into the combine kernel
+/// (sharded_block_scores + allreduce_scores across GPUs, tp_sim.cpp:12-49).
+inline void score_blocks_peer(cudaStream_t s, const VarlenBatch& b, const HeadLayout& h, const ScoreConfig& cfg,
+                              const void* q, const void* k, int32_t rank, const std::vector<void*>& peer_buffers,
+                              int64_t capacity, float* block_scores, int32_t* cu_blocks, Workspace& ws) {
+    const up_batch bc = b.c();
+    const up_heads hc = h.c();
+    const up_score_config cc = cfg.c();
+    check(up_score_blocks_peer(s, &bc, &hc, &cc, q, k, rank, static_cast<int32_t>(peer_buffers.size()),
+                               peer_buffers.data(), capacity, block_scores, cu_blocks, ws.data(), ws.bytes()),
+          "score_blocks_peer");
+}
+
 /// attention_readout (model.cpp:215-263) at a drop layer (propagation.cpp:195-205): every
 /// retained row of `compacted` attends to its segment's retained keys with position in
 /// (pos - window, pos]; out bf16 [max_tokens][out_row_stride].
