@@ -213,7 +213,9 @@ up_status up_decode_seqused(void* stream, int32_t num_layers, int32_t num_reques
  * Hkv_local, D] (both heads->k_row_stride); positions: int64, strictly increasing within
  * each segment; out: bf16 [max_tokens, Hq_local, D] (out_row_stride elements per row).
  * D in {64, 128, 256}.  A row with no visible key raises the sticky UP_ERR_CONTRACT
- * (model.cpp:237; read by up_device_status). */
+ * (model.cpp:237; read by up_device_status).  workspace: >= 256 bytes, zeroed once (the
+ * shared workspace of the other entry points will do); the persistent D <= 128 kernel keeps
+ * its work-item counter in bytes [128, 136) and returns it to 0 on exit. */
 up_status up_attention_varlen(void* stream, const up_batch* batch, const up_heads* heads, const void* q,
                               const void* k, const void* v, const int64_t* positions, int64_t window,
                               void* out, int64_t out_row_stride, void* workspace, size_t workspace_bytes);
