@@ -242,7 +242,8 @@ def _random_case(seed):
     return (Hq, Hkv, D), cfgd, lengths, en, veto_frac
 
 
-@pytest.mark.parametrize("seed", list(range(24)))
+# 24 seeds in the default run; UP_SWEEP_SEEDS=N widens the sweep (profiles/parity_sweep_r01.txt)
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("UP_SWEEP_SEEDS", "24")))))
 def test_drop_layer_random_configs_vs_oracle(up, port, seed):
     """Seeded sweep over the knobs (n, G, A, p), head layouts (every scorer kernel), varlen
     segments incl. single-token and n > N, drop-disabled segments and a no-readmission veto:
