@@ -169,12 +169,38 @@ __device__ void keep_all_request(const SelectParams& p, int r, int N, int nb, in
 // thread over the sorted order; returns k*.  Bit-exact by construction.
 __device__ int exact_crossing(const float* sc, int nb, const uint32_t* skey, const int32_t* sval,
                               double p_d) {
+    // Both loops are serial dependency chains of double adds; the loads and float->double
+    // conversions of 8 terms are issued ahead of the adds, so only the add latency remains.
+    constexpr int U = 8;
     double tot = 0.0;
-    for (int g = 0; g < nb; ++g) tot += sc[g];
+    int g = 0;
+    for (; g + U <= nb; g += U) {
+        double x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = static_cast<double>(sc[g + u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) tot += x[u];
+    }
+    for (; g < nb; ++g) tot += sc[g];
+    // Below lo the reference's test fl(c / tot) >= p is false for certain (c / tot < p by a
+    // relative 1e-12, far above the rounding of either side), so the double division only
+    // runs near the crossing.
+    const double lo = p_d * tot * (1.0 - 1e-12);
     double c = 0.0;
-    for (int q = 0; q < nb; ++q) {
+    int q = 0;
+    for (; q + U <= nb; q += U) {
+        double x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = static_cast<double>(phi_decode_dev(skey[q + u]));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            c += x[u];
+            if (c >= lo && c / tot >= p_d) return q + u + 1;
+        }
+    }
+    for (; q < nb; ++q) {
         c += static_cast<double>(phi_decode_dev(skey[q]));
-        if (c / tot >= p_d) return q + 1;
+        if (c >= lo && c / tot >= p_d) return q + 1;
     }
     (void)sval;
     return nb;
