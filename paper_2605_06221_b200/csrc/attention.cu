@@ -63,6 +63,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return r;
 }
 
+// Rows [r0, rows) of a K/V stage ([nch boxes][rows][128 B], swizzle permutes 16-byte chunks
+// within a row only) -> 0.  Rows past the batch's last row hold whatever the caller's buffer
+// holds there; their keys are masked (P = 0), but 0 * NaN in the PV MMA would still poison
+// O, so the V rows of a tile that runs past the batch are cleared before the MMA reads them.
+__device__ __forceinline__ void zero_stage_rows(uint8_t* stage, int nch, int box_bytes, int r0, int rows, int tid,
+                                                int nthreads) {
+    const int per_box = (rows - r0) * 8;  // 16-byte chunks
+    for (int x = tid; x < nch * per_box; x += nthreads) {
+        const int c = x / per_box, rem = x - c * per_box;
+        reinterpret_cast<uint4*>(stage + c * box_bytes + (r0 + rem / 8) * 128)[rem % 8] = make_uint4(0, 0, 0, 0);
+    }
+}
+
 // first index i in [b, e) with pos[i] > x (upper_bound) / >= x (lower_bound)
 __device__ __forceinline__ int64_t upper_pos(const int64_t* pos, int64_t b, int64_t e, int64_t x) {
     while (b < e) {
@@ -237,6 +250,7 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             if (lo >= hi) raise_error(p.err, kErrNoVisibleKey);
         }
         const float c = p.scale_log2;
+        const int64_t total_rows = p.cu_seqlens[p.num_requests];
         float m_run = -INFINITY, l_run = 0.f;
         for (int j = 0; j < nt; ++j) {
             const int64_t kb = k_begin + static_cast<int64_t>(j) * C::BN;
@@ -344,6 +358,13 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             }
             }
             l_run += lsum;
+            if (kb + C::BN > total_rows) {  // V rows past the batch -> 0 before PV_j reads them
+                const int vs = j % C::VST;
+                mbar_wait(&v_full[vs], (j / C::VST) & 1);
+                zero_stage_rows(sv + vs * C::KV_STAGE, C::NCH, C::KBOX,
+                                static_cast<int>(total_rows - kb > 0 ? total_rows - kb : 0), C::BN, threadIdx.x - 64, 128);
+                fence_proxy_async_smem();
+            }
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -644,6 +665,7 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const uint32_t s_addr = tmem + lane_base + C::S_COL + t * C::BN;
         const uint32_t o_addr = tmem + lane_base + C::O_COL + t * D;
         const float c = p.scale_log2;
+        const int64_t total_rows = p.cu_seqlens[p.num_requests];
         uint32_t js = 0;
         for (int it = 0;; ++it) {
             const PairPlan pl = take_plan(it);
@@ -770,6 +792,14 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                     lsum += lo_f(a2) + hi_f(a2);
                 }
                 l_run += lsum;
+                if (t == 0 && kb + C::BN > total_rows) {  // V rows past the batch -> 0 before PV0 reads them
+                    const uint32_t g = js + j;
+                    mbar_wait(&v_full[g % C::VST], (g / C::VST) & 1);
+                    zero_stage_rows(sv + (g % C::VST) * C::KV_STAGE, C::NCH, C::BOX,
+                                    static_cast<int>(total_rows - kb > 0 ? total_rows - kb : 0), C::BN,
+                                    threadIdx.x - 128, 128);
+                    fence_proxy_async_smem();
+                }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();

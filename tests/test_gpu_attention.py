@@ -127,3 +127,22 @@ def test_attention_cuda_graph_and_launch_count(up):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, eager)
+
+
+@pytest.mark.parametrize("D,Hq,Hkv", [(128, 8, 2), (256, 4, 2)])
+def test_attention_ignores_garbage_past_the_batch(up, D, Hq, Hkv):
+    """Capacity-sized buffers: rows past cu_seqlens[-1] hold NaN (an uninitialised compaction
+    output).  Masked keys must contribute exactly nothing -- no 0 * NaN from the PV MMA."""
+    lengths = [300, 77]
+    q, k, v, pos, cu = _inputs(lengths, Hq, Hkv, D, seed=31)
+    n, cap = sum(lengths), 1000
+    def padded(x):
+        y = torch.full((cap,) + tuple(x.shape[1:]), float("nan"), dtype=x.dtype)
+        y[:n] = x
+        return y.cuda()
+    qp, kp, vp = padded(q), padded(k), padded(v)
+    pp = torch.zeros(cap, dtype=torch.int64)
+    pp[:n] = pos
+    got = up.attention_varlen(qp, kp, vp, cu.cuda(), pp.cuda(), max_tokens=cap, check=True)[:n]
+    assert bool(torch.isfinite(got.float()).all())
+    _close(got, _torch_ref(q.cuda(), k.cuda(), v.cuda(), pos.cuda(), cu, 0))
