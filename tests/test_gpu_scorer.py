@@ -201,3 +201,29 @@ def test_unaligned_q_takes_the_simt_path(up, port):
     res = up.score_blocks_varlen(q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), up.HeadLayout(4, 1, 128), check=True)
     _, want = _oracle_blocks(port, sb, 0, 4, 1, cfg)
     _assert_blocks_close(res.block_scores[:len(want)].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("Hq,Hkv,D,lengths", [
+    (32, 8, 128, [1000, 50]),     # wide scorer, HPC 4; the last segment is shorter than n
+    (16, 2, 256, [700, 90]),      # TS scorer (HPC 2, Q in TMEM)
+    (4, 4, 64, [500, 33]),        # two-warpgroup scorer
+])
+def test_scores_ignore_garbage_past_the_batch(up, Hq, Hkv, D, lengths):
+    """Capacity-sized q/k buffers whose rows past cu_seqlens[-1] hold NaN: the query-window
+    tile of a short last segment and its ragged last key tile read those rows, yet the block
+    scores equal the clean-buffer scores bit for bit."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    sb = make_batch(lengths, Hq, Hkv, D, 32, regime="planted", seed=9)
+    n, cap = sum(lengths), sum(lengths) + 300
+    cfg = up.ScoreConfig()
+    heads = up.HeadLayout(Hq, Hkv, D)
+    clean = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, cfg, heads, check=True)
+    qp = torch.full((cap, Hq, D), float("nan"), dtype=torch.bfloat16, device="cuda")
+    kp = torch.full((cap, Hkv, D), float("nan"), dtype=torch.bfloat16, device="cuda")
+    qp[:n] = sb.q
+    kp[:n] = sb.k
+    dirty = up.score_blocks_varlen(qp, kp, sb.cu_seqlens, cfg, heads, max_tokens=cap, check=True)
+    nb = int(clean.cu_blocks[-1])
+    a, b = clean.block_scores[:nb], dirty.block_scores[:nb]
+    assert bool(torch.isfinite(b).all())
+    assert torch.equal(a, b)
