@@ -26,21 +26,21 @@ namespace up {
 
 template <int D>
 struct AttnCfg {
-    // D=256: 64-key tiles so that Q (64 KB) + 3 K + 2 V stages fit in 227 KB of smem and
-    // S0, S1, O, P0, P1 fit in the 512 TMEM columns (64 + 64 + 256 + 32 + 32).
+    // D=256: 64-key tiles; Q resident in TMEM (the S MMA reads A from tensor memory, so it
+    // streams only K from smem: with A in smem an M=128, N=64 MMA needs 6 KB per 32 cycles,
+    // above the 128 B/clk smem port); P_j is written over the columns of S_j.  TMEM:
+    // S0 [0,64), S1 [64,128), O [128,384), Q [384,512).  The freed smem holds 4 K + 3 V stages.
     static constexpr int BM = 128, BN = D > 128 ? 64 : 128;
     static constexpr int NCH = D / 64;                    // 64-element (128-byte) column boxes
-    static constexpr int QBOX = BM * 128;                 // one box of the Q tile: 16 KB
     static constexpr int KBOX = BN * 128;                 // one box of a K/V tile
-    static constexpr int Q_BYTES = NCH * QBOX;
     static constexpr int KV_STAGE = NCH * KBOX;
-    static constexpr int KST = 3, VST = 2;
+    static constexpr int KST = 4, VST = 3;
     static constexpr int NBAR = 1 + 2 * KST + 2 * VST + 2 + 2 + 2;
     static constexpr int THREADS = 192;
-    static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, P_COL = 2 * BN + D;
-    static_assert(P_COL + BN <= 512, "TMEM columns");
-    static constexpr int smem() { return 1024 + Q_BYTES + (KST + VST) * KV_STAGE + NBAR * 8 + 64; }
-    static_assert(smem() <= 232448, "shared memory");
+    static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, Q_COL = 2 * BN + D;
+    static_assert(Q_COL + D / 2 <= 512, "TMEM columns");
+    static constexpr int smem() { return 1024 + (KST + VST) * KV_STAGE + NBAR * 8 + 64; }
+    static_assert(smem() <= 232448 - 1024, "shared memory");
 };
 
 // Of every 16 element pairs of a full tile, this many take exp2 on the FMA pipe
@@ -100,11 +100,10 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    uint8_t* sq = smem;
-    uint8_t* sk = sq + C::Q_BYTES;
+    uint8_t* sk = smem;
     uint8_t* sv = sk + C::KST * C::KV_STAGE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sv + C::VST * C::KV_STAGE);
-    uint64_t* q_full = bars;
+    uint64_t* q_full = bars;  // the four softmax warps have stored their Q rows in TMEM
     uint64_t* k_full = bars + 1;
     uint64_t* k_empty = k_full + C::KST;
     uint64_t* v_full = k_empty + C::KST;
@@ -150,7 +149,7 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         plan[2] = se;
         plan[3] = kb;
         plan[4] = ke;
-        mbar_init(q_full, 1);
+        mbar_init(q_full, 4);
         for (int s = 0; s < C::KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
         for (int s = 0; s < C::VST; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
         for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&p_full[s], 4); mbar_init(&pv_done[s], 1); }
@@ -175,9 +174,6 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             prefetch_tensormap(&qmap);
             prefetch_tensormap(&kmap);
             prefetch_tensormap(&vmap);
-            mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-            for (int c = 0; c < C::NCH; ++c)
-                tma_load_2d(sq + c * C::QBOX, &qmap, q_full, h * D + c * 64, static_cast<int32_t>(q0));
             for (int j = 0; j < nt; ++j) {
                 const int32_t row = static_cast<int32_t>(k_begin + static_cast<int64_t>(j) * C::BN);
                 const int ks = j % C::KST;
@@ -196,7 +192,6 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         if (lane == 0) {
             constexpr uint32_t kIdescS = idesc_bf16_f32(128, C::BN);
             constexpr uint32_t kIdescO = idesc_bf16_f32(128, D) | (1u << 16);  // B (V) MN-major
-            const uint64_t a_base = smem_desc_sw128(smem_u32(sq));
             const uint64_t k_base = smem_desc_sw128(smem_u32(sk));
             const uint64_t v_base = smem_desc_sw128_mn(smem_u32(sv), C::KBOX, 1024);
             mbar_wait(q_full, 0);
@@ -207,9 +202,9 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 tc_fence_after();
                 const uint32_t d_tmem = tmem + C::S_COL + (j & 1) * C::BN;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
+                for (int kk = 0; kk < D / 16; ++kk) {  // A = Q columns [kk*8, kk*8+8) in TMEM
                     const uint32_t koff = (kk & 3) * 32;
-                    mma_bf16_ss(d_tmem, a_base + (((kk >> 2) * C::QBOX + koff) >> 4),
+                    mma_bf16_ts(d_tmem, tmem + C::Q_COL + kk * 8,
                                 k_base + ((ks * C::KV_STAGE + (kk >> 2) * C::KBOX + koff) >> 4), kIdescS,
                                 kk > 0 ? 1u : 0u);
                 }
@@ -223,7 +218,7 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 const int vs = j % C::VST;
                 mbar_wait(&v_full[vs], (j / C::VST) & 1);
                 tc_fence_after();
-                const uint32_t a_tmem = tmem + C::P_COL + (j & 1) * (C::BN / 2);
+                const uint32_t a_tmem = tmem + C::S_COL + (j & 1) * C::BN;  // P_j over S_j
 #pragma unroll
                 for (int kk = 0; kk < C::BN / 16; ++kk)  // 16 keys = two 8-row swizzle atoms
                     mma_bf16_ts(tmem + C::O_COL, a_tmem + kk * 8,
@@ -248,6 +243,25 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             hi = p.window > 0 ? upper_pos(p.positions, seg_begin, seg_end, qp) : qi + 1;
             lo = p.window > 0 ? lower_pos(p.positions, seg_begin, seg_end, qp - p.window + 1) : seg_begin;
             if (lo >= hi) raise_error(p.err, kErrNoVisibleKey);
+        }
+        {
+            // this row of Q into TMEM (column c = bf16 elements 2c, 2c+1; zero past the segment)
+            const __nv_bfloat16* qsrc = p.q + qi * p.q_row_stride + static_cast<int64_t>(h) * D;
+#pragma unroll
+            for (int c0 = 0; c0 < D / 2; c0 += 32) {
+                uint32_t v[32];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                    if (valid) w = __ldg(reinterpret_cast<const uint4*>(qsrc + c0 * 2) + x);
+                    v[4 * x + 0] = w.x; v[4 * x + 1] = w.y; v[4 * x + 2] = w.z; v[4 * x + 3] = w.w;
+                }
+                tmem_st32(tmem + lane_base + C::Q_COL + c0, v);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(q_full);
         }
         const float c = p.scale_log2;
         const int64_t total_rows = p.cu_seqlens[p.num_requests];
@@ -304,14 +318,11 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                     tmem_st32(tmem + lane_base + C::O_COL + q * 32, o);
                 }
             }
-            // P_j goes to P[j&1], last read by PV_{j-2}
-            if (j >= 2) {
-                mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
-                tc_fence_after();
-            }
+            // P_j goes over S_j (all of S_j is in registers); S_j was issued after PV_{j-2},
+            // so the MMA pipe already consumed P_{j-2} from these columns
             const float mref = m_run == -INFINITY ? 0.f : m_run;
             float lsum = 0.f;
-            const uint32_t p_addr = tmem + lane_base + C::P_COL + (j & 1) * (C::BN / 2);
+            const uint32_t p_addr = s_addr;
             if (full) {
                 // packed FFMA2 arguments; of every 16 pairs kAttnPolyPairs take 2^x on the FMA
                 // pipe (exp2_poly2) instead of MUFU.EX2, which alone would need as many cycles

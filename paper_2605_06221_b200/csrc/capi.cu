@@ -724,6 +724,8 @@ up_status up_attention_varlen(void* stream, const up_batch* b, const up_heads* h
     p.cu_seqlens = b->cu_seqlens;
     p.positions = positions;
     p.out = static_cast<__nv_bfloat16*>(out);
+    p.q = static_cast<const __nv_bfloat16*>(q);
+    p.q_row_stride = h->q_row_stride;
     p.err = static_cast<uint32_t*>(ws);
     p.max_tokens = b->max_tokens;
     p.out_row_stride = out_row_stride;

@@ -168,6 +168,8 @@ struct AttnParams {
     const int32_t* cu_seqlens;   // [R+1] segments of the (compacted) batch
     const int64_t* positions;    // [rows] logical positions, strictly increasing per segment
     __nv_bfloat16* out;          // [rows][out_row_stride], head h at column h*D
+    const __nv_bfloat16* q;      // [rows][q_row_stride] (D = 256: rows copied into TMEM)
+    int64_t q_row_stride;
     uint32_t* err;
     int64_t max_tokens;
     int64_t out_row_stride;
