@@ -393,7 +393,7 @@ class LayerRunner:
     def compact(self, sb, cu):
         L = self.layer
         self.up.compact_varlen(L.sel.keep, cu, self.planes(sb), max_tokens=self.T, workspace=L.ws,
-                               result=L.out)
+                               result=L.out, after_select=True)
         return self.up.lib.up_last_launch_count()
 
     def __call__(self, sb, cu):

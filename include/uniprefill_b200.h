@@ -165,6 +165,15 @@ up_status up_compact(void* stream, const up_batch* batch, const uint8_t* keep,
                      int32_t* retained_index, int32_t* num_tokens_out, void* workspace,
                      size_t workspace_bytes);
 
+/* up_compact for a keep mask that up_select just wrote on this workspace (same batch,
+ * drop_enabled and stream, keep unmodified since): up_select's expansion already counted
+ * the retained rows per tile, so the count pass is skipped (one launch fewer; what
+ * up_drop_layer does). */
+up_status up_compact_selected(void* stream, const up_batch* batch, const uint8_t* keep,
+                              const up_plane* planes, int32_t num_planes, int32_t* cu_seqlens_out,
+                              int32_t* retained_index, int32_t* num_tokens_out, void* workspace,
+                              size_t workspace_bytes);
+
 /* Row scatter, the inverse of up_compact's gather: for o < *num_rows (device int32; or
  * max_rows when num_rows is NULL) and index[o] >= 0, row o of every plane's src is copied
  * to row index[o] of its dst.  Passing up_compact's retained_index and num_tokens_out

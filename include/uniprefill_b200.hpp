@@ -177,6 +177,17 @@ inline void compact(cudaStream_t s, const VarlenBatch& b, const uint8_t* keep, c
           "compact");
 }
 
+/// compact() right after top_p_select() on the same workspace and keep mask: the
+/// selection already counted the retained rows per tile (up_compact_selected).
+inline void compact_selected(cudaStream_t s, const VarlenBatch& b, const uint8_t* keep,
+                             const std::vector<up_plane>& planes, int32_t* cu_seqlens_out, int32_t* retained_index,
+                             int32_t* num_tokens_out, Workspace& ws) {
+    const up_batch bc = b.c();
+    check(up_compact_selected(s, &bc, keep, planes.data(), static_cast<int32_t>(planes.size()), cu_seqlens_out,
+                              retained_index, num_tokens_out, ws.data(), ws.bytes()),
+          "compact_selected");
+}
+
 /// Reconstitution step (propagation.cpp:79-100): rows 0..*num_rows of every plane's src
 /// go back to rows index[o] of its dst (up_compact's retained_index unwinds a drop).
 inline void scatter_rows(cudaStream_t s, const int32_t* index, const int32_t* num_rows, int64_t max_rows,

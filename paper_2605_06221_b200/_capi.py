@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libuniprefill_b200.so")
 EXPORTED = (
     "up_abi_version", "up_status_string", "up_config_validate", "up_max_blocks",
     "up_workspace_bytes", "up_score_blocks", "up_score_blocks_tp", "up_reduce_block_scores", "up_select",
-    "up_compact", "up_scatter_rows", "up_slot_mapping", "up_decode_seqused", "up_drop_layer", "up_attention_varlen", "up_peer_buffer_bytes", "up_peer_buffer_alloc",
+    "up_compact", "up_compact_selected", "up_scatter_rows", "up_slot_mapping", "up_decode_seqused", "up_drop_layer", "up_attention_varlen", "up_peer_buffer_bytes", "up_peer_buffer_alloc",
     "up_peer_buffer_free", "up_ipc_get_handle", "up_ipc_open_handle", "up_ipc_close_handle",
     "up_peer_allreduce_scores", "up_score_blocks_peer", "up_device_status", "up_scorer_kind", "up_last_launch_count",
 )
@@ -74,6 +74,7 @@ def _load():
         "up_select": ([vp, P(BatchC), P(ScoreConfigC), vp, vp, vp, vp, P(SelectionOutC), vp, sz],
                       ctypes.c_int),
         "up_compact": ([vp, P(BatchC), vp, P(PlaneC), i32, vp, vp, vp, vp, sz], ctypes.c_int),
+        "up_compact_selected": ([vp, P(BatchC), vp, P(PlaneC), i32, vp, vp, vp, vp, sz], ctypes.c_int),
         "up_scatter_rows": ([vp, vp, vp, i64, P(PlaneC), i32], ctypes.c_int),
         "up_slot_mapping": ([vp, vp, i32, vp, i64, vp, vp, i32, i32, i32, vp, i64, vp, sz], ctypes.c_int),
         "up_decode_seqused": ([vp, i32, i32, vp, i32, P(i32), P(vp), vp, vp], ctypes.c_int),

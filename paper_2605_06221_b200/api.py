@@ -324,9 +324,11 @@ class Compacted:
 def compact_varlen(keep: torch.Tensor, cu_seqlens, planes: Sequence[torch.Tensor], drop_enabled=None,
                    max_tokens: Optional[int] = None, outs: Optional[Sequence[torch.Tensor]] = None,
                    workspace: Optional[Workspace] = None, result: Optional[Compacted] = None,
-                   check: bool = False) -> Compacted:
+                   check: bool = False, after_select: bool = False) -> Compacted:
     """Segmented prefix sum + gather of retained rows (up_compact).  planes: [T, ...] tensors on
-    the device, or in pinned host memory (read in place: only retained rows cross PCIe)."""
+    the device, or in pinned host memory (read in place: only retained rows cross PCIe).
+    after_select: `keep` is select_varlen's output on the same workspace, unmodified since
+    (up_compact_selected: the selection already counted the rows per tile)."""
     dev = keep.device
     cu = _as_i32_cuda(cu_seqlens, dev)
     R = cu.numel() - 1
@@ -334,7 +336,12 @@ def compact_varlen(keep: torch.Tensor, cu_seqlens, planes: Sequence[torch.Tensor
     en = None if drop_enabled is None else drop_enabled.to(device=dev, dtype=torch.uint8).contiguous()
     b = _batch(cu, T, en)
     ws = workspace or _ws(dev)
-    buf = ws.get(b, None, ScoreConfig(1, 1, 0, 1.0).c())
+    before = ws.buf
+    # block size only sizes the block-decision region, which compaction does not use: a
+    # huge G keeps this layout inside the selection's (same offsets, no regrowth)
+    buf = ws.get(b, None, ScoreConfig(1, 1 << 20, 0, 1.0).c())
+    if buf is not before:
+        after_select = False  # a fresh workspace holds no tile counts from a selection
     if result is None:
         if outs is None:
             outs = [torch.empty_like(p) for p in planes]
@@ -352,9 +359,9 @@ def compact_varlen(keep: torch.Tensor, cu_seqlens, planes: Sequence[torch.Tensor
                                     "destinations on the device")
         rb = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
         arr[i] = PlaneC(src.data_ptr(), dst.data_ptr(), rb, 0, 0)
-    st = lib.up_compact(_stream_ptr(dev), ctypes.byref(b), _ptr(keep), arr, len(planes),
-                        _ptr(result.cu_seqlens), _ptr(result.retained_index), _ptr(result.num_out),
-                        ctypes.c_void_p(buf.data_ptr()), buf.numel())
+    fn = lib.up_compact_selected if after_select else lib.up_compact
+    st = fn(_stream_ptr(dev), ctypes.byref(b), _ptr(keep), arr, len(planes), _ptr(result.cu_seqlens),
+            _ptr(result.retained_index), _ptr(result.num_out), ctypes.c_void_p(buf.data_ptr()), buf.numel())
     _check(st, "compact")
     if check:
         ws.device_status()
@@ -412,7 +419,7 @@ def slot_mapping(cu_seqlens: torch.Tensor, positions: torch.Tensor, block_tables
         out = torch.empty(L, rows, dtype=torch.int64, device=dev)
     ws = workspace or _ws(dev)
     b = _batch(cu, max(rows, 1), None)
-    buf = ws.get(b, None, ScoreConfig(1, 1, 0, 1.0).c())
+    buf = ws.get(b, None, ScoreConfig(1, 1 << 20, 0, 1.0).c())  # only the error word is used
     _check(lib.up_slot_mapping(_stream_ptr(dev), _ptr(cu), R, _ptr(num_rows), rows,
                                _ptr(positions.contiguous()), _ptr(block_tables.contiguous()), L, max_pages,
                                int(block_size), _ptr(out), out.stride(0), ctypes.c_void_p(buf.data_ptr()),
@@ -549,7 +556,7 @@ class DropLayer:
                       drop_enabled, max_tokens=self.max_tokens, workspace=self.ws, out=self.sel)
         n += lib.up_last_launch_count()
         compact_varlen(self.sel.keep, cu_seqlens, planes, drop_enabled, max_tokens=self.max_tokens,
-                       workspace=self.ws, result=self.out)
+                       workspace=self.ws, result=self.out, after_select=True)
         n += lib.up_last_launch_count()
         self.last_launches = n
         return self.out

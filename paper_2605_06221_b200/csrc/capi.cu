@@ -43,7 +43,7 @@ cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_reque
                           cudaStream_t stream);
 cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t count, float* out,
                                  int num_sms, cudaStream_t stream);
-cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream, bool counts_ready);
 cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_slot_mapping(const SlotMapParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_decode_seqused(const SequsedParams& p, cudaStream_t stream);
@@ -544,6 +544,7 @@ up_status up_select(void* stream, const up_batch* b, const up_score_config* c,
     p.top_p = c->top_p;
     p.dbg = select_debug_buffer();
     p.blk_keep = at<uint8_t>(ws, L.blk_keep);
+    p.tile_counts = at<int32_t>(ws, L.tile_counts);
     p.max_tokens = b->max_tokens;
     const int64_t per_req = (b->max_tokens + c->block_size_g - 1) / c->block_size_g;
     const cudaError_t e = launch_select(p, b->num_requests, static_cast<int>(per_req < kMaxSortBlocks ? per_req : kMaxSortBlocks),
@@ -552,16 +553,18 @@ up_status up_select(void* stream, const up_batch* b, const up_score_config* c,
     return cuda_status(e);
 }
 
-up_status up_compact(void* stream, const up_batch* b, const uint8_t* keep, const up_plane* planes,
-                     int32_t num_planes, int32_t* cu_out, int32_t* retained_index,
-                     int32_t* num_out, void* ws, size_t ws_bytes) {
+static up_status compact_impl(void* stream, const up_batch* b, const uint8_t* keep, const up_plane* planes,
+                              int32_t num_planes, int32_t* cu_out, int32_t* retained_index, int32_t* num_out,
+                              void* ws, size_t ws_bytes, bool counts_ready) {
     g_launches = 0;
     up_status st = check_batch(b);
     if (st != UP_OK) return st;
     if (keep == nullptr || cu_out == nullptr) return UP_ERR_INVALID_ARGUMENT;
     if (num_planes < 0 || num_planes > compact_max_planes()) return UP_ERR_UNSUPPORTED;
     if (num_planes > 0 && planes == nullptr) return UP_ERR_INVALID_ARGUMENT;
-    up_score_config dummy{1, 1, 0, 1.0f};
+    // G only sizes the block-decision region, unused here: a huge G keeps this layout a
+    // prefix of up_select's (same tile-count offset, no larger workspace requirement)
+    up_score_config dummy{1, 1 << 20, 0, 1.0f};
     const Layout L = layout_for(b, nullptr, &dummy);
     if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
     CompactParams p{};
@@ -585,9 +588,21 @@ up_status up_compact(void* stream, const up_batch* b, const uint8_t* keep, const
         p.dst_stride[i] = pl.dst_stride_bytes > 0 ? pl.dst_stride_bytes : pl.row_bytes;
         if (p.src_stride[i] < pl.row_bytes || p.dst_stride[i] < pl.row_bytes) return UP_ERR_CONTRACT;
     }
-    const cudaError_t e = launch_compact(p, num_sms(), static_cast<cudaStream_t>(stream));
-    g_launches = num_planes > 0 ? 3 : 2;
+    const cudaError_t e = launch_compact(p, num_sms(), static_cast<cudaStream_t>(stream), counts_ready);
+    g_launches = (num_planes > 0 ? 3 : 2) - (counts_ready ? 1 : 0);
     return cuda_status(e);
+}
+
+up_status up_compact(void* stream, const up_batch* b, const uint8_t* keep, const up_plane* planes,
+                     int32_t num_planes, int32_t* cu_out, int32_t* retained_index,
+                     int32_t* num_out, void* ws, size_t ws_bytes) {
+    return compact_impl(stream, b, keep, planes, num_planes, cu_out, retained_index, num_out, ws, ws_bytes, false);
+}
+
+up_status up_compact_selected(void* stream, const up_batch* b, const uint8_t* keep, const up_plane* planes,
+                              int32_t num_planes, int32_t* cu_out, int32_t* retained_index, int32_t* num_out,
+                              void* ws, size_t ws_bytes) {
+    return compact_impl(stream, b, keep, planes, num_planes, cu_out, retained_index, num_out, ws, ws_bytes, true);
 }
 
 up_status up_scatter_rows(void* stream, const int32_t* index, const int32_t* num_rows, int64_t max_rows,
@@ -629,7 +644,7 @@ up_status up_drop_layer(void* stream, const up_batch* b, const up_heads* h,
     st = up_select(stream, b, c, block_scores, cu_blocks, veto, keep, sel, ws, ws_bytes);
     if (st != UP_OK) return st;
     const int n2 = g_launches;
-    st = up_compact(stream, b, keep, planes, num_planes, cu_out, retained_index, num_out, ws, ws_bytes);
+    st = up_compact_selected(stream, b, keep, planes, num_planes, cu_out, retained_index, num_out, ws, ws_bytes);
     g_launches += n1 + n2;
     return st;
 }

@@ -203,10 +203,15 @@ cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_
     return launch_k(kPdlCompact, scatter_rows_kernel, copy_grid(num_sms, p.max_tokens), kCopyThreads, 0, stream, p);
 }
 
-cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream) {
+// counts_ready: tile_counts already hold the kept rows per kCompactTile tile (written by
+// up_select's expand kernel for this keep mask), so the count pass is skipped.
+cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream, bool counts_ready) {
     const int64_t tiles = (p.max_tokens + kCompactTile - 1) / kCompactTile;
-    cudaError_t e = launch_k(kPdlCompactScan, compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    if (!counts_ready &&
+        (e = launch_k(kPdlCompactScan, compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) !=
+            cudaSuccess)
+        return e;
     if ((e = launch_k(kPdlCompactScan, compact_index_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) != cudaSuccess)
         return e;
     if (p.num_planes > 0) {

@@ -110,6 +110,7 @@ struct SelectParams {
     int32_t sink_count_a;
     float top_p;
     uint8_t* blk_keep;        // workspace [max_blocks]: per-block decisions for the expand kernel
+    int32_t* tile_counts;     // workspace: kept tokens per 1024-token tile (read by up_compact_selected)
     int64_t max_tokens;
     unsigned long long* dbg;  // optional phase clocks of CTA 0 (UP_SELECT_DEBUG), else null
     int32_t nb_lo, nb_hi;     // this launch handles the requests with nb_lo < blocks <= nb_hi

@@ -477,39 +477,58 @@ __global__ void __launch_bounds__(256)
 expand_kernel(const SelectParams p, int R) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
+    __shared__ int red[8];
     const int T = p.cu_seqlens[R];
     const int64_t A = p.sink_count_a;
     const int G = p.block_size_g;
     const bool aligned = (reinterpret_cast<uintptr_t>(p.keep) & 3) == 0;
-    // 4 tokens per thread (one 32-bit store): enough threads to cover the batch in one wave
-    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c * 4 < T;
-         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int i0 = static_cast<int>(c * 4);
-        int r = find_segment(p.cu_seqlens, R, i0);
-        int seg0 = p.cu_seqlens[r], seg1 = p.cu_seqlens[r + 1];
+    // one 1024-token tile per CTA iteration, 4 tokens per thread (one 32-bit store); the
+    // tile's kept count goes to tile_counts (the compaction's count pass, done here)
+    for (int64_t tile = blockIdx.x; tile * 1024 < T; tile += gridDim.x) {
+        const int i0 = static_cast<int>(tile * 1024) + 4 * static_cast<int>(threadIdx.x);
         uint32_t w = 0u;
+        if (i0 < T) {
+            int r = find_segment(p.cu_seqlens, R, i0);
+            int seg0 = p.cu_seqlens[r], seg1 = p.cu_seqlens[r + 1];
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-            const int i = i0 + x;
-            if (i >= T) break;
-            while (i >= seg1) { ++r; seg0 = seg1; seg1 = p.cu_seqlens[r + 1]; }
-            uint32_t k = 1;
-            if (p.drop_enabled == nullptr || p.drop_enabled[r]) {
-                const int li = i - seg0;
-                const int N = seg1 - seg0;
-                const int neff = min(p.query_window_n, N);
-                k = (p.blk_keep[p.cu_blocks[r] + li / G] != 0 || li < A || li >= N - neff) ? 1u : 0u;
-                if (k && p.veto != nullptr && p.veto[i]) k = 0;
+            for (int x = 0; x < 4; ++x) {
+                const int i = i0 + x;
+                if (i >= T) break;
+                while (i >= seg1) { ++r; seg0 = seg1; seg1 = p.cu_seqlens[r + 1]; }
+                uint32_t k = 1;
+                if (p.drop_enabled == nullptr || p.drop_enabled[r]) {
+                    const int li = i - seg0;
+                    const int N = seg1 - seg0;
+                    const int neff = min(p.query_window_n, N);
+                    k = (p.blk_keep[p.cu_blocks[r] + li / G] != 0 || li < A || li >= N - neff) ? 1u : 0u;
+                    if (k && p.veto != nullptr && p.veto[i]) k = 0;
+                }
+                w |= k << (8 * x);
             }
-            w |= k << (8 * x);
+            if (aligned && i0 + 4 <= T) {
+                *reinterpret_cast<uint32_t*>(p.keep + i0) = w;
+            } else {
+                for (int x = 0; x < 4 && i0 + x < T; ++x) p.keep[i0 + x] = static_cast<uint8_t>(w >> (8 * x));
+            }
         }
-        if (aligned && i0 + 4 <= T) {
-            *reinterpret_cast<uint32_t*>(p.keep + i0) = w;
-        } else {
-            for (int x = 0; x < 4 && i0 + x < T; ++x) p.keep[i0 + x] = static_cast<uint8_t>(w >> (8 * x));
+        if (p.tile_counts != nullptr) {
+            int c = __popc(w);  // one bit per kept token (bytes are 0 or 1)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int s = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s += red[q];
+                p.tile_counts[tile] = s;
+            }
+            __syncthreads();
         }
     }
 }
+
+constexpr int kExpandTile = 1024;
 
 size_t select_smem_bytes(int max_blocks_per_request) {
     int P2 = 1;
@@ -542,8 +561,8 @@ cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_reque
         e = launch_k(kPdlSelect, select_kernel, R, kSelThreads, smem, stream, q);
     }
     if (e != cudaSuccess) return e;
-    const int64_t chunks = (p.max_tokens + 3) / 4;
-    int64_t grid = (chunks + 255) / 256;
+    static_assert(kExpandTile == 1024, "expand tiles = compaction scan tiles");
+    int64_t grid = (p.max_tokens + kExpandTile - 1) / kExpandTile;  // one tile per CTA
     if (grid > num_sms * 8) grid = num_sms * 8;
     if (grid < 1) grid = 1;
     return launch_k(kPdlSelect, expand_kernel, static_cast<unsigned>(grid), 256, 0, stream, q, R);

@@ -203,3 +203,32 @@ def test_reconstitute_varlen_unwinds_drops_in_reverse(up, ref):
         if want is None:
             continue
         assert np.array_equal(got[s:e].view(np.uint32), want.view(np.uint32)), f"request {r}"
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_compact_after_select_matches_full_scan(up, seed):
+    """up_compact_selected (the tile counts come from up_select's expansion) equals up_compact
+    on the same keep mask: drop-disabled segments, a veto, lengths across tile boundaries."""
+    rng = np.random.default_rng(seed)
+    lengths = [int(x) for x in rng.choice([1, 63, 1023, 1024, 1025, 3000, 5000], size=5)]
+    T, R = sum(lengths), len(lengths)
+    G = 64
+    nbs = [(n + G - 1) // G for n in lengths]
+    scores = torch.from_numpy((rng.random(sum(nbs)) ** 8).astype(np.float32)).cuda()
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(lengths)]), dtype=torch.int32, device="cuda")
+    cub = torch.tensor(np.concatenate([[0], np.cumsum(nbs)]), dtype=torch.int32, device="cuda")
+    en = torch.from_numpy((rng.random(R) < 0.7).astype(np.uint8)).cuda()
+    veto = torch.from_numpy((rng.random(T) < 0.05).astype(np.uint8)).cuda()
+    ws = up.Workspace("cuda")
+    cfg = up.ScoreConfig(top_p=0.9)
+    sel = up.select_varlen(scores, cub, cu, cfg, veto=veto, drop_enabled=en, workspace=ws, check=True)
+    hid = torch.randn(T, 48, device="cuda").to(torch.bfloat16)
+    pos = torch.arange(T, dtype=torch.int64, device="cuda")
+    a = up.compact_varlen(sel.keep, cu, [hid, pos], drop_enabled=en, workspace=ws, after_select=True, check=True)
+    b = up.compact_varlen(sel.keep, cu, [hid, pos], drop_enabled=en, check=True)
+    n = int(b.num_out.item())
+    assert int(a.num_out.item()) == n
+    assert torch.equal(a.cu_seqlens, b.cu_seqlens)
+    assert torch.equal(a.retained_index[:n], b.retained_index[:n])
+    for x, y in zip(a.planes, b.planes):
+        assert torch.equal(x[:n], y[:n])
