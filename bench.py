@@ -276,10 +276,14 @@ def attention_stage(up, runner, sb, cu, Hq, D, stream, dev, tf_peak, reps=5):
             up.attention_varlen(q, kc, vc, cu_out, pc, heads=heads, max_tokens=runner.T, out=out)
         run()
         L.check()
+        g = torch.cuda.CUDAGraph()  # device time only (a short launch is host-bound otherwise)
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(reps):
+                run()
+        g.replay()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(reps):
-            run()
+        g.replay()
         e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / reps

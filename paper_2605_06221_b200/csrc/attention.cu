@@ -439,7 +439,7 @@ struct Attn2Cfg {
     static constexpr int KV_STAGE = NCH * BOX;
     static constexpr int KST = 2, VST = 2;
     static constexpr int PLANS = 2;                       // work-item ring depth
-    static constexpr int NBAR = 2 + 2 * KST + 2 * VST + 2 + 2 + 2 + 2 * PLANS;
+    static constexpr int NBAR = 2 + 2 * KST + 2 * VST + 2 + 4 + 2 + 2 * PLANS;
     static constexpr int THREADS = 384;
     static constexpr uint32_t S_COL = 0, O_COL = 2 * BN;
     static_assert(O_COL + 2 * D <= 512, "TMEM columns");
@@ -506,8 +506,8 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     uint64_t* v_full = k_empty + C::KST;
     uint64_t* v_empty = v_full + C::VST;
     uint64_t* s_full = v_empty + C::VST;                  // [tile]
-    uint64_t* p_full = s_full + 2;                        // [tile]
-    uint64_t* o_done = p_full + 2;                        // [tile]
+    uint64_t* p_full = s_full + 2;                        // [tile][key half]
+    uint64_t* o_done = p_full + 4;                        // [tile]
     uint64_t* plan_full = o_done + 2;                     // [PLANS]
     uint64_t* plan_empty = plan_full + C::PLANS;          // [PLANS]
     PairPlan* plans = reinterpret_cast<PairPlan*>(bars + C::NBAR);
@@ -522,7 +522,8 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         mbar_init(q_empty, 1);
         for (int s = 0; s < C::KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
         for (int s = 0; s < C::VST; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&p_full[s], 4); mbar_init(&o_done[s], 1); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&o_done[s], 1); }
+        for (int s = 0; s < 4; ++s) mbar_init(&p_full[s], 4);
         // a plan is read by the TMA warp, the MMA warp and the eight softmax warps
         for (int s = 0; s < C::PLANS; ++s) { mbar_init(&plan_full[s], 1); mbar_init(&plan_empty[s], 10); }
         fence_barrier_init();
@@ -592,13 +593,20 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             }
             mma_commit(&s_full[t]);
         };
-        auto issue_pv = [&](int t, uint32_t kvi, bool first) {  // O_t += P_t V (P over S_t)
+        // O_t += P_t V (P over S_t), one 64-key half at a time: the half's MMAs go out as
+        // soon as the softmax has stored that half of P
+        auto issue_pv = [&](int t, uint32_t kvi, bool first, uint32_t ph) {
             const uint32_t vs = kvi % C::VST;
 #pragma unroll
-            for (int kk = 0; kk < C::BN / 16; ++kk)  // 16 keys = 8 bf16-pair columns of P
-                mma_bf16_ts(tmem + C::O_COL + t * D, tmem + C::S_COL + t * C::BN + kk * 8,
-                            v_base + ((vs * C::KV_STAGE + kk * 2048) >> 4), kIdescO,
-                            (!first || kk > 0) ? 1u : 0u);
+            for (int hf = 0; hf < 2; ++hf) {
+                mbar_wait(&p_full[t * 2 + hf], ph);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = hf * (C::BN / 32); kk < (hf + 1) * (C::BN / 32); ++kk)  // 16 keys = 8 P columns
+                    mma_bf16_ts(tmem + C::O_COL + t * D, tmem + C::S_COL + t * C::BN + kk * 8,
+                                v_base + ((vs * C::KV_STAGE + kk * 2048) >> 4), kIdescO,
+                                (!first || kk > 0) ? 1u : 0u);
+            }
         };
         uint32_t kv = 0, js = 0;  // K/V ring position, S/P phases (tiles so far, per query tile)
         for (int it = 0;; ++it) {
@@ -617,18 +625,14 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                     const uint32_t kj = kv + j;
                     const bool more = j + 1 < nt;
                     mbar_wait(&v_full[kj % C::VST], (kj / C::VST) & 1);
-                    mbar_wait(&p_full[0], (js + j) & 1);
-                    tc_fence_after();
-                    issue_pv(0, kj, j == 0);
+                    issue_pv(0, kj, j == 0, (js + j) & 1);
                     if (!more) mma_commit(&o_done[0]);
                     if (more) {
                         mbar_wait(&k_full[(kj + 1) % C::KST], ((kj + 1) / C::KST) & 1);
                         tc_fence_after();
                         issue_s(0, kj + 1);
                     }
-                    mbar_wait(&p_full[1], (js + j) & 1);
-                    tc_fence_after();
-                    issue_pv(1, kj, j == 0);
+                    issue_pv(1, kj, j == 0, (js + j) & 1);
                     mma_commit(&v_empty[kj % C::VST]);
                     if (!more) mma_commit(&o_done[1]);
                     if (more) {
@@ -757,6 +761,14 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                     }
                 }
                 const float mref = m_run == -INFINITY ? 0.f : m_run;
+                if (t == 0 && kb + C::BN > total_rows) {  // V rows past the batch -> 0 before PV0 reads them
+                    const uint32_t g = js + j;
+                    mbar_wait(&v_full[g % C::VST], (g / C::VST) & 1);
+                    zero_stage_rows(sv + (g % C::VST) * C::KV_STAGE, C::NCH, C::BOX,
+                                    static_cast<int>(total_rows - kb > 0 ? total_rows - kb : 0), C::BN,
+                                    threadIdx.x - 128, 128);
+                    fence_proxy_async_smem();
+                }
                 float lsum = 0.f;
                 const uint64_t c2 = pk(c, c), m2 = pk(-mref, -mref);
                 uint64_t acc0 = 0, acc1 = 0;
@@ -797,24 +809,18 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                         }
                         tmem_st16(s_addr + hf * 32 + q * 16, pk16);
                     }
+                    // this half of P is in TMEM: its PV MMAs may start
+                    tmem_st_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&p_full[t * 2 + hf]);
                 }
                 {
                     const uint64_t a2 = add2(acc0, acc1);
                     lsum += lo_f(a2) + hi_f(a2);
                 }
                 l_run += lsum;
-                if (t == 0 && kb + C::BN > total_rows) {  // V rows past the batch -> 0 before PV0 reads them
-                    const uint32_t g = js + j;
-                    mbar_wait(&v_full[g % C::VST], (g / C::VST) & 1);
-                    zero_stage_rows(sv + (g % C::VST) * C::KV_STAGE, C::NCH, C::BOX,
-                                    static_cast<int>(total_rows - kb > 0 ? total_rows - kb : 0), C::BN,
-                                    threadIdx.x - 128, 128);
-                    fence_proxy_async_smem();
-                }
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&p_full[t]);
+
             }
             // epilogue: O_t / l -> bf16.  The next item's PV_t,0 (which overwrites O_t) is
             // issued only after this warpgroup's next p_full arrival, i.e. after these loads.
