@@ -43,12 +43,20 @@ struct AttnCfg {
     static_assert(smem() <= 232448 - 1024, "shared memory");
 };
 
+// K / V ring depths of the two-tile kernel (D <= 128)
+#ifndef UP_ATTN2_KST
+#define UP_ATTN2_KST 2
+#endif
+#ifndef UP_ATTN2_VST
+#define UP_ATTN2_VST 2
+#endif
+
 // Of every 16 element pairs of a full tile, this many take exp2 on the FMA pipe
-// (tools/attn_sweep.sh on B200: 2 is best at D = 128, 0 at D = 256).
+// (tools/attn_sweep.sh, tools/attn2_sweep.sh on B200: 1 is best at D = 128, 0 at D = 256).
 #ifdef UP_ATTN_POLY_PAIRS
 template <int D> constexpr int kAttnPolyPairs = UP_ATTN_POLY_PAIRS;
 #else
-template <int D> constexpr int kAttnPolyPairs = D > 128 ? 0 : 2;
+template <int D> constexpr int kAttnPolyPairs = D > 128 ? 0 : 1;
 #endif
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
@@ -437,7 +445,7 @@ struct Attn2Cfg {
     static constexpr int BOX = 128 * 128;                 // 128 rows x 128 bytes
     static constexpr int Q_BYTES = NCH * BOX;             // one query tile
     static constexpr int KV_STAGE = NCH * BOX;
-    static constexpr int KST = 2, VST = 2;
+    static constexpr int KST = UP_ATTN2_KST, VST = UP_ATTN2_VST;
     static constexpr int PLANS = 2;                       // work-item ring depth
     static constexpr int NBAR = 2 + 2 * KST + 2 * VST + 2 + 4 + 2 + 2 * PLANS;
     static constexpr int THREADS = 384;
