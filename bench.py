@@ -12,13 +12,18 @@ synthetic random-init bf16 activations (no network), a distinct activation set p
 Arms
   default            this repo's sm_100a kernels through the C ABI (CUDA-graph captured);
                      prints value (device-resident inputs), e2e (host buffers through the
-                     public API, H2D/D2H inside the timed region), per-stage rooflines,
+                     public API, H2D/D2H inside the timed region), per-stage rooflines
+                     (score, select, compact; plus the drop layer's attention over the
+                     retained rows, reported beside the path and not part of `value`),
                      the CPU baseline (the reference on the host cores) and clocks.
   --impl reference   the unmodified reference C++ implementation (oracle/_ref, compiled
                      from /root/reference/proj/core/src) on the host cores, same metric.
 
 Launched as `python bench.py --gpus N ...` or under torchrun for N > 1: each rank runs
-its own batch (request sharding, weak scaling; no collective on the data path).
+its own batch (request sharding, weak scaling; no collective on the data path).  --config
+c3 shards heads (TP): at N > 1 each rank scores its slice with the all-reduce fused into the
+combine kernel over peer memory (UP_TP_REDUCE=nccl: NCCL all-gather + ordered reduce).
+--config c1..c5 selects the other BASELINE.json configurations.
 """
 from __future__ import annotations
 
