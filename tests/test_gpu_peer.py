@@ -84,20 +84,21 @@ def _worker(rank, tp, port, q):
         q.put((rank, [tb.strip().splitlines()[-1]]))
 
 
-@pytest.mark.timeout(240)
-def test_peer_allreduce_bitwise_two_ranks_one_device():
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("tp", [2, 3])
+def test_peer_allreduce_bitwise_ranks_one_device(tp):
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, tp, port, q)) for r in range(tp)]
     for p in procs:
         p.start()
-    results = dict(q.get(timeout=200) for _ in procs)
+    results = dict(q.get(timeout=250) for _ in procs)
     for p in procs:
         p.join(timeout=30)
-    assert results == {0: [], 1: []}, results
+    assert results == {r: [] for r in range(tp)}, results
 
 
 def _worker_fused(rank, tp, port, q):
