@@ -2,7 +2,7 @@
 // (include/uniprefill_b200.hpp) over the C ABI, no Python anywhere.  What an engine written
 // in C++ (the reference's Engine::run_batch, scheduler.cpp:293-332) does at its drop layers:
 //
-//   for every drop layer:  score_blocks -> top_p_select -> compact   (one CUDA stream)
+//   for every drop layer:  score_blocks -> top_p_select -> compact_selected   (one CUDA stream)
 //
 // The layer loop is captured once into a CUDA graph and replayed; prints one JSON line
 // with tokens/s over the timed replays.  Synthetic activations ("planted" regime of
@@ -151,7 +151,8 @@ int main(int argc, char** argv) {
         launches += up_last_launch_count();
         b2::top_p_select(s, batch, cfg, d_bs, d_cub, d_keep, up_selection_out{d_cut, nullptr, nullptr, nullptr}, ws);
         launches += up_last_launch_count();
-        b2::compact(s, batch, d_keep, planes, d_cu_out, d_idx, d_nout, ws);
+        // the keep mask is top_p_select's output on this workspace: its tile counts are reused
+        b2::compact_selected(s, batch, d_keep, planes, d_cu_out, d_idx, d_nout, ws);
         launches += up_last_launch_count();
     };
     layer();
