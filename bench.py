@@ -669,7 +669,7 @@ def run_ours(args):
                        "tokens_per_request": lengths[0] if len(set(lengths)) == 1 else lengths,
                        "tokens_per_rank": T, "drop_layers": layers, "regime": args.regime,
                        "retention_rho": rho, "activation_sets": n_sets,
-                       "seeds": "make_batch seed = 1000 * rank + activation-set index (splitmix-free torch RNG)",
+                       "seeds": "make_batch seed = 1000 * rank + activation-set index (torch.Generator on the device)",
                        "l2": "inputs larger than L2 (distinct per-layer sets, each >> 126 MB)",
                        "cuda_graph": use_graph, "parallelism": par, **cfgd},
             "roofline": roofline, "stages": stage_info, "cpu_baseline": cpu, "e2e": e2e,
