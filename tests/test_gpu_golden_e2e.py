@@ -289,3 +289,30 @@ def test_drop_layer_random_configs_vs_oracle(up, port, seed):
     ii = torch.from_numpy(idx).cuda()
     assert torch.equal(out.planes[0][:n], sb.hidden[ii])
     assert torch.equal(out.planes[1][:n], sb.positions[ii])
+
+
+def test_run_to_run_bitwise_determinism(up):
+    """Fixed reduction orders: two runs of the drop layer and of the attention
+    over its retained rows on the same inputs agree bit for bit -- block scores, keep mask,
+    compacted planes, attention output (the persistent kernels' work distribution does not
+    leak into the arithmetic)."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    lengths = [5000, 3000, 700]
+    Hq, Hkv, D = 32, 8, 128
+    sb = make_batch(lengths, Hq, Hkv, D, 64, regime="planted", seed=77)
+    T = sum(lengths)
+    outs = []
+    for _ in range(2):
+        layer = up.DropLayer(up.ScoreConfig(), up.HeadLayout(Hq, Hkv, D), T, len(lengths),
+                             [(64,), (Hkv, D), (Hkv, D), (), (Hq, D)],
+                             [torch.bfloat16, torch.bfloat16, torch.bfloat16, torch.int64, torch.bfloat16])
+        res = layer(sb.q, sb.k, sb.cu_seqlens, [sb.hidden, sb.k, sb.v, sb.positions, sb.q])
+        layer.check()
+        n = int(res.num_out.item())
+        att = up.attention_varlen(res.planes[4], res.planes[1], res.planes[2], res.cu_seqlens, res.planes[3],
+                                  max_tokens=T, check=True)
+        nb = int(layer.scores.cu_blocks[-1])  # past it: capacity padding, never written
+        outs.append([layer.scores.block_scores[:nb].clone(), layer.sel.keep[:T].clone(),
+                     *[p[:n].clone() for p in res.planes], att[:n].clone()])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
