@@ -316,3 +316,32 @@ def test_run_to_run_bitwise_determinism(up):
                      *[p[:n].clone() for p in res.planes], att[:n].clone()])
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_batching_transparency(up):
+    """A request's block scores do not depend on what it is batched with (scheduler
+    batching transparency, test_scheduler.cpp:85-119): each request of a varlen batch vs the
+    same request scored alone, within 1e-5 relative (the persistent scorer's partition moves
+    with the batch, so rounding may differ in the last bits), and the same keep mask."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    lengths = [3000, 777, 5000, 64]
+    Hq, Hkv, D = 32, 8, 128
+    sb = make_batch(lengths, Hq, Hkv, D, 16, regime="planted", seed=5)
+    cfg = up.ScoreConfig()
+    heads = up.HeadLayout(Hq, Hkv, D)
+    full = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, cfg, heads, check=True)
+    fsel = up.select_varlen(full.block_scores, full.cu_blocks, sb.cu_seqlens, cfg, check=True)
+    cu = sb.cu_seqlens.tolist()
+    cub = full.cu_blocks.tolist()
+    for r in range(len(lengths)):
+        s, e = cu[r], cu[r + 1]
+        one = up.score_blocks_varlen(sb.q[s:e].contiguous(), sb.k[s:e].contiguous(),
+                                     torch.tensor([0, e - s], dtype=torch.int32, device="cuda"), cfg, heads,
+                                     check=True)
+        nb = cub[r + 1] - cub[r]
+        a, b = full.block_scores[cub[r]:cub[r + 1]].double(), one.block_scores[:nb].double()
+        assert bool(((a - b).abs() <= 1e-5 * b.abs() + 1e-12).all()), f"request {r}"
+        osel = up.select_varlen(one.block_scores, one.cu_blocks,
+                                torch.tensor([0, e - s], dtype=torch.int32, device="cuda"), cfg, check=True)
+        if torch.equal(a, b):
+            assert torch.equal(fsel.keep[s:e], osel.keep[:e - s])
