@@ -345,3 +345,33 @@ def test_batching_transparency(up):
                                 torch.tensor([0, e - s], dtype=torch.int32, device="cuda"), cfg, check=True)
         if torch.equal(a, b):
             assert torch.equal(fsel.keep[s:e], osel.keep[:e - s])
+
+
+def test_p_one_keeps_everything_and_counts_are_monotone_in_p(up):
+    """p = 1 keeps every row and compaction is the identity (test_propagation.cpp:171-194);
+    the retained count never decreases as p grows (:232-253); the query window and the
+    sinks always survive (:310-327)."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    lengths = [2500, 900, 4100]
+    Hq, Hkv, D = 8, 2, 128
+    sb = make_batch(lengths, Hq, Hkv, D, 32, regime="planted", seed=12)
+    T = sum(lengths)
+    cu = sb.cu_seqlens.tolist()
+    prev = -1
+    for p in (0.3, 0.6, 0.9, 0.99, 1.0):
+        cfg = up.ScoreConfig(top_p=p)
+        layer = up.DropLayer(cfg, up.HeadLayout(Hq, Hkv, D), T, len(lengths), [(32,), ()],
+                             [torch.bfloat16, torch.int64])
+        res = layer(sb.q, sb.k, sb.cu_seqlens, [sb.hidden, sb.positions])
+        layer.check()
+        n = int(res.num_out.item())
+        assert n >= prev, (p, n, prev)
+        prev = n
+        keep = layer.sel.keep[:T].bool()
+        for r in range(len(lengths)):
+            s, e = cu[r], cu[r + 1]
+            neff = min(cfg.query_window_n, e - s)
+            assert bool(keep[e - neff:e].all()) and bool(keep[s:s + min(cfg.sink_count_a, e - s)].all())
+        if p == 1.0:
+            assert n == T
+            assert torch.equal(res.planes[0][:T], sb.hidden) and torch.equal(res.planes[1][:T], sb.positions)
