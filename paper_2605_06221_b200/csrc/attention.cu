@@ -135,7 +135,9 @@ attention_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         int total = 0;
         for (int r = 0; r < R; ++r) total += (p.cu_seqlens[r + 1] - p.cu_seqlens[r] + C::BM - 1) / C::BM;
         int64_t q0 = -1, sb = 0, se = 0, kb = 0, ke = 0;
-        if (trev < total) {
+        const bool bad = p.cu_seqlens[R] > p.max_tokens;  // malformed batch: no rows touched
+        if (bad && blockIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
+        if (trev < total && !bad) {
             int t = total - 1 - trev;
             for (int r = 0; r < R; ++r) {
                 const int n = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
@@ -659,7 +661,9 @@ attention2q_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         // ahead of the consumers
         if (lane == 0) {
             uint32_t* ctr = p.err + 32;
-            const int total = total_pairs(p);
+            const bool bad = p.cu_seqlens[p.num_requests] > p.max_tokens;  // malformed: no items
+            if (bad && blockIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
+            const int total = bad ? 0 : total_pairs(p);
             const int items = total * H;
             for (int it = 0;; ++it) {
                 const int slot = it % C::PLANS;

@@ -35,7 +35,8 @@ compact_count_kernel(const CompactParams p) {
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     constexpr int PER = kCompactTile / kCompactThreads;
     __shared__ int red[kCompactThreads / 32];
-    const int T = p.cu_seqlens[p.num_requests];
+    // clamp: a malformed batch (flagged by the scorer / select) must not read past capacity
+    const int T = static_cast<int>(min(static_cast<int64_t>(p.cu_seqlens[p.num_requests]), p.max_tokens));
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kCompactTile;
     int c = 0;
     if (t0 < T) {
@@ -62,7 +63,8 @@ compact_index_kernel(const CompactParams p) {
     __shared__ int red[kCompactThreads / 32];
     __shared__ int warp_tot[kCompactThreads / 32];
     __shared__ int s_offset;
-    const int T = p.cu_seqlens[p.num_requests];
+    // clamp: a malformed batch (flagged by the scorer / select) must not read past capacity
+    const int T = static_cast<int>(min(static_cast<int64_t>(p.cu_seqlens[p.num_requests]), p.max_tokens));
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kCompactTile;
     if (t0 >= T) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -222,6 +222,10 @@ __global__ void __launch_bounds__(THREADS)
 select_radix_kernel(const SelectParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
+    if (p.cu_seqlens[gridDim.x] > p.max_tokens) {  // malformed batch (grid = R): no write past capacity
+        if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
+        return;
+    }
     using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, int32_t, UP_SELECT_RADIX_BITS>;
     constexpr int CAP = THREADS * ITEMS;
     __shared__ union {
@@ -355,6 +359,10 @@ __global__ void __launch_bounds__(kSelThreads)
 select_kernel(const SelectParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
+    if (p.cu_seqlens[gridDim.x] > p.max_tokens) {  // malformed batch (grid = R): no write past capacity
+        if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
+        return;
+    }
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ double red_d[32];
     __shared__ int red_i[32];
@@ -477,6 +485,10 @@ __global__ void __launch_bounds__(256)
 expand_kernel(const SelectParams p, int R) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
+    if (p.cu_seqlens[R] > p.max_tokens) {  // malformed batch: no write past capacity
+        if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
+        return;
+    }
     __shared__ int red[8];
     const int T = p.cu_seqlens[R];
     const int64_t A = p.sink_count_a;

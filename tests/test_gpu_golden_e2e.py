@@ -375,3 +375,28 @@ def test_p_one_keeps_everything_and_counts_are_monotone_in_p(up):
         if p == 1.0:
             assert n == T
             assert torch.equal(res.planes[0][:T], sb.hidden) and torch.equal(res.planes[1][:T], sb.positions)
+
+
+def test_batch_past_capacity_is_a_contract_violation(up):
+    """cu_seqlens ending past max_tokens (a malformed batch): the device raises the sticky
+    ContractViolation and no kernel reads or writes past the capacity-sized buffers."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    lengths = [700, 500]
+    Hq, Hkv, D = 8, 2, 128
+    sb = make_batch(lengths, Hq, Hkv, D, 32, regime="planted", seed=3)
+    T = sum(lengths)
+    cap = T - 100  # the batch claims 100 rows more than the buffers hold
+    layer = up.DropLayer(up.ScoreConfig(), up.HeadLayout(Hq, Hkv, D), cap, len(lengths),
+                         [(32,), (Hkv, D), (Hkv, D), (), (Hq, D)],
+                         [torch.bfloat16, torch.bfloat16, torch.bfloat16, torch.int64, torch.bfloat16])
+    planes = [sb.hidden[:cap], sb.k[:cap], sb.v[:cap], sb.positions[:cap], sb.q[:cap]]
+    res = layer(sb.q[:cap], sb.k[:cap], sb.cu_seqlens, planes)
+    with pytest.raises(up.ContractViolation):
+        layer.check()
+    ws = up.Workspace("cuda")
+    up.attention_varlen(sb.q[:cap], sb.k[:cap], sb.v[:cap], sb.cu_seqlens, sb.positions[:cap], max_tokens=cap,
+                        workspace=ws)
+    with pytest.raises(up.ContractViolation):
+        ws.device_status()
+    torch.cuda.synchronize()  # the context is still healthy (no out-of-bounds fault)
+    assert int(res.num_out.item()) <= cap
