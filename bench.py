@@ -179,78 +179,176 @@ def ncu_traffic(prefix):
 
 
 # --------------------------------------------------------------------------- CPU reference
-class CpuReferenceSample:
-    """The reference (oracle/_ref) hot path on the host cores over a bounded sample of the
-    same workload: `cores` concurrent 2048-token requests of the same model shape, each
-    worker thread running score_tokens -> top_p_select on its request, then
-    patch_metadata compacting the batch (scheduler.cpp:293-332)."""
+# The reference arm imports nothing of this repo's product package (no repo .so is mapped):
+# inputs come from numpy, the work from oracle/_ref (the unmodified reference build).
+MODEL_SHAPES_REF = {  # the same layer shapes as paper_2605_06221_b200.synthetic.MODEL_SHAPES
+    "llama3.1-8b": dict(num_q_heads=32, num_kv_heads=8, head_dim=128, hidden=4096),
+    "qwen3-next-80b-a3b": dict(num_q_heads=16, num_kv_heads=2, head_dim=256, hidden=2048),
+    "gemma3-12b": dict(num_q_heads=16, num_kv_heads=8, head_dim=256, hidden=3840),
+}
 
-    SEG = 2048
 
-    def __init__(self, model, cfg, regime, seed=1234, threads=None):
+def loguniform_lengths_ref(count, lo, hi, seed):
+    """BASELINE config 5's request lengths (synthetic.loguniform_lengths restated)."""
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    u = torch.rand(count, generator=g, dtype=torch.float64)
+    return [int(round(math.exp(math.log(lo) + float(x) * (math.log(hi) - math.log(lo))))) for x in u]
+
+
+def cpu_model_name():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _bf16_exact(x):
+    """Round float32 to the nearest bf16 (ties to even), returned as float32."""
+    import numpy as np
+    u = x.astype(np.float32).view(np.uint32)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.view(np.float32)
+
+
+class CpuReferenceUnits:
+    """The reference hot path on the host cores, timed on units of the configured workload:
+    a unit is one (request, drop layer) pair of the reference's varlen layer loop
+    (scheduler.cpp:293-332) at the config's real request length -- score (the reference's
+    TP=8 path sharded_block_scores + allreduce_scores, propagation.cpp:163-170, one shard per
+    host thread) -> top_p_select -> apply_drop -> patch_metadata (oracle/_ref
+    ref_drop_unit).  A step runs `units` units concurrently (units x 8 threads <= the host
+    cores, bounded by memory); single_core() times one unit on ONE core through the
+    unsharded score_tokens.  Inputs: numpy, bf16-exact, the planted/iid regimes of
+    synthetic.make_batch restated (gamma 0.8, hot-block fraction 0.25)."""
+
+    TP = 8
+
+    def __init__(self, model, lengths, cfg, regime, seed=1234):
         import numpy as np
         import oracle
-        from paper_2605_06221_b200.synthetic import MODEL_SHAPES, make_batch
+        if not oracle.ref_available():
+            raise RuntimeError("oracle/_ref (the reference build) is missing")
+        self.ref = oracle.ref()
+        self.model, self.cfg, self.regime = model, cfg, regime
+        self.shp = shp = MODEL_SHAPES_REF[model]
+        self.nproc = os.cpu_count() or 1
+        # distinct request lengths of the config, longest first (one input set per length)
+        self.lengths = sorted(set(lengths), reverse=True)[:4]
+        N = self.lengths[0]
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except Exception:
+            avail = 32 << 30
+        unit_bytes = N * (4 * shp["hidden"] * 5 + 4 * shp["num_kv_heads"] * shp["head_dim"] * 3 +
+                          4 * 128 * shp["num_q_heads"] // self.TP * 3)
+        self.units = max(1, min(self.nproc // self.TP, int(avail * 0.5 // max(unit_bytes, 1)), 16))
+        self.threads = self.units * self.TP
+        rng = np.random.default_rng(seed)
+        Hq, Hkv, D, HID = shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"], shp["hidden"]
+        group = Hq // Hkv
+        G = cfg["block_size_g"]
+        n = cfg["query_window_n"]
+        self.inputs = []
+        for L in self.lengths:
+            k = rng.standard_normal((L, Hkv, D), dtype=np.float32)
+            qt = rng.standard_normal((min(n, L), Hq, D), dtype=np.float32)
+            if regime == "planted":
+                m = rng.standard_normal((Hkv, D), dtype=np.float32)
+                qt += 0.8 * np.repeat(m, group, axis=0)[None]
+                hot = np.repeat(rng.random((L + G - 1) // G) < 0.25, G)[:L]
+                k[hot] += 0.8 * m[None]
+            self.inputs.append((_bf16_exact(qt).reshape(len(qt), Hq * D), _bf16_exact(k).reshape(L, Hkv * D)))
+        # hidden-state values do not change the reference's work: one shared bf16-exact buffer
+        self.hidden = _bf16_exact(rng.standard_normal((N, HID), dtype=np.float32))
+        self.desc = (f"(request, drop layer) units of the workload at their real lengths "
+                     f"{self.lengths} ({model} shape, {regime} bf16-exact inputs from numpy): the reference "
+                     f"(oracle/_ref) score -> top_p_select -> apply_drop -> patch_metadata; {self.units} "
+                     f"concurrent unit(s) per step, each scored through the reference's TP={self.TP} path "
+                     f"(sharded_block_scores + allreduce_scores) with one shard per thread = {self.threads} "
+                     f"threads on {self.nproc} host cores")
+        self._next = 0
 
-        self.shp = MODEL_SHAPES[model]
-        self.cfg = cfg
-        self.cores = threads or min(os.cpu_count() or 1, 64)
-        if oracle.ref_available():
-            self.impl, self.kind = oracle.ref(), "reference"
-        else:
-            self.impl, self.kind = oracle.port(), "port"
-            self.cores = 1
+    def _unit(self, idx, tp, threads):
+        qt, k = self.inputs[idx % len(self.inputs)]
+        L = k.shape[0]
         shp = self.shp
-        sb = make_batch([self.SEG] * self.cores, shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"],
-                        shp["hidden"], regime=regime, seed=seed, device="cpu")
-        self.T = self.SEG * self.cores
-        self.q = sb.q.float().reshape(self.T, -1).numpy()
-        self.k = sb.k.float().reshape(self.T, -1).numpy()
-        self.hid = sb.hidden.float().numpy()
-        self.cu = sb.cu_seqlens.numpy().astype(np.int64)
-        self.desc = (f"{self.cores} concurrent {self.SEG}-token requests ({model} shape, {regime}) through the "
-                     f"reference score_tokens -> top_p_select -> patch_metadata, {self.cores} threads")
+        sec, kept = self.ref.drop_unit(qt, k, self.hidden[:L], shp["num_q_heads"], shp["num_kv_heads"], tp,
+                                       threads, **self.cfg)
+        return L, sec, kept
 
-    def run(self):
-        """Returns tokens/s of one pass over the sample."""
-        shp = self.shp
+    def step(self):
+        """One step: `units` concurrent units; returns (tokens/s, tokens, seconds)."""
+        import concurrent.futures as cf
+        idx = [self._next + u for u in range(self.units)]
+        self._next += self.units
         t0 = time.perf_counter()
-        if self.kind == "reference":
-            self.impl.drop_layer_varlen(self.q, self.k, self.hid, self.cu, shp["num_q_heads"],
-                                        shp["num_kv_heads"], threads=self.cores, **self.cfg)
-            T = self.T
-        else:  # single-threaded restatement (no reference build available): one request
-            seg = self.SEG
-            tok, blk, _ = self.impl.score_tokens(self.q[:seg], self.k[:seg], shp["num_q_heads"],
-                                                 shp["num_kv_heads"], **self.cfg)
-            self.impl.top_p_select(blk, seg, **self.cfg)
-            T = seg
-        return T / (time.perf_counter() - t0)
+        with cf.ThreadPoolExecutor(self.units) as ex:
+            res = list(ex.map(lambda i: self._unit(i, self.TP, self.TP), idx))
+        sec = time.perf_counter() - t0
+        tokens = sum(r[0] for r in res)
+        return tokens / sec, tokens, sec
+
+    def single_core(self):
+        """One unit of the longest request on one core through the unsharded score_tokens."""
+        L, sec, kept = self._unit(0, 1, 1)
+        return L / sec, sec, L
+
+
+def cpu_reference_report(units, step_values, single):
+    value = statistics.mean(step_values)
+    return {"value": value, "unit": "tokens/s", "cores": units.threads, "kind": "reference",
+            "sample": units.desc, "nproc": units.nproc, "cpu_model": cpu_model_name(),
+            "single_core": {"value": single[0], "unit": "tokens/s", "cores": 1, "seconds": single[1],
+                            "tokens": single[2],
+                            "path": "one unit of the longest request, unsharded score_tokens, one thread"}}
 
 
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
-    model, _, layers, cfg, _ = CONFIGS[args.config]
-    if rank != 0:
+    if rank != 0:  # rank 0 alone measures the host; the other ranks exit without work
         return
-    sample = CpuReferenceSample(model, cfg, args.regime)
+    model, lspec, layers, cfg, _ = CONFIGS[args.config]
+    if isinstance(lspec, str):
+        _, count, lo, hi, seed = lspec.split(":")
+        lengths = loguniform_lengths_ref(int(count), int(lo), int(hi), int(seed))
+    else:
+        lengths = list(lspec)
+    units = CpuReferenceUnits(model, lengths, cfg, args.regime)
     vals = []
     for i in range(args.warmup + args.steps):
-        v = sample.run()
+        v, _, _ = units.step()
         if i >= args.warmup:
             vals.append(v)
-    value = statistics.mean(vals)
-    cores, kind, desc = sample.cores, sample.kind, sample.desc
+    single = units.single_core()
+    cpu = cpu_reference_report(units, vals, single)
+    value = cpu["value"]
     line = {
         "impl": "reference", "metric": "score+drop+compact tokens/s", "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 (fp64 accumulation)", "data": "synthetic",
-        "config": {"workload": WORKLOAD_NAME[args.config], "regime": args.regime, **cfg},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": desc},
+        "config": workload_config(args.config, args.regime),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(name, regime):
+    """The `config` object both arms print (identical, so the arms are comparable)."""
+    model, lspec, layers, cfg, mode = CONFIGS[name]
+    lengths = lspec if isinstance(lspec, str) else (lspec[0] if len(set(lspec)) == 1 else list(lspec))
+    return {"workload": WORKLOAD_NAME[name], "model_shape": model,
+            "requests": int(lspec.split(":")[1]) if isinstance(lspec, str) else len(lspec),
+            "tokens_per_request": lengths, "drop_layers": layers, "regime": regime,
+            "unit": "(request, drop layer) pair; tokens = tokens entering the drop layer",
+            "l2": "inputs larger than L2 (per-layer activation sets >> 126 MB)", **cfg}
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -644,11 +742,10 @@ def run_ours(args):
     # ---- CPU baseline (rank 0 only, N=1 semantics) ----
     cpu = None
     if rank == 0 and ws == 1 and not args.skip_cpu:  # reported at N=1 only
-        try:
-            sample = CpuReferenceSample(model, cfgd, args.regime)
-            v = sample.run()
-            cpu = {"value": v, "unit": "tokens/s", "cores": sample.cores, "kind": sample.kind,
-                   "sample": sample.desc}
+        try:  # one step of the reference arm's units (all cores) + one unit on one core
+            units = CpuReferenceUnits(model, all_lengths, cfgd, args.regime)
+            cpu = cpu_reference_report(units, [units.step()[0]], units.single_core())
+            del units
         except Exception as exc:  # the baseline is reported, never fatal
             cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": None, "sample": f"failed: {exc}"}
 
@@ -665,13 +762,12 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD_NAME[args.config], "model_shape": model, "requests": R,
-                       "tokens_per_request": lengths[0] if len(set(lengths)) == 1 else lengths,
-                       "tokens_per_rank": T, "drop_layers": layers, "regime": args.regime,
-                       "retention_rho": rho, "activation_sets": n_sets,
-                       "seeds": "make_batch seed = 1000 * rank + activation-set index (torch.Generator on the device)",
-                       "l2": "inputs larger than L2 (distinct per-layer sets, each >> 126 MB)",
-                       "cuda_graph": use_graph, "parallelism": par, **cfgd},
+            "config": workload_config(args.config, args.regime),
+            "details": {"requests_per_rank": R, "tokens_per_rank": T, "retention_rho": rho,
+                        "activation_sets": n_sets,
+                        "seeds": "make_batch seed = 1000 * rank + activation-set index (torch.Generator on the device)",
+                        "l2": "inputs larger than L2 (distinct per-layer activation sets, each >> 126 MB)",
+                        "cuda_graph": use_graph, "parallelism": par},
             "roofline": roofline, "stages": stage_info, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk, "gpu_launches": launches_per_layer * layers * args.steps,
         }

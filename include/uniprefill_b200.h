@@ -231,7 +231,9 @@ up_status up_attention_varlen(void* stream, const up_batch* batch, const up_head
 
 /* ---- TP score all-reduce over peer memory (NVLink P2P / NVSwitch) ----------------------
  * allreduce_scores (tp_sim.cpp:29-49) for a TP group of one process per GPU, as one kernel:
- * every rank stores its partial into row `rank` of every peer's exchange buffer, raises a
+ * every rank stores its partial into row `rank` of every peer's exchange buffer (one of two
+ * banks, alternating per call, so a fast rank's next call never overwrites rows a slow peer
+ * is still summing), raises a
  * flag per peer, waits for the tp rows of its own buffer and sums them in ascending rank
  * order from 0.0f -- bitwise the reference's reduction on every rank (an NCCL sum is not).
  * Exchange buffers: one per rank from up_peer_buffer_alloc(tp, capacity) (zeroed), shared

@@ -295,10 +295,44 @@ class Port(_Lib):
         n = int(nout.value)
         return [d[:n] for d in dsts], cu_out, ridx[:n]
 
-    def rng_normal_array(self, seed: int, stream: int, count: int, stddev: float) -> np.ndarray:
-        key = self.lib.orc_rng_key(seed, stream)
-        fn = self.lib.orc_rng_normal
-        return np.fromiter((fn(key, i, stddev) for i in range(count)), np.float32, count)
+    def rng_normal_array(self, seed: int, stream: int, count: int, stddev: float, first: int = 0) -> np.ndarray:
+        """CounterRng(seed, stream).normal(first + j, stddev) for j < count (rng.cpp:34-40)."""
+        out = np.empty(max(count, 1), np.float32)
+        fn = self.lib.orc_rng_normal_fill
+        fn.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_double,
+                       ctypes.POINTER(ctypes.c_float)]
+        fn.restype = None
+        fn(self.lib.orc_rng_key(seed, stream), first, count, stddev, _ptr(out, ctypes.c_float))
+        return out[:count]
+
+    def c3_vectors(self, num_trials: int = 100000):
+        """Acceptance criterion 3's inputs (acceptance_main.cpp:175-199), trials 0..num_trials-1:
+        (scores concatenated fp32, offsets int64[num_trials+1], top_p fp32[num_trials])."""
+        fn = self.lib.orc_c3_vector
+        fn.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, ctypes.POINTER(ctypes.c_float),
+                       ctypes.POINTER(ctypes.c_float)]
+        fn.restype = ctypes.c_int64
+        ctr = ctypes.c_uint64(0)
+        buf = np.empty(4096, np.float32)
+        p = ctypes.c_float(0)
+        chunks, offsets, ps = [], [0], np.empty(num_trials, np.float32)
+        for t in range(num_trials):
+            n = fn(ctypes.byref(ctr), t, _ptr(buf, ctypes.c_float), ctypes.byref(p))
+            chunks.append(buf[:n].copy())
+            offsets.append(offsets[-1] + n)
+            ps[t] = p.value
+        return np.concatenate(chunks), np.asarray(offsets, np.int64), ps
+
+    def c3_reference_blocks(self, scores, top_p: float) -> np.ndarray:
+        """reference_blocks (acceptance_main.cpp:148-173) + the forced last token, as a mask."""
+        s = np.ascontiguousarray(scores, dtype=np.float32)
+        keep = np.zeros(max(s.size, 1), np.uint8)
+        fn = self.lib.orc_c3_reference_blocks
+        fn.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_double,
+                       ctypes.POINTER(ctypes.c_uint8)]
+        fn.restype = None
+        fn(_ptr(s, ctypes.c_float), s.size, float(np.float32(top_p)), _ptr(keep, ctypes.c_uint8))
+        return keep[:s.size]
 
     def rng_uniform(self, seed: int, stream: int, i: int) -> float:
         return float(self.lib.orc_rng_uniform(self.lib.orc_rng_key(seed, stream), i))
@@ -308,6 +342,23 @@ class Port(_Lib):
 
 
 class Ref(_Lib):
+    def top_p_select_batch(self, scores, offsets, top_ps, **cfg):
+        """The reference top_p_select on every vector scores[offsets[i]:offsets[i+1]] with
+        top_p = top_ps[i]: (keep masks concatenated, cutoff ranks)."""
+        s = np.ascontiguousarray(scores, dtype=np.float32)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        ps = np.ascontiguousarray(top_ps, dtype=np.float32)
+        keep = np.zeros(max(s.size, 1), np.uint8)
+        cut = np.zeros(max(ps.size, 1), np.int64)
+        fn = self.lib.ref_top_p_select_batch
+        P = ctypes.POINTER
+        fn.argtypes = [P(ctypes.c_float), P(ctypes.c_int64), P(ctypes.c_float), ctypes.c_int32, P(_Cfg),
+                       P(ctypes.c_uint8), P(ctypes.c_int64)]
+        c = _cfg(**cfg)
+        _raise(fn(_ptr(s, ctypes.c_float), _ptr(off, ctypes.c_int64), _ptr(ps, ctypes.c_float), ps.size,
+                  ctypes.byref(c), _ptr(keep, ctypes.c_uint8), _ptr(cut, ctypes.c_int64)), "top_p_select_batch")
+        return keep[:s.size], cut[:ps.size]
+
     """The unmodified reference core (oracle/_ref)."""
 
     def __init__(self, path: str = REF_SO):
@@ -473,6 +524,48 @@ class Ref(_Lib):
                                             _ptr(red, ctypes.c_float))
         _raise(st, "sharded_allreduce")
         return shards, red
+
+    def sharded_allreduce_mt(self, q_tail, k, num_heads, num_kv_heads, tp_degree, threads, **cfg):
+        """sharded_block_scores + allreduce_scores with the shards on `threads` host threads
+        (bitwise the sequential reference).  q_tail: the request's last >= n_eff query rows
+        [rows, num_heads*D]; k: [N, num_kv_heads*D].  Returns (shards [tp, nb], reduced [nb])."""
+        q = np.ascontiguousarray(q_tail, dtype=np.float32)
+        k = np.ascontiguousarray(k, dtype=np.float32)
+        N = k.shape[0]
+        D = q.shape[1] // num_heads
+        c = _cfg(**cfg)
+        nb = (N + c.block_size_g - 1) // c.block_size_g
+        shards = np.zeros((tp_degree, nb), np.float32)
+        red = np.zeros(nb, np.float32)
+        fn = self.lib.ref_sharded_allreduce_mt
+        P = ctypes.POINTER
+        fn.argtypes = [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, P(ctypes.c_float), ctypes.c_int64,
+                       ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P(_Cfg), ctypes.c_int, ctypes.c_int,
+                       P(ctypes.c_float), P(ctypes.c_float)]
+        _raise(fn(_ptr(q, ctypes.c_float), q.shape[1], q.shape[0], _ptr(k, ctypes.c_float), k.shape[1], N,
+                  num_heads, num_kv_heads, D, ctypes.byref(c), tp_degree, threads,
+                  _ptr(shards, ctypes.c_float), _ptr(red, ctypes.c_float)), "sharded_allreduce_mt")
+        return shards, red
+
+    def drop_unit(self, q_tail, k, hidden, num_heads, num_kv_heads, tp_degree=1, threads=1, **cfg):
+        """One (request, drop layer) unit of the reference's varlen loop, hot path only
+        (ref_drop_unit): returns (seconds, retained rows)."""
+        q = np.ascontiguousarray(q_tail, dtype=np.float32)
+        k = np.ascontiguousarray(k, dtype=np.float32)
+        h = np.ascontiguousarray(hidden, dtype=np.float32)
+        N = k.shape[0]
+        D = q.shape[1] // num_heads
+        c = _cfg(**cfg)
+        fn = self.lib.ref_drop_unit
+        P = ctypes.POINTER
+        fn.argtypes = [P(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, P(ctypes.c_float), ctypes.c_int64,
+                       ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P(ctypes.c_float), ctypes.c_int64,
+                       P(_Cfg), ctypes.c_int, ctypes.c_int, P(ctypes.c_int64), P(ctypes.c_double)]
+        ret, sec = ctypes.c_int64(0), ctypes.c_double(0)
+        _raise(fn(_ptr(q, ctypes.c_float), q.shape[1], q.shape[0], _ptr(k, ctypes.c_float), k.shape[1], N,
+                  num_heads, num_kv_heads, D, _ptr(h, ctypes.c_float), h.shape[1], ctypes.byref(c), tp_degree,
+                  threads, ctypes.byref(ret), ctypes.byref(sec)), "drop_unit")
+        return float(sec.value), int(ret.value)
 
     def drop_layer_varlen(self, q, k, hidden, cu_seqlens, num_heads, num_kv_heads, threads=1, **cfg):
         """The reference's per-layer hot path over a varlen batch (score -> select -> compact)."""

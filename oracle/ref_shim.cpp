@@ -17,6 +17,7 @@
 #include "uniprefill/tp_sim.hpp"
 
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <optional>
@@ -218,6 +219,115 @@ int ref_sharded_allreduce(const float* q, int64_t q_ld, const float* k, int64_t 
     });
 }
 
+// sharded_block_scores + allreduce_scores (tp_sim.cpp:12-49) with the shards scored on up to
+// `threads` host threads -- for BASELINE-size parity runs and the timed CPU reference arm.
+// Bit-identical to the sequential reference: shard t is score_tokens_heads over its own
+// heads only (each head's arithmetic reads only that head's columns, importance.cpp:104-119),
+// on a query matrix holding just the last n_eff rows (the only rows score_tokens_heads reads,
+// :109-112), and the shards are reduced by the reference's allreduce_scores.  With
+// tp_degree == 1 the single shard IS score_tokens (importance.cpp:129-132) and its block
+// scores are returned unreduced.  q: the LAST q_rows rows of the request (q_rows >= min(n, N)),
+// [q_rows, num_heads*D]; k: [N, num_kv_heads*D].
+static std::vector<float> sharded_scores_mt(const float* q, int64_t q_ld, int64_t q_rows, const float* k,
+                                            int64_t k_ld, int64_t N, int num_heads, int num_kv_heads,
+                                            int head_dim, const ScoreConfig& sc, int tp_degree, int threads,
+                                            float* shard_out) {
+    if (tp_degree <= 0 || num_heads % tp_degree != 0) throw ConfigError("bad tp_degree");
+    const int hps = num_heads / tp_degree;
+    const int group = num_heads / num_kv_heads;
+    const int64_t neff = std::min<int64_t>(sc.query_window_n, N);
+    if (q_rows < neff) throw ContractViolation("need the last n_eff query rows");
+    std::vector<ShardScores> shards(static_cast<size_t>(tp_degree));
+    std::vector<int> status(static_cast<size_t>(tp_degree), 0);
+    auto work = [&](int t) {
+        status[static_cast<size_t>(t)] = guarded([&] {
+            Matrix qm(neff, static_cast<int64_t>(hps) * head_dim);
+            Matrix km(N, static_cast<int64_t>(hps) * head_dim);
+            for (int hh = 0; hh < hps; ++hh) {
+                const int h = t * hps + hh;
+                for (int64_t j = 0; j < neff; ++j)
+                    std::memcpy(qm.row(j) + static_cast<int64_t>(hh) * head_dim,
+                                q + (q_rows - neff + j) * q_ld + static_cast<int64_t>(h) * head_dim,
+                                sizeof(float) * static_cast<size_t>(head_dim));
+                for (int64_t i = 0; i < N; ++i)
+                    std::memcpy(km.row(i) + static_cast<int64_t>(hh) * head_dim,
+                                k + i * k_ld + static_cast<int64_t>(h / group) * head_dim,
+                                sizeof(float) * static_cast<size_t>(head_dim));
+            }
+            const ImportanceScores sc_t = score_tokens_heads(qm, km, hps, 0, hps, sc);
+            shards[static_cast<size_t>(t)] = ShardScores{t, sc_t.block_scores};
+        });
+    };
+    const int nt = std::max(1, std::min(threads, tp_degree));
+    if (nt == 1) {
+        for (int t = 0; t < tp_degree; ++t) work(t);
+    } else {
+        std::vector<std::thread> pool;
+        std::atomic<int> next{0};
+        for (int w = 0; w < nt; ++w)
+            pool.emplace_back([&] { for (int t = next++; t < tp_degree; t = next++) work(t); });
+        for (auto& th : pool) th.join();
+    }
+    for (int st : status) {
+        if (st == 1) throw ConfigError("shard failed");
+        if (st != 0) throw ContractViolation("shard failed");
+    }
+    if (shard_out) {
+        size_t off = 0;
+        for (const auto& sh : shards) {
+            std::memcpy(shard_out + off, sh.block_scores.data(), sh.block_scores.size() * 4);
+            off += sh.block_scores.size();
+        }
+    }
+    if (tp_degree == 1) return shards[0].block_scores;
+    return allreduce_scores(shards);
+}
+
+int ref_sharded_allreduce_mt(const float* q, int64_t q_ld, int64_t q_rows, const float* k, int64_t k_ld,
+                             int64_t N, int num_heads, int num_kv_heads, int head_dim, const RefScoreConfig* cfg,
+                             int tp_degree, int threads, float* shard_out /* tp x nb or NULL */, float* reduced) {
+    return guarded([&] {
+        const std::vector<float> r = sharded_scores_mt(q, q_ld, q_rows, k, k_ld, N, num_heads, num_kv_heads,
+                                                       head_dim, to_cfg(cfg), tp_degree, threads, shard_out);
+        std::memcpy(reduced, r.data(), r.size() * 4);
+    });
+}
+
+// One unit of the reference's varlen layer loop -- a (request, drop layer) pair at
+// scheduler.cpp:293-332, hot path only: score (score_tokens; with tp_degree > 1 the
+// reference's TP path sharded_block_scores + allreduce_scores, propagation.cpp:163-170, its
+// shards on `threads` host threads), top_p_select (:172), apply_drop on the request's
+// TokenStream (scheduler.cpp:318), patch_metadata on its packed segment (:332).  The stream
+// and batch are built from `hidden` [N, hidden_cols] before the clock starts; *seconds is the
+// hot path's steady_clock time, *retained the rows kept.
+int ref_drop_unit(const float* q, int64_t q_ld, int64_t q_rows, const float* k, int64_t k_ld, int64_t N,
+                  int num_heads, int num_kv_heads, int head_dim, const float* hidden, int64_t hidden_cols,
+                  const RefScoreConfig* cfg, int tp_degree, int threads, int64_t* retained, double* seconds) {
+    return guarded([&] {
+        const ScoreConfig sc = to_cfg(cfg);
+        Matrix prompt(N, hidden_cols);
+        std::memcpy(prompt.data.data(), hidden, sizeof(float) * static_cast<size_t>(N * hidden_cols));
+        TokenStream stream = TokenStream::from_prompt(prompt);
+        DropHistory history;
+        history.original_length = N;
+        PackedBatch batch;
+        batch.tokens = std::move(prompt);
+        batch.cu_seqlens = {0, N};
+        batch.request_ids = {0};
+        batch.phases = {Phase::Prefill};
+        const auto t0 = std::chrono::steady_clock::now();
+        const std::vector<float> blocks = sharded_scores_mt(q, q_ld, q_rows, k, k_ld, N, num_heads, num_kv_heads,
+                                                            head_dim, sc, tp_degree, threads, nullptr);
+        std::vector<std::optional<Selection>> sels(1);
+        sels[0] = top_p_select(blocks, sc, N);
+        apply_drop(stream, *sels[0], 0, history);
+        patch_metadata(batch, sels, 0);
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+        *retained = batch.cu_seqlens.back();
+    });
+}
+
 // allreduce_scores (tp_sim.hpp:31) on explicit shards.
 int ref_allreduce_scores(const float* const* shards, const int32_t* shard_ids, int32_t tp,
                          int64_t length, float* out) {
@@ -245,6 +355,23 @@ int ref_top_p_select(const float* block_scores, int64_t num_blocks, const RefSco
         info->covered_mass = sel.covered_mass;
         info->degenerate_keep_all = sel.degenerate_keep_all ? 1 : 0;
     });
+}
+
+// top_p_select over `count` independent score vectors (vector i = scores[offsets[i] ..
+// offsets[i+1]), top_p = top_ps[i], the other knobs from *base); keep masks concatenated
+// the same way, cutoff ranks per vector.  Returns the first non-zero status.
+int ref_top_p_select_batch(const float* scores, const int64_t* offsets, const float* top_ps, int32_t count,
+                           const RefScoreConfig* base, uint8_t* keep, int64_t* cutoff_rank) {
+    for (int32_t i = 0; i < count; ++i) {
+        RefScoreConfig c = *base;
+        c.top_p = top_ps[i];
+        const int64_t b = offsets[i], n = offsets[i + 1] - offsets[i];
+        RefSelectionInfo info{};
+        const int st = ref_top_p_select(scores + b, n, &c, n, keep + b, &info);
+        if (st != 0) return st;
+        cutoff_rank[i] = info.cutoff_rank;
+    }
+    return 0;
 }
 
 // expand_mask (selection.hpp:46-47).

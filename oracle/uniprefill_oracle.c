@@ -95,6 +95,65 @@ float orc_rng_normal(uint64_t key, uint64_t i, double stddev) {
     return (float)(z * stddev);
 }
 
+void orc_rng_normal_fill(uint64_t key, uint64_t first, int64_t count, double stddev, float* out) {
+    for (int64_t j = 0; j < count; ++j) out[j] = orc_rng_normal(key, first + (uint64_t)j, stddev);
+}
+
+/* ------------------------------------------------------------------ acceptance c3 inputs */
+
+/* The vector stream of criterion_3 (acceptance_main.cpp:175-199), counter for counter. */
+int64_t orc_c3_vector(uint64_t* ctr, int trial, float* scores, float* top_p) {
+    const uint64_t key = orc_rng_key(31, 0x6333ULL);
+    const double u = orc_rng_uniform(key, (*ctr)++);
+    int64_t len = (int64_t)pow(2.0, u * 12.0);
+    if (len < 1) len = 1;
+    for (int64_t i = 0; i < len; ++i) {
+        float v;
+        switch (orc_rng_bits(key, (*ctr)++) % 5) {
+        case 0: v = 0.0f; break;
+        case 1: v = (float)(int)(orc_rng_uniform(key, (*ctr)++) * 8.0) * 0.125f; break;
+        case 2: v = 1.40129846e-45f * (float)(1 + orc_rng_bits(key, (*ctr)++) % 7); break;
+        default: v = (float)orc_rng_uniform(key, (*ctr)++); break;
+        }
+        scores[i] = v;
+    }
+    *top_p = trial % 7 == 0 ? 1.0f : (float)(0.3 + 0.7 * orc_rng_uniform(key, (*ctr)++));
+    return len;
+}
+
+static const float* g_c3_scores;
+static int cmp_c3_order(const void* a, const void* b) {  /* score desc, index asc (stable) */
+    const int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+    const float sx = g_c3_scores[x], sy = g_c3_scores[y];
+    if (sx != sy) return sx > sy ? -1 : 1;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* reference_blocks (acceptance_main.cpp:148-173) + the forced last token (:205-206). */
+void orc_c3_reference_blocks(const float* scores, int64_t len, double top_p, uint8_t* keep) {
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(len > 0 ? len : 1));
+    double total = 0.0;
+    for (int64_t i = 0; i < len; ++i) {
+        order[i] = i;
+        total += scores[i];
+        keep[i] = 0;
+    }
+    g_c3_scores = scores;
+    qsort(order, (size_t)len, sizeof(int64_t), cmp_c3_order);
+    if (total <= 0.0) {
+        for (int64_t i = 0; i < len; ++i) keep[i] = 1;
+    } else {
+        double cum = 0.0;
+        for (int64_t r = 0; r < len; ++r) {
+            keep[order[r]] = 1;
+            cum += scores[order[r]];
+            if (cum / total >= top_p) break;
+        }
+    }
+    if (len > 0) keep[len - 1] = 1;
+    free(order);
+}
+
 /* ------------------------------------------------------------------ scorer */
 
 /* block_reduce (importance.cpp:76-90): float token scores summed in double in index order,

@@ -66,6 +66,20 @@ uint64_t orc_rng_bits(uint64_t key, uint64_t i);
 double orc_rng_uniform(uint64_t key, uint64_t i);
 float orc_rng_normal(uint64_t key, uint64_t i, double stddev);
 
+/* out[j] = normal(first + j, stddev) for j < count (CounterRng::normal, rng.cpp:34-40). */
+void orc_rng_normal_fill(uint64_t key, uint64_t first, int64_t count, double stddev, float* out);
+
+/* Acceptance criterion 3's vector stream (acceptance_main.cpp:175-199): draws trial
+ * `trial`'s scores (length returned, <= 4096; scores must hold 4096 floats) and top_p from
+ * CounterRng(31, 0x6333) at the running counter *ctr, which it advances exactly as the
+ * reference loop does.  Call for trial = 0, 1, 2, ... in order with one counter. */
+int64_t orc_c3_vector(uint64_t* ctr, int trial, float* scores, float* top_p);
+
+/* reference_blocks (acceptance_main.cpp:148-173) -- the independent stable-sort +
+ * double-cumsum oracle of criterion 3 -- plus the forced one-token query window (:205-206),
+ * as a keep mask of len bytes. */
+void orc_c3_reference_blocks(const float* scores, int64_t len, double top_p, uint8_t* keep);
+
 /* Importance scorer for one request (importance.cpp:17-132).
  *   q: N x (num_heads*head_dim) fp32 row-major with row stride q_ld (floats)
  *   k: N x (num_kv_heads*head_dim) fp32 row-major with row stride k_ld

@@ -451,6 +451,7 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
     p.kv_head_offset = h->kv_head_offset;
     p.query_window_n = c->query_window_n;
     p.simt_n = L.simt_n;
+    p.max_tokens = b->max_tokens;
     p.block_size_g = G;
     p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(h->head_dim)));
     if ((e = launch_score_simt(p, b->max_tokens, num_sms(), stream)) != cudaSuccess) return UP_ERR_CUDA;
@@ -763,7 +764,8 @@ up_status up_attention_varlen(void* stream, const up_batch* b, const up_heads* h
 
 size_t up_peer_buffer_bytes(int32_t tp, int64_t capacity) {
     if (tp < 1 || tp > kPeerMaxRanks || capacity < 0) return 0;
-    return static_cast<size_t>(kPeerSlotsOffset) + static_cast<size_t>(tp) * static_cast<size_t>(capacity) * 4;
+    // two banks of [tp][capacity] fp32, alternating by epoch parity (peer.cuh)
+    return static_cast<size_t>(kPeerSlotsOffset) + 2 * static_cast<size_t>(tp) * static_cast<size_t>(capacity) * 4;
 }
 
 up_status up_peer_buffer_alloc(int32_t tp, int64_t capacity, void** buffer) {

@@ -366,6 +366,17 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
 }
 
 // Binary search: largest s in [0, R) with cu[s] <= x (cu is non-decreasing, cu[0] = 0).
+// PackedBatch::validate (scheduler.cpp:33-48) on the device, plus the capacity bound:
+// cu[0] == 0, strictly increasing, cu[R] <= max_tokens.  Every thread of the CTA calls it
+// (one __syncthreads_and); kernels that index by segment return early on false so a
+// malformed batch never reads or writes past its buffers.
+__device__ __forceinline__ bool cta_batch_valid(const int32_t* cu, int R, int64_t max_tokens) {
+    bool ok = true;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) ok = ok && cu[r + 1] > cu[r];
+    if (threadIdx.x == 0) ok = ok && cu[0] == 0 && static_cast<int64_t>(cu[R]) <= max_tokens;
+    return __syncthreads_and(ok) != 0;
+}
+
 __device__ __forceinline__ int find_segment(const int32_t* cu, int R, int64_t x) {
     int lo = 0, hi = R - 1;
     while (lo < hi) {

@@ -35,8 +35,10 @@ compact_count_kernel(const CompactParams p) {
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     constexpr int PER = kCompactTile / kCompactThreads;
     __shared__ int red[kCompactThreads / 32];
-    // clamp: a malformed batch (flagged by the scorer / select) must not read past capacity
-    const int T = static_cast<int>(min(static_cast<int64_t>(p.cu_seqlens[p.num_requests]), p.max_tokens));
+    // a malformed batch (flagged by the scorer / select) counts nothing; the index pass then
+    // emits an empty result
+    const bool valid = cta_batch_valid(p.cu_seqlens, p.num_requests, p.max_tokens);
+    const int T = valid ? p.cu_seqlens[p.num_requests] : 0;
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kCompactTile;
     int c = 0;
     if (t0 < T) {
@@ -63,8 +65,17 @@ compact_index_kernel(const CompactParams p) {
     __shared__ int red[kCompactThreads / 32];
     __shared__ int warp_tot[kCompactThreads / 32];
     __shared__ int s_offset;
-    // clamp: a malformed batch (flagged by the scorer / select) must not read past capacity
-    const int T = static_cast<int>(min(static_cast<int64_t>(p.cu_seqlens[p.num_requests]), p.max_tokens));
+    // A malformed batch (cu_seqlens not 0-based / strictly increasing / past capacity, flagged
+    // by the scorer / select) compacts to an empty result: the keep mask and the tile counts
+    // of such a batch are stale, so nothing is derived from them.
+    if (!cta_batch_valid(p.cu_seqlens, p.num_requests, p.max_tokens)) {
+        if (blockIdx.x == 0) {
+            for (int s = threadIdx.x; s <= p.num_requests; s += blockDim.x) p.cu_out[s] = 0;
+            if (threadIdx.x == 0 && p.num_out) *p.num_out = 0;
+        }
+        return;
+    }
+    const int T = p.cu_seqlens[p.num_requests];
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kCompactTile;
     if (t0 >= T) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -89,6 +89,7 @@ struct ScoreSimtParams {
     int32_t kv_head_offset;
     int32_t query_window_n;
     int32_t simt_n;  // row capacity of row_m / row_l per (head, request)
+    int64_t max_tokens;
     int32_t block_size_g;
     float scale;     // 1 / sqrt(D)
 };
@@ -187,10 +188,10 @@ struct AttnParams {
 constexpr int kPeerMaxRanks = 16;
 constexpr int kPeerMaxChunks = 256;
 constexpr int64_t kPeerFlagsOffset = 256;   // bytes: epoch[2] at 0, flags[kPeerMaxChunks] here,
-constexpr int64_t kPeerSlotsOffset = 2048;  // slots[tp][capacity] here
+constexpr int64_t kPeerSlotsOffset = 2048;  // slots[2][tp][capacity] here (bank = epoch & 1)
 struct PeerReduceParams {
     const float* partial;                 // [count] this rank's partial
-    float* peer_slots[kPeerMaxRanks];     // rank t's slots (mapped), row-major [tp][capacity]
+    float* peer_slots[kPeerMaxRanks];     // rank t's slots (mapped), row-major [2][tp][capacity]
     uint32_t* peer_flags[kPeerMaxRanks];  // rank t's flags (mapped)
     const float* slots;                   // own slots
     const uint32_t* flags;                // own flags

@@ -18,12 +18,14 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const PeerReducePar
     const int64_t g1 = g0 + p.chunk < p.count ? g0 + p.chunk : p.count;
     __shared__ uint32_t s_epoch;
     if (threadIdx.x == 0) s_epoch = peer_epoch(p);
+    __syncthreads();
+    const int64_t row = peer_row_offset(p, s_epoch, p.rank);
     for (int t = 0; t < p.tp; ++t) {
-        float* dst = p.peer_slots[t] + static_cast<int64_t>(p.rank) * p.capacity;
+        float* dst = p.peer_slots[t] + row;
         for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x) dst[g] = p.partial[g];
     }
     peer_publish_and_wait(p, c, s_epoch);
-    peer_sum_chunk(p, g0, g1);
+    peer_sum_chunk(p, g0, g1, s_epoch);
     pdl_trigger();
     peer_epoch_advance(p);
 }

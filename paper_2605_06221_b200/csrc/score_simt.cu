@@ -28,6 +28,7 @@ __device__ __forceinline__ int kv_of(const ScoreSimtParams& p, int h) {
 __global__ void simt_row_stats_kernel(const ScoreSimtParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
+    if (!cta_batch_valid(p.cu_seqlens, p.num_requests, p.max_tokens)) return;  // flagged by the plan
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.x * (blockDim.x >> 5) + warp;
     const int r = blockIdx.y / p.num_heads;
@@ -67,6 +68,7 @@ __global__ void simt_row_stats_kernel(const ScoreSimtParams p) {
 __global__ void simt_token_kernel(const ScoreSimtParams p, int64_t total_tokens_cap) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
+    if (!cta_batch_valid(p.cu_seqlens, p.num_requests, p.max_tokens)) return;  // flagged by the plan
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
     const int T = p.cu_seqlens[p.num_requests];

@@ -418,8 +418,9 @@ block_combine_kernel(const BlockCombineParams p) {
 // tp_sim.cpp:43-47) to block_scores.  Fixed grid peer_grid() on every rank.
 struct StorePeers {
     const PeerReduceParams* pr;
+    int64_t row;  // peer_row_offset(epoch, rank): this launch's bank
     __device__ __forceinline__ void operator()(int gb, float v) const {
-        for (int t = 0; t < pr->tp; ++t) pr->peer_slots[t][static_cast<int64_t>(pr->rank) * pr->capacity + gb] = v;
+        for (int t = 0; t < pr->tp; ++t) pr->peer_slots[t][row + gb] = v;
     }
 };
 
@@ -428,6 +429,7 @@ block_combine_peer_kernel(const __grid_constant__ BlockCombineParams p, const __
     pdl_wait();
     __shared__ uint32_t s_epoch;
     if (threadIdx.x == 0) s_epoch = peer_epoch(pr);
+    __syncthreads();
     int64_t total = p.cu_blocks[p.num_requests];
     if (total > pr.capacity) {  // more blocks than the exchange buffers hold
         if (threadIdx.x == 0) raise_error(pr.err, kErrTooManyBlocks);
@@ -435,9 +437,10 @@ block_combine_peer_kernel(const __grid_constant__ BlockCombineParams p, const __
     }
     const int64_t chunk = (total + gridDim.x - 1) / gridDim.x;
     const int64_t c0 = min(static_cast<int64_t>(blockIdx.x) * chunk, total), c1 = min(c0 + chunk, total);
-    block_combine_run(p, c0 + (threadIdx.x >> 5), blockDim.x >> 5, c1, StorePeers{&pr});
+    block_combine_run(p, c0 + (threadIdx.x >> 5), blockDim.x >> 5, c1,
+                      StorePeers{&pr, peer_row_offset(pr, s_epoch, pr.rank)});
     peer_publish_and_wait(pr, blockIdx.x, s_epoch);
-    peer_sum_chunk(pr, c0, c1);
+    peer_sum_chunk(pr, c0, c1, s_epoch);
     pdl_trigger();
     peer_epoch_advance(pr);
 }
@@ -467,11 +470,13 @@ __global__ void blocks_plan_kernel(const int32_t* __restrict__ cu, int R, int64_
         if (r < R) cu_blocks[r + 1] = carry + y;
         carry += __shfl_sync(0xffffffffu, y, 31);
     }
-    ok = __all_sync(0xffffffffu, ok);
+    ok = __all_sync(0xffffffffu, ok) && cu[R] <= max_tokens;
     if (lane == 0) {
         cu_blocks[0] = 0;
-        if (!ok || cu[R] > max_tokens) raise_error(err, kErrBadSeqlens);
+        if (!ok) raise_error(err, kErrBadSeqlens);
     }
+    if (!ok)  // malformed batch: no blocks, so nothing downstream indexes past its buffers
+        for (int r = lane; r <= R; r += 32) cu_blocks[r] = 0;
 }
 
 // ---------------------------------------------------------------- host launchers

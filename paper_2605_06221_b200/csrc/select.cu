@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(THREADS)
 select_radix_kernel(const SelectParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
-    if (p.cu_seqlens[gridDim.x] > p.max_tokens) {  // malformed batch (grid = R): no write past capacity
+    if (!cta_batch_valid(p.cu_seqlens, gridDim.x, p.max_tokens)) {  // malformed batch (grid = R)
         if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
         return;
     }
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kSelThreads)
 select_kernel(const SelectParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
-    if (p.cu_seqlens[gridDim.x] > p.max_tokens) {  // malformed batch (grid = R): no write past capacity
+    if (!cta_batch_valid(p.cu_seqlens, gridDim.x, p.max_tokens)) {  // malformed batch (grid = R)
         if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
         return;
     }
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(256)
 expand_kernel(const SelectParams p, int R) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
-    if (p.cu_seqlens[R] > p.max_tokens) {  // malformed batch: no write past capacity
+    if (!cta_batch_valid(p.cu_seqlens, R, p.max_tokens)) {  // malformed batch: nothing written
         if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(p.err, kErrBadSeqlens);
         return;
     }

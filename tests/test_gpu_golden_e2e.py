@@ -400,3 +400,49 @@ def test_batch_past_capacity_is_a_contract_violation(up):
         ws.device_status()
     torch.cuda.synchronize()  # the context is still healthy (no out-of-bounds fault)
     assert int(res.num_out.item()) <= cap
+
+
+def test_malformed_batch_after_a_good_one_compacts_to_nothing(up):
+    """A well-formed short batch, then malformed batches on the SAME DropLayer (capacity of
+    five 1024-row tiles, so stale per-tile counts and keep bytes from the first call are
+    present): past capacity, cu[0] != 0, non-increasing.  Each raises the sticky
+    ContractViolation (PackedBatch::validate, scheduler.cpp:33-48) and compacts to an empty
+    result (cu_seqlens_out all zero, num_out 0) instead of deriving rows from stale state."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    Hq, Hkv, D = 8, 2, 128
+    cap = 5000
+    sb = make_batch([2900, 2100], Hq, Hkv, D, 32, regime="planted", seed=31)
+    layer = up.DropLayer(up.ScoreConfig(), up.HeadLayout(Hq, Hkv, D), cap, 2,
+                         [(32,), (Hkv, D), ()], [torch.bfloat16, torch.bfloat16, torch.int64])
+    planes = [sb.hidden, sb.k, sb.positions]
+    short = torch.tensor([0, 1000, 1800], dtype=torch.int32, device="cuda")
+    res = layer(sb.q, sb.k, short, planes)
+    layer.check()
+    assert 0 < int(res.num_out.item()) <= 1800
+    for bad in ([0, 2900, 6000], [5, 2900, 5000], [0, 2900, 2900], [0, 3000, 2000]):
+        res = layer(sb.q, sb.k, torch.tensor(bad, dtype=torch.int32, device="cuda"), planes)
+        with pytest.raises(up.ContractViolation):
+            layer.check()
+        assert int(res.num_out.item()) == 0, bad
+        assert res.cu_seqlens.tolist() == [0, 0, 0], bad
+    res = layer(sb.q, sb.k, short, planes)  # and the layer still works afterwards
+    layer.check()
+    assert 0 < int(res.num_out.item()) <= 1800
+
+
+@pytest.mark.parametrize("shape", ["token_scores", "simt_head_dim"])
+def test_malformed_batch_on_the_simt_scorer(up, shape):
+    """The SIMT scorer (per-token scores requested, or a head dim off the tensor-core
+    envelope) under a batch ending past max_tokens: ContractViolation, cu_blocks zeroed, no
+    out-of-bounds access (the context stays healthy)."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    Hq, Hkv, D = (8, 2, 128) if shape == "token_scores" else (4, 2, 96)
+    sb = make_batch([700, 500], Hq, Hkv, D, 16, regime="planted", seed=4)
+    cap = 1100
+    ws = up.Workspace("cuda")
+    out = up.score_blocks_varlen(sb.q[:cap], sb.k[:cap], sb.cu_seqlens, up.ScoreConfig(), up.HeadLayout(Hq, Hkv, D),
+                                 want_token_scores=shape == "token_scores", max_tokens=cap, workspace=ws)
+    with pytest.raises(up.ContractViolation):
+        ws.device_status()
+    torch.cuda.synchronize()
+    assert out.cu_blocks.tolist() == [0, 0, 0]

@@ -72,6 +72,39 @@ def _worker(rank, tp, port, q):
             if not np.array_equal(out.cpu().numpy().view(np.uint32), _expected(tp, step, n).view(np.uint32)):
                 bad.append(f"graph replay {step}")
         red.check()
+        # back-to-back stress, no host sync between calls (the write-after-read window of a
+        # single-bank exchange): STRESS calls with different data and counts, eager and then
+        # captured in one graph, every output checked bitwise afterwards.
+        STRESS = 128
+        ns = [1 + (37 * i) % 6000 for i in range(STRESS)]
+        parts = [_partial(rank, 100 + i, n).cuda() for i, n in enumerate(ns)]
+        outs = [torch.full_like(pt, float("nan")) for pt in parts]
+        want = [_expected(tp, 100 + i, n).view(np.uint32) for i, n in enumerate(ns)]
+        torch.cuda.synchronize()
+        dist.barrier()
+        with torch.cuda.stream(s):
+            for pt, o in zip(parts, outs):
+                red(pt, o)
+        torch.cuda.synchronize()
+        red.check()
+        bad += [f"stress eager call {i}" for i in range(STRESS)
+                if not np.array_equal(outs[i].cpu().numpy().view(np.uint32), want[i])]
+        for o in outs:
+            o.fill_(float("nan"))
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2, stream=s):
+                for pt, o in zip(parts[:64], outs[:64]):
+                    red(pt, o)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for rep in range(3):
+            g2.replay()  # replays back to back, no sync in between
+        torch.cuda.synchronize()
+        red.check()
+        bad += [f"stress graph call {i}" for i in range(64)
+                if not np.array_equal(outs[i].cpu().numpy().view(np.uint32), want[i])]
         red.close()
         dist.destroy_process_group()
         q.put((rank, bad))

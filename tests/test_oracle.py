@@ -242,3 +242,39 @@ def test_port_slot_for_and_seqused_match_reference(port, ref):
     for layer in range(12):
         assert port.decode_seqused(100, 7, [2, 5, 9], [80, 50, 20], layer) == \
             ref.decode_seqused(100, 7, [2, 5, 9], [80, 50, 20], layer)
+
+
+# ----------------------------------------------------------------------- acceptance c3 / c8
+def test_acceptance_c3_full_on_the_reference(port, ref):
+    """Acceptance criterion 3 in full (acceptance_main.cpp:175-217): the 100,000 vectors of
+    its CounterRng(31, 0x6333) stream, the reference's top_p_select vs the independent
+    sort-and-cumsum oracle reference_blocks (+ the forced window token), exact set equality.
+    Pins the vector generator the GPU test (test_gpu_acceptance.py) replays."""
+    s, off, ps = port.c3_vectors(100000)
+    assert off.size == 100001
+    assert int(np.sum(ps == 1.0)) >= 100000 // 7  # trial % 7 == 0 -> p = 1
+    keep, _ = ref.top_p_select_batch(s, off, ps, **cfg(1, 1, 0, 0.9))
+    bad = [t for t in range(100000)
+           if not np.array_equal(keep[off[t]:off[t + 1]], port.c3_reference_blocks(s[off[t]:off[t + 1]], ps[t]))]
+    assert bad == []
+
+
+def test_acceptance_c8_inputs_on_the_reference(port, ref):
+    """Acceptance criterion 8's inputs (acceptance_main.cpp:445-478) regenerated through the
+    port's CounterRng: the reference gives identical selections for T in {1,2,4,8} on all 100
+    (the criterion itself), and the threaded sharded scorer used for BASELINE-size parity is
+    bitwise the sequential one."""
+    c = cfg(8, 8, 8, 0.9)
+    for trial in range(100):
+        n = 16 + port.rng_bits(trial, 0x6338, 0) % 497
+        q = port.rng_normal_array(trial, 0x64617461, n * 64, 0.7).reshape(n, 64)
+        k = port.rng_normal_array(trial, 0x64617461, n * 64, 0.7, first=1000000).reshape(n, 64)
+        base = None
+        for tp in (1, 2, 4, 8):
+            shards, red = ref.sharded_allreduce(q, k, 8, 8, tp, **c)
+            s2, r2 = ref.sharded_allreduce_mt(q[-8:], k, 8, 8, tp, 4, **c)
+            assert np.array_equal(shards, s2) and np.array_equal(red, r2)
+            sel = ref.top_p_select(red, n, **c)
+            if base is None:
+                base = sel
+            assert np.array_equal(sel.keep_mask, base.keep_mask) and sel.cutoff_rank == base.cutoff_rank, trial
