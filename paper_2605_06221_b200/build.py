@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libuniprefill_b200.so")
-SOURCES = ["capi.cu", "score_tc.cu", "score_tcw.cu", "score_simt.cu", "select.cu", "compact.cu", "meta.cu", "attention.cu", "peer.cu"]
+SOURCES = ["capi.cu", "score_tc.cu", "score_tcw.cu", "score_tc2.cu", "score_simt.cu", "select.cu", "compact.cu", "meta.cu", "attention.cu", "peer.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -25,6 +26,12 @@ cudaError_t launch_score_tcw(int D, int HPC, const CUtensorMap& qm, const CUtens
                              const ScoreTcParams& p, int grid, cudaStream_t stream);
 bool tcw_supported(int D, int HPC, int G, int R);
 int tcw_stage_keys(int D);
+bool tc2_enabled();
+bool tc2_supported(int D, int HPC, int G, int R);
+int tc2_stage_keys();
+int tc2_grid(int num_sms);
+cudaError_t launch_score_tc2(const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p, int grid,
+                             cudaStream_t stream);
 cudaError_t launch_blocks_plan(const int32_t* cu, int R, int64_t max_tokens, int G, int32_t* cu_blocks,
                                uint32_t* err, cudaStream_t stream);
 struct BlockCombineParams;
@@ -119,7 +126,7 @@ Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c
     L.max_blocks = T / G + R + 1;
     // Σ_r ceil(N_r / unit) * num_hgroups * HPC * npar <= Hq * npar * (T / 128 + R): bounds
     // the item statistics rows (npar = 2 for the two-warpgroups-per-head scorer).
-    const int64_t npar = h ? 2 : 1;
+    const int64_t npar = h ? (tc2_enabled() ? 4 : 2) : 1;  // score_tc2 keeps four statistics rows per head
     L.max_units = (H > 0 ? H : 1) * npar * (T / kTileKeys + R + 1);
     const int64_t n = c->query_window_n < T ? c->query_window_n : T;
     L.simt_n = static_cast<int32_t>(n > 0 ? n : 1);
@@ -217,10 +224,12 @@ int pick_hpc(const up_heads* h, int max_hpc, int shard_heads) {
     return hpc < 1 ? 1 : hpc;
 }
 
-// Which tensor-core scorer serves this shape: the four-warpgroup kernel (score_tcw.cu,
-// wide = true) when it applies, else score_tc.cu.  npar = epilogue warpgroups per head.
+// Which tensor-core scorer serves this shape: the CTA-pair kernel (score_tc2.cu, pair =
+// true) for four q-heads per kv-head at D = 128, else the four-warpgroup kernel
+// (score_tcw.cu, wide = true) when it applies, else score_tc.cu.  npar = statistics rows
+// (epilogue warpgroups) per head.
 struct TcPlan {
-    bool wide;
+    bool wide, pair;
     int hpc, npar;
 };
 
@@ -232,9 +241,10 @@ TcPlan tc_plan(const up_batch* b, const up_heads* h, const up_score_config* c, i
         return s ? std::atoi(s) : 0;
     }();
     t.hpc = pick_hpc(h, max_hpc_env > 0 ? max_hpc_env : (D == 256 ? 2 : 4), shard_heads);
-    t.wide = (t.hpc == 4 || t.hpc == 2) && tcw_supported(D, t.hpc, c->block_size_g, b->num_requests);
-    if (!t.wide) t.hpc = pick_hpc(h, tc_max_hpc(D), shard_heads);
-    t.npar = t.wide ? 4 / t.hpc : 1;
+    t.pair = tc2_supported(D, t.hpc, c->block_size_g, b->num_requests);
+    t.wide = !t.pair && (t.hpc == 4 || t.hpc == 2) && tcw_supported(D, t.hpc, c->block_size_g, b->num_requests);
+    if (!t.wide && !t.pair) t.hpc = pick_hpc(h, tc_max_hpc(D), shard_heads);
+    t.npar = t.pair ? 4 : (t.wide ? 4 / t.hpc : 1);
     return t;
 }
 
@@ -320,7 +330,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     CUtensorMap qm, km;
     if (!make_map(&qm, q, b->max_tokens, static_cast<int64_t>(h->num_q_heads) * D, h->q_row_stride, 128) ||
         !make_map(&km, k, b->max_tokens, static_cast<int64_t>(h->num_kv_heads) * D, h->k_row_stride,
-                  plan.wide ? tcw_stage_keys(D) : 128))
+                  plan.pair ? tc2_stage_keys() : (plan.wide ? tcw_stage_keys(D) : 128)))
         return UP_ERR_CUDA;
     ScoreTcParams p{};
     p.q = static_cast<const __nv_bfloat16*>(q);
@@ -350,10 +360,15 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
         const char* s = std::getenv("UP_SCORE_GRID");
         return s ? std::atoi(s) : 0;
     }();
-    const int grid = grid_override > 0 ? grid_override : num_sms();
+    const int grid = plan.pair ? tc2_grid(num_sms()) : (grid_override > 0 ? grid_override : num_sms());
+    // work ranges: one per CTA, or one per CTA pair
+    const int ranges = plan.pair ? grid / 2 : grid;
     p.dbg = score_debug_buffer();
-    cudaError_t e = plan.wide ? launch_score_tcw(D, hpc, qm, km, p, grid, stream)
-                              : launch_score_tc(D, hpc, qm, km, p, grid, stream);
+    if (std::getenv("UP_SCORE_VERBOSE"))
+        fprintf(stderr, "scorer: pair=%d wide=%d hpc=%d npar=%d grid=%d\n", plan.pair, plan.wide, hpc, plan.npar, grid);
+    cudaError_t e = plan.pair ? launch_score_tc2(qm, km, p, grid, stream)
+                    : plan.wide ? launch_score_tcw(D, hpc, qm, km, p, grid, stream)
+                                : launch_score_tc(D, hpc, qm, km, p, grid, stream);
     if (e != cudaSuccess) return e == cudaErrorInvalidValue ? UP_ERR_UNSUPPORTED : UP_ERR_CUDA;
     PairWeightsParams wp{};
     wp.cu_seqlens = b->cu_seqlens;
@@ -366,12 +381,12 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     wp.num_hgroups = nhg;
     wp.hpc = hpc;
     wp.npar = plan.npar;
-    wp.score_grid = grid;
+    wp.score_grid = ranges;
     wp.query_window_n = c->query_window_n;
     const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
     const int wgrid = static_cast<int>(wtasks < num_sms() * 8 ? wtasks : num_sms() * 8);
     // CTAs one (request, head-group) pair spans, for equal-length requests
-    const int items_est = grid / (R * nhg > 0 ? R * nhg : 1) + 2;
+    const int items_est = ranges / (R * nhg > 0 ? R * nhg : 1) + 2;
     if ((e = launch_pair_weights(wp, wgrid, items_est, stream)) != cudaSuccess) return UP_ERR_CUDA;
     BlockCombineParams bp{};
     bp.cu_seqlens = b->cu_seqlens;
@@ -389,6 +404,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     bp.num_shards = tp;
     bp.hpc = hpc;
     bp.npar = plan.npar;
+    bp.par_shift = plan.pair ? 7 : 6;
     bp.block_size_g = G;
     bp.unit_keys = p.unit_keys;
     if (peer != nullptr) {  // fused with the TP all-reduce over peer memory

@@ -128,6 +128,24 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
         : "memory");
 }
 
+// Variants on a precomputed shared::cta address (hot loops: no per-call address math).
+__device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t addr) {
+    asm volatile(
+        "{\n\t.reg .b64 st;\n\t"
+        "mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(addr)
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     const uint32_t addr = smem_u32(bar);
     asm volatile(

@@ -65,6 +65,7 @@ struct BlockCombineParams {
     int32_t num_shards;       // 1, or T contiguous head shards summed in ascending order
     int32_t hpc;
     int32_t npar;             // epilogue warpgroups per head (score_tcw): stats row hh*npar+par
+    int32_t par_shift;        // par = (block start key >> par_shift) % npar: 6 (score_tcw), 7 (score_tc2)
     int32_t block_size_g;
     int32_t unit_keys;
 };

@@ -84,6 +84,32 @@ __device__ __forceinline__ float group_sum_pk(const uint32_t* v, uint64_t sc2, u
     return lo_f(a) + hi_f(a);
 }
 
+// Packed partial Σ 2^(v_k * sc - m) over 2*PAIRS TMEM values (the last NP pairs on the FMA
+// pipe): lo/hi halves of the returned pair are the two accumulation chains.
+template <int PAIRS, int NP>
+__device__ __forceinline__ uint64_t chunk_sum_pk(const uint32_t* v, uint64_t sc2, uint64_t m2) {
+    uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+    for (int i = 0; i < PAIRS; ++i) {
+        const uint64_t x = fma2(static_cast<uint64_t>(v[2 * i]) | (static_cast<uint64_t>(v[2 * i + 1]) << 32), sc2, m2);
+        const uint64_t e = i < PAIRS - NP ? pk(ex2_approx(lo_f(x)), ex2_approx(hi_f(x))) : exp2_poly2(x);
+        if (i == 0) a0 = e;
+        else if (i == 1) a1 = e;
+        else if (i & 1) a1 = add2(a1, e);
+        else a0 = add2(a0, e);
+    }
+    return add2(a0, a1);
+}
+
+// Makes `v` a fresh definition at this point of the program: code using it cannot be
+// scheduled above this statement (used to keep a TMEM load of the next chunk in flight
+// while the current chunk is summed).
+__device__ __forceinline__ void pin16(uint32_t (&v)[16]) {
+    asm volatile("" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+                 "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]),
+                 "+r"(v[14]), "+r"(v[15]));
+}
+
 // Cold path of a rebase: rescale the partials this thread already wrote for the item.
 static __device__ __noinline__ void rescale_rows(float* prow, int g0, int g1, float f) {
 #pragma unroll 4

@@ -59,29 +59,30 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
             if (k > 0 && b == range_begin(P, c_first + k + 1)) return -1;
             return b > seg_start ? b : seg_start;
         };
-        // statistics rows of head hh: (sid * hpc + hh) * npar + par, par < npar (the
-        // parity warpgroups of score_tcw keep separate running (m, l) for one head).
+        // statistics rows of head hh: (sid * hpc + hh) * npar + par, par < npar <= 4 (the
+        // parity warpgroups of score_tcw / score_tc2 keep separate running (m, l) for one
+        // head).
         // Two items per warp iteration: their loads are issued before the merges.
         float M = -INFINITY, L = 0.f;
         for (int k = warp; warp < nwarps && k < n_items; k += 2 * nwarps) {
-            float mc[4], lc[4];
+            float mc[8], lc[8];
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
                 const int kk = k + x * nwarps;
                 const int64_t sid = kk < n_items ? sid_of(kk) : -1;
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    mc[x * 2 + q] = -INFINITY;
-                    lc[x * 2 + q] = 0.f;
+                for (int q = 0; q < 4; ++q) {
+                    mc[x * 4 + q] = -INFINITY;
+                    lc[x * 4 + q] = 0.f;
                     if (sid >= 0 && q < npar) {
                         const int64_t xx = ((sid * hpc + hh) * npar + q) * kRows + j;
-                        mc[x * 2 + q] = __ldcg(&p.stat_m[xx]);
-                        lc[x * 2 + q] = __ldcg(&p.stat_l[xx]);
+                        mc[x * 4 + q] = __ldcg(&p.stat_m[xx]);
+                        lc[x * 4 + q] = __ldcg(&p.stat_l[xx]);
                     }
                 }
             }
 #pragma unroll
-            for (int y = 0; y < 4; ++y) lse_merge(M, L, mc[y], lc[y]);
+            for (int y = 0; y < 8; ++y) lse_merge(M, L, mc[y], lc[y]);
         }
         if (warp < nwarps) {
             sM[warp][lane] = M;
@@ -146,8 +147,9 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
         const int size = min(p.block_size_g, N - g * p.block_size_g);
         const int u = (g * p.block_size_g) / p.unit_keys;
         const int64_t pair0 = static_cast<int64_t>(p.cu_units[r]) * nhg;
-        // statistics row of head hh: hh * npar + (parity of the block's 64-key subtile)
-        const int par = p.npar > 1 ? ((g * p.block_size_g) >> 6) % p.npar : 0;
+        // statistics row of head hh: hh * npar + (parity of the block's subtile: 64 keys in
+        // score_tcw, 128 in score_tc2)
+        const int par = p.npar > 1 ? ((g * p.block_size_g) >> p.par_shift) % p.npar : 0;
         const int hpcv = p.hpc * p.npar;
         if (T > 1) {
             // Sharded: every head's dot product is reduced across the warp and added, in

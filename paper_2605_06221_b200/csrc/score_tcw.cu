@@ -44,6 +44,9 @@ namespace up {
 #ifndef UP_TCW_LD_PIPE
 #define UP_TCW_LD_PIPE 1
 #endif
+#ifndef UP_TCW_LEAN
+#define UP_TCW_LEAN 1
+#endif
 
 template <int D, int HPC>
 struct TcwCfg {
@@ -291,6 +294,10 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         const int j = quarter * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const float sc = p.scale_log2;
+        // Lean path (HPC = 4, G = 64: every 128-key subtile is exactly two blocks): barrier
+        // addresses held in registers, static block bookkeeping, no per-group branches.
+        const uint32_t tfull_addr = smem_u32(t_full), tempty_addr = smem_u32(t_empty);
+        const bool lean = NPAR == 1 && C::NG == 4 && G == 64 && UP_TCW_DIAG == 0 && UP_TCW_LEAN;
         uint32_t u = 0;
         uint32_t qiter = 0;
         for (int64_t pos = my_begin; pos < my_end;) {
@@ -345,6 +352,43 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 if (NPAR > 1 && (t % NPAR) != par) continue;  // the other warpgroup's subtile
                 const int cbase = key0 + t * C::SUBN;
                 const uint32_t reg = hh * NB + u % NB;
+                if constexpr (NPAR == 1 && C::NG == 4) {
+                    // Lean fast path: the whole subtile inside the segment and left of every
+                    // row's causal limit (warp-uniform), blocks [blk, blk+2) complete here.
+                    if (lean && cbase + C::SUBN <= N - neff + 1) {
+                        mbar_wait_u32(tfull_addr + reg * 8, (u / NB) & 1);
+                        tc_fence_after();
+                        const uint32_t taddr = tmem_base + lane_base + C::Q_COLS + reg * C::SUBN;
+                        uint32_t va[32], vb[32];
+                        tmem_ld32(taddr, va);
+                        tmem_ld_wait();
+                        tmem_ld32(taddr + 32, vb);
+                        const float g0 = group_sum_pk<C::NP>(va, pk(sc, sc), pk(-m, -m));
+                        tmem_ld_wait();
+                        tmem_ld32(taddr + 64, va);
+                        const float g1 = group_sum_pk<C::NP>(vb, pk(sc, sc), pk(-m, -m));
+                        tmem_ld_wait();
+                        tmem_ld32(taddr + 96, vb);
+                        const float g2 = group_sum_pk<C::NP>(va, pk(sc, sc), pk(-m, -m));
+                        tmem_ld_wait();
+                        const float g3 = group_sum_pk<C::NP>(vb, pk(sc, sc), pk(-m, -m));
+                        const float b0 = g0 + g1, b1 = g2 + g3;
+                        // rows past n_eff carry no statistics: never a reason to leave the lean path
+                        if (__all_sync(0xffffffffu, !row_valid || b0 + b1 <= 0x1p40f)) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_u32(tempty_addr + reg * 8);
+                            Prow[static_cast<int64_t>(blk) * kRows] = row_valid ? b0 : 0.f;
+                            Prow[static_cast<int64_t>(blk + 1) * kRows] = row_valid ? b1 : 0.f;
+                            l += b0;
+                            l += b1;
+                            blk += 2;
+                            continue;
+                        }
+                        // some row must rebase: the general path below redoes this subtile
+                        // (its wait returns at once, the region is still held)
+                    }
+                }
                 mbar_wait(&t_full[reg], (u / NB) & 1);
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + lane_base + C::Q_COLS + reg * C::SUBN;

@@ -227,3 +227,43 @@ def test_scores_ignore_garbage_past_the_batch(up, Hq, Hkv, D, lengths):
     a, b = clean.block_scores[:nb], dirty.block_scores[:nb]
     assert bool(torch.isfinite(b).all())
     assert torch.equal(a, b)
+
+
+_TC2_CHILD = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import oracle, paper_2605_06221_b200 as up
+from paper_2605_06221_b200.synthetic import make_batch
+port = oracle.port()
+bad = []
+for Hq, Hkv, lengths, n, G in [(8, 2, [1000], 128, 64), (8, 2, [700, 129, 64, 2000], 128, 64),
+                               (8, 2, [1024, 513], 64, 32), (8, 2, [2048, 300], 128, 128), (4, 1, [300, 1], 128, 64)]:
+    cfg = dict(query_window_n=n, block_size_g=G, sink_count_a=128, top_p=0.99)
+    sb = make_batch(lengths, Hq, Hkv, 128, 64, regime="planted", block_size_g=G, seed=sum(lengths) + 5)
+    res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), up.HeadLayout(Hq, Hkv, 128), check=True)
+    cu, cub, bs = sb.cu_seqlens.cpu().numpy(), res.cu_blocks.cpu().numpy(), res.block_scores.cpu().numpy().astype(np.float64)
+    for r in range(len(lengths)):
+        s, e = int(cu[r]), int(cu[r + 1])
+        _, want, _ = port.score_tokens(sb.q[s:e].float().reshape(e - s, -1).cpu().numpy(),
+                                       sb.k[s:e].float().reshape(e - s, -1).cpu().numpy(), Hq, Hkv, **cfg)
+        got = bs[cub[r]:cub[r + 1]]
+        atol = 1e-6 * max(want.sum(), 1e-30) / len(want)
+        if len(got) != len(want) or (np.abs(got - want) > 1e-3 * np.abs(want) + atol).any():
+            bad.append((Hq, Hkv, lengths, G, r))
+print("TC2_BAD", bad)
+'''
+
+
+def test_cta_pair_scorer_opt_in_matches_oracle(up):
+    """score_tc2 (tcgen05.mma.cta_group::2, M = 256 over a CTA pair; opt-in with UP_TC2=1,
+    see DESIGN.md 3(a)) in a child process: block scores vs the oracle within rtol 1e-3
+    for GQA-4 at D = 128, G in {32, 64, 128}, varlen and single-token segments."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _TC2_CHILD, root], capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, UP_TC2="1", UP_SCORE_VERBOSE="1"))
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "pair=1" in out.stderr  # the CTA-pair kernel actually ran
+    assert "TC2_BAD []" in out.stdout, out.stdout[-2000:]
