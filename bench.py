@@ -53,7 +53,33 @@ CONFIGS = {
     "c4": ("gemma3-12b", [65536] * 16, 8, dict(SPEC, top_p=0.98), "dp"),
     # 64-request stream, N_r log-uniform in [4K, 128K] (seed 5), LPT-sharded over the ranks
     "c5": ("llama3.1-8b", "loguniform:64:4096:131072:5", 32, SPEC, "dp-split"),
+    # one TP=8 rank's slice of c3 (2 q-heads, 1 kv-head, 128K) through the fused peer path
+    "c3-rank": ("qwen3-next-80b-a3b", [131072], 12, SPEC, "tp-rank"),
+    # envelope: c5's 64 prefills, each followed by 7 single-token decode segments (drop
+    # disabled, passed through) -- 512 segments per launch
+    "c5-mixed": ("llama3.1-8b", "mixed:64:4096:131072:5:7", 32, SPEC, "dp"),
 }
+# Block structure of each config (the reference's layer pattern, config.hpp:40 /
+# model.hpp:48-50): a block is one full-attention drop layer followed by the sublayers that
+# consume its compacted stream, and the block boundary reconstitutes the full stream
+# (accelerated_prefill, propagation.cpp:258-283; Engine::run_batch, scheduler.cpp:283-361).
+#   downstream: (kind, count) of the non-drop sublayers of a block -- their compute is the
+#   model's, outside this path; "swa" layers own a paged KV cache, so the block recomputes
+#   their Eq. 16 slot mapping from the compacted stream (up_slot_mapping);
+#   reconstitute: scatter the block's retained rows back over the pre-drop hidden states at
+#   the boundary (up_scatter_rows).  --stack S stacks S cascaded full-attention drop layers
+#   per block (the reference's pure-full archetype, test_propagation.cpp:24-38): drop s+1
+#   scores the stream drop s compacted, under drop s's device-resident cu_seqlens_out.
+BLOCKS = {
+    "c1": dict(downstream=("ffn", 0), reconstitute=False),   # one layer, no block boundary
+    "c2": dict(downstream=("ffn", 0), reconstitute=True),    # LLaMA layer = [attention(drop), FFN]
+    "c3": dict(downstream=("linear", 3), reconstitute=True),  # Qwen3-Next 3:1 = [full(drop), linear x3]
+    "c3-rank": dict(downstream=("linear", 3), reconstitute=True),
+    "c4": dict(downstream=("swa", 5), reconstitute=True),    # Gemma-3 5:1 = [full(drop), SWA x5]
+    "c5": dict(downstream=("ffn", 0), reconstitute=True),
+    "c5-mixed": dict(downstream=("ffn", 0), reconstitute=True),
+}
+KV_PAGE = 16  # paged-KV block size for the SWA layers' slot mapping (kvcache.hpp:36 default)
 WORKLOAD_NAME = {
     "c1": "llama3.1-8b layer shape, 1x4096 tokens, 1 drop layer, score+select+compact",
     "c2": "llama3.1-8b layer shape, varlen 4x32768 tokens, 32 full-attn drop layers, score+select+compact",
@@ -63,15 +89,32 @@ WORKLOAD_NAME = {
           "score+select+compact",
     "c5": "llama3.1-8b layer shape, 64-request varlen stream (4K-128K log-uniform), 32 drop layers, "
           "LPT request-sharded, score+select+compact",
+    "c3-rank": "qwen3-next-80b-a3b full-attn layer shape, ONE TP=8 rank's slice (2 q-heads, 1 kv-head) of "
+               "1x131072 tokens, 12 drop layers: fused scorer+peer reduce (tp=1 group), select, compact",
+    "c5-mixed": "llama3.1-8b layer shape, c5's 64 prefill requests each followed by 7 single-token decode "
+                "segments (drop disabled): 512 segments, 32 drop layers, score+select+compact",
 }
 
 
 def config_lengths(spec):
     if isinstance(spec, str):
-        _, count, lo, hi, seed = spec.split(":")
-        from paper_2605_06221_b200.synthetic import loguniform_lengths
-        return loguniform_lengths(int(count), int(lo), int(hi), int(seed))
+        kind, count, lo, hi, seed = spec.split(":")[:5]
+        # the restatement below imports nothing of the product package (the reference arm
+        # calls this too and must not map the repo's library)
+        pre = loguniform_lengths_ref(int(count), int(lo), int(hi), int(seed))
+        if kind == "mixed":  # each prefill followed by `dec` single-token decode segments
+            dec = int(spec.split(":")[5])
+            return [x for n in pre for x in [n] + [1] * dec]
+        return pre
     return list(spec)
+
+
+def config_drop_enabled(spec):
+    """Per-segment drop_enabled flags (None = every segment is a prefill)."""
+    if isinstance(spec, str) and spec.startswith("mixed:"):
+        dec = int(spec.split(":")[5])
+        return [x for _ in range(int(spec.split(":")[1])) for x in [1] + [0] * dec]
+    return None
 
 
 def parse():
@@ -88,6 +131,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--profile-stages", action="store_true", default=True)
+    ap.add_argument("--stack", type=int, default=1,
+                    help="cascaded full-attention drop layers per block (drop s+1 scores drop s's compacted stream)")
     return ap.parse_args()
 
 
@@ -315,7 +360,7 @@ def run_reference_arm(args):
         return
     model, lspec, layers, cfg, _ = CONFIGS[args.config]
     if isinstance(lspec, str):
-        _, count, lo, hi, seed = lspec.split(":")
+        _, count, lo, hi, seed = lspec.split(":")[:5]  # prefills (decode segments are not scored)
         lengths = loguniform_lengths_ref(int(count), int(lo), int(hi), int(seed))
     else:
         lengths = list(lspec)
@@ -345,7 +390,7 @@ def workload_config(name, regime):
     model, lspec, layers, cfg, mode = CONFIGS[name]
     lengths = lspec if isinstance(lspec, str) else (lspec[0] if len(set(lspec)) == 1 else list(lspec))
     return {"workload": WORKLOAD_NAME[name], "model_shape": model,
-            "requests": int(lspec.split(":")[1]) if isinstance(lspec, str) else len(lspec),
+            "requests": len(config_lengths(lspec)) if isinstance(lspec, str) else len(lspec),
             "tokens_per_request": lengths, "drop_layers": layers, "regime": regime,
             "unit": "(request, drop layer) pair; tokens = tokens entering the drop layer",
             "l2": "inputs larger than L2 (per-layer activation sets >> 126 MB)", **cfg}
@@ -400,8 +445,10 @@ class LayerRunner:
     """One drop layer (score -> [shard reduce] -> select -> compact) of the configured
     workload on this rank, through the public API (paper_2605_06221_b200.api)."""
 
-    def __init__(self, up, torch, mode, shp, lengths, cfg, dev, world, rank):
+    def __init__(self, up, torch, mode, shp, lengths, cfg, dev, world, rank, peer=None, drop_enabled=None):
         from paper_2605_06221_b200.distributed import head_slice
+        # per-segment flags (decode segments pass through unscored, scheduler.cpp:59-62)
+        self.en = None if drop_enabled is None else torch.tensor(drop_enabled, dtype=torch.uint8, device=dev)
 
         self.up, self.torch, self.mode, self.cfg, self.dev = up, torch, mode, cfg, dev
         Hq, Hkv, D, HID = shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"], shp["hidden"]
@@ -417,6 +464,11 @@ class LayerRunner:
             self.tp = 8 if world == 1 else world
             slices = [head_slice(Hq, Hkv, t, self.tp) for t in range(self.tp)]
             self.shards = slices if world == 1 else [slices[rank]]
+        elif mode == "tp-rank":
+            # what ONE rank of the TP=8 group runs: its head slice only (rank 0's), scored
+            # through the fused scorer + peer reduction on a one-rank group
+            self.tp = 8
+            self.shards = [head_slice(Hq, Hkv, 0, self.tp)]
         else:
             self.tp, self.shards = 1, [((0, Hq), (0, Hkv))]
         # planes compacted per layer: hidden, K, V of the local kv-heads, positions
@@ -424,8 +476,9 @@ class LayerRunner:
         ke = max(sh[1][1] for sh in self.shards)
         self.kv_range = (kb, ke)
         self.Hkv_local = ke - kb
-        # At N>1 (tp) the activation tensors hold only this rank's heads (localize()).
-        self.local = mode == "tp" and world > 1
+        # At N>1 (tp) and in tp-rank mode the activation tensors hold only this rank's heads
+        # (localize()).
+        self.local = (mode == "tp" and world > 1) or mode == "tp-rank"
         self.heads = []
         for (qb, qe), (skb, ske) in self.shards:
             qi = (0, qe - qb) if self.local else (qb, qe)
@@ -440,8 +493,9 @@ class LayerRunner:
         plane_dtypes = [torch.bfloat16, torch.bfloat16, torch.bfloat16, torch.int64]
         self.layer = up.DropLayer(cfg, up.HeadLayout(Hq, Hkv, D), self.T, self.R, plane_shapes, plane_dtypes,
                                   device=dev)
-        self.peer = None
-        if mode == "tp" and world > 1 and os.environ.get("UP_TP_REDUCE", "peer") == "peer":
+        self.peer = peer
+        if peer is None and ((mode == "tp" and world > 1 and os.environ.get("UP_TP_REDUCE", "peer") == "peer")
+                             or mode == "tp-rank"):
             from paper_2605_06221_b200.distributed import PeerScoreReducer
             self.peer = PeerScoreReducer(self.T // G + self.R + 1, device=dev)  # up_max_blocks
         if mode == "tp" and world == 1:
@@ -458,19 +512,23 @@ class LayerRunner:
             sb.v = sb.v[:, kb:ke].contiguous()
         return sb
 
-    def planes(self, sb):
+    def planes(self, sb, hidden=None, positions=None):
+        """Planes compacted at the drop layer: the hidden states and positions of the stream
+        entering it (default: the activation set's), the layer's K and V."""
+        h = sb.hidden if hidden is None else hidden
+        pos = sb.positions if positions is None else positions
         if self.local:
-            return [sb.hidden, sb.k, sb.v, sb.positions]
+            return [h, sb.k, sb.v, pos]
         kb, ke = self.kv_range
-        return [sb.hidden, sb.k[:, kb:ke], sb.v[:, kb:ke], sb.positions]
+        return [h, sb.k[:, kb:ke], sb.v[:, kb:ke], pos]
 
     def score(self, sb, cu):
         up, L = self.up, self.layer
-        if self.mode != "tp":
-            up.score_blocks_varlen(sb.q, sb.k, cu, self.cfg, L.heads, max_tokens=self.T, workspace=L.ws,
+        if self.mode not in ("tp", "tp-rank"):
+            up.score_blocks_varlen(sb.q, sb.k, cu, self.cfg, L.heads, self.en, max_tokens=self.T, workspace=L.ws,
                                    out=L.scores)
             return up.lib.up_last_launch_count()
-        if self.world == 1:
+        if self.world == 1 and self.peer is None:
             # the whole TP group on one device: per-shard partials + ascending-shard sum in
             # one up_score_blocks_tp call (sharded_block_scores + allreduce_scores)
             up.score_blocks_tp(sb.q, sb.k, cu, self.cfg, self.tp, L.heads, max_tokens=self.T, workspace=L.ws,
@@ -493,18 +551,110 @@ class LayerRunner:
 
     def select(self, cu):
         L = self.layer
-        self.up.select_varlen(L.scores.block_scores, L.scores.cu_blocks, cu, self.cfg, max_tokens=self.T,
-                              workspace=L.ws, out=L.sel)
+        self.up.select_varlen(L.scores.block_scores, L.scores.cu_blocks, cu, self.cfg, drop_enabled=self.en,
+                              max_tokens=self.T, workspace=L.ws, out=L.sel)
         return self.up.lib.up_last_launch_count()
 
-    def compact(self, sb, cu):
+    def compact(self, sb, cu, hidden=None, positions=None):
         L = self.layer
-        self.up.compact_varlen(L.sel.keep, cu, self.planes(sb), max_tokens=self.T, workspace=L.ws,
-                               result=L.out, after_select=True)
+        self.up.compact_varlen(L.sel.keep, cu, self.planes(sb, hidden, positions), drop_enabled=self.en,
+                               max_tokens=self.T, workspace=L.ws, result=L.out, after_select=True)
         return self.up.lib.up_last_launch_count()
 
-    def __call__(self, sb, cu):
-        self.launches = self.score(sb, cu) + self.select(cu) + self.compact(sb, cu)
+    def __call__(self, sb, cu, hidden=None, positions=None):
+        self.launches = self.score(sb, cu) + self.select(cu) + self.compact(sb, cu, hidden, positions)
+
+
+class BlockSchedule:
+    """One step of the configured model on this rank: for every block, S cascaded drop
+    layers (drop 0 on the full stream entering the block; drop s+1 on drop s's compacted
+    planes under its device-resident cu_seqlens_out), the downstream sublayers' Eq. 16 slot
+    mapping where they own a paged KV cache, and the reconstitution at the block boundary
+    (the retained rows' states scattered back over the pre-drop hidden states, last drop
+    first; propagation.cpp:79-100, scheduler.cpp:349-360).  Launch sizes depend only on
+    capacities, so the whole step is one CUDA graph."""
+
+    def __init__(self, up, torch, runners, resid, positions, cu, blocks, block_spec, sets, dev):
+        self.up, self.torch = up, torch
+        self.runners, self.resid, self.positions, self.cu = runners, resid, positions, cu
+        self.blocks, self.S = blocks, len(runners)
+        self.sets, self.n_sets = sets, len(sets)
+        kind, count = block_spec["downstream"]
+        self.reconstitute = block_spec["reconstitute"]
+        self.slot_layers = count if kind == "swa" else 0
+        self.launches = 0
+        self.slots = self.tables = None
+        if self.slot_layers:
+            # identity page tables of the downstream SWA layers: request r's page i of layer
+            # l is page (l * R + r) * max_pages + i
+            R = cu.numel() - 1
+            lens = (cu[1:] - cu[:-1]).tolist()
+            max_pages = (max(lens) + KV_PAGE - 1) // KV_PAGE
+            base = torch.arange(self.slot_layers * R, dtype=torch.int32, device=dev) * max_pages
+            self.tables = (base[:, None] + torch.arange(max_pages, dtype=torch.int32, device=dev)[None]
+                           ).reshape(self.slot_layers, R, max_pages).contiguous()
+            self.slots = torch.empty(self.slot_layers, runners[0].T, dtype=torch.int64, device=dev)
+
+    def layer_input(self, s):
+        """(cu_seqlens, hidden, positions) of the stream entering drop s of a block."""
+        if s == 0:
+            return self.cu, self.resid, self.positions
+        o = self.runners[s - 1].layer.out
+        return o.cu_seqlens, o.planes[0], o.planes[3]
+
+    def drop(self, b, s, stage=None):
+        r = self.runners[s]
+        act = self.sets[(b * self.S + s) % self.n_sets]
+        cu, h, pos = self.layer_input(s)
+        if stage is None:
+            r(act, cu, h, pos)
+            return r.launches
+        if stage == "score":
+            return r.score(act, cu)
+        if stage == "select":
+            return r.select(cu)
+        return r.compact(act, cu, h, pos)
+
+    def slot_map(self):
+        if not self.slot_layers:
+            return 0
+        last = self.runners[-1].layer
+        o = last.out
+        self.up.slot_mapping(o.cu_seqlens, o.planes[3], self.tables, KV_PAGE, num_rows=o.num_out, out=self.slots,
+                             workspace=last.ws)
+        return self.up.lib.up_last_launch_count()
+
+    def reconstitute_block(self):
+        if not self.reconstitute:
+            return 0
+        n = 0
+        for s in reversed(range(self.S)):
+            o = self.runners[s].layer.out
+            dst = self.resid if s == 0 else self.runners[s - 1].layer.out.planes[0]
+            self.up.scatter_rows(o.retained_index, [o.planes[0]], [dst], num_rows=o.num_out)
+            n += self.up.lib.up_last_launch_count()
+        return n
+
+    def step(self, record=None):
+        n = 0
+        for b in range(self.blocks):
+            for s in range(self.S):
+                n += self.drop(b, s)
+                if record is not None:
+                    record.append(self.runners[s].layer.out.num_out.clone())
+            n += self.slot_map()
+            n += self.reconstitute_block()
+        self.launches = n
+
+    def stage_pass(self, stage):
+        for b in range(self.blocks):
+            if stage in ("score", "select", "compact"):
+                for s in range(self.S):
+                    self.drop(b, s, stage)
+            elif stage == "slots":
+                self.slot_map()
+            elif stage == "reconstitute":
+                self.reconstitute_block()
 
 
 def run_ours(args):
@@ -523,13 +673,19 @@ def run_ours(args):
         local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    model, lspec, layers, cfgd, mode = CONFIGS[args.config]
     if ws > 1:
+        if mode == "tp-rank":
+            raise SystemExit("--config c3-rank is the 1-GPU measurement of one TP rank's slice")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+    elif mode == "tp-rank":
+        # a one-rank group: the fused scorer + peer reduction runs exactly the kernels a TP
+        # rank runs (its exchange is with itself)
+        dist.init_process_group("gloo", store=dist.HashStore(), rank=0, world_size=1)
 
-    model, lspec, layers, cfgd, mode = CONFIGS[args.config]
     shp = MODEL_SHAPES[model]
     Hq, Hkv, D, HID = shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"], shp["hidden"]
     cfg = up.ScoreConfig(**cfgd)
@@ -542,50 +698,86 @@ def run_ours(args):
         job_tokens, scaling = sum(all_lengths), "strong"
         if ws > 1 and Hq % ws:
             raise SystemExit(f"--config {args.config}: {Hq} q-heads do not split over {ws} ranks")
-    else:                    # every rank runs its own batch
+    else:                    # every rank runs its own batch (tp-rank: one rank's slice)
         lengths = all_lengths
         job_tokens, scaling = ws * sum(all_lengths), "weak"
     R, T = len(lengths), sum(lengths)
     n = cfg.query_window_n
-    runner = LayerRunner(up, torch, mode, shp, lengths, cfg, dev, ws, rank)
+    S = max(1, args.stack)
+    if layers % S:
+        raise SystemExit(f"--stack {S} does not divide the config's {layers} drop layers")
+    blocks = layers // S
+    block_spec = BLOCKS[args.config]
+    en = config_drop_enabled(lspec)
+    runners = [LayerRunner(up, torch, mode, shp, lengths, cfg, dev, ws, rank, drop_enabled=en)]
+    runners += [LayerRunner(up, torch, mode, shp, lengths, cfg, dev, ws, rank, peer=runners[0].peer,
+                            drop_enabled=en) for _ in range(S - 1)]  # one exchange buffer per rank
+    runner = runners[0]
 
-    # ---- activations: one set per layer (or --layer-sets distinct sets, cycled) ----
+    # ---- activations: one set per drop layer (or --layer-sets distinct sets, cycled) ----
+    # Per-layer q, k, v (the layer's own projections); the hidden states are ONE residual
+    # stream per rank that every block compacts and reconstitutes.
     free, _ = torch.cuda.mem_get_info(dev)
-    per_set = T * (Hq * D + 2 * Hkv * D + HID) * 2 + T * 8
+    per_set = T * (Hq * D + 2 * Hkv * D) * 2 + T * 8
     n_sets = args.layer_sets or layers
-    n_sets = max(1, min(n_sets, int((free * 0.7 - 3 * per_set) // per_set)))
+    n_sets = max(1, min(n_sets, int((free * 0.6 - 3 * per_set - T * HID * 2) // per_set)))
     sets = [runner.localize(make_batch(lengths, Hq, Hkv, D, HID, regime=args.regime,
-                                       seed=1000 * (rank if mode != "tp" else 0) + s, device=dev))
+                                       seed=1000 * (rank if mode not in ("tp", "tp-rank") else 0) + s, device=dev,
+                                       with_hidden=False))
             for s in range(n_sets)]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7 + rank)
+    resid = torch.randn(T, HID, generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    for sb in sets:
+        sb.hidden = resid
     torch.cuda.empty_cache()
     cu = sets[0].cu_seqlens
+    sched = BlockSchedule(up, torch, runners, resid, sets[0].positions, cu, blocks, block_spec, sets, dev)
+    resid_ref = resid.clone()
 
-    def step():
-        for l in range(layers):
-            runner(sets[l % n_sets], cu)
-
-    # correctness guard on the first layer (device status), then warm-up
-    runner(sets[0], cu)
-    runner.layer.check()
-    launches_per_layer = runner.launches
-    use_graph = not args.no_graph and not (mode == "tp" and ws > 1)
+    # correctness guard on the first block + the retained count of every drop layer of the
+    # step (data-dependent with --stack: tokens entering drop s+1 = drop s's num_out)
+    record = []
+    sched.step(record)
+    for r in runners:
+        r.layer.check()
+    retained = [int(x.item()) for x in record]
+    if block_spec["reconstitute"] and not torch.equal(resid, resid_ref):
+        # no model compute between the drop and the boundary: reconstitution must restore
+        # the residual stream bit for bit (reconstitute, propagation.cpp:79-100)
+        raise SystemExit("reconstitution did not restore the residual stream")
+    del resid_ref
+    entering = []
+    for b in range(blocks):
+        entering.append(T)
+        entering.extend(retained[b * S:(b + 1) * S - 1])
+    # tokens entering drop layers per step over the job: the ranks' own streams summed
+    # (request sharding), or the one stream every TP rank scores a head slice of
+    tokens_per_step = float(sum(entering))
+    if ws > 1 and mode != "tp":
+        t = torch.tensor([tokens_per_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        tokens_per_step = float(t.item())
+    launches_per_step = sched.launches
+    use_graph = not args.no_graph and not (mode == "tp" and ws > 1 and runner.peer is None)
     stream = torch.cuda.Stream(device=dev)
     if use_graph:
         with torch.cuda.stream(stream):
-            step()
+            sched.step()
         torch.cuda.synchronize(dev)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
-            step()
+            sched.step()
         run_step = graph.replay
     else:
-        run_step = step
+        run_step = sched.step
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             run_step()
     torch.cuda.synchronize(dev)
-    runner.layer.check()
+    for r in runners:
+        r.layer.check()
 
     # ---- timed region (device-resident inputs) ----
     if ws > 1:
@@ -610,7 +802,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = job_tokens * layers / (ms_per_step / 1e3)
+    value = tokens_per_step / (ms_per_step / 1e3)
     rho = float(runner.layer.out.num_out.item()) / T
 
     # ---- per-stage timing: each stage over all layers captured in its own CUDA graph
@@ -618,13 +810,14 @@ def run_ours(args):
     stage_info, roofline = {}, None
     if args.profile_stages:
         names = ["score", "select", "compact"]
-        fns = {"score": lambda sb: runner.score(sb, cu), "select": lambda sb: runner.select(cu),
-               "compact": lambda sb: runner.compact(sb, cu)}
+        if sched.slot_layers:
+            names.append("slots")
+        if block_spec["reconstitute"]:
+            names.append("reconstitute")
         stages = {}
         for nm in names:
             def stage_pass(nm=nm):
-                for l in range(layers):
-                    fns[nm](sets[l % n_sets])
+                sched.stage_pass(nm)
             with torch.cuda.stream(stream):
                 stage_pass()
             torch.cuda.synchronize(dev)
@@ -642,21 +835,24 @@ def run_ours(args):
                 run()
                 e1.record(stream)
             torch.cuda.synchronize(dev)
-            stages[nm] = e0.elapsed_time(e1) / layers
+            stages[nm] = e0.elapsed_time(e1) / (layers if nm in ("score", "select", "compact") else blocks)
             del run
-        retained = int(runner.layer.out.num_out.item())
         hbm_peak, tf_peak, peak_kind = measured_peaks()
 
         def prof_traffic(prefix):  # the committed ncu capture is of the c2 workload
-            return ncu_traffic(prefix) if args.config == "c2" else None
+            return ncu_traffic(prefix) if args.config == "c2" and S == 1 else None
 
-        comp_bytes = T * 1 + (R + 1) * 4 * 2 + retained * (2 * runner.row_bytes + 4)
-        score_ach = runner.flops / (stages["score"] / 1e3) / 1e12
+        # per drop layer averages over the step's drop layers
+        mean_in = sum(entering) / len(entering)
+        mean_kept = sum(retained) / len(retained)
+        flops = runner.flops * mean_in / T  # scoring_flops is linear in N_r at N_r >= n
+        comp_bytes = mean_in * 1 + (R + 1) * 4 * 2 + mean_kept * (2 * runner.row_bytes + 4)
+        score_ach = flops / (stages["score"] / 1e3) / 1e12
         comp_ach = comp_bytes / (stages["compact"] / 1e3) / 1e9
         stage_info = {
             "score": {"bound": "tensor", "achieved": score_ach, "peak": tf_peak, "unit": "TFLOP/s",
                       "frac": score_ach / tf_peak, "ms_per_layer": stages["score"],
-                      "algorithmic_flops_per_layer": runner.flops,
+                      "algorithmic_flops_per_layer": flops,
                       "traffic": prof_traffic("score_tcw")},
             "select": {"bound": "latency", "us_per_event": stages["select"] * 1e3, "requests": R},
             "compact": {"bound": "hbm", "achieved": comp_ach, "peak": hbm_peak, "unit": "GB/s",
@@ -664,28 +860,39 @@ def run_ours(args):
                         "algorithmic_bytes_per_layer": comp_bytes,
                         "traffic": prof_traffic("compact_copy")},
         }
+        if "reconstitute" in stages:
+            # per block: every drop's retained hidden rows read + written, and its index
+            rec_bytes = sum(retained[:S]) * (2 * HID * 2 + 4)
+            ach = rec_bytes / (stages["reconstitute"] / 1e3) / 1e9
+            stage_info["reconstitute"] = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                                          "frac": ach / hbm_peak, "ms_per_block": stages["reconstitute"],
+                                          "algorithmic_bytes_per_block": rec_bytes}
+        if "slots" in stages:
+            stage_info["slots"] = {"bound": "latency", "us_per_block": stages["slots"] * 1e3,
+                                   "downstream_layers": sched.slot_layers}
         dominant = "score" if stages["score"] >= stages["compact"] else "compact"
         d = stage_info[dominant]
         roofline = {"kernel": dominant, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                     "unit": d["unit"], "frac": d["frac"], "traffic": d["traffic"],
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json burst)"}
-        if not runner.local:
+        if not runner.local and S == 1:
             stage_info["attention"] = attention_stage(up, runner, sets[0], cu, Hq, D, stream, dev, tf_peak)
             stage_info["attention"]["traffic"] = prof_traffic("attention")
 
     # ---- e2e through the public API with host buffers ----
     # Inputs start in pinned host memory every step.  The scorer needs the query-window rows
-    # and all of K on the device (TMA), so those are copied H2D; hidden, V and positions are
-    # handed to up_compact as pinned host planes and read in place over PCIe by the copy
-    # kernel, so only the retained rows cross the bus (counted in h2d_bytes_per_step).
+    # and all of K on the device (TMA), so those are copied H2D; the residual stream, V and
+    # positions stay in pinned host memory: the compaction kernel reads the retained rows in
+    # place over PCIe and the reconstitution scatter writes them back in place, so only
+    # retained rows cross the bus (counted in h2d/d2h_bytes_per_step).
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and S == 1:
         src = sets[0]
         cu_h = cu.cpu().tolist()
         tails = [(max(cu_h[r], cu_h[r + 1] - n), cu_h[r + 1]) for r in range(R)]
         h_qt = [src.q[a:b].cpu().pin_memory() for a, b in tails]
         h_k, h_v, h_hid, h_pos, h_cu = (x.cpu().pin_memory() for x in
-                                        (src.k, src.v, src.hidden, src.positions, cu))
+                                        (src.k, src.v, resid, src.positions, cu))
         d_in = type(src)(torch.empty_like(src.q), torch.empty_like(src.k), h_v, h_hid, h_pos,
                          torch.empty_like(cu), src.lengths)
         o_keep = torch.empty(T, dtype=torch.uint8).pin_memory()
@@ -695,6 +902,7 @@ def run_ours(args):
             t.numel() * t.element_size() for t in (h_k, h_cu))
         host_row_bytes = HID * 2 + runner.Hkv_local * D * 2 + 8  # hidden + V + position per retained row
         d2h = o_keep.numel() + o_cu.numel() * 4 + o_cut.numel() * 8
+        L0 = runner.layer
 
         def e2e_step():
             for l in range(layers):
@@ -703,9 +911,11 @@ def run_ours(args):
                 d_in.k.copy_(h_k, non_blocking=True)
                 d_in.cu_seqlens.copy_(h_cu, non_blocking=True)
                 runner(d_in, d_in.cu_seqlens)
-                o_keep.copy_(runner.layer.sel.keep, non_blocking=True)
-                o_cu.copy_(runner.layer.out.cu_seqlens, non_blocking=True)
-                o_cut.copy_(runner.layer.sel.cutoff_rank, non_blocking=True)
+                if block_spec["reconstitute"]:
+                    up.scatter_rows(L0.out.retained_index, [L0.out.planes[0]], [h_hid], num_rows=L0.out.num_out)
+                o_keep.copy_(L0.sel.keep, non_blocking=True)
+                o_cu.copy_(L0.out.cu_seqlens, non_blocking=True)
+                o_cut.copy_(L0.sel.cutoff_rank, non_blocking=True)
 
         with torch.cuda.stream(stream):
             e2e_step()
@@ -720,28 +930,33 @@ def run_ours(args):
             b.record(stream)
         torch.cuda.synchronize(dev)
         ems = a.elapsed_time(b)
-        retained_e2e = int(runner.layer.out.num_out.item())
-        # correctness of the zero-copy path: same compacted hidden rows as the device path
-        ref_rows = src.hidden[runner.layer.out.retained_index[:retained_e2e].long()]
-        if not torch.equal(runner.layer.out.planes[0][:retained_e2e], ref_rows):
+        retained_e2e = int(L0.out.num_out.item())
+        # correctness of the zero-copy path: same compacted hidden rows as the device path,
+        # and the host residual stream restored by the in-place reconstitution
+        ref_rows = resid[L0.out.retained_index[:retained_e2e].long()]
+        if not torch.equal(L0.out.planes[0][:retained_e2e], ref_rows):
             raise SystemExit("e2e: zero-copy compaction differs from the device-resident path")
+        if block_spec["reconstitute"] and not torch.equal(h_hid, resid.cpu()):
+            raise SystemExit("e2e: host reconstitution did not restore the residual stream")
         if ws > 1:
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         h2d = h2d_copies + retained_e2e * host_row_bytes
+        d2h_all = d2h + (retained_e2e * HID * 2 if block_spec["reconstitute"] else 0)
         e2e = {"value": job_tokens * layers / (ems / args.e2e_steps / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": h2d * layers, "d2h_bytes_per_step": d2h * layers,
+               "h2d_bytes_per_step": h2d * layers, "d2h_bytes_per_step": d2h_all * layers,
                "steps": args.e2e_steps,
-               "pcie_gbs": (h2d + d2h) * layers / (ems / args.e2e_steps / 1e3) / 1e9,
+               "pcie_gbs": (h2d + d2h_all) * layers / (ems / args.e2e_steps / 1e3) / 1e9,
                "note": "per layer: H2D copies of the query-window rows, K and cu_seqlens from pinned host "
-                       "memory; hidden, V and positions read in place from pinned host memory by the "
-                       "compaction kernel (retained rows only); D2H of keep mask, new cu_seqlens, cutoff "
-                       "ranks"}
+                       "memory; residual stream, V and positions read in place from pinned host memory by the "
+                       "compaction kernel (retained rows only); reconstitution scatters the retained hidden "
+                       "rows back into the pinned host residual stream; D2H of keep mask, new cu_seqlens, "
+                       "cutoff ranks"}
 
     # ---- CPU baseline (rank 0 only, N=1 semantics) ----
     cpu = None
-    if rank == 0 and ws == 1 and not args.skip_cpu:  # reported at N=1 only
+    if rank == 0 and ws == 1 and not args.skip_cpu and mode != "tp-rank":  # reported at N=1 only
         try:  # one step of the reference arm's units (all cores) + one unit on one core
             units = CpuReferenceUnits(model, all_lengths, cfgd, args.regime)
             cpu = cpu_reference_report(units, [units.step()[0]], units.single_core())
@@ -752,11 +967,16 @@ def run_ours(args):
     if rank == 0:
         if mode == "tp":
             par = f"tp{runner.tp} head-sharded" + (" (whole TP group on 1 GPU: per-shard partials + ordered "
-                                                   "shard sum in one up_score_blocks_tp call)" if ws == 1 else "")
+                                                   "shard sum in one up_score_blocks_tp call)" if ws == 1 else
+                                                   (" (fused scorer + peer-memory reduce)" if runner.peer else
+                                                    " (NCCL all-gather + ordered reduce)"))
+        elif mode == "tp-rank":
+            par = "one rank of tp8 (rank 0's heads; fused scorer + peer-memory reduce on a one-rank group)"
         elif mode == "dp-split":
             par = f"LPT request-sharded over {ws} GPU(s)"
         else:
             par = f"request-sharded dp{ws}"
+        kind, count = block_spec["downstream"]
         line = {
             "metric": "score+drop+compact tokens/s", "value": value, "unit": "tokens/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -765,18 +985,25 @@ def run_ours(args):
             "config": workload_config(args.config, args.regime),
             "details": {"requests_per_rank": R, "tokens_per_rank": T, "retention_rho": rho,
                         "activation_sets": n_sets,
-                        "seeds": "make_batch seed = 1000 * rank + activation-set index (torch.Generator on the device)",
+                        "blocks": blocks, "drops_per_block": S,
+                        "block": f"{S} x full-attn drop layer" + (f" + {count} x {kind} sublayers" if count else "")
+                                 + (" + reconstitution at the boundary" if block_spec["reconstitute"] else ""),
+                        "tokens_entering_drops_per_step": sum(entering),
+                        "retained_per_drop_first_block": retained[:S],
+                        "seeds": "make_batch seed = 1000 * rank + activation-set index; residual stream seed 7 + rank "
+                                 "(torch.Generator on the device)",
                         "l2": "inputs larger than L2 (distinct per-layer activation sets, each >> 126 MB)",
                         "cuda_graph": use_graph, "parallelism": par},
             "roofline": roofline, "stages": stage_info, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clk, "gpu_launches": launches_per_layer * layers * args.steps,
+            "clocks": clk, "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        if runner.peer is not None:
-            runner.layer.check()
-            runner.peer.check()
-            runner.peer.close()
+    if runner.peer is not None:
+        for r in runners:
+            r.layer.check()
+        runner.peer.check()
+        runner.peer.close()
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

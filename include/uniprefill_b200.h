@@ -179,7 +179,9 @@ up_status up_compact_selected(void* stream, const up_batch* batch, const uint8_t
  * to row index[o] of its dst.  Passing up_compact's retained_index and num_tokens_out
  * writes the current compacted states back over their pre-drop rows, turning the pre-drop
  * buffer into the reconstituted stream (reconstitute, propagation.cpp:79-100; unwind the
- * drops of a block in reverse order).  Also re-admits parked rows at their positions. */
+ * drops of a block in reverse order).  Also re-admits parked rows at their positions.
+ * dst may be pinned host memory (unified addressing): the kernel writes the scattered
+ * rows in place over PCIe, the mirror of up_compact reading pinned host sources. */
 up_status up_scatter_rows(void* stream, const int32_t* index, const int32_t* num_rows, int64_t max_rows,
                           const up_plane* planes, int32_t num_planes);
 

@@ -372,7 +372,8 @@ def scatter_rows(index: torch.Tensor, planes: Sequence[torch.Tensor], outs: Sequ
                  num_rows: Optional[torch.Tensor] = None) -> None:
     """Row scatter (up_scatter_rows), the inverse of compact_varlen's gather:
     outs[p][index[o]] = planes[p][o] for o < num_rows (device int32 count; default: all
-    rows of index), skipping index[o] < 0."""
+    rows of index), skipping index[o] < 0.  Destinations may be pinned host memory
+    (written in place over PCIe, only the scattered rows cross the bus)."""
     if index.dtype != torch.int32 or not index.is_contiguous():
         raise ContractViolation("scatter_rows: index must be contiguous int32")
     dev = index.device
@@ -380,8 +381,9 @@ def scatter_rows(index: torch.Tensor, planes: Sequence[torch.Tensor], outs: Sequ
     for i, (src, dst) in enumerate(zip(planes, outs)):
         if not (src.is_contiguous() and dst.is_contiguous()):
             raise ContractViolation("scatter planes must be contiguous")
-        if src.device != dev or dst.device != dev:
-            raise ContractViolation("scatter planes must be on the index's device")
+        if src.device != dev or (dst.device != dev and not (dst.device.type == "cpu" and dst.is_pinned())):
+            raise ContractViolation("scatter planes: sources on the index's device, destinations on the "
+                                    "device or pinned host")
         rb = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
         if (dst[0].numel() * dst.element_size() if dst.dim() > 1 else dst.element_size()) != rb:
             raise ContractViolation("scatter planes: row size mismatch")

@@ -27,6 +27,7 @@ cudaError_t launch_score_tcw(int D, int HPC, const CUtensorMap& qm, const CUtens
 bool tcw_supported(int D, int HPC, int G, int R);
 int tcw_stage_keys(int D);
 bool tc2_enabled();
+int tcw_npar(int D, int HPC, int G, int64_t max_tokens, int nhg, int grid);
 bool tc2_supported(int D, int HPC, int G, int R);
 int tc2_stage_keys();
 int tc2_grid(int num_sms);
@@ -48,6 +49,8 @@ cudaError_t launch_score_simt(const ScoreSimtParams& p, int64_t max_tokens, int 
                               cudaStream_t stream);
 cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request, int num_sms,
                           cudaStream_t stream);
+bool select_fuses_expand(int64_t max_tokens);
+bool compact_is_small(int64_t max_tokens);
 cudaError_t launch_reduce_shards(const float* const* shards, int tp, int64_t count, float* out,
                                  int num_sms, cudaStream_t stream);
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream, bool counts_ready);
@@ -233,6 +236,15 @@ struct TcPlan {
     int hpc, npar;
 };
 
+// CTAs of the single-CTA scorers: one per SM (UP_SCORE_GRID overrides, dev sweeps)
+int score_grid() {
+    static const int grid_override = [] {
+        const char* s = std::getenv("UP_SCORE_GRID");
+        return s ? std::atoi(s) : 0;
+    }();
+    return grid_override > 0 ? grid_override : num_sms();
+}
+
 TcPlan tc_plan(const up_batch* b, const up_heads* h, const up_score_config* c, int shard_heads) {
     const int D = h->head_dim;
     TcPlan t{};
@@ -244,7 +256,10 @@ TcPlan tc_plan(const up_batch* b, const up_heads* h, const up_score_config* c, i
     t.pair = tc2_supported(D, t.hpc, c->block_size_g, b->num_requests);
     t.wide = !t.pair && (t.hpc == 4 || t.hpc == 2) && tcw_supported(D, t.hpc, c->block_size_g, b->num_requests);
     if (!t.wide && !t.pair) t.hpc = pick_hpc(h, tc_max_hpc(D), shard_heads);
-    t.npar = t.pair ? 4 : (t.wide ? 4 / t.hpc : 1);
+    t.npar = t.pair ? 4
+                    : (t.wide ? tcw_npar(D, t.hpc, c->block_size_g, b->max_tokens, h->num_q_heads / t.hpc,
+                                         score_grid())
+                              : 1);
     return t;
 }
 
@@ -356,11 +371,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     p.kv_head_offset = h->kv_head_offset;
     p.gqa_group = h->gqa_group;
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
-    static const int grid_override = [] {
-        const char* s = std::getenv("UP_SCORE_GRID");
-        return s ? std::atoi(s) : 0;
-    }();
-    const int grid = plan.pair ? tc2_grid(num_sms()) : (grid_override > 0 ? grid_override : num_sms());
+    const int grid = plan.pair ? tc2_grid(num_sms()) : score_grid();
     // work ranges: one per CTA, or one per CTA pair
     const int ranges = plan.pair ? grid / 2 : grid;
     p.dbg = score_debug_buffer();
@@ -564,9 +575,11 @@ up_status up_select(void* stream, const up_batch* b, const up_score_config* c,
     p.tile_counts = at<int32_t>(ws, L.tile_counts);
     p.max_tokens = b->max_tokens;
     const int64_t per_req = (b->max_tokens + c->block_size_g - 1) / c->block_size_g;
+    p.fuse_expand = select_fuses_expand(b->max_tokens) ? 1 : 0;
     const cudaError_t e = launch_select(p, b->num_requests, static_cast<int>(per_req < kMaxSortBlocks ? per_req : kMaxSortBlocks),
                                         num_sms(), static_cast<cudaStream_t>(stream));
-    g_launches = 2 + (per_req > 512 ? 1 : 0) + (per_req > 2048 ? 1 : 0);  // size classes + expand
+    // size classes + the expand launch (folded into the select CTAs at small capacities)
+    g_launches = 1 + (per_req > 512 ? 1 : 0) + (per_req > 2048 ? 1 : 0) + (p.fuse_expand ? 0 : 1);
     return cuda_status(e);
 }
 
@@ -606,7 +619,7 @@ static up_status compact_impl(void* stream, const up_batch* b, const uint8_t* ke
         if (p.src_stride[i] < pl.row_bytes || p.dst_stride[i] < pl.row_bytes) return UP_ERR_CONTRACT;
     }
     const cudaError_t e = launch_compact(p, num_sms(), static_cast<cudaStream_t>(stream), counts_ready);
-    g_launches = (num_planes > 0 ? 3 : 2) - (counts_ready ? 1 : 0);
+    g_launches = compact_is_small(b->max_tokens) ? 1 : (num_planes > 0 ? 3 : 2) - (counts_ready ? 1 : 0);
     return cuda_status(e);
 }
 

@@ -199,6 +199,81 @@ scatter_rows_kernel(const CompactParams p) {
     }
 }
 
+// Small capacities (<= kSmallCompactRows source rows, e.g. BASELINE C1's single 4K request):
+// the count / index / copy kernels collapse into one launch.  Every CTA scans the whole keep
+// mask (a few KB, L2-resident) into its own shared-memory retained index -- CTA 0 also
+// publishes retained_index, cu_seqlens_out and num_out -- then copies its share of the
+// output rows exactly as compact_copy_kernel does.
+constexpr int kSmallCompactRows = 8192;
+
+__global__ void __launch_bounds__(kCopyThreads)
+compact_small_kernel(const CompactParams p) {
+    pdl_wait();     // predecessor's outputs are visible past this point
+    pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
+    constexpr int PER = 4;
+    constexpr int CHUNK = kCopyThreads * PER;
+    __shared__ int32_t idx[kSmallCompactRows];
+    __shared__ int warp_tot[kCopyThreads / 32];
+    const bool lead = blockIdx.x == 0;
+    if (!cta_batch_valid(p.cu_seqlens, p.num_requests, p.max_tokens)) {  // empty result, as compact_index
+        if (lead) {
+            for (int s = threadIdx.x; s <= p.num_requests; s += blockDim.x) p.cu_out[s] = 0;
+            if (threadIdx.x == 0 && p.num_out) *p.num_out = 0;
+        }
+        return;
+    }
+    const int T = p.cu_seqlens[p.num_requests];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int carry = 0;
+    for (int base = 0; base < T; base += CHUNK) {
+        const int i0 = base + tid * PER;
+        uint32_t bits = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) bits |= (row_kept(p, i0 + q, T) ? 1u : 0u) << q;
+        const int cnt = __popc(bits);
+        int x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[warp] = x;
+        __syncthreads();
+        int wbase = 0, chunk_total = 0;
+#pragma unroll
+        for (int w = 0; w < kCopyThreads / 32; ++w) {
+            if (w < warp) wbase += warp_tot[w];
+            chunk_total += warp_tot[w];
+        }
+        int pos = carry + wbase + x - cnt;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int i = i0 + q;
+            if (lead && i < T) {
+                const int s = find_segment(p.cu_seqlens, p.num_requests, i);
+                if (p.cu_seqlens[s] == i) p.cu_out[s] = pos;
+            }
+            if (bits & (1u << q)) {
+                idx[pos] = i;
+                if (lead) p.retained_index[pos] = i;
+                ++pos;
+            }
+        }
+        carry += chunk_total;
+        __syncthreads();  // warp_tot reused by the next chunk
+    }
+    if (lead && tid == 0) {
+        p.cu_out[p.num_requests] = carry;
+        if (p.num_out) *p.num_out = carry;
+    }
+    if (p.num_planes == 0) return;
+    const int gw = (blockIdx.x * kCopyThreads + tid) >> 5;
+    const int nw = (gridDim.x * kCopyThreads) >> 5;
+    for (int o = gw; o < carry; o += nw) copy_row_planes(p, idx[o], o, lane);
+}
+
+bool compact_is_small(int64_t max_tokens) { return max_tokens <= kSmallCompactRows; }
+
 static int copy_grid(int num_sms, int64_t rows) {
     static int occ = 0;
     if (occ == 0) {
@@ -221,6 +296,12 @@ cudaError_t launch_scatter_rows(const CompactParams& p, int num_sms, cudaStream_
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream, bool counts_ready) {
     const int64_t tiles = (p.max_tokens + kCompactTile - 1) / kCompactTile;
     cudaError_t e = cudaSuccess;
+    if (compact_is_small(p.max_tokens)) {
+        int64_t grid = (p.max_tokens + kCopyThreads / 32 - 1) / (kCopyThreads / 32);  // warp per row at most
+        if (grid > 2LL * num_sms) grid = 2LL * num_sms;
+        return launch_k(kPdlCompact, compact_small_kernel, static_cast<unsigned>(grid < 1 ? 1 : grid), kCopyThreads,
+                        0, stream, p);
+    }
     if (!counts_ready &&
         (e = launch_k(kPdlCompactScan, compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) !=
             cudaSuccess)

@@ -116,6 +116,7 @@ struct SelectParams {
     int64_t max_tokens;
     unsigned long long* dbg;  // optional phase clocks of CTA 0 (UP_SELECT_DEBUG), else null
     int32_t nb_lo, nb_hi;     // this launch handles the requests with nb_lo < blocks <= nb_hi
+    int32_t fuse_expand;      // small capacity: each select CTA writes its request's token mask
 };
 
 constexpr int kMaxPlanes = 8;

@@ -7,7 +7,12 @@
 namespace up {
 
 
-constexpr int kTcwMaxRequests = 256;  // segments per launch of score_tcw (plan kept in smem)
+// Segments per launch of score_tcw: its work plan (per-request unit and block prefix sums)
+// lives in shared memory, 8 bytes per segment.  4096 segments (32 KB) still leave the K ring
+// its 2 (D <= 128, HPC = 4) / 3 (D = 256) stages, so continuous batches with hundreds of
+// decode pass-through segments keep the fast scorer; the CTA-pair kernel keeps 256.
+constexpr int kTcwMaxRequests = 4096;
+constexpr int kTc2MaxRequests = 256;
 
 // ---------------------------------------------------------------- partition
 struct Part {

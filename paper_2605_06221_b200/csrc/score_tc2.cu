@@ -108,7 +108,7 @@ struct Tc2Cfg {
     static constexpr int KSUB = HK * 128;         // [64 keys x 64 bf16] K tile
     static constexpr int Q_BYTES = SLOTS * KC * QSUB;
     static constexpr int K_STAGE = KC * KSUB;
-    static constexpr int R_RESERVE = 2 * (kTcwMaxRequests + 1) * 4;
+    static constexpr int R_RESERVE = 2 * (kTc2MaxRequests + 1) * 4;
     static constexpr int BUDGET = 232448 - 1024 - 512 - R_RESERVE;
     static constexpr int KST = (BUDGET - Q_BYTES) / K_STAGE > 8 ? 8 : (BUDGET - Q_BYTES) / K_STAGE;
     static constexpr int NREG = 4;                // TMEM regions of 128 columns (jobs round-robin)
@@ -520,7 +520,7 @@ bool tc2_enabled() {
 }
 
 bool tc2_supported(int D, int HPC, int G, int R) {
-    return tc2_enabled() && D == 128 && HPC == 4 && (G == 32 || G == 64 || G == 128) && R <= kTcwMaxRequests;
+    return tc2_enabled() && D == 128 && HPC == 4 && (G == 32 || G == 64 || G == 128) && R <= kTc2MaxRequests;
 }
 
 int tc2_stage_keys() { return Tc2Cfg<128>::HK; }
@@ -534,7 +534,7 @@ int tc2_grid(int num_sms) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(num_sms & ~1);
         cfg.blockDim = dim3(C::THREADS);
-        cfg.dynamicSmemBytes = C::smem(kTcwMaxRequests);
+        cfg.dynamicSmemBytes = C::smem(kTc2MaxRequests);
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
@@ -554,7 +554,7 @@ cudaError_t launch_score_tc2(const CUtensorMap& qm, const CUtensorMap& km, const
                              cudaStream_t stream) {
     using C = Tc2Cfg<128>;
     const int smem = C::smem(p.num_requests);
-    if (p.num_requests > kTcwMaxRequests || smem > 232448 || (grid & 1)) return cudaErrorInvalidValue;
+    if (p.num_requests > kTc2MaxRequests || smem > 232448 || (grid & 1)) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(score_tc2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};

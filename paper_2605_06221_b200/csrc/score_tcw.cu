@@ -48,7 +48,7 @@ namespace up {
 #define UP_TCW_LEAN 1
 #endif
 
-template <int D, int HPC>
+template <int D, int HPC, bool SPLIT = false>
 struct TcwCfg {
     // TS: with two q-heads per CTA, Q lives in TMEM (tcgen05.mma A operand from tensor
     // memory): the MMA then reads only K from shared memory, which keeps the D = 256
@@ -59,7 +59,9 @@ struct TcwCfg {
     static constexpr int SUBN = HPC == 4 ? UP_TCW_SUBN_HPC4 : 64;
     static constexpr int NG = SUBN / 32;          // 32-column groups per subtile
     static constexpr int SPS = SK / SUBN;         // subtiles per K stage
-    static constexpr int NPAR = 4 / HPC;          // epilogue warpgroups per head
+    // epilogue warpgroups per head = statistics rows per head; SPLIT (HPC = 4): two, one per
+    // 64-key half of every subtile
+    static constexpr int NPAR = SPLIT ? 2 : 4 / HPC;
     static constexpr int NB = (512 - (TS ? HPC * D / 2 : 0)) / (HPC * SUBN);  // TMEM regions per head
     static constexpr int KC = D / 64;             // 128-byte K-chunks per row
     static constexpr int QSUB = 128 * 128;        // [128 rows x 64 bf16] Q tile
@@ -76,6 +78,7 @@ struct TcwCfg {
     static constexpr int NP = D <= 128 ? UP_TCW_POLY_PAIRS_D128 : UP_TCW_POLY_PAIRS_D256;
     static int smem(int R) { return Q_BYTES + KST * K_STAGE + NBAR * 8 + 64 + 1024 + 2 * (R + 1) * 4; }
     static_assert(KST >= 2, "K ring too small");
+    static_assert(!SPLIT || (HPC == 4 && SUBN == 128 && NB == 1), "SPLIT drains one 128-column region per head");
 };
 
 // Rebase (cold): rescale the partials this thread already wrote for the item -- blocks
@@ -86,13 +89,13 @@ static __device__ __noinline__ void rescale_rows_par(float* prow, int g0, int g1
         if (((g * G) >> 6) % npar == par) prow[static_cast<int64_t>(g) * kRows] *= f;
 }
 
-template <int D, int HPC>
+template <int D, int HPC, bool SPLIT>
 __global__ void __launch_bounds__(576, 1)
 score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                  const ScoreTcParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
-    using C = TcwCfg<D, HPC>;
+    using C = TcwCfg<D, HPC, SPLIT>;
     constexpr int NPAR = C::NPAR, NB = C::NB;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -122,7 +125,8 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         mbar_init(q_full, C::TS ? 16 : 1);  // TS: every epilogue warp stores its Q slice
         mbar_init(q_empty, 1);
         for (int s = 0; s < C::KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
-        for (int s = 0; s < C::NREG; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 4); }
+        // a region is released by the warps that drain it: one warpgroup, or two with SPLIT
+        for (int s = 0; s < C::NREG; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], SPLIT ? 8 : 4); }
         fence_barrier_init();
         prefetch_tensormap(&qmap);
         prefetch_tensormap(&kmap);
@@ -282,6 +286,141 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 }
                 mma_commit(q_empty);
             }
+        }
+    } else if constexpr (SPLIT) {
+        // ===== SPLIT epilogue (HPC = 4, G in {32, 64}): warpgroup wg drains column half
+        // c = wg & 1 of every 128-key subtile for the two heads hp = wg >> 1 and hp + 2, so
+        // every region is drained by two warpgroups and every warpgroup alternates between two
+        // regions: while it sums one head's half, the MMA warp refills the other head's
+        // region, and a region is always full again before its drainers come back (with one
+        // region per head and one warpgroup per region, each drain was followed by a wait on
+        // the tensor pipe).  Statistics rows per (head, half): virtual head hh * 2 + c -- the
+        // parity pair_weights / block_combine take at 64-key granularity (par_shift 6).
+        const int etid = threadIdx.x - 64;   // 0..511
+        const int wg = (warp - 2) >> 2;
+        const int c = wg & 1;
+        const int hp = wg >> 1;
+        const int quarter = warp & 3;        // TMEM lane quarter this warp may access
+        const int j = quarter * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+        const float sc = p.scale_log2;
+        const uint32_t tfull_addr = smem_u32(t_full), tempty_addr = smem_u32(t_empty);
+        const int gshift = G == 64 ? 6 : 5;  // log2 G
+        uint32_t u = 0;
+        for (int64_t pos = my_begin; pos < my_end;) {
+            const Item it = make_item(P, pos, my_end);
+            pos += it.u1 - it.u0;
+            const int seg0 = p.cu_seqlens[it.r];
+            const int N = p.cu_seqlens[it.r + 1] - seg0;
+            const int neff = min(p.query_window_n, N);
+            const int key0 = it.u0 * unit_keys;
+            const int key1 = min(it.u1 * unit_keys, N);
+            const int nsub = (key1 - key0 + C::SK - 1) / C::SK * C::SPS;  // as issued by the MMA warp
+            const bool row_valid = j < neff;
+            const int qpos = N - neff + j;  // row j's causal limit (importance.cpp:27)
+            const int64_t gb_seg = s_cu_blocks[it.r];
+            const int blk0 = key0 >> gshift;
+            float* Prow[2];
+            float m[2], l[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                Prow[e] = p.P + (static_cast<int64_t>(it.hg * HPC + hp + 2 * e) * p.max_blocks + gb_seg) * kRows + j;
+                m[e] = -INFINITY;
+                l[e] = 0.f;
+            }
+#pragma unroll 1
+            for (int t = 0; t < nsub; ++t, ++u) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int reg = hp + 2 * e;  // NB = 1: region = head
+                    const int cb = key0 + t * C::SUBN + 64 * c;  // this warpgroup's 64 keys
+                    mbar_wait_u32(tfull_addr + reg * 8, u & 1);
+                    tc_fence_after();
+                    const uint32_t taddr = tmem_base + lane_base + reg * C::SUBN + 64 * c;
+                    float gs0 = 0.f, gs1 = 0.f;
+                    bool redo;
+                    if (cb + 64 <= N - neff + 1) {
+                        // whole half inside the segment and left of every row's causal limit
+                        uint32_t va[32], vb[32];
+                        tmem_ld32(taddr, va);
+                        tmem_ld_wait();
+                        tmem_ld32(taddr + 32, vb);
+                        gs0 = group_sum_pk<C::NP>(va, pk(sc, sc), pk(-m[e], -m[e]));
+                        tmem_ld_wait();
+                        gs1 = group_sum_pk<C::NP>(vb, pk(sc, sc), pk(-m[e], -m[e]));
+                        // rows past n_eff carry no statistics: never a reason to rebase
+                        redo = !__all_sync(0xffffffffu, !row_valid || gs0 + gs1 <= 0x1p40f);
+                    } else {
+                        redo = cb < N;
+                    }
+                    if (redo) {
+                        // Generic path: causal tail, ragged segment end, or a rebase of m.
+#pragma unroll 1
+                        for (int q2 = 0; q2 < 2; ++q2) {
+                            const int c0 = cb + q2 * 32;
+                            const int lim = min(qpos - c0, min(31, N - 1 - c0));  // last valid column
+                            uint32_t v[32];
+                            tmem_ld32(taddr + q2 * 32, v);
+                            tmem_ld_wait();
+                            float gs = 0.f;
+                            if (lim >= 0) {
+                                float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+                                for (int k = 0; k < 32; k += 2) {
+                                    const float e0 = ex2_approx(fmaf(__uint_as_float(v[k + 0]), sc, -m[e]));
+                                    const float e1 = ex2_approx(fmaf(__uint_as_float(v[k + 1]), sc, -m[e]));
+                                    a0 += (k + 0 <= lim) ? e0 : 0.f;
+                                    a1 += (k + 1 <= lim) ? e1 : 0.f;
+                                }
+                                gs = a0 + a1;
+                            }
+                            if (!(gs <= 0x1p40f)) {
+                                // Rebase: move m to this group's maximum (see score_tc.cu).
+                                float gmax = -INFINITY;
+#pragma unroll
+                                for (int k = 0; k < 32; ++k)
+                                    if (k <= lim) gmax = fmaxf(gmax, __uint_as_float(v[k]));
+                                const float mnew = fmaxf(m[e], gmax * sc);
+                                if (m[e] != -INFINITY) {
+                                    const float f = ex2_approx(m[e] - mnew);
+                                    l[e] *= f;
+                                    gs0 *= f;  // the half's first group when q2 = 1
+                                    // blocks of this half already written for the item
+                                    rescale_rows_par(Prow[e], blk0, cb >> gshift, G, 2, c, f);
+                                }
+                                m[e] = mnew;
+                                gs = 0.f;
+#pragma unroll
+                                for (int k = 0; k < 32; ++k) {
+                                    const float x = ex2_approx(fmaf(__uint_as_float(v[k]), sc, -mnew));
+                                    gs += (k <= lim) ? x : 0.f;
+                                }
+                            }
+                            if (q2 == 0) gs0 = gs;
+                            else gs1 = gs;
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_u32(tempty_addr + reg * 8);
+                    if (cb >= N) continue;  // warp-uniform: padding past the segment end
+                    const int b = cb >> gshift;
+                    if (G == 64) {
+                        Prow[e][static_cast<int64_t>(b) * kRows] = row_valid ? gs0 + gs1 : 0.f;
+                    } else {
+                        Prow[e][static_cast<int64_t>(b) * kRows] = row_valid ? gs0 : 0.f;
+                        if (cb + 32 < N) Prow[e][static_cast<int64_t>(b + 1) * kRows] = row_valid ? gs1 : 0.f;
+                    }
+                    l[e] += gs0 + gs1;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t x = (it.sid * (HPC * 2) + (hp + 2 * e) * 2 + c) * kRows + j;
+                p.stat_m[x] = row_valid ? m[e] : -INFINITY;
+                p.stat_l[x] = row_valid ? l[e] : 0.f;
+            }
+            for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
         }
     } else {
         // ===== epilogue: warpgroup wg -> head hh, subtile parity par; thread = query row =====
@@ -542,15 +681,37 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
     }
 }
 
-template <int D, int HPC>
+template <int D, int HPC, bool SPLIT = false>
 static cudaError_t launch_tcw(const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p, int grid,
                               cudaStream_t stream) {
-    using C = TcwCfg<D, HPC>;
+    using C = TcwCfg<D, HPC, SPLIT>;
     const int smem = C::smem(p.num_requests);
     if (p.num_requests > kTcwMaxRequests || smem > 232448) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(score_tcw_kernel<D, HPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(score_tcw_kernel<D, HPC, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem);
     if (e != cudaSuccess) return e;
-    return launch_k(kPdlScore, score_tcw_kernel<D, HPC>, grid, C::THREADS, smem, stream, qm, km, p);
+    return launch_k(kPdlScore, score_tcw_kernel<D, HPC, SPLIT>, grid, C::THREADS, smem, stream, qm, km, p);
+}
+
+// SPLIT epilogue for four q-heads per kv-head when every block lies inside a 64-key half,
+// chosen for small launches (at most ~4 128-key units per CTA under the capacity: the
+// latency-bound C1-class batches, LLaMA 1x4K scorer stage 30.4 -> 29.4 us).  On large
+// launches the one-warpgroup-per-head epilogue is 1.4% faster (LLaMA 4x32K 157.9 vs
+// 160.1 us): there the idle warpgroup's MUFU share goes to the other three.
+// UP_TCW_SPLIT=0/1 forces either epilogue (A/B timing).
+bool tcw_split(int D, int HPC, int G, int64_t max_tokens, int nhg, int grid) {
+    static const int force = [] {
+        const char* s = std::getenv("UP_TCW_SPLIT");
+        return s == nullptr ? -1 : (s[0] == '0' ? 0 : 1);
+    }();
+    if (!(HPC == 4 && (D == 64 || D == 128) && (G == 32 || G == 64))) return false;
+    if (force >= 0) return force == 1;
+    return (max_tokens / kTileKeys + 1) * nhg <= 4LL * grid;
+}
+
+// statistics rows per head the tail kernels must merge
+int tcw_npar(int D, int HPC, int G, int64_t max_tokens, int nhg, int grid) {
+    return tcw_split(D, HPC, G, max_tokens, nhg, grid) ? 2 : 4 / HPC;
 }
 
 // Keys per K stage (the K tensor map's box rows).
@@ -567,6 +728,10 @@ bool tcw_supported(int D, int HPC, int G, int R) {
 
 cudaError_t launch_score_tcw(int D, int HPC, const CUtensorMap& qm, const CUtensorMap& km, const ScoreTcParams& p,
                              int grid, cudaStream_t stream) {
+    if (tcw_split(D, HPC, p.block_size_g, p.max_tokens, p.num_hgroups, grid)) {
+        if (D == 64) return launch_tcw<64, 4, true>(qm, km, p, grid, stream);
+        return launch_tcw<128, 4, true>(qm, km, p, grid, stream);
+    }
     if (D == 64 && HPC == 4) return launch_tcw<64, 4>(qm, km, p, grid, stream);
     if (D == 64 && HPC == 2) return launch_tcw<64, 2>(qm, km, p, grid, stream);
     if (D == 128 && HPC == 4) return launch_tcw<128, 4>(qm, km, p, grid, stream);

@@ -97,6 +97,26 @@ __device__ double block_exclusive_scan(double v, double* scratch) {
         p.dbg[k] = c_;                                                    \
     }
 
+// expand_mask (selection.cpp:36-49) of one request by its own select CTA, for small
+// capacities (kSmallExpandTokens) where the grid-wide expand_kernel's launch costs more than
+// the CTA's N_r byte stores.  Same decisions as expand_kernel; reads the block decisions this
+// CTA just published (the caller synchronises the CTA first).
+constexpr int64_t kSmallExpandTokens = 8192;
+
+__device__ void expand_request(const SelectParams& p, int r, int seg0, int N, int neff, bool enabled) {
+    const int64_t A = p.sink_count_a;
+    const int G = p.block_size_g;
+    const uint8_t* blk = p.blk_keep + p.cu_blocks[r];
+    for (int li = threadIdx.x; li < N; li += blockDim.x) {
+        uint8_t k = 1;
+        if (enabled) {
+            k = (blk[li / G] != 0 || li < A || li >= N - neff) ? 1 : 0;
+            if (k && p.veto != nullptr && p.veto[seg0 + li]) k = 0;
+        }
+        p.keep[seg0 + li] = k;
+    }
+}
+
 // Per-request epilogue shared by both select kernels: blk[] (smem) holds the block
 // decisions and sc[] the block scores.  Publishes the decisions for the expand kernel and
 // computes retained count / covered mass (selection.cpp:98-120): analytically per block
@@ -141,6 +161,10 @@ __device__ void finish_request(const SelectParams& p, int r, int seg0, int N, in
         // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g|.
         covered += static_cast<double>(sc[g]) * (static_cast<double>(kept) / static_cast<double>(size));
     }
+    if (p.fuse_expand) {
+        __syncthreads();  // the block decisions of every thread are in p.blk_keep
+        expand_request(p, r, seg0, N, neff, true);
+    }
     retained = block_sum<int>(retained, red_i);
     covered = block_sum<double>(covered, red_d);
     if (tid == 0) {
@@ -162,6 +186,12 @@ __device__ void keep_all_request(const SelectParams& p, int r, int N, int nb, in
         if (p.retained_count) p.retained_count[r] = N;
         if (p.covered_mass) p.covered_mass[r] = 1.0;
         if (p.degenerate) p.degenerate[r] = 0;
+    }
+    if (p.fuse_expand) {
+        __syncthreads();
+        const int seg0 = p.cu_seqlens[r];
+        const bool enabled = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
+        expand_request(p, r, seg0, N, min(p.query_window_n, N), enabled);
     }
 }
 
@@ -216,6 +246,149 @@ __device__ __forceinline__ bool crossing_certain(bool reached, int rc, double ra
     return certain;
 }
 
+// -DUP_SELECT_ALWAYS_SORT: always sort (A/B timing of the radix select)
+__device__ __forceinline__ bool use_radix_select() {
+#ifdef UP_SELECT_ALWAYS_SORT
+    return false;
+#else
+    return true;
+#endif
+}
+
+// ---- radix select of the crossing rank (no sort) ------------------------------------
+// The sorted order is needed only up to the crossing: k* = count(keys > K*) + t, where K*
+// is the key of rank k* and t its rank inside the tie group of equal keys (ascending block
+// index, PackedScore's ~g).  K* is found MSB-first one 8-bit digit at a time: per level a
+// shared-memory histogram of the still-candidate keys (count and double mass per digit),
+// one warp scans the 256 digits descending for the bucket where the mass above plus the
+// bucket's reaches p * total.  Ends early when the bucket holds one key.  The masses are
+// summed in an arbitrary order, so the result is accepted under the same error guard as
+// the parallel scan (crossing_certain); otherwise the caller sorts and replays exactly.
+struct RadixSel {
+    uint32_t cnt[256];
+    double mass[256];
+    uint32_t key;       // K* (or the running digit prefix)
+    int bucket;         // crossing digit of the level, -1 = p never reached
+    uint32_t bcount;    // keys in the crossing bucket
+    int cabove;         // keys strictly above the bucket
+    double above;       // their mass
+};
+
+template <int THREADS, int ITEMS>
+__device__ bool radix_crossing(const uint32_t (&key)[ITEMS], const float (&dec)[ITEMS], double total,
+                               double p_d, int nb, RadixSel& rs, int& kstar, uint32_t& kkey, int& tkeep) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const double target = p_d * total;
+    uint32_t prefix = 0, pmask = 0;
+    double above = 0.0;
+    int cabove = 0;
+    uint32_t bcount = 0;
+#pragma unroll 1
+    for (int level = 0; level < 4; ++level) {
+        const int shift = 24 - 8 * level;
+        for (int b = tid; b < 256; b += THREADS) { rs.cnt[b] = 0u; rs.mass[b] = 0.0; }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            if (key[i] != 0u && (key[i] & pmask) == prefix) {  // key 0 = padding
+                const uint32_t d = (key[i] >> shift) & 255u;
+                atomicAdd(&rs.cnt[d], 1u);
+                atomicAdd(&rs.mass[d], static_cast<double>(dec[i]));
+            }
+        }
+        __syncthreads();
+        if (tid < 32) {
+            // lane l owns digits 255 - 8l .. 248 - 8l (descending)
+            double m[8];
+            uint32_t c[8];
+            double ms = 0.0;
+            uint32_t cs = 0;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                m[x] = rs.mass[255 - 8 * lane - x];
+                c[x] = rs.cnt[255 - 8 * lane - x];
+                ms += m[x];
+                cs += c[x];
+            }
+            double mi = ms;  // inclusive scans over lanes (descending digits)
+            uint32_t ci = cs;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, mi, o);
+                const uint32_t z = __shfl_up_sync(0xffffffffu, ci, o);
+                if (lane >= o) { mi += y; ci += z; }
+            }
+            const bool hit = above + mi >= target;
+            const uint32_t hits = __ballot_sync(0xffffffffu, hit);
+            if (hits == 0u) {
+                if (lane == 0) rs.bucket = -1;
+            } else if (lane == __ffs(hits) - 1) {
+                double a = above + mi - ms;
+                uint32_t ca = static_cast<uint32_t>(cabove) + ci - cs;
+                int x = 0;
+                for (; x < 7; ++x) {
+                    if (a + m[x] >= target) break;
+                    a += m[x];
+                    ca += c[x];
+                }
+                rs.bucket = 255 - 8 * lane - x;
+                rs.bcount = c[x];
+                rs.cabove = static_cast<int>(ca);
+                rs.above = a;
+            }
+        }
+        __syncthreads();
+        const int b = rs.bucket;
+        if (b < 0) {  // the whole mass stays below p * total (within rounding): not reached
+            if (level > 0) return false;  // rounding disagreed with the level above: sort
+            above = 0.0;
+            cabove = nb;
+            bcount = 0;
+            break;
+        }
+        above = rs.above;
+        cabove = rs.cabove;
+        bcount = rs.bcount;
+        prefix |= static_cast<uint32_t>(b) << shift;
+        pmask |= 255u << shift;
+        if (bcount == 1u && level < 3) {  // one key left: it is K*
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i)
+                if (key[i] != 0u && (key[i] & pmask) == prefix) rs.key = key[i];
+            __syncthreads();
+            prefix = rs.key;
+            break;
+        }
+        __syncthreads();  // rs.* read by every thread before the next level clears it
+    }
+    bool reached = bcount > 0;
+    double ratio_c, ratio_prev = -1.0;
+    int rc;
+    if (reached) {
+        const double s = static_cast<double>(phi_decode_dev(prefix));
+        if (!(s > 0.0)) return false;  // zero-mass crossing: only rounding can get here
+        // smallest t in [1, bcount] with above + t * s >= target (t * s is exact in double)
+        double tt = ceil((target - above) / s);
+        int t = tt < 1.0 ? 1 : (tt > static_cast<double>(bcount) ? static_cast<int>(bcount) : static_cast<int>(tt));
+        kstar = cabove + t;
+        kkey = prefix;
+        tkeep = t;
+        rc = kstar - 1;
+        ratio_c = (above + static_cast<double>(t) * s) / total;
+        ratio_prev = (above + static_cast<double>(t - 1) * s) / total;
+    } else {
+        kstar = nb;
+        kkey = 0u;  // every valid key is above
+        tkeep = 0;
+        rc = nb - 1;
+        double a = 0.0;
+        for (int b = 0; b < 256; ++b) a += rs.mass[b];  // level-0 histogram = every key
+        ratio_c = a / total;
+    }
+    return crossing_certain(reached, rc, ratio_c, ratio_prev, p_d, nb);
+}
+
 // ---- CUB radix-sort variant (nb <= THREADS * ITEMS) ---------------------------------
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
@@ -229,6 +402,7 @@ select_radix_kernel(const SelectParams p) {
     using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, int32_t, UP_SELECT_RADIX_BITS>;
     constexpr int CAP = THREADS * ITEMS;
     __shared__ union {
+        RadixSel sel;
         typename Sort::TempStorage sort;
         struct { uint32_t key[CAP]; int32_t val[CAP]; } sorted;  // fallback replay only
     } u;
@@ -290,7 +464,37 @@ select_radix_kernel(const SelectParams p) {
         for (int g = tid; g < nb; g += THREADS) blk[g] = 1;
     } else {
         SEL_STAMP(1)
-        // 2. stable descending radix sort of phi(s): ties keep ascending block index, the
+        const double p_d = static_cast<double>(p.top_p);
+        // 2a. radix select of the crossing key K* and its rank t inside the tie group
+        float dsc[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) dsc[i] = val[i] >= 0 ? phi_decode_dev(key[i]) : 0.0f;
+        uint32_t kkey = 0u;
+        int tkeep = 0;
+        const bool sel_ok = use_radix_select() &&
+                            radix_crossing<THREADS, ITEMS>(key, dsc, total, p_d, nb, u.sel, kstar, kkey, tkeep);
+        __syncthreads();  // u.sel is dead past this point
+        if (sel_ok) {
+            SEL_STAMP(2)
+            // kept = key > K*, or key == K* among the first t of the tie group in block order
+            int ties = 0;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) ties += (val[i] >= 0 && key[i] == kkey) ? 1 : 0;
+            int rank = static_cast<int>(block_exclusive_scan(static_cast<double>(ties), red_d));
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                if (val[i] < 0) continue;
+                bool k = key[i] > kkey;
+                if (key[i] == kkey) k = rank++ < tkeep;
+                blk[val[i]] = k ? 1 : 0;
+            }
+            __syncthreads();
+            SEL_STAMP(4)
+            finish_request(p, r, seg0, N, nb, neff, blk, sc, kstar, degenerate, total, red_d, red_i);
+            SEL_STAMP(5)
+            return;
+        }
+        // 2b. stable descending radix sort of phi(s): ties keep ascending block index, the
         //    order of PackedScore's ~g low word (selection.cpp:27-34).
         Sort(u.sort).SortDescending(key, val);
         SEL_STAMP(2)
@@ -303,7 +507,6 @@ select_radix_kernel(const SelectParams p) {
             local += static_cast<double>(dec[i]);
         }
         const double base = block_exclusive_scan(local, red_d);
-        const double p_d = static_cast<double>(p.top_p);
         if (tid == 0) { s_kstar = nb + 1; s_ratio[0] = -1.0; s_ratio[1] = -1.0; }
         __syncthreads();
         double cum = base;
@@ -548,6 +751,8 @@ size_t select_smem_bytes(int max_blocks_per_request) {
     return static_cast<size_t>(P2) * 8 + static_cast<size_t>(max_blocks_per_request) * 5 + 16;
 }
 
+bool select_fuses_expand(int64_t max_tokens) { return max_tokens <= kSmallExpandTokens; }
+
 cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request, int num_sms,
                           cudaStream_t stream) {
     // One launch per request size class present under the capacity (the sort's cost
@@ -573,6 +778,7 @@ cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_reque
         e = launch_k(kPdlSelect, select_kernel, R, kSelThreads, smem, stream, q);
     }
     if (e != cudaSuccess) return e;
+    if (p.fuse_expand) return cudaSuccess;  // the select CTAs wrote the token masks
     static_assert(kExpandTile == 1024, "expand tiles = compaction scan tiles");
     int64_t grid = (p.max_tokens + kExpandTile - 1) / kExpandTile;  // one tile per CTA
     if (grid > num_sms * 8) grid = num_sms * 8;

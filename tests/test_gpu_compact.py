@@ -232,3 +232,50 @@ def test_compact_after_select_matches_full_scan(up, seed):
     assert torch.equal(a.retained_index[:n], b.retained_index[:n])
     for x, y in zip(a.planes, b.planes):
         assert torch.equal(x[:n], y[:n])
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_small_capacity_paths_match_large(up, seed):
+    """At capacities <= 8192 rows the select CTAs expand their own token masks (no
+    expand_kernel launch) and compaction is one launch (compact_small_kernel); the same
+    batch under a larger capacity takes the grid-wide expand + count/index/copy kernels.
+    Both must give identical keep masks, selections and compacted outputs (drop-disabled
+    segments, a veto, lengths across the 1024-row tiles)."""
+    rng = np.random.default_rng(seed)
+    lengths = [int(x) for x in rng.choice([1, 63, 700, 1024, 1025, 2000], size=4)]
+    T, R = sum(lengths), len(lengths)
+    assert T <= 8192
+    G = 64
+    nbs = [(n + G - 1) // G for n in lengths]
+    scores = torch.from_numpy((rng.random(sum(nbs)) ** 8).astype(np.float32)).cuda()
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(lengths)]), dtype=torch.int32, device="cuda")
+    cub = torch.tensor(np.concatenate([[0], np.cumsum(nbs)]), dtype=torch.int32, device="cuda")
+    en = torch.from_numpy((rng.random(R) < 0.75).astype(np.uint8)).cuda()
+    veto = torch.from_numpy((rng.random(T) < 0.05).astype(np.uint8)).cuda()
+    cfg = up.ScoreConfig(top_p=0.9)
+    hid = torch.randn(T, 40, device="cuda").to(torch.bfloat16)
+    pos = torch.arange(T, dtype=torch.int64, device="cuda")
+    outs = []
+    for cap in (T, T + 9000):
+        ws = up.Workspace("cuda")
+        sc = torch.zeros(cap // G + R + 1, dtype=torch.float32, device="cuda")
+        sc[:scores.numel()] = scores
+        sel = up.select_varlen(sc, cub, cu, cfg, veto=veto, drop_enabled=en, max_tokens=cap, workspace=ws,
+                               check=True)
+        n_sel = up.lib.up_last_launch_count()
+        planes = [torch.cat([hid, torch.zeros(cap - T, 40, dtype=hid.dtype, device="cuda")]),
+                  torch.cat([pos, torch.zeros(cap - T, dtype=pos.dtype, device="cuda")])]
+        c = up.compact_varlen(sel.keep, cu, planes, drop_enabled=en, max_tokens=cap, workspace=ws,
+                              after_select=True, check=True)
+        n_cmp = up.lib.up_last_launch_count()
+        outs.append((sel, c, n_sel, n_cmp))
+    (s0, c0, ns0, nc0), (s1, c1, ns1, nc1) = outs
+    assert (ns0, nc0) == (1, 1) and ns1 >= 2 and nc1 >= 2  # the small paths actually ran
+    assert torch.equal(s0.keep[:T], s1.keep[:T])
+    assert torch.equal(s0.cutoff_rank, s1.cutoff_rank)
+    n = int(c1.num_out.item())
+    assert int(c0.num_out.item()) == n
+    assert torch.equal(c0.cu_seqlens, c1.cu_seqlens)
+    assert torch.equal(c0.retained_index[:n], c1.retained_index[:n])
+    for x, y in zip(c0.planes, c1.planes):
+        assert torch.equal(x[:n], y[:n])

@@ -172,11 +172,13 @@ def test_score_blocks_tp_rejects_bad_degree(up):
             up.score_blocks_tp(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(), tp, up.HeadLayout(8, 2, 128))
 
 
-def test_many_requests_fallback_kernel(up, port):
-    """More segments than score_tcw plans in shared memory (R > 256): the two-warpgroup
-    kernel serves the batch; every segment still matches the oracle."""
+@pytest.mark.parametrize("R,maxlen", [(300, 400), (4100, 40)])
+def test_many_requests(up, port, R, maxlen):
+    """Continuous batches with many segments: up to 4096 (kTcwMaxRequests) score_tcw plans
+    them in shared memory; beyond, the two-warpgroup kernel serves the batch.  Every
+    sampled segment matches the oracle."""
     rng = np.random.default_rng(8)
-    lengths = [int(x) for x in rng.integers(1, 400, size=300)]
+    lengths = [int(x) for x in rng.integers(1, maxlen, size=R)]
     cfg = dict(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99)
     sb = make_batch(lengths, 8, 2, 128, 16, regime="planted", seed=8)
     res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), up.HeadLayout(8, 2, 128),
@@ -254,16 +256,24 @@ print("TC2_BAD", bad)
 '''
 
 
-def test_cta_pair_scorer_opt_in_matches_oracle(up):
-    """score_tc2 (tcgen05.mma.cta_group::2, M = 256 over a CTA pair; opt-in with UP_TC2=1,
-    see DESIGN.md 3(a)) in a child process: block scores vs the oracle within rtol 1e-3
-    for GQA-4 at D = 128, G in {32, 64, 128}, varlen and single-token segments."""
+@pytest.mark.parametrize("env,marker", [
+    ({"UP_TC2": "1"}, "pair=1"),                    # score_tc2, CTA pairs (opt-in)
+    ({"UP_TCW_SPLIT": "1"}, "wide=1 hpc=4 npar=2"),  # score_tcw, SPLIT epilogue forced
+    ({"UP_TCW_SPLIT": "0"}, "wide=1 hpc=4 npar=1"),  # score_tcw, one warpgroup per head forced
+])
+def test_scorer_variants_match_oracle(up, env, marker):
+    """The GQA-4 D = 128 scorer variants, each forced in a child process (the selection is
+    read once per process): score_tc2 (tcgen05.mma.cta_group::2, M = 256 over a CTA pair),
+    and score_tcw with either epilogue (SPLIT: two warpgroups per head, one per 64-key half,
+    each alternating between two heads; chosen automatically for small launches, see
+    DESIGN.md 3(a)).  Block scores vs the oracle within rtol 1e-3 for G in {32, 64, 128},
+    varlen and single-token segments."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", _TC2_CHILD, root], capture_output=True, text=True, timeout=600,
-                         env=dict(os.environ, UP_TC2="1", UP_SCORE_VERBOSE="1"))
+                         env=dict(os.environ, UP_SCORE_VERBOSE="1", **env))
     assert out.returncode == 0, out.stderr[-2000:]
-    assert "pair=1" in out.stderr  # the CTA-pair kernel actually ran
+    assert marker in out.stderr  # the variant actually ran
     assert "TC2_BAD []" in out.stdout, out.stdout[-2000:]

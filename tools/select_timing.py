@@ -41,3 +41,5 @@ if os.environ.get("UP_SELECT_DEBUG"):
         buf=np.zeros(16,np.uint64)
         up.lib.up_internal_select_debug(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)))
         b=buf.astype(np.int64); print(lengths[0], p, "phase cycles:", np.diff(b[:6]).tolist())
+from paper_2605_06221_b200.synthetic import loguniform_lengths
+run(loguniform_lengths(64, 4096, 131072, 5), 0.99)
