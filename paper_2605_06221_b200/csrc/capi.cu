@@ -242,7 +242,8 @@ int score_grid() {
         const char* s = std::getenv("UP_SCORE_GRID");
         return s ? std::atoi(s) : 0;
     }();
-    return grid_override > 0 ? grid_override : num_sms();
+    // at most kPwMaxRanges work ranges (the tail's shared-memory table of range boundaries)
+    return grid_override > 0 ? (grid_override < 1024 ? grid_override : 1024) : num_sms();
 }
 
 TcPlan tc_plan(const up_batch* b, const up_heads* h, const up_score_config* c, int shard_heads) {
@@ -452,8 +453,13 @@ up_status up_score_blocks(void* stream_, const up_batch* b, const up_heads* h,
 
     // TMA needs 16-byte aligned bases (strides are checked by tc_eligible)
     const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15) == 0;
-    if (aligned && tc_eligible(h, c, token_scores != nullptr))
-        return score_tc_path(stream, b, h, c, q, k, 1, nullptr, 0, block_scores, cu_blocks, L, ws);
+    if (aligned && tc_eligible(h, c, token_scores != nullptr)) {
+        st = score_tc_path(stream, b, h, c, q, k, 1, nullptr, 0, block_scores, cu_blocks, L, ws);
+        // UNSUPPORTED = the tensor-core kernels' shared-memory plan cannot hold R segments
+        // (score_tcw: 4096; score_tc: ~5900 at D = 128); nothing was enqueued, so the SIMT
+        // path below serves the batch
+        if (st != UP_ERR_UNSUPPORTED) return st;
+    }
 
     // Generic SIMT path.
     cudaError_t e = launch_blocks_plan(b->cu_seqlens, R, b->max_tokens, G, cu_blocks, err, stream);

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kCopyThreads)
 compact_small_kernel(const CompactParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
-    constexpr int PER = 4;
+    constexpr int PER = 16;  // rows per thread per chunk: one 16-byte load of the keep mask
     constexpr int CHUNK = kCopyThreads * PER;
     __shared__ int32_t idx[kSmallCompactRows];
     __shared__ int warp_tot[kCopyThreads / 32];
@@ -228,8 +228,15 @@ compact_small_kernel(const CompactParams p) {
     for (int base = 0; base < T; base += CHUNK) {
         const int i0 = base + tid * PER;
         uint32_t bits = 0;
+        if (p.drop_enabled == nullptr && i0 + PER <= T && (reinterpret_cast<uintptr_t>(p.keep + i0) & 15) == 0) {
+            const uint4 w = *reinterpret_cast<const uint4*>(p.keep + i0);  // keep bytes are 0 / 1
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int q = 0; q < PER; ++q) bits |= (row_kept(p, i0 + q, T) ? 1u : 0u) << q;
+            for (int q = 0; q < PER; ++q) bits |= ((ws[q >> 2] >> (8 * (q & 3))) & 1u) << q;
+        } else {
+#pragma unroll
+            for (int q = 0; q < PER; ++q) bits |= (row_kept(p, i0 + q, T) ? 1u : 0u) << q;
+        }
         const int cnt = __popc(bits);
         int x = cnt;
 #pragma unroll

@@ -62,6 +62,13 @@ __device__ __forceinline__ Item make_item(const Part& P, int64_t pos, int64_t en
     return it;
 }
 
+// ---------------------------------------------------------------- pair statistics
+__device__ __forceinline__ void lse_merge(float& M, float& L, float mc, float lc) {
+    if (mc == -INFINITY) return;
+    if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
+    else L += lc * ex2_approx(mc - M);
+}
+
 // Of the 16 element pairs of a 32-column group, NP evaluate 2^x with the FMA-pipe
 // polynomial (exp2_poly2) instead of MUFU.EX2.  Measured on B200: the four-warpgroup
 // scorer (score_tcw.cu) is fastest at NP = 3..5 for D = 128 (MUFU-bound) and NP = 0 for

@@ -1,6 +1,7 @@
 // score_tail.cuh -- the scorer's tail, shared by the standalone kernels (score_tc.cu) and
-// the fused cooperative path of score_tcw.cu: per-pair row weights from the per-item
-// softmax statistics, then the per-block combine over heads (and TP shards).
+// the peer-fused combine (peer.cu): per-pair row weights from the per-item softmax
+// statistics, then the per-block combine over heads (and TP shards).  (An in-kernel tail
+// behind a grid barrier in score_tcw was measured slower than the two PDL launches.)
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -13,21 +14,22 @@ namespace up {
 // scorer wrote: w[item][hh][j] = 2^(m_item - M) / (L n_eff), M = max_items m,
 // L = Σ_items l 2^(m - M) -- the softmax denominator over the full key range
 // (online_softmax_reduce pass 1, importance.cpp:41-58) assembled from the items' partial
-// denominators.  One CTA per (pair, head, 32-row chunk): warp w folds items w, w+8, ...
-// (lane = row, coalesced), the eight partial (M, L) are merged in warp order
-// (deterministic), then the warps write the weights.
-constexpr int kPwWarps = 16;
+// denominators.  One CTA per (pair, head, 32-row chunk): warp w folds items w, w+W, ...
+// (lane = row, coalesced; 4 items' loads in flight per warp), the W partial (M, L) are
+// merged in warp order (deterministic), then the warps write the weights.
+constexpr int kPwWarps = 32;
 
-__device__ __forceinline__ void lse_merge(float& M, float& L, float mc, float lc) {
-    if (mc == -INFINITY) return;
-    if (mc > M) { L = L * ex2_approx(M - mc) + lc; M = mc; }
-    else L += lc * ex2_approx(mc - M);
-}
 
 // Pair weights for tasks t0, t0 + tstep, ... (task = (pair, head, 32-row chunk)); every
 // thread of the CTA calls it (CTA barriers inside); warps >= nwarps only join the barriers.
+// rb: shared-memory table of the scorer's range boundaries range_begin(c), c <= score_grid
+// (kPwMaxRanges entries): the items of a pair are looked up there instead of by 64-bit
+// divisions per item and lane (measured: those divisions made the tail 18 us for one long
+// request spread over 148 items).
+constexpr int kPwMaxRanges = 1024;
+
 __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int64_t t0, int64_t tstep, int nwarps,
-                                                 float (*sM)[32], float (*sL)[32]) {
+                                                 float (*sM)[32], float (*sL)[32], int64_t* rb) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int R = p.num_requests, hpc = p.hpc, nhg = p.num_hgroups, npar = p.npar;
     Part P;
@@ -37,6 +39,8 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
     P.U = static_cast<int64_t>(p.cu_units[R]) * nhg;
     P.grid = p.score_grid;
     if (P.U == 0) return;  // uniform across the CTA
+    for (int c = threadIdx.x; c <= P.grid; c += blockDim.x) rb[c] = range_begin(P, c);
+    __syncthreads();
     const int64_t tasks = static_cast<int64_t>(R) * nhg * hpc * 4;
     for (int64_t t = t0; t < tasks; t += tstep) {
         const int chunk = static_cast<int>(t & 3);
@@ -55,19 +59,22 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
         // Item k = the part of the pair in CTA c_first + k; CTAs with empty ranges (more
         // CTAs than units) hold no item.
         auto sid_of = [&](int k) -> int64_t {
-            const int64_t b = range_begin(P, c_first + k);
-            if (k > 0 && b == range_begin(P, c_first + k + 1)) return -1;
+            const int64_t b = rb[c_first + k];
+            if (k > 0 && b == rb[c_first + k + 1]) return -1;
             return b > seg_start ? b : seg_start;
         };
         // statistics rows of head hh: (sid * hpc + hh) * npar + par, par < npar <= 4 (the
         // parity warpgroups of score_tcw / score_tc2 keep separate running (m, l) for one
         // head).
-        // Two items per warp iteration: their loads are issued before the merges.
+        // KB items per warp step: all their loads are issued before the merges (a pair
+        // spread over many CTAs -- one long request -- has ~148 items, so the merge is a
+        // chain of L2 round trips unless many are in flight).
+        constexpr int KB = 4;
         float M = -INFINITY, L = 0.f;
-        for (int k = warp; warp < nwarps && k < n_items; k += 2 * nwarps) {
-            float mc[8], lc[8];
+        for (int k = warp; warp < nwarps && k < n_items; k += KB * nwarps) {
+            float mc[KB * 4], lc[KB * 4];
 #pragma unroll
-            for (int x = 0; x < 2; ++x) {
+            for (int x = 0; x < KB; ++x) {
                 const int kk = k + x * nwarps;
                 const int64_t sid = kk < n_items ? sid_of(kk) : -1;
 #pragma unroll
@@ -82,7 +89,7 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
                 }
             }
 #pragma unroll
-            for (int y = 0; y < 8; ++y) lse_merge(M, L, mc[y], lc[y]);
+            for (int y = 0; y < KB * 4; ++y) lse_merge(M, L, mc[y], lc[y]);
         }
         if (warp < nwarps) {
             sM[warp][lane] = M;
@@ -96,14 +103,22 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
         const bool valid = j < neff;
         if (valid && !(L > 0.f) && warp == 0) raise_error(p.err, kErrMaskedRow);
         const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
-        for (int k = warp; warp < nwarps && k < n_items; k += nwarps) {
-            const int64_t sid = sid_of(k);
-            if (sid < 0) continue;
-            for (int q = 0; q < npar; ++q) {
-                const int64_t x = ((sid * hpc + hh) * npar + q) * kRows + j;
-                const float mc = __ldcg(&p.stat_m[x]);
-                p.stat_w[x] = mc != -INFINITY ? ex2_approx(mc - M) * inv : 0.f;
+        for (int k = warp; warp < nwarps && k < n_items; k += KB * nwarps) {
+            int64_t xs[KB * 4];
+            float mc[KB * 4];
+#pragma unroll
+            for (int x = 0; x < KB; ++x) {
+                const int kk = k + x * nwarps;
+                const int64_t sid = kk < n_items ? sid_of(kk) : -1;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    xs[x * 4 + q] = sid >= 0 && q < npar ? ((sid * hpc + hh) * npar + q) * kRows + j : -1;
+                    mc[x * 4 + q] = xs[x * 4 + q] >= 0 ? __ldcg(&p.stat_m[xs[x * 4 + q]]) : -INFINITY;
+                }
             }
+#pragma unroll
+            for (int y = 0; y < KB * 4; ++y)
+                if (xs[y] >= 0) p.stat_w[xs[y]] = mc[y] != -INFINITY ? ex2_approx(mc[y] - M) * inv : 0.f;
         }
     }
 }

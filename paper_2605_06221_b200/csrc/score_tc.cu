@@ -393,13 +393,14 @@ pair_weights_kernel(const PairWeightsParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     __shared__ float sM[kPwWarps][32], sL[kPwWarps][32];
-    pair_weights_run(p, blockIdx.x, gridDim.x, blockDim.x >> 5, sM, sL);
+    __shared__ int64_t rb[kPwMaxRanges + 1];
+    pair_weights_run(p, blockIdx.x, gridDim.x, blockDim.x >> 5, sM, sL, rb);
 }
 
 // items_per_pair: the launcher's estimate of the CTAs one pair spans (sizes the CTA).
 cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream) {
     int warps = 2;
-    while (warps < kPwWarps && 2 * warps < items_per_pair) warps *= 2;
+    while (warps < kPwWarps && 4 * warps < items_per_pair) warps *= 2;  // 4 items per warp step
     return launch_k(kPdlScore, pair_weights_kernel, grid, warps * 32, 0, stream, p);
 }
 

@@ -107,14 +107,26 @@ __device__ void expand_request(const SelectParams& p, int r, int seg0, int N, in
     const int64_t A = p.sink_count_a;
     const int G = p.block_size_g;
     const uint8_t* blk = p.blk_keep + p.cu_blocks[r];
-    for (int li = threadIdx.x; li < N; li += blockDim.x) {
-        uint8_t k = 1;
-        if (enabled) {
-            k = (blk[li / G] != 0 || li < A || li >= N - neff) ? 1 : 0;
-            if (k && p.veto != nullptr && p.veto[seg0 + li]) k = 0;
-        }
-        p.keep[seg0 + li] = k;
+    uint8_t* keep = p.keep + seg0;
+    // 16 tokens per thread step with one 16-byte store; the unaligned head and the tail bytewise
+    const int head = min(N, static_cast<int>((16 - (reinterpret_cast<uintptr_t>(keep) & 15)) & 15));
+    auto tok = [&](int li) -> uint32_t {
+        if (!enabled) return 1u;
+        uint32_t k = (blk[li / G] != 0 || li < A || li >= N - neff) ? 1u : 0u;
+        if (k && p.veto != nullptr && p.veto[seg0 + li]) k = 0u;
+        return k;
+    };
+    for (int li = threadIdx.x; li < head; li += blockDim.x) keep[li] = static_cast<uint8_t>(tok(li));
+    const int nvec = (N - head) >> 4;
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+        const int l0 = head + 16 * v;
+        uint32_t w[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+            w[x] = tok(l0 + 4 * x) | (tok(l0 + 4 * x + 1) << 8) | (tok(l0 + 4 * x + 2) << 16) | (tok(l0 + 4 * x + 3) << 24);
+        *reinterpret_cast<uint4*>(keep + l0) = make_uint4(w[0], w[1], w[2], w[3]);
     }
+    for (int li = head + 16 * nvec + threadIdx.x; li < N; li += blockDim.x) keep[li] = static_cast<uint8_t>(tok(li));
 }
 
 // Per-request epilogue shared by both select kernels: blk[] (smem) holds the block
@@ -246,145 +258,204 @@ __device__ __forceinline__ bool crossing_certain(bool reached, int rc, double ra
     return certain;
 }
 
-// -DUP_SELECT_ALWAYS_SORT: always sort (A/B timing of the radix select)
+// The radix select serves the small class (<= 512 blocks per request, 128 threads): LLaMA
+// 1x4K 11.8 -> 11.1 us, 4 x 2 blocks 8.2 -> 5.7 us, 4 x 512 blocks even (13.4 / 13.6).  In
+// the 512-thread class (<= 2048 blocks) the CUB sort stays: there the select measured slower
+// (1 x 2048 blocks 19.0 vs 20.0 us, the 64-request stream 36.3 vs 41.0 us).
+// -DUP_SELECT_ALWAYS_SORT: always sort (A/B timing).
+template <int THREADS>
 __device__ __forceinline__ bool use_radix_select() {
 #ifdef UP_SELECT_ALWAYS_SORT
     return false;
 #else
-    return true;
+    return THREADS <= 128;
 #endif
 }
 
 // ---- radix select of the crossing rank (no sort) ------------------------------------
 // The sorted order is needed only up to the crossing: k* = count(keys > K*) + t, where K*
 // is the key of rank k* and t its rank inside the tie group of equal keys (ascending block
-// index, PackedScore's ~g).  K* is found MSB-first one 8-bit digit at a time: per level a
-// shared-memory histogram of the still-candidate keys (count and double mass per digit),
-// one warp scans the 256 digits descending for the bucket where the mass above plus the
-// bucket's reaches p * total.  Ends early when the bucket holds one key.  The masses are
-// summed in an arbitrary order, so the result is accepted under the same error guard as
+// index, PackedScore's ~g).  K* is found MSB-first, 4 bits at a time, below the prefix all
+// keys share (block AND / OR): per level every thread bins its candidate keys into 16
+// register buckets (count, double mass), a warp reduce-scatter and a fixed-order sum over
+// the warps give the level's histogram -- no atomics, so clustered scores (many keys in one
+// bucket) cost nothing extra, and the sums are deterministic -- and one warp scans the 16
+// buckets descending for the one where the mass above plus the bucket's reaches p * total.
+// Ends early when the bucket holds one key.  The masses are summed in another order than
+// the reference's sequential sum, so the result is accepted under the same error guard as
 // the parallel scan (crossing_certain); otherwise the caller sorts and replays exactly.
 struct RadixSel {
-    uint32_t cnt[256];
-    double mass[256];
-    uint32_t key;       // K* (or the running digit prefix)
-    int bucket;         // crossing digit of the level, -1 = p never reached
-    uint32_t bcount;    // keys in the crossing bucket
-    int cabove;         // keys strictly above the bucket
-    double above;       // their mass
+    double wmass[32][16];  // per-warp bucket masses of the level
+    int wcnt[32][16];
+    uint32_t and_all[32], or_all[32];
+    uint32_t key;
+    int bucket;            // crossing digit of the level, -1 = p never reached
+    int bcount;            // keys in the crossing bucket
+    int cabove;            // keys strictly above the bucket
+    double above;          // their mass
+    double all;            // mass of every candidate at the first level
 };
+
+// Sum of 16 per-lane values across the warp: lane l ends with bucket (l >> 1) & 15.
+template <typename T>
+__device__ __forceinline__ T warp_reduce_scatter16(T (&v)[16]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // 16 -> 8 values (lane bit 4 picks the half kept)
+        const bool hi = lane & 16;
+        const T send = hi ? v[j] : v[j + 8];
+        const T keep = hi ? v[j + 8] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // 8 -> 4 (bit 3)
+        const bool hi = lane & 8;
+        const T send = hi ? v[j] : v[j + 4];
+        const T keep = hi ? v[j + 4] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {  // 4 -> 2 (bit 2)
+        const bool hi = lane & 4;
+        const T send = hi ? v[j] : v[j + 2];
+        const T keep = hi ? v[j + 2] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    {  // 2 -> 1 (bit 1)
+        const bool hi = lane & 2;
+        const T send = hi ? v[0] : v[1];
+        const T keep = hi ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
 
 template <int THREADS, int ITEMS>
 __device__ bool radix_crossing(const uint32_t (&key)[ITEMS], const float (&dec)[ITEMS], double total,
                                double p_d, int nb, RadixSel& rs, int& kstar, uint32_t& kkey, int& tkeep) {
-    const int tid = threadIdx.x, lane = tid & 31;
+    constexpr int WARPS = THREADS / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double target = p_d * total;
-    uint32_t prefix = 0, pmask = 0;
+    // common prefix of every valid key (key 0 = padding)
+    uint32_t a = 0xFFFFFFFFu, o = 0u;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+        if (key[i] != 0u) { a &= key[i]; o |= key[i]; }
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) {
+        a &= __shfl_xor_sync(0xffffffffu, a, x);
+        o |= __shfl_xor_sync(0xffffffffu, o, x);
+    }
+    if (lane == 0) { rs.and_all[warp] = a; rs.or_all[warp] = o; }
+    __syncthreads();
+    a = 0xFFFFFFFFu;
+    o = 0u;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) { a &= rs.and_all[w]; o |= rs.or_all[w]; }
+    const uint32_t diff = a ^ o;
+    int shift = diff == 0u ? 0 : 32 - __clz(diff);  // bits [0, shift) still undecided
+    uint32_t pmask = shift == 32 ? 0u : ~((1u << shift) - 1u);
+    uint32_t prefix = a & pmask;
     double above = 0.0;
     int cabove = 0;
-    uint32_t bcount = 0;
+    int bcount = nb;     // all keys equal (shift = 0): one tie group
+    bool first = true;
 #pragma unroll 1
-    for (int level = 0; level < 4; ++level) {
-        const int shift = 24 - 8 * level;
-        for (int b = tid; b < 256; b += THREADS) { rs.cnt[b] = 0u; rs.mass[b] = 0.0; }
-        __syncthreads();
+    while (shift > 0) {
+        const int dshift = shift > 4 ? shift - 4 : 0;
+        const uint32_t dmask = (1u << (shift - dshift)) - 1u;
+        double m[16];
+        int c[16];
+#pragma unroll
+        for (int b = 0; b < 16; ++b) { m[b] = 0.0; c[b] = 0; }
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            if (key[i] != 0u && (key[i] & pmask) == prefix) {  // key 0 = padding
-                const uint32_t d = (key[i] >> shift) & 255u;
-                atomicAdd(&rs.cnt[d], 1u);
-                atomicAdd(&rs.mass[d], static_cast<double>(dec[i]));
+            const bool cand = key[i] != 0u && (key[i] & pmask) == prefix;
+            const uint32_t d = (key[i] >> dshift) & dmask;
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const bool hit = cand && d == static_cast<uint32_t>(b);
+                m[b] += hit ? static_cast<double>(dec[i]) : 0.0;
+                c[b] += hit ? 1 : 0;
             }
         }
+        const double ms = warp_reduce_scatter16<double>(m);
+        const int cs = warp_reduce_scatter16<int>(c);
+        if ((lane & 1) == 0) { rs.wmass[warp][lane >> 1] = ms; rs.wcnt[warp][lane >> 1] = cs; }
         __syncthreads();
         if (tid < 32) {
-            // lane l owns digits 255 - 8l .. 248 - 8l (descending)
-            double m[8];
-            uint32_t c[8];
-            double ms = 0.0;
-            uint32_t cs = 0;
-#pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                m[x] = rs.mass[255 - 8 * lane - x];
-                c[x] = rs.cnt[255 - 8 * lane - x];
-                ms += m[x];
-                cs += c[x];
+            // lane l < 16 owns digit 15 - l (descending); fixed-order sum over the warps
+            double bm = 0.0;
+            int bc = 0;
+            if (lane < 16) {
+#pragma unroll 4
+                for (int w = 0; w < WARPS; ++w) { bm += rs.wmass[w][15 - lane]; bc += rs.wcnt[w][15 - lane]; }
             }
-            double mi = ms;  // inclusive scans over lanes (descending digits)
-            uint32_t ci = cs;
+            double mi = bm;
+            int ci = bc;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, mi, o);
-                const uint32_t z = __shfl_up_sync(0xffffffffu, ci, o);
-                if (lane >= o) { mi += y; ci += z; }
+            for (int x = 1; x < 16; x <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, mi, x);
+                const int z = __shfl_up_sync(0xffffffffu, ci, x);
+                if (lane >= x) { mi += y; ci += z; }
             }
-            const bool hit = above + mi >= target;
-            const uint32_t hits = __ballot_sync(0xffffffffu, hit);
+            const unsigned hits = __ballot_sync(0xffffffffu, lane < 16 && above + mi >= target);
+            if (first && lane == 15) rs.all = mi;  // every candidate: the whole mass
             if (hits == 0u) {
                 if (lane == 0) rs.bucket = -1;
             } else if (lane == __ffs(hits) - 1) {
-                double a = above + mi - ms;
-                uint32_t ca = static_cast<uint32_t>(cabove) + ci - cs;
-                int x = 0;
-                for (; x < 7; ++x) {
-                    if (a + m[x] >= target) break;
-                    a += m[x];
-                    ca += c[x];
-                }
-                rs.bucket = 255 - 8 * lane - x;
-                rs.bcount = c[x];
-                rs.cabove = static_cast<int>(ca);
-                rs.above = a;
+                rs.bucket = 15 - lane;
+                rs.bcount = bc;
+                rs.cabove = cabove + ci - bc;
+                rs.above = above + mi - bm;
             }
         }
         __syncthreads();
         const int b = rs.bucket;
         if (b < 0) {  // the whole mass stays below p * total (within rounding): not reached
-            if (level > 0) return false;  // rounding disagreed with the level above: sort
-            above = 0.0;
-            cabove = nb;
+            if (!first) return false;  // rounding disagreed with the level above: sort
             bcount = 0;
             break;
         }
         above = rs.above;
         cabove = rs.cabove;
         bcount = rs.bcount;
-        prefix |= static_cast<uint32_t>(b) << shift;
-        pmask |= 255u << shift;
-        if (bcount == 1u && level < 3) {  // one key left: it is K*
+        prefix |= static_cast<uint32_t>(b) << dshift;
+        pmask |= dmask << dshift;
+        shift = dshift;
+        first = false;
+        if (bcount == 1 && shift > 0) {  // one key left: it is K*
             __syncthreads();
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i)
                 if (key[i] != 0u && (key[i] & pmask) == prefix) rs.key = key[i];
             __syncthreads();
             prefix = rs.key;
-            break;
+            shift = 0;
         }
-        __syncthreads();  // rs.* read by every thread before the next level clears it
+        __syncthreads();  // rs.* read by every thread before the next level rewrites it
     }
-    bool reached = bcount > 0;
+    const bool reached = bcount > 0;
     double ratio_c, ratio_prev = -1.0;
     int rc;
     if (reached) {
-        const double s = static_cast<double>(phi_decode_dev(prefix));
-        if (!(s > 0.0)) return false;  // zero-mass crossing: only rounding can get here
+        const double sv = static_cast<double>(phi_decode_dev(prefix));
+        if (!(sv > 0.0)) return false;  // zero-mass crossing: only rounding can get here
         // smallest t in [1, bcount] with above + t * s >= target (t * s is exact in double)
-        double tt = ceil((target - above) / s);
-        int t = tt < 1.0 ? 1 : (tt > static_cast<double>(bcount) ? static_cast<int>(bcount) : static_cast<int>(tt));
+        const double tt = ceil((target - above) / sv);
+        const int t = tt < 1.0 ? 1 : (tt > static_cast<double>(bcount) ? bcount : static_cast<int>(tt));
         kstar = cabove + t;
         kkey = prefix;
         tkeep = t;
         rc = kstar - 1;
-        ratio_c = (above + static_cast<double>(t) * s) / total;
-        ratio_prev = (above + static_cast<double>(t - 1) * s) / total;
+        ratio_c = (above + static_cast<double>(t) * sv) / total;
+        ratio_prev = (above + static_cast<double>(t - 1) * sv) / total;
     } else {
         kstar = nb;
         kkey = 0u;  // every valid key is above
         tkeep = 0;
         rc = nb - 1;
-        double a = 0.0;
-        for (int b = 0; b < 256; ++b) a += rs.mass[b];  // level-0 histogram = every key
-        ratio_c = a / total;
+        ratio_c = rs.all / total;
     }
     return crossing_certain(reached, rc, ratio_c, ratio_prev, p_d, nb);
 }
@@ -471,7 +542,7 @@ select_radix_kernel(const SelectParams p) {
         for (int i = 0; i < ITEMS; ++i) dsc[i] = val[i] >= 0 ? phi_decode_dev(key[i]) : 0.0f;
         uint32_t kkey = 0u;
         int tkeep = 0;
-        const bool sel_ok = use_radix_select() &&
+        const bool sel_ok = use_radix_select<THREADS>() &&
                             radix_crossing<THREADS, ITEMS>(key, dsc, total, p_d, nb, u.sel, kstar, kkey, tkeep);
         __syncthreads();  // u.sel is dead past this point
         if (sel_ok) {

@@ -175,8 +175,8 @@ def test_score_blocks_tp_rejects_bad_degree(up):
 @pytest.mark.parametrize("R,maxlen", [(300, 400), (4100, 40)])
 def test_many_requests(up, port, R, maxlen):
     """Continuous batches with many segments: up to 4096 (kTcwMaxRequests) score_tcw plans
-    them in shared memory; beyond, the two-warpgroup kernel serves the batch.  Every
-    sampled segment matches the oracle."""
+    them in shared memory; beyond, the two-warpgroup kernel or, when its plan does not fit
+    either, the SIMT scorer serves the batch.  Every sampled segment matches the oracle."""
     rng = np.random.default_rng(8)
     lengths = [int(x) for x in rng.integers(1, maxlen, size=R)]
     cfg = dict(query_window_n=128, block_size_g=64, sink_count_a=128, top_p=0.99)
