@@ -130,7 +130,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--profile-stages", action="store_true", default=True)
+    ap.add_argument("--no-stages", dest="profile_stages", action="store_false",
+                    help="skip the per-stage timing (stages / roofline keys)")
     ap.add_argument("--stack", type=int, default=1,
                     help="cascaded full-attention drop layers per block (drop s+1 scores drop s's compacted stream)")
     return ap.parse_args()
@@ -815,6 +816,9 @@ def run_ours(args):
         if block_spec["reconstitute"]:
             names.append("reconstitute")
         stages = {}
+        # short configs (C1: one layer) repeat the pass inside the graph so a stage's time
+        # is its kernels' device time, not one graph launch's latency
+        reps = max(1, 32 // layers) if use_graph else 1
         for nm in names:
             def stage_pass(nm=nm):
                 sched.stage_pass(nm)
@@ -824,7 +828,8 @@ def run_ours(args):
             if use_graph:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
-                    stage_pass()
+                    for _ in range(reps):
+                        stage_pass()
                 run = g.replay
             else:
                 run = stage_pass
@@ -835,7 +840,7 @@ def run_ours(args):
                 run()
                 e1.record(stream)
             torch.cuda.synchronize(dev)
-            stages[nm] = e0.elapsed_time(e1) / (layers if nm in ("score", "select", "compact") else blocks)
+            stages[nm] = e0.elapsed_time(e1) / reps / (layers if nm in ("score", "select", "compact") else blocks)
             del run
         hbm_peak, tf_peak, peak_kind = measured_peaks()
 

@@ -40,7 +40,7 @@ struct PairWeightsParams;
 struct SlotMapParams;
 struct SequsedParams;
 struct PeerReduceParams;
-cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, int sms, cudaStream_t stream);
 cudaError_t launch_block_combine_peer(const BlockCombineParams& p, const PeerReduceParams& pr, int grid,
                                       cudaStream_t stream);
 int peer_grid(int num_sms);
@@ -426,7 +426,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
         return UP_OK;
     }
     const int64_t cgrid = (L.max_blocks + 7) / 8;  // warp per block, 8 warps per CTA
-    if ((e = launch_block_combine(bp, static_cast<int>(cgrid < num_sms() * 8 ? cgrid : num_sms() * 8), stream)) !=
+    if ((e = launch_block_combine(bp, static_cast<int>(cgrid < num_sms() * 8 ? cgrid : num_sms() * 8), num_sms(), stream)) !=
         cudaSuccess)
         return UP_ERR_CUDA;
     g_launches = 3;

@@ -252,4 +252,66 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
     }
 }
 
+// Unsharded combine with the heads of a block split over NCH warps of the CTA (8 heads per
+// warp, one batch of loads in flight each), for Hq <= 64: a block's 32 heads cost one L2
+// round trip instead of four.  The warp partials are added in chunk order by the block's
+// first warp (deterministic).  blockDim = 256: 8 / NCH blocks per CTA step.
+__device__ __forceinline__ void block_combine_chunked(const BlockCombineParams& p, float* s_part) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int R = p.num_requests;
+    const int total = p.cu_blocks[R];
+    const int nhg = p.num_heads / p.hpc;
+    const int nch = (p.num_heads + 7) / 8;           // head chunks per block (<= 8)
+    const int bpc = 8 / nch;                          // blocks per CTA step
+    const int bl = warp / nch, ch = warp - bl * nch;  // this warp's block slot and chunk
+    const int hpcv = p.hpc * p.npar;
+    for (int64_t gb0 = static_cast<int64_t>(blockIdx.x) * bpc; gb0 < total; gb0 += static_cast<int64_t>(gridDim.x) * bpc) {
+        const int64_t gbl = gb0 + bl;
+        float part = 0.f;
+        int size = 1;
+        bool pass = false;
+        if (bl < bpc && gbl < total) {
+            const int gb = static_cast<int>(gbl);
+            const int r = find_segment(p.cu_blocks, R, gb);
+            const int units_r = p.cu_units[r + 1] - p.cu_units[r];
+            pass = units_r == 0;
+            if (!pass) {
+                const int g = gb - p.cu_blocks[r];
+                const int N = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+                size = min(p.block_size_g, N - g * p.block_size_g);
+                const int u = (g * p.block_size_g) / p.unit_keys;
+                const int64_t pair0 = static_cast<int64_t>(p.cu_units[r]) * nhg;
+                const int par = p.npar > 1 ? ((g * p.block_size_g) >> p.par_shift) % p.npar : 0;
+                const int h0 = ch * 8, h1 = min(h0 + 8, p.num_heads);
+                float4 pv[8], wv[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    const int hx = min(h0 + x, h1 - 1);
+                    const int hgx = hx / p.hpc;
+                    const int64_t sid = p.unit_sid[pair0 + static_cast<int64_t>(hgx) * units_r + u];
+                    pv[x] = __ldcs(reinterpret_cast<const float4*>(p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
+                    wv[x] = __ldg(reinterpret_cast<const float4*>(
+                                p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);
+                }
+                float acc[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                    acc[x] = h0 + x < h1 ? fmaf(pv[x].x, wv[x].x, fmaf(pv[x].y, wv[x].y, fmaf(pv[x].z, wv[x].z, pv[x].w * wv[x].w)))
+                                         : 0.f;
+                part = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            }
+        }
+        if (lane == 0) s_part[warp] = part;
+        __syncthreads();
+        if (ch == 0 && lane == 0 && bl < bpc && gbl < total) {
+            float a = 0.f;
+            for (int c = 0; c < nch; ++c) a += s_part[bl * nch + c];
+            p.block_scores[gbl] = pass ? 0.f : a / static_cast<float>(size);
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace up

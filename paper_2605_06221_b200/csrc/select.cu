@@ -103,16 +103,16 @@ __device__ double block_exclusive_scan(double v, double* scratch) {
 // CTA just published (the caller synchronises the CTA first).
 constexpr int64_t kSmallExpandTokens = 8192;
 
-__device__ void expand_request(const SelectParams& p, int r, int seg0, int N, int neff, bool enabled) {
+// blk: the CTA's block decisions in shared memory, or null = every block kept.
+__device__ void expand_request(const SelectParams& p, int seg0, int N, int neff, bool enabled, const uint8_t* blk) {
     const int64_t A = p.sink_count_a;
     const int G = p.block_size_g;
-    const uint8_t* blk = p.blk_keep + p.cu_blocks[r];
     uint8_t* keep = p.keep + seg0;
     // 16 tokens per thread step with one 16-byte store; the unaligned head and the tail bytewise
     const int head = min(N, static_cast<int>((16 - (reinterpret_cast<uintptr_t>(keep) & 15)) & 15));
     auto tok = [&](int li) -> uint32_t {
         if (!enabled) return 1u;
-        uint32_t k = (blk[li / G] != 0 || li < A || li >= N - neff) ? 1u : 0u;
+        uint32_t k = (blk == nullptr || blk[li / G] != 0 || li < A || li >= N - neff) ? 1u : 0u;
         if (k && p.veto != nullptr && p.veto[seg0 + li]) k = 0u;
         return k;
     };
@@ -173,10 +173,7 @@ __device__ void finish_request(const SelectParams& p, int r, int seg0, int N, in
         // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g|.
         covered += static_cast<double>(sc[g]) * (static_cast<double>(kept) / static_cast<double>(size));
     }
-    if (p.fuse_expand) {
-        __syncthreads();  // the block decisions of every thread are in p.blk_keep
-        expand_request(p, r, seg0, N, neff, true);
-    }
+    if (p.fuse_expand) expand_request(p, seg0, N, neff, true, blk);  // blk: complete in smem (caller synced)
     retained = block_sum<int>(retained, red_i);
     covered = block_sum<double>(covered, red_d);
     if (tid == 0) {
@@ -203,14 +200,15 @@ __device__ void keep_all_request(const SelectParams& p, int r, int N, int nb, in
         __syncthreads();
         const int seg0 = p.cu_seqlens[r];
         const bool enabled = p.drop_enabled == nullptr || p.drop_enabled[r] != 0;
-        expand_request(p, r, seg0, N, min(p.query_window_n, N), enabled);
+        expand_request(p, seg0, N, min(p.query_window_n, N), enabled, nullptr);
     }
 }
 
 // The reference's exact sequential sums (selection.cpp:61-67, :84-93) replayed by one
 // thread over the sorted order; returns k*.  Bit-exact by construction.
-__device__ int exact_crossing(const float* sc, int nb, const uint32_t* skey, const int32_t* sval,
-                              double p_d) {
+// KeyAt: rank q -> phi key of the q-th largest block.
+template <class KeyAt>
+__device__ int exact_crossing_t(const float* sc, int nb, KeyAt key_at, double p_d) {
     // Both loops are serial dependency chains of double adds; the loads and float->double
     // conversions of 8 terms are issued ahead of the adds, so only the add latency remains.
     constexpr int U = 8;
@@ -233,7 +231,7 @@ __device__ int exact_crossing(const float* sc, int nb, const uint32_t* skey, con
     for (; q + U <= nb; q += U) {
         double x[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = static_cast<double>(phi_decode_dev(skey[q + u]));
+        for (int u = 0; u < U; ++u) x[u] = static_cast<double>(phi_decode_dev(key_at(q + u)));
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             c += x[u];
@@ -241,11 +239,46 @@ __device__ int exact_crossing(const float* sc, int nb, const uint32_t* skey, con
         }
     }
     for (; q < nb; ++q) {
-        c += static_cast<double>(phi_decode_dev(skey[q]));
+        c += static_cast<double>(phi_decode_dev(key_at(q)));
         if (c >= lo && c / tot >= p_d) return q + 1;
     }
-    (void)sval;
     return nb;
+}
+
+__device__ int exact_crossing(const float* sc, int nb, const uint32_t* skey, double p_d) {
+    return exact_crossing_t(sc, nb, [skey](int q) { return skey[q]; }, p_d);
+}
+
+// Tiny requests (<= kTinySelect blocks): warp 0 bitonic-sorts the packed words
+// phi(s) << 32 | ~g (descending = the reference's std::sort order, ties to the lower
+// block) in shared memory and lane 0 replays the reference's exact sequential sums -- no
+// histogram levels, no guard, bit-exact by construction.  LLaMA 1x4K (64 blocks): the
+// crossing search 7.1K -> ~2K cycles.
+constexpr int kTinySelect = 128;
+
+__device__ int tiny_crossing(const float* sc, int nb, uint64_t* w, double p_d) {
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < kTinySelect; i += 32)
+        w[i] = i < nb ? (static_cast<uint64_t>(phi_encode_dev(sc[i])) << 32) | static_cast<uint64_t>(~static_cast<uint32_t>(i))
+                      : 0ull;
+    __syncwarp();
+    int P2 = 2;
+    while (P2 < nb) P2 <<= 1;
+    for (int k = 2; k <= P2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P2; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t a = w[i], b = w[ixj];
+                    if (((i & k) == 0) ? (a < b) : (a > b)) { w[i] = b; w[ixj] = a; }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    int k = 0;
+    if (lane == 0) k = exact_crossing_t(sc, nb, [w](int q) { return static_cast<uint32_t>(w[q] >> 32); }, p_d);
+    return __shfl_sync(0xffffffffu, k, 0);
 }
 
 // Guard (see file header): the sequential ratio is monotone in the rank and within delta
@@ -474,6 +507,7 @@ select_radix_kernel(const SelectParams p) {
     constexpr int CAP = THREADS * ITEMS;
     __shared__ union {
         RadixSel sel;
+        uint64_t tiny[kTinySelect];
         typename Sort::TempStorage sort;
         struct { uint32_t key[CAP]; int32_t val[CAP]; } sorted;  // fallback replay only
     } u;
@@ -536,6 +570,21 @@ select_radix_kernel(const SelectParams p) {
     } else {
         SEL_STAMP(1)
         const double p_d = static_cast<double>(p.top_p);
+        if (nb <= kTinySelect && THREADS <= 128) {
+            // 2t. tiny request: warp-sorted words + the exact sequential replay
+            if (tid < 32) {
+                const int k = tiny_crossing(sc, nb, u.tiny, p_d);
+                if (tid == 0) s_kstar = k;
+            }
+            __syncthreads();
+            kstar = s_kstar;
+            for (int q = tid; q < nb; q += THREADS) blk[~static_cast<uint32_t>(u.tiny[q] & 0xFFFFFFFFull)] = q < kstar ? 1 : 0;
+            __syncthreads();
+            SEL_STAMP(4)
+            finish_request(p, r, seg0, N, nb, neff, blk, sc, kstar, degenerate, total, red_d, red_i);
+            SEL_STAMP(5)
+            return;
+        }
         // 2a. radix select of the crossing key K* and its rank t inside the tie group
         float dsc[ITEMS];
 #pragma unroll
@@ -610,7 +659,7 @@ select_radix_kernel(const SelectParams p) {
                 u.sorted.val[tid * ITEMS + i] = val[i];
             }
             __syncthreads();
-            if (tid == 0) s_kstar = exact_crossing(sc, nb, u.sorted.key, u.sorted.val, p_d);
+            if (tid == 0) s_kstar = exact_crossing(sc, nb, u.sorted.key, p_d);
             __syncthreads();
             kstar = s_kstar;
         }

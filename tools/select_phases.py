@@ -21,5 +21,5 @@ for N in (4096, 32768):
     torch.cuda.synchronize()
     h = (ctypes.c_ulonglong * 16)()
     up.lib.up_internal_select_debug(h)
-    st = [h[i] for i in range(6)]
-    print(f"N={N}: " + " ".join(f"{k}->{k+1}:{(st[k+1]-st[k]) if st[k+1] and st[k] else 0}" for k in range(5)), "cycles")
+    st = [(i, h[i]) for i in range(6) if h[i]]
+    print(f"N={N}: " + " ".join(f"{a}->{b}:{tb - ta}" for (a, ta), (b, tb) in zip(st, st[1:])), "cycles")
