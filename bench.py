@@ -132,6 +132,9 @@ def parse():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--no-stages", dest="profile_stages", action="store_false",
                     help="skip the per-stage timing (stages / roofline keys)")
+    ap.add_argument("--query-window", type=int, default=0,
+                    help="override the config's n (the paper's ablation: 32, 128, 512)")
+    ap.add_argument("--block-size", type=int, default=0, help="override the config's G (ablation: 32, 64, 128)")
     ap.add_argument("--stack", type=int, default=1,
                     help="cascaded full-attention drop layers per block (drop s+1 scores drop s's compacted stream)")
     return ap.parse_args()
@@ -1014,6 +1017,14 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.query_window or args.block_size:  # ablation shapes: both arms see the same config
+        model, lspec, layers, cfgd, mode = CONFIGS[args.config]
+        cfgd = dict(cfgd)
+        if args.query_window:
+            cfgd["query_window_n"] = args.query_window
+        if args.block_size:
+            cfgd["block_size_g"] = args.block_size
+        CONFIGS[args.config] = (model, lspec, layers, cfgd, mode)
     if args.impl == "reference":
         run_reference_arm(args)
     else:

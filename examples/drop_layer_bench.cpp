@@ -154,6 +154,11 @@ int main(int argc, char** argv) {
         // the keep mask is top_p_select's output on this workspace: its tile counts are reused
         b2::compact_selected(s, batch, d_keep, planes, d_cu_out, d_idx, d_nout, ws);
         launches += up_last_launch_count();
+        // block boundary (a LLaMA block = [attention (drop), FFN]): reconstitute the residual
+        // stream -- the retained rows' current states back over their pre-drop rows
+        // (reconstitute, propagation.cpp:79-100; scheduler.cpp:349-360)
+        b2::scatter_rows(s, d_idx, d_nout, T, {up_plane{o_h, d_h, int64_t(hidden) * 2, 0, 0}});
+        launches += up_last_launch_count();
     };
     layer();
     b2::check_device(s, ws);  // ContractViolation -> exception

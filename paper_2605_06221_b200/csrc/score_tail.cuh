@@ -96,10 +96,17 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
             sL[warp][lane] = L;
         }
         __syncthreads();
-        M = -INFINITY;
-        L = 0.f;
-        for (int w = 0; w < nwarps; ++w) lse_merge(M, L, sM[w][lane], sL[w][lane]);
+        if (warp == 0) {  // one warp merges the warp partials (in warp order) for every warp
+            M = -INFINITY;
+            L = 0.f;
+            for (int w = 0; w < nwarps; ++w) lse_merge(M, L, sM[w][lane], sL[w][lane]);
+            sM[0][lane] = M;
+            sL[0][lane] = L;
+        }
         __syncthreads();
+        M = sM[0][lane];
+        L = sL[0][lane];
+        __syncthreads();  // sM / sL are rewritten by the next task
         const bool valid = j < neff;
         if (valid && !(L > 0.f) && warp == 0) raise_error(p.err, kErrMaskedRow);
         const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
