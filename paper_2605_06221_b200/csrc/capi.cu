@@ -120,12 +120,30 @@ struct Layout {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Query tiles: a query window of n > 128 rows is scored as ceil(n/128) tiles of 128 rows
+// (the tcgen05 M); tile t of q-head h is the virtual head h * Tt + t.  Each row's softmax
+// is independent and the reference sums over rows (importance.cpp:41-74), so the virtual
+// heads are summed like heads, with the 1/n_eff of the whole window.
+constexpr int kMaxQTiles = 8;  // n <= 1024 on the tensor cores
+int q_tiles(const up_score_config* c) {
+    const int n = c->query_window_n > 0 ? c->query_window_n : 1;
+    return (n + kRows - 1) / kRows;
+}
+up_heads virtual_heads(const up_heads* h, int Tt) {
+    up_heads v = *h;
+    v.num_q_heads *= Tt;
+    v.gqa_group *= Tt;
+    v.q_head_offset *= Tt;
+    return v;
+}
+
 Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c) {
     Layout L{};
     const int64_t T = b->max_tokens;
     const int64_t R = b->num_requests;
     const int64_t G = c->block_size_g > 0 ? c->block_size_g : 1;
-    const int64_t H = h ? h->num_q_heads : 0;
+    // query tiles (n > 128): the scorer's P partials and statistics are per virtual head
+    const int64_t H = h ? static_cast<int64_t>(h->num_q_heads) * q_tiles(c) : 0;
     L.max_blocks = T / G + R + 1;
     // Σ_r ceil(N_r / unit) * num_hgroups * HPC * npar <= Hq * npar * (T / 128 + R): bounds
     // the item statistics rows (npar = 2 for the two-warpgroups-per-head scorer).
@@ -268,7 +286,7 @@ bool tc_eligible(const up_heads* h, const up_score_config* c, int want_tokens) {
     const int D = h->head_dim;
     if (want_tokens) return false;
     if (!(D == 64 || D == 128 || D == 256)) return false;
-    if (c->query_window_n > kRows) return false;
+    if (c->query_window_n > kRows * kMaxQTiles) return false;  // n > 128: query tiles (score_tcw only)
     if (c->block_size_g % 32 != 0) return false;
     if ((static_cast<int64_t>(h->q_row_stride) * 2) % 16 || (static_cast<int64_t>(h->k_row_stride) * 2) % 16)
         return false;
@@ -340,9 +358,12 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     const int R = b->num_requests;
     const int G = c->block_size_g;
     uint32_t* err = at<uint32_t>(ws, L.err);
-    const TcPlan plan = tc_plan(b, h, c, h->num_q_heads / tp);
+    const int Tt = q_tiles(c);
+    const up_heads hv = virtual_heads(h, Tt);  // the scorer works on virtual heads
+    const TcPlan plan = tc_plan(b, &hv, c, hv.num_q_heads / tp);
+    if (Tt > 1 && !plan.wide) return UP_ERR_UNSUPPORTED;  // query tiles: score_tcw only (nothing enqueued)
     const int hpc = plan.hpc;
-    const int nhg = h->num_q_heads / hpc;
+    const int nhg = hv.num_q_heads / hpc;
     CUtensorMap qm, km;
     if (!make_map(&qm, q, b->max_tokens, static_cast<int64_t>(h->num_q_heads) * D, h->q_row_stride, 128) ||
         !make_map(&km, k, b->max_tokens, static_cast<int64_t>(h->num_kv_heads) * D, h->k_row_stride,
@@ -371,6 +392,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     p.q_head_offset = h->q_head_offset;
     p.kv_head_offset = h->kv_head_offset;
     p.gqa_group = h->gqa_group;
+    p.q_tiles = Tt;
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
     const int grid = plan.pair ? tc2_grid(num_sms()) : score_grid();
     // work ranges: one per CTA, or one per CTA pair
@@ -395,6 +417,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     wp.npar = plan.npar;
     wp.score_grid = ranges;
     wp.query_window_n = c->query_window_n;
+    wp.q_tiles = Tt;
     const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
     const int wgrid = static_cast<int>(wtasks < num_sms() * 8 ? wtasks : num_sms() * 8);
     // CTAs one (request, head-group) pair spans, for equal-length requests
@@ -412,7 +435,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     bp.shard_stride = shard_stride;
     bp.max_blocks = L.max_blocks;
     bp.num_requests = R;
-    bp.num_heads = h->num_q_heads;
+    bp.num_heads = hv.num_q_heads;
     bp.num_shards = tp;
     bp.hpc = hpc;
     bp.npar = plan.npar;
@@ -510,8 +533,10 @@ up_status up_score_blocks_tp(void* stream_, const up_batch* b, const up_heads* h
     const Layout L = layout_for(b, h, c);
     if (ws == nullptr || ws_bytes < L.total) return UP_ERR_WORKSPACE;
     const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15) == 0;
-    if (aligned && tc_eligible(h, c, 0) && tp <= 32)  // the combine holds one shard sum per lane
-        return score_tc_path(stream, b, h, c, q, k, tp, shard_scores, shard_stride, block_scores, cu_blocks, L, ws);
+    if (aligned && tc_eligible(h, c, 0) && tp <= 32) {  // the combine holds one shard sum per lane
+        st = score_tc_path(stream, b, h, c, q, k, tp, shard_scores, shard_stride, block_scores, cu_blocks, L, ws);
+        if (st != UP_ERR_UNSUPPORTED) return st;  // else nothing was enqueued: the per-shard path below
+    }
     // Generic shapes: one SIMT scoring pass per shard, then the ordered shard sum.
     if (tp > 16) return UP_ERR_UNSUPPORTED;
     const int hps = h->num_q_heads / tp;
@@ -902,8 +927,10 @@ up_status up_score_blocks_peer(void* stream_, const up_batch* b, const up_heads*
     if ((st = peer_params(rank, tp, peer_buffers, capacity, block_scores, at<uint32_t>(ws, L.err), &pr)) != UP_OK)
         return st;
     const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15) == 0;
-    if (aligned && tc_eligible(h, c, 0))
-        return score_tc_path(stream, b, h, c, q, k, 1, nullptr, 0, block_scores, cu_blocks, L, ws, &pr);
+    if (aligned && tc_eligible(h, c, 0)) {
+        st = score_tc_path(stream, b, h, c, q, k, 1, nullptr, 0, block_scores, cu_blocks, L, ws, &pr);
+        if (st != UP_ERR_UNSUPPORTED) return st;  // else nothing was enqueued: SIMT + peer all-reduce below
+    }
     // off the tensor-core envelope: SIMT scoring, then the stand-alone peer all-reduce over
     // the capacity-sized vector (the same count on every rank)
     if ((st = up_score_blocks(stream_, b, h, c, q, k, block_scores, cu_blocks, nullptr, ws, ws_bytes)) != UP_OK)

@@ -30,6 +30,10 @@ struct ScoreTcParams {
     int32_t q_head_offset;
     int32_t kv_head_offset;
     int32_t gqa_group;
+    // query tiles: n > 128 query rows are ceil(n/128) tiles of 128 rows; tile t of local
+    // q-head h is VIRTUAL head h * q_tiles + t (num_hgroups, P and the statistics count
+    // virtual heads; q_head_offset / gqa_group above are in real heads)
+    int32_t q_tiles;
     float scale_log2;         // log2(e) / sqrt(D)
     unsigned long long* dbg;  // optional per-CTA timing [grid][4] (UP_SCORE_DEBUG), else null
 };
@@ -47,6 +51,7 @@ struct PairWeightsParams {
     int32_t npar;             // statistics rows per head (parity warpgroups of score_tcw)
     int32_t score_grid;       // the scorer's gridDim.x (defines the item ranges)
     int32_t query_window_n;
+    int32_t q_tiles;          // query tiles per q-head (virtual head = h * q_tiles + t)
 };
 
 struct BlockCombineParams {

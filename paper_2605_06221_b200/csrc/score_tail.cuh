@@ -107,7 +107,9 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
         M = sM[0][lane];
         L = sL[0][lane];
         __syncthreads();  // sM / sL are rewritten by the next task
-        const bool valid = j < neff;
+        // row j of this virtual head's query tile is window row 128 t + j
+        const int tile = p.q_tiles > 1 ? static_cast<int>((static_cast<int64_t>(hg) * hpc + hh) % p.q_tiles) : 0;
+        const bool valid = tile * kRows + j < neff;
         if (valid && !(L > 0.f) && warp == 0) raise_error(p.err, kErrMaskedRow);
         const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
         for (int k = warp; warp < nwarps && k < n_items; k += KB * nwarps) {
@@ -212,50 +214,36 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
             if (lane == 0) out(gb, red);
             continue;
         }
+        // Unsharded: heads in chunks of 8 (one batch of loads in flight), per chunk an FMA
+        // chain per head slot, a fixed tree and a warp sum, the chunk sums added in order --
+        // the same arithmetic as block_combine_chunked (so the peer-fused combine, which runs
+        // this path, stays bitwise the ascending sum of the plain scorer's partials).
         float red = 0.f;
-        for (int t = 0; t < T; ++t) {
-            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            const int hg_begin = t * hps / p.hpc, hg_end = (t + 1) * hps / p.hpc;
-            for (int hg0 = hg_begin; hg0 < hg_end; hg0 += 32) {
-                // Item ids of up to 32 head groups, one per lane, then broadcast.
-                const int my_hg = hg0 + lane;
-                const int my_sid = my_hg < hg_end ? p.unit_sid[pair0 + static_cast<int64_t>(my_hg) * units_r + u] : 0;
-                const int h_end = min((t + 1) * hps, (hg0 + 32) * p.hpc);
-                int h = hg0 * p.hpc;
-                for (; h + 8 <= h_end; h += 8) {
-                    float4 pv[8], wv[8];
+        for (int h0 = 0; h0 < p.num_heads; h0 += 8) {
+            const int h1 = min(h0 + 8, p.num_heads);
+            float4 pv[8], wv[8];
 #pragma unroll
-                    for (int x = 0; x < 8; ++x) {
-                        const int hx = h + x;
-                        const int hgx = hx / p.hpc;
-                        const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
-                        pv[x] = __ldcs(reinterpret_cast<const float4*>(
-                                    p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
-                        wv[x] = __ldg(reinterpret_cast<const float4*>(
-                                    p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);
-                    }
-#pragma unroll
-                    for (int x = 0; x < 8; ++x)
-                        acc[x] = fmaf(pv[x].x, wv[x].x, fmaf(pv[x].y, wv[x].y, fmaf(pv[x].z, wv[x].z, fmaf(pv[x].w, wv[x].w, acc[x]))));
-                }
-                for (; h < h_end; ++h) {
-                    const int hgx = h / p.hpc;
-                    const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
-                    const float4 pv = __ldcs(reinterpret_cast<const float4*>(
-                        p.P + (static_cast<int64_t>(h) * p.max_blocks + gb) * kRows) + lane);
-                    const float4 wv = __ldg(reinterpret_cast<const float4*>(
-                        p.stat_w + (sid * hpcv + (h - hgx * p.hpc) * p.npar + par) * kRows) + lane);
-                    acc[0] = fmaf(pv.x, wv.x, fmaf(pv.y, wv.y, fmaf(pv.z, wv.z, fmaf(pv.w, wv.w, acc[0]))));
-                }
+            for (int x = 0; x < 8; ++x) {
+                const int hx = min(h0 + x, h1 - 1);
+                const int hgx = hx / p.hpc;
+                const int64_t sid = p.unit_sid[pair0 + static_cast<int64_t>(hgx) * units_r + u];
+                pv[x] = __ldcs(reinterpret_cast<const float4*>(p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
+                wv[x] = __ldg(reinterpret_cast<const float4*>(
+                            p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);
             }
-            float a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+            float acc[8];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-            const float bt = a / static_cast<float>(size);
-            if (p.shard_scores != nullptr && lane == 0) p.shard_scores[static_cast<int64_t>(t) * p.shard_stride + gb] = bt;
-            red = T == 1 ? bt : red + bt;
+            for (int x = 0; x < 8; ++x)
+                acc[x] = h0 + x < h1 ? fmaf(pv[x].x, wv[x].x, fmaf(pv[x].y, wv[x].y, fmaf(pv[x].z, wv[x].z, pv[x].w * wv[x].w)))
+                                     : 0.f;
+            float part = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            red += part;
         }
-        if (lane == 0) out(gb, red);
+        const float bt = red / static_cast<float>(size);
+        if (p.shard_scores != nullptr && lane == 0) p.shard_scores[gb] = bt;
+        if (lane == 0) out(gb, bt);
     }
 }
 

@@ -205,7 +205,8 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 const int key0 = it.u0 * unit_keys;
                 const int key1 = min(it.u1 * unit_keys, N);
                 const int nst = (key1 - key0 + C::SK - 1) / C::SK;
-                const int kv_local = (p.q_head_offset + it.hg * HPC) / p.gqa_group - p.kv_head_offset;
+                const int Tt = p.q_tiles;
+                const int kv_local = (p.q_head_offset + it.hg * HPC / Tt) / p.gqa_group - p.kv_head_offset;
                 if (!C::TS) {
                     mbar_wait(q_empty, (qiter & 1) ^ 1);
                     ++qiter;
@@ -213,10 +214,12 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                     const int qrow = seg0 + N - neff;
 #pragma unroll
                     for (int hh = 0; hh < HPC; ++hh) {
+                        const int v = it.hg * HPC + hh;  // virtual head = q-head * Tt + query tile
+                        const int h = v / Tt;
 #pragma unroll
                         for (int kc = 0; kc < C::KC; ++kc)
-                            tma_load_2d(sq + (hh * C::KC + kc) * C::QSUB, &qmap, q_full,
-                                        (it.hg * HPC + hh) * D + kc * 64, qrow);
+                            tma_load_2d(sq + (hh * C::KC + kc) * C::QSUB, &qmap, q_full, h * D + kc * 64,
+                                        qrow + (v - h * Tt) * kRows);
                     }
                 }
                 for (int t = 0; t < nst; ++t) {
@@ -316,15 +319,19 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             const int key0 = it.u0 * unit_keys;
             const int key1 = min(it.u1 * unit_keys, N);
             const int nsub = (key1 - key0 + C::SK - 1) / C::SK * C::SPS;  // as issued by the MMA warp
-            const bool row_valid = j < neff;
-            const int qpos = N - neff + j;  // row j's causal limit (importance.cpp:27)
             const int64_t gb_seg = s_cu_blocks[it.r];
             const int blk0 = key0 >> gshift;
             float* Prow[2];
             float m[2], l[2];
+            bool valid2[2];
+            int qpos2[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                Prow[e] = p.P + (static_cast<int64_t>(it.hg * HPC + hp + 2 * e) * p.max_blocks + gb_seg) * kRows + j;
+                const int v = it.hg * HPC + hp + 2 * e;
+                const int jr = (v % p.q_tiles) * kRows + j;  // window row of this virtual head's row j
+                valid2[e] = jr < neff;
+                qpos2[e] = N - neff + jr;  // its causal limit (importance.cpp:27)
+                Prow[e] = p.P + (static_cast<int64_t>(v) * p.max_blocks + gb_seg) * kRows + j;
                 m[e] = -INFINITY;
                 l[e] = 0.f;
             }
@@ -334,6 +341,8 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 for (int e = 0; e < 2; ++e) {
                     const int reg = hp + 2 * e;  // NB = 1: region = head
                     const int cb = key0 + t * C::SUBN + 64 * c;  // this warpgroup's 64 keys
+                    const bool row_valid = valid2[e];
+                    const int qpos = qpos2[e];
                     mbar_wait_u32(tfull_addr + reg * 8, u & 1);
                     tc_fence_after();
                     const uint32_t taddr = tmem_base + lane_base + reg * C::SUBN + 64 * c;
@@ -417,8 +426,8 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int64_t x = (it.sid * (HPC * 2) + (hp + 2 * e) * 2 + c) * kRows + j;
-                p.stat_m[x] = row_valid ? m[e] : -INFINITY;
-                p.stat_l[x] = row_valid ? l[e] : 0.f;
+                p.stat_m[x] = valid2[e] ? m[e] : -INFINITY;
+                p.stat_l[x] = valid2[e] ? l[e] : 0.f;
             }
             for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
         }
@@ -448,11 +457,13 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             const int key0 = it.u0 * unit_keys;
             const int key1 = min(it.u1 * unit_keys, N);
             const int nsub = (key1 - key0 + C::SK - 1) / C::SK * C::SPS;  // as issued by the MMA warp
-            const bool row_valid = j < neff;
-            const int qpos = N - neff + j;  // row j's causal limit (importance.cpp:27)
+            const int vhead = it.hg * HPC + hh;                  // virtual head (q-head * Tt + tile)
+            const int jr = (vhead % p.q_tiles) * kRows + j;     // window row of this row
+            const bool row_valid = jr < neff;
+            const int qpos = N - neff + jr;  // row jr's causal limit (importance.cpp:27)
             const int64_t gb_seg = s_cu_blocks[it.r];
             const int blk0 = key0 / G;
-            float* Prow = p.P + (static_cast<int64_t>(it.hg * HPC + hh) * p.max_blocks + gb_seg) * kRows + j;
+            float* Prow = p.P + (static_cast<int64_t>(vhead) * p.max_blocks + gb_seg) * kRows + j;
             if (C::TS) {
                 // Q of this item into TMEM: warpgroup (hh, par) stores its half of head hh's
                 // D/2 columns (column c = bf16 elements 2c, 2c+1 of row j; zero rows past
@@ -461,8 +472,8 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 ++qiter;
                 tc_fence_after();
                 constexpr int COLS = D / 2 / NPAR;  // 64 at D = 256, 32 at D = 128
-                const __nv_bfloat16* qsrc = p.q + static_cast<int64_t>(seg0 + N - neff + j) * p.q_row_stride +
-                                            static_cast<int64_t>(it.hg * HPC + hh) * D + par * COLS * 2;
+                const __nv_bfloat16* qsrc = p.q + static_cast<int64_t>(seg0 + N - neff + jr) * p.q_row_stride +
+                                            static_cast<int64_t>(vhead / p.q_tiles) * D + par * COLS * 2;
 #pragma unroll
                 for (int c0 = 0; c0 < COLS; c0 += 32) {
                     uint32_t v[32];

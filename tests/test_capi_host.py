@@ -67,7 +67,10 @@ def test_scorer_dispatch():
     h = HeadsC(8, 8, 8, 1, 0, 0, 64, 64)
     assert lib.up_scorer_kind(ctypes.byref(h), ctypes.byref(ScoreConfigC(16, 8, 8, 0.9)), 0) == 2
     h = HeadsC(8, 2, 128, 4, 0, 0, 1024, 256)
-    assert lib.up_scorer_kind(ctypes.byref(h), ctypes.byref(ScoreConfigC(256, 64, 8, 0.9)), 0) == 2
+    # n > 128: query tiles on the tensor cores up to 1024 rows (8 tiles), SIMT beyond
+    assert lib.up_scorer_kind(ctypes.byref(h), ctypes.byref(ScoreConfigC(256, 64, 8, 0.9)), 0) == 1
+    assert lib.up_scorer_kind(ctypes.byref(h), ctypes.byref(ScoreConfigC(1024, 64, 8, 0.9)), 0) == 1
+    assert lib.up_scorer_kind(ctypes.byref(h), ctypes.byref(ScoreConfigC(1025, 64, 8, 0.9)), 0) == 2
 
 
 def test_entry_points_reject_bad_arguments_before_device_work():

@@ -277,3 +277,62 @@ def test_scorer_variants_match_oracle(up, env, marker):
     assert out.returncode == 0, out.stderr[-2000:]
     assert marker in out.stderr  # the variant actually ran
     assert "TC2_BAD []" in out.stdout, out.stdout[-2000:]
+
+
+_TILES_CHILD = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import oracle, paper_2605_06221_b200 as up
+from paper_2605_06221_b200.synthetic import make_batch
+port = oracle.port()
+bad = []
+for Hq, Hkv, D, lengths, n, G in [(8, 2, 128, [1000, 2000, 130], 256, 64),   # Tt = 2 < HPC
+                                  (32, 8, 128, [4096, 700], 512, 64),       # LLaMA heads, Tt = 4 = HPC
+                                  (4, 1, 128, [1500, 90], 300, 32),         # ragged last tile
+                                  (16, 2, 256, [3000, 600], 512, 64),       # Qwen3-Next heads, HPC 2 TS
+                                  (8, 4, 128, [2500], 384, 128)]:           # G = 128
+    cfg = dict(query_window_n=n, block_size_g=G, sink_count_a=128, top_p=0.99)
+    sb = make_batch(lengths, Hq, Hkv, D, 64, regime="planted", block_size_g=G, seed=sum(lengths) + n)
+    res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), up.HeadLayout(Hq, Hkv, D), check=True)
+    cu, cub, bs = sb.cu_seqlens.cpu().numpy(), res.cu_blocks.cpu().numpy(), res.block_scores.cpu().numpy().astype(np.float64)
+    for r in range(len(lengths)):
+        s, e = int(cu[r]), int(cu[r + 1])
+        _, want, _ = port.score_tokens(sb.q[s:e].float().reshape(e - s, -1).cpu().numpy(),
+                                       sb.k[s:e].float().reshape(e - s, -1).cpu().numpy(), Hq, Hkv, **cfg)
+        got = bs[cub[r]:cub[r + 1]]
+        atol = 1e-6 * max(want.sum(), 1e-30) / len(want)
+        if len(got) != len(want) or (np.abs(got - want) > 1e-3 * np.abs(want) + atol).any():
+            bad.append((Hq, Hkv, D, lengths, n, G, r))
+print("TILES_BAD", bad)
+'''
+
+
+def test_query_window_beyond_128_on_tensor_cores(up):
+    """n > 128 (the paper's n ablation: 32 / 128 / 512, PAPER.md Table 'last n'): the query
+    window is scored as ceil(n/128) tiles of 128 rows on score_tcw (tile t of q-head h =
+    virtual head h*Tt + t), not on the SIMT fallback.  Block scores vs the oracle within
+    rtol 1e-3 for Tt in {2, 3, 4}, GQA 1/2/4, D 128/256, G 32/64/128, short requests."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _TILES_CHILD, root], capture_output=True, text=True, timeout=900,
+                         env=dict(os.environ, UP_SCORE_VERBOSE="1"))
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "wide=0" not in out.stderr and "wide=1" in out.stderr  # every call on score_tcw
+    assert "TILES_BAD []" in out.stdout, out.stdout[-2000:]
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_query_tiles_tp_shards_match_reference(up, port, tp):
+    """n = 256 with TP head shards (virtual heads stay contiguous per shard): the sharded
+    scores' ascending-shard sum vs the oracle."""
+    Hq, Hkv, D, lengths = 8, 2, 128, [1500, 700]
+    cfg = dict(query_window_n=256, block_size_g=64, sink_count_a=128, top_p=0.99)
+    sb = make_batch(lengths, Hq, Hkv, D, 64, regime="planted", seed=4242)
+    res = up.score_blocks_tp(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), tp, up.HeadLayout(Hq, Hkv, D))
+    cub = res.cu_blocks.cpu().numpy()
+    bs = res.block_scores.cpu().numpy()
+    for r in range(len(lengths)):
+        _, want = _oracle_blocks(port, sb, r, Hq, Hkv, cfg)
+        _assert_blocks_close(bs[cub[r]:cub[r + 1]], want)
