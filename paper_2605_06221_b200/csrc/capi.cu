@@ -129,6 +129,28 @@ int q_tiles(const up_score_config* c) {
     const int n = c->query_window_n > 0 ? c->query_window_n : 1;
     return (n + kRows - 1) / kRows;
 }
+// Query-row packing: a window of n <= 64 rows leaves most of a 128-row S tile empty, so P
+// q-heads of one kv-group share it -- virtual head v holds q-heads [vP, vP + P), row r
+// being window row r % (128/P) of q-head vP + r / (128/P).  Served by score_tcw's TS
+// variant (Q loaded row by row by the epilogue threads), i.e. two virtual heads per
+// kv-head at D >= 128: P = the largest power of two with P * npad <= 128 and 2P | gqa.
+int q_pack(const up_heads* h, const up_score_config* c, int shard_heads) {
+    const int n = c->query_window_n;
+    if (n > 64 || h->head_dim < 128) return 1;
+    int npad = 1;
+    while (npad < n) npad <<= 1;
+    int P = kRows / npad;
+    while (P > 1 && (h->gqa_group % (2 * P) || h->num_q_heads % P || h->q_head_offset % P || shard_heads % (2 * P)))
+        P >>= 1;
+    return P;
+}
+up_heads packed_heads(const up_heads* h, int P) {
+    up_heads v = *h;
+    v.num_q_heads /= P;
+    v.gqa_group /= P;
+    v.q_head_offset /= P;
+    return v;
+}
 up_heads virtual_heads(const up_heads* h, int Tt) {
     up_heads v = *h;
     v.num_q_heads *= Tt;
@@ -358,9 +380,16 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     const int R = b->num_requests;
     const int G = c->block_size_g;
     uint32_t* err = at<uint32_t>(ws, L.err);
+    // the scorer works on virtual heads: query tiles (n > 128) or packed heads (n <= 64)
     const int Tt = q_tiles(c);
-    const up_heads hv = virtual_heads(h, Tt);  // the scorer works on virtual heads
-    const TcPlan plan = tc_plan(b, &hv, c, hv.num_q_heads / tp);
+    int Pk = Tt == 1 && !std::getenv("UP_NO_QPACK") ? q_pack(h, c, h->num_q_heads / tp) : 1;
+    up_heads hv = Pk > 1 ? packed_heads(h, Pk) : virtual_heads(h, Tt);
+    TcPlan plan = tc_plan(b, &hv, c, hv.num_q_heads / tp);
+    if (Pk > 1 && !(plan.wide && plan.hpc == 2)) {  // packing needs score_tcw's TS variant
+        Pk = 1;
+        hv = *h;
+        plan = tc_plan(b, &hv, c, hv.num_q_heads / tp);
+    }
     if (Tt > 1 && !plan.wide) return UP_ERR_UNSUPPORTED;  // query tiles: score_tcw only (nothing enqueued)
     const int hpc = plan.hpc;
     const int nhg = hv.num_q_heads / hpc;
@@ -393,13 +422,15 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     p.kv_head_offset = h->kv_head_offset;
     p.gqa_group = h->gqa_group;
     p.q_tiles = Tt;
+    p.q_pack = Pk;
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
     const int grid = plan.pair ? tc2_grid(num_sms()) : score_grid();
     // work ranges: one per CTA, or one per CTA pair
     const int ranges = plan.pair ? grid / 2 : grid;
     p.dbg = score_debug_buffer();
     if (std::getenv("UP_SCORE_VERBOSE"))
-        fprintf(stderr, "scorer: pair=%d wide=%d hpc=%d npar=%d grid=%d\n", plan.pair, plan.wide, hpc, plan.npar, grid);
+        fprintf(stderr, "scorer: pair=%d wide=%d hpc=%d npar=%d grid=%d tiles=%d pack=%d\n", plan.pair, plan.wide, hpc,
+                plan.npar, grid, Tt, Pk);
     cudaError_t e = plan.pair ? launch_score_tc2(qm, km, p, grid, stream)
                     : plan.wide ? launch_score_tcw(D, hpc, qm, km, p, grid, stream)
                                 : launch_score_tc(D, hpc, qm, km, p, grid, stream);
@@ -418,6 +449,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     wp.score_grid = ranges;
     wp.query_window_n = c->query_window_n;
     wp.q_tiles = Tt;
+    wp.q_pack = Pk;
     const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
     const int wgrid = static_cast<int>(wtasks < num_sms() * 8 ? wtasks : num_sms() * 8);
     // CTAs one (request, head-group) pair spans, for equal-length requests

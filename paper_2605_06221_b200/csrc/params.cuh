@@ -34,6 +34,10 @@ struct ScoreTcParams {
     // q-head h is VIRTUAL head h * q_tiles + t (num_hgroups, P and the statistics count
     // virtual heads; q_head_offset / gqa_group above are in real heads)
     int32_t q_tiles;
+    // query-row packing (n <= 64, the TS variant): q_pack q-heads of one kv-group share a
+    // 128-row S tile -- row r of virtual head v is window row r % (128 / q_pack) of q-head
+    // v * q_pack + r / (128 / q_pack); 1 = no packing (exclusive with q_tiles > 1)
+    int32_t q_pack;
     float scale_log2;         // log2(e) / sqrt(D)
     unsigned long long* dbg;  // optional per-CTA timing [grid][4] (UP_SCORE_DEBUG), else null
 };
@@ -52,6 +56,7 @@ struct PairWeightsParams {
     int32_t score_grid;       // the scorer's gridDim.x (defines the item ranges)
     int32_t query_window_n;
     int32_t q_tiles;          // query tiles per q-head (virtual head = h * q_tiles + t)
+    int32_t q_pack;           // q-heads packed per virtual head (row r -> window row r % (128 / q_pack))
 };
 
 struct BlockCombineParams {

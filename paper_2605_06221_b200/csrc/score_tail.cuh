@@ -109,7 +109,8 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
         __syncthreads();  // sM / sL are rewritten by the next task
         // row j of this virtual head's query tile is window row 128 t + j
         const int tile = p.q_tiles > 1 ? static_cast<int>((static_cast<int64_t>(hg) * hpc + hh) % p.q_tiles) : 0;
-        const bool valid = tile * kRows + j < neff;
+        const int jr = p.q_pack > 1 ? j % (kRows / p.q_pack) : tile * kRows + j;  // window row
+        const bool valid = jr < neff;
         if (valid && !(L > 0.f) && warp == 0) raise_error(p.err, kErrMaskedRow);
         const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
         for (int k = warp; warp < nwarps && k < n_items; k += KB * nwarps) {

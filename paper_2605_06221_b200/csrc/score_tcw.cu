@@ -206,7 +206,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 const int key1 = min(it.u1 * unit_keys, N);
                 const int nst = (key1 - key0 + C::SK - 1) / C::SK;
                 const int Tt = p.q_tiles;
-                const int kv_local = (p.q_head_offset + it.hg * HPC / Tt) / p.gqa_group - p.kv_head_offset;
+                const int kv_local = (p.q_head_offset + it.hg * HPC * p.q_pack / Tt) / p.gqa_group - p.kv_head_offset;
                 if (!C::TS) {
                     mbar_wait(q_empty, (qiter & 1) ^ 1);
                     ++qiter;
@@ -458,7 +458,10 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             const int key1 = min(it.u1 * unit_keys, N);
             const int nsub = (key1 - key0 + C::SK - 1) / C::SK * C::SPS;  // as issued by the MMA warp
             const int vhead = it.hg * HPC + hh;                  // virtual head (q-head * Tt + tile)
-            const int jr = (vhead % p.q_tiles) * kRows + j;     // window row of this row
+            // window row of this row, and (packing) which q-head of the virtual head it is
+            const int npad = kRows / p.q_pack;
+            const int jr = p.q_pack > 1 ? j % npad : (vhead % p.q_tiles) * kRows + j;
+            const int qhead = p.q_pack > 1 ? vhead * p.q_pack + j / npad : vhead / p.q_tiles;
             const bool row_valid = jr < neff;
             const int qpos = N - neff + jr;  // row jr's causal limit (importance.cpp:27)
             const int64_t gb_seg = s_cu_blocks[it.r];
@@ -473,7 +476,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 tc_fence_after();
                 constexpr int COLS = D / 2 / NPAR;  // 64 at D = 256, 32 at D = 128
                 const __nv_bfloat16* qsrc = p.q + static_cast<int64_t>(seg0 + N - neff + jr) * p.q_row_stride +
-                                            static_cast<int64_t>(vhead / p.q_tiles) * D + par * COLS * 2;
+                                            static_cast<int64_t>(qhead) * D + par * COLS * 2;
 #pragma unroll
                 for (int c0 = 0; c0 < COLS; c0 += 32) {
                     uint32_t v[32];

@@ -210,3 +210,17 @@ def test_one_million_token_request_tp_rank(up, port, ref):
     sb = make_batch(lengths, 2, 1, 256, 512, regime="planted", seed=15)
     rho = _check_layer(up, port, sb, 2, 1, 256, lengths, CFG, ref=ref, ref_requests=(0,), ref_tp=2)
     assert 0.05 < rho < 0.8
+
+
+def test_llama_32k_query_window_512(up, port, ref):
+    """The paper's n = 512 ablation at a BASELINE request length (LLaMA-3.1-8B shape, 2 x
+    32K): the query-tile scorer (4 tiles of 128 rows per q-head as virtual heads) vs an fp64
+    restatement (request 0) and end to end vs the reference (request 1, its heads as 8
+    shards on host threads)."""
+    shp = MODEL_SHAPES["llama3.1-8b"]
+    lengths = [32768] * 2
+    cfg = dict(CFG, query_window_n=512)
+    sb = make_batch(lengths, shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"], shp["hidden"],
+                    regime="planted", seed=16)
+    _check_layer(up, port, sb, shp["num_q_heads"], shp["num_kv_heads"], shp["head_dim"], lengths, cfg,
+                 exact_requests=(0,), ref=ref, ref_requests=(1,), ref_tp=8)

@@ -336,3 +336,47 @@ def test_query_tiles_tp_shards_match_reference(up, port, tp):
     for r in range(len(lengths)):
         _, want = _oracle_blocks(port, sb, r, Hq, Hkv, cfg)
         _assert_blocks_close(bs[cub[r]:cub[r + 1]], want)
+
+
+_PACK_CHILD = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import oracle, paper_2605_06221_b200 as up
+from paper_2605_06221_b200.synthetic import make_batch
+port = oracle.port()
+bad = []
+for Hq, Hkv, D, lengths, n, G in [(8, 2, 128, [1000, 2000, 40], 32, 64),    # GQA 4: 2 heads per tile
+                                  (8, 2, 128, [1500, 63], 64, 32),          # n = 64
+                                  (16, 2, 256, [3000, 700], 32, 64),        # Qwen3-Next heads: 4 per tile
+                                  (8, 2, 128, [900, 5], 20, 64),            # npad 32, short requests
+                                  (8, 2, 128, [777], 1, 64)]:               # n = 1
+    cfg = dict(query_window_n=n, block_size_g=G, sink_count_a=128, top_p=0.99)
+    sb = make_batch(lengths, Hq, Hkv, D, 64, regime="planted", block_size_g=G, seed=sum(lengths) + 3 * n)
+    res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(**cfg), up.HeadLayout(Hq, Hkv, D), check=True)
+    cu, cub, bs = sb.cu_seqlens.cpu().numpy(), res.cu_blocks.cpu().numpy(), res.block_scores.cpu().numpy().astype(np.float64)
+    for r in range(len(lengths)):
+        s, e = int(cu[r]), int(cu[r + 1])
+        _, want, _ = port.score_tokens(sb.q[s:e].float().reshape(e - s, -1).cpu().numpy(),
+                                       sb.k[s:e].float().reshape(e - s, -1).cpu().numpy(), Hq, Hkv, **cfg)
+        got = bs[cub[r]:cub[r + 1]]
+        atol = 1e-6 * max(want.sum(), 1e-30) / len(want)
+        if len(got) != len(want) or (np.abs(got - want) > 1e-3 * np.abs(want) + atol).any():
+            bad.append((Hq, Hkv, D, lengths, n, G, r))
+print("PACK_BAD", bad)
+'''
+
+
+def test_short_query_window_packs_heads_into_one_tile(up):
+    """n <= 64 (the paper's n = 32 ablation): P q-heads of a kv-group share one 128-row S
+    tile (score_tcw's TS variant loads each row's Q from its own head), so a 32-row window
+    does not pay for 128 rows.  Block scores vs the oracle within rtol 1e-3; the child
+    process asserts packing served every call."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _PACK_CHILD, root], capture_output=True, text=True, timeout=900,
+                         env=dict(os.environ, UP_SCORE_VERBOSE="1"))
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "pack=1" not in out.stderr and "pack=" in out.stderr
+    assert "PACK_BAD []" in out.stdout, out.stdout[-2000:]
