@@ -95,7 +95,7 @@ up_status cuda_status(cudaError_t e) { return e == cudaSuccess ? UP_OK : UP_ERR_
 unsigned long long* score_debug_buffer() {
     static unsigned long long* d = [] {
         unsigned long long* x = nullptr;
-        if (std::getenv("UP_SCORE_DEBUG")) cudaMalloc(&x, sizeof(unsigned long long) * 4 * 4096);
+        if (std::getenv("UP_SCORE_DEBUG")) cudaMalloc(&x, sizeof(unsigned long long) * 8 * 4096);
         return x;
     }();
     return d;
@@ -428,6 +428,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     // work ranges: one per CTA, or one per CTA pair
     const int ranges = plan.pair ? grid / 2 : grid;
     p.dbg = score_debug_buffer();
+    if (p.dbg != nullptr) cudaMemsetAsync(p.dbg + 4 * 4096, 0, sizeof(unsigned long long) * 4 * 4096, stream);
     if (std::getenv("UP_SCORE_VERBOSE"))
         fprintf(stderr, "scorer: pair=%d wide=%d hpc=%d npar=%d grid=%d tiles=%d pack=%d\n", plan.pair, plan.wide, hpc,
                 plan.npar, grid, Tt, Pk);
@@ -1006,6 +1007,16 @@ extern "C" int up_internal_select_debug(unsigned long long* host) {
 
 // Diagnostics (not part of the ABI header): copy the scorer's per-CTA timing records
 // [cta][start_ns, end_ns, units, smid] of the last launch to host memory.
+// Diagnostics: score_tcw's per-CTA phase clocks [cta][first Q landed (MMA warp), first S
+// region drained start (epilogue warp 2), first item done (epilogue warp 2), -].
+extern "C" int up_internal_score_phases(unsigned long long* host, int max_ctas) {
+    unsigned long long* d = score_debug_buffer();
+    if (d == nullptr || host == nullptr) return -1;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+    return cudaMemcpy(host, d + 4 * 4096, sizeof(unsigned long long) * 4 * max_ctas, cudaMemcpyDeviceToHost) ==
+                   cudaSuccess ? 0 : -3;
+}
+
 extern "C" int up_internal_score_debug(unsigned long long* host, int max_ctas) {
     unsigned long long* d = score_debug_buffer();
     if (d == nullptr || host == nullptr) return -1;

@@ -89,6 +89,14 @@ static __device__ __noinline__ void rescale_rows_par(float* prow, int g0, int g1
         if (((g * G) >> 6) % npar == par) prow[static_cast<int64_t>(g) * kRows] *= f;
 }
 
+// UP_SCORE_DEBUG phase clocks (second region of the debug buffer): slot k of this CTA
+#define TCW_PHASE(k)                                                                   \
+    if (p.dbg != nullptr) {                                                            \
+        unsigned long long t_;                                                         \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+        if (p.dbg[4 * 4096 + blockIdx.x * 4 + (k)] == 0ull) p.dbg[4 * 4096 + blockIdx.x * 4 + (k)] = t_; \
+    }
+
 template <int D, int HPC, bool SPLIT>
 __global__ void __launch_bounds__(576, 1)
 score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
@@ -256,6 +264,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 mbar_wait(q_full, qiter & 1);
                 ++qiter;
                 tc_fence_after();
+                TCW_PHASE(0)
                 for (int t = 0; t < nst; ++t) {
                     mbar_wait(&k_full[stage], phase);
                     tc_fence_after();
@@ -345,6 +354,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                     const int qpos = qpos2[e];
                     mbar_wait_u32(tfull_addr + reg * 8, u & 1);
                     tc_fence_after();
+                    if (warp == 2 && lane == 0) TCW_PHASE(1)
                     const uint32_t taddr = tmem_base + lane_base + reg * C::SUBN + 64 * c;
                     float gs0 = 0.f, gs1 = 0.f;
                     bool redo;
@@ -430,6 +440,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 p.stat_l[x] = valid2[e] ? l[e] : 0.f;
             }
             for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
+            if (warp == 2 && lane == 0) TCW_PHASE(2)
         }
     } else {
         // ===== epilogue: warpgroup wg -> head hh, subtile parity par; thread = query row =====
@@ -544,6 +555,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 }
                 mbar_wait(&t_full[reg], (u / NB) & 1);
                 tc_fence_after();
+                if (warp == 2 && lane == 0) TCW_PHASE(1)
                 const uint32_t taddr = tmem_base + lane_base + C::Q_COLS + reg * C::SUBN;
                 // Fast path (warp-uniform): all 64 keys inside the segment and left of every
                 // row's causal limit -> two packed group sums and one overflow check.  The
@@ -674,6 +686,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 p.stat_l[x] = row_valid ? l : 0.f;
             }
             for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
+            if (warp == 2 && lane == 0) TCW_PHASE(2)
         }
     }
 

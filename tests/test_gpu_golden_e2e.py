@@ -203,9 +203,14 @@ def test_tp_head_sharded_scores_and_ordered_reduce(up, port):
         assert np.array_equal(red.cpu().numpy(), want)  # ascending-rank fp32 order, bitwise
         sel = up.select_varlen(red, full.cu_blocks, sb.cu_seqlens, cfg, check=True)
         keeps.append(sel.keep.cpu().numpy())
-    # c8: identical selection for every TP degree, except in the fp32 tie band
+        if tp == 1:
+            red1 = red.cpu().numpy()
+            cut1 = red1[np.argsort(-red1, kind="stable")[int(sel.cutoff_rank[0]) - 1]]
+    # c8 (acceptance_main.cpp:445-478): identical selection for every TP degree -- tokens may
+    # differ only in blocks whose TP=1 score lies within rtol of the TP=1 cutoff score (the
+    # shard sums round differently, the tie band of north-star rule 2)
     for k in keeps[1:]:
-        assert (k != keeps[0]).sum() <= 64
+        assert _tie_band_ok(k, keeps[0], red1, 64, cut1)
 
 
 def test_cuda_graph_capture_of_drop_layer(up):

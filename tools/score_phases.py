@@ -24,3 +24,9 @@ ends = sorted((r[1] - t0) / 1e3 for r in rec)
 units = sorted(r[2] for r in rec)
 print(f"lengths={L}: start spread {starts[0]:.2f}..{starts[-1]:.2f} us; CTA span min/med/max "
       f"{durs[0]:.2f}/{durs[len(durs)//2]:.2f}/{durs[-1]:.2f} us; last end {ends[-1]:.2f} us; units/CTA {units[0]}..{units[-1]}")
+ph = (ctypes.c_ulonglong * (4 * n))()
+if up.lib.up_internal_score_phases(ph, n) == 0:
+    for k, name in enumerate(["Q landed (MMA warp)", "first S region (epilogue)", "first item done"]):
+        d = sorted((ph[4 * i + k] - rec[i][0]) / 1e3 for i in range(n) if ph[4 * i + k])
+        if d:
+            print(f"  {name}: min/med/max {d[0]:.2f}/{d[len(d)//2]:.2f}/{d[-1]:.2f} us after CTA start")
