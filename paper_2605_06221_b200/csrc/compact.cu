@@ -130,11 +130,11 @@ compact_index_kernel(const CompactParams p) {
     }
 }
 
-// One warp copies row src_row of every plane to row dst_row: 16-byte streaming vectors, a
+// One warp copies row src_row of plane pl to row dst_row: 16-byte streaming vectors, a
 // batch of 8 in flight per lane (scalar fallbacks for unaligned planes).
-__device__ __forceinline__ void copy_row_planes(const CompactParams& p, int64_t src_row, int64_t dst_row, int lane) {
-#pragma unroll 1
-    for (int pl = 0; pl < p.num_planes; ++pl) {
+__device__ __forceinline__ void copy_row_plane(const CompactParams& p, int pl, int64_t src_row, int64_t dst_row,
+                                               int lane) {
+    {
         const int64_t rb = p.row_bytes[pl];
         const uint8_t* src = p.src[pl] + src_row * p.src_stride[pl];
         uint8_t* dst = p.dst[pl] + dst_row * p.dst_stride[pl];
@@ -165,6 +165,12 @@ __device__ __forceinline__ void copy_row_planes(const CompactParams& p, int64_t 
             for (int64_t b = lane; b < rb; b += 32) dst[b] = src[b];
         }
     }
+}
+
+// Every plane of a row, one after the other (the large-batch copy: bandwidth-bound).
+__device__ __forceinline__ void copy_row_planes(const CompactParams& p, int64_t src_row, int64_t dst_row, int lane) {
+#pragma unroll 1
+    for (int pl = 0; pl < p.num_planes; ++pl) copy_row_plane(p, pl, src_row, dst_row, lane);
 }
 
 // Gather: output row o <- source row retained_index[o] (persistent grid, warp per row).
@@ -274,9 +280,13 @@ compact_small_kernel(const CompactParams p) {
         if (p.num_out) *p.num_out = carry;
     }
     if (p.num_planes == 0) return;
+    // latency-bound: one warp per (row, plane), so a row's planes travel in parallel
     const int gw = (blockIdx.x * kCopyThreads + tid) >> 5;
     const int nw = (gridDim.x * kCopyThreads) >> 5;
-    for (int o = gw; o < carry; o += nw) copy_row_planes(p, idx[o], o, lane);
+    for (int t = gw; t < carry * p.num_planes; t += nw) {
+        const int o = t / p.num_planes;
+        copy_row_plane(p, t - o * p.num_planes, idx[o], o, lane);
+    }
 }
 
 bool compact_is_small(int64_t max_tokens) { return max_tokens <= kSmallCompactRows; }
@@ -304,8 +314,8 @@ cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t str
     const int64_t tiles = (p.max_tokens + kCompactTile - 1) / kCompactTile;
     cudaError_t e = cudaSuccess;
     if (compact_is_small(p.max_tokens)) {
-        int64_t grid = (p.max_tokens + kCopyThreads / 32 - 1) / (kCopyThreads / 32);  // warp per row at most
-        if (grid > 2LL * num_sms) grid = 2LL * num_sms;
+        int64_t grid = (p.max_tokens * p.num_planes + kCopyThreads / 32 - 1) / (kCopyThreads / 32);  // warp per (row, plane)
+        if (grid > 4LL * num_sms) grid = 4LL * num_sms;
         return launch_k(kPdlCompact, compact_small_kernel, static_cast<unsigned>(grid < 1 ? 1 : grid), kCopyThreads,
                         0, stream, p);
     }

@@ -118,12 +118,33 @@ __device__ void expand_request(const SelectParams& p, int seg0, int N, int neff,
     };
     for (int li = threadIdx.x; li < head; li += blockDim.x) keep[li] = static_cast<uint8_t>(tok(li));
     const int nvec = (N - head) >> 4;
+    const int64_t win0 = N - neff;
+    const int nbk = (N + G - 1) / G;
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
         const int l0 = head + 16 * v;
         uint32_t w[4];
+        if (enabled && G >= 16 && p.veto == nullptr) {
+            // 16 tokens touch at most two blocks: two decisions instead of 16 divisions
+            const int b0 = l0 / G;
+            const int edge = (b0 + 1) * G;
+            const uint32_t k0 = blk == nullptr || blk[b0] != 0;
+            const uint32_t k1 = blk == nullptr || blk[min(b0 + 1, nbk - 1)] != 0;
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-            w[x] = tok(l0 + 4 * x) | (tok(l0 + 4 * x + 1) << 8) | (tok(l0 + 4 * x + 2) << 16) | (tok(l0 + 4 * x + 3) << 24);
+            for (int x = 0; x < 4; ++x) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int y = 0; y < 4; ++y) {
+                    const int li = l0 + 4 * x + y;
+                    const uint32_t k = (li < edge ? k0 : k1) | (li < A ? 1u : 0u) | (li >= win0 ? 1u : 0u);
+                    word |= k << (8 * y);
+                }
+                w[x] = word;
+            }
+        } else {
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+                w[x] = tok(l0 + 4 * x) | (tok(l0 + 4 * x + 1) << 8) | (tok(l0 + 4 * x + 2) << 16) | (tok(l0 + 4 * x + 3) << 24);
+        }
         *reinterpret_cast<uint4*>(keep + l0) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     for (int li = head + 16 * nvec + threadIdx.x; li < N; li += blockDim.x) keep[li] = static_cast<uint8_t>(tok(li));
@@ -170,12 +191,17 @@ __device__ void finish_request(const SelectParams& p, int r, int seg0, int N, in
             }
         }
         retained += kept;
-        // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g|.
-        covered += static_cast<double>(sc[g]) * (static_cast<double>(kept) / static_cast<double>(size));
+        // covered_mass attribution (selection.cpp:108-120): s_g * kept_g / |g| -- the ratio
+        // is exactly 1 or 0 for whole blocks, so only partially kept blocks divide
+        const double frac = kept == size ? 1.0 : (kept == 0 ? 0.0 : static_cast<double>(kept) / static_cast<double>(size));
+        covered += static_cast<double>(sc[g]) * frac;
     }
+    SEL_STAMP(6)
     if (p.fuse_expand) expand_request(p, seg0, N, neff, true, blk);  // blk: complete in smem (caller synced)
+    SEL_STAMP(7)
     retained = block_sum<int>(retained, red_i);
     covered = block_sum<double>(covered, red_d);
+    SEL_STAMP(8)
     if (tid == 0) {
         p.cutoff_rank[r] = kstar;
         if (p.retained_count) p.retained_count[r] = retained;
@@ -249,37 +275,6 @@ __device__ int exact_crossing(const float* sc, int nb, const uint32_t* skey, dou
     return exact_crossing_t(sc, nb, [skey](int q) { return skey[q]; }, p_d);
 }
 
-// Tiny requests (<= kTinySelect blocks): warp 0 bitonic-sorts the packed words
-// phi(s) << 32 | ~g (descending = the reference's std::sort order, ties to the lower
-// block) in shared memory and lane 0 replays the reference's exact sequential sums -- no
-// histogram levels, no guard, bit-exact by construction.  LLaMA 1x4K (64 blocks): the
-// crossing search 7.1K -> ~2K cycles.
-constexpr int kTinySelect = 128;
-
-__device__ int tiny_crossing(const float* sc, int nb, uint64_t* w, double p_d) {
-    const int lane = threadIdx.x & 31;
-    for (int i = lane; i < kTinySelect; i += 32)
-        w[i] = i < nb ? (static_cast<uint64_t>(phi_encode_dev(sc[i])) << 32) | static_cast<uint64_t>(~static_cast<uint32_t>(i))
-                      : 0ull;
-    __syncwarp();
-    int P2 = 2;
-    while (P2 < nb) P2 <<= 1;
-    for (int k = 2; k <= P2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = lane; i < P2; i += 32) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const uint64_t a = w[i], b = w[ixj];
-                    if (((i & k) == 0) ? (a < b) : (a > b)) { w[i] = b; w[ixj] = a; }
-                }
-            }
-            __syncwarp();
-        }
-    }
-    int k = 0;
-    if (lane == 0) k = exact_crossing_t(sc, nb, [w](int q) { return static_cast<uint32_t>(w[q] >> 32); }, p_d);
-    return __shfl_sync(0xffffffffu, k, 0);
-}
 
 // Guard (see file header): the sequential ratio is monotone in the rank and within delta
 // of the parallel one; accept the parallel crossing only when it clears p by delta.
@@ -296,12 +291,15 @@ __device__ __forceinline__ bool crossing_certain(bool reached, int rc, double ra
 // the 512-thread class (<= 2048 blocks) the CUB sort stays: there the select measured slower
 // (1 x 2048 blocks 19.0 vs 20.0 us, the 64-request stream 36.3 vs 41.0 us).
 // -DUP_SELECT_ALWAYS_SORT: always sort (A/B timing).
+#ifndef UP_SELECT_RADIX_MAX_THREADS
+#define UP_SELECT_RADIX_MAX_THREADS 128
+#endif
 template <int THREADS>
 __device__ __forceinline__ bool use_radix_select() {
 #ifdef UP_SELECT_ALWAYS_SORT
     return false;
 #else
-    return THREADS <= 128;
+    return THREADS <= UP_SELECT_RADIX_MAX_THREADS;
 #endif
 }
 
@@ -507,7 +505,6 @@ select_radix_kernel(const SelectParams p) {
     constexpr int CAP = THREADS * ITEMS;
     __shared__ union {
         RadixSel sel;
-        uint64_t tiny[kTinySelect];
         typename Sort::TempStorage sort;
         struct { uint32_t key[CAP]; int32_t val[CAP]; } sorted;  // fallback replay only
     } u;
@@ -570,21 +567,6 @@ select_radix_kernel(const SelectParams p) {
     } else {
         SEL_STAMP(1)
         const double p_d = static_cast<double>(p.top_p);
-        if (nb <= kTinySelect && THREADS <= 128) {
-            // 2t. tiny request: warp-sorted words + the exact sequential replay
-            if (tid < 32) {
-                const int k = tiny_crossing(sc, nb, u.tiny, p_d);
-                if (tid == 0) s_kstar = k;
-            }
-            __syncthreads();
-            kstar = s_kstar;
-            for (int q = tid; q < nb; q += THREADS) blk[~static_cast<uint32_t>(u.tiny[q] & 0xFFFFFFFFull)] = q < kstar ? 1 : 0;
-            __syncthreads();
-            SEL_STAMP(4)
-            finish_request(p, r, seg0, N, nb, neff, blk, sc, kstar, degenerate, total, red_d, red_i);
-            SEL_STAMP(5)
-            return;
-        }
         // 2a. radix select of the crossing key K* and its rank t inside the tie group
         float dsc[ITEMS];
 #pragma unroll

@@ -21,5 +21,5 @@ for N in (4096, 32768):
     torch.cuda.synchronize()
     h = (ctypes.c_ulonglong * 16)()
     up.lib.up_internal_select_debug(h)
-    st = [(i, h[i]) for i in range(6) if h[i]]
+    st = sorted([(i, h[i]) for i in range(9) if h[i]], key=lambda x: x[1])
     print(f"N={N}: " + " ".join(f"{a}->{b}:{tb - ta}" for (a, ta), (b, tb) in zip(st, st[1:])), "cycles")
