@@ -277,14 +277,21 @@ class CpuReferenceUnits:
 
     TP = 8
 
-    def __init__(self, model, lengths, cfg, regime, seed=1234):
+    def __init__(self, model, lengths, cfg, regime, seed=1234, rank_slice=False):
         import numpy as np
         import oracle
         if not oracle.ref_available():
             raise RuntimeError("oracle/_ref (the reference build) is missing")
         self.ref = oracle.ref()
         self.model, self.cfg, self.regime = model, cfg, regime
-        self.shp = shp = MODEL_SHAPES_REF[model]
+        self.shp = shp = dict(MODEL_SHAPES_REF[model])
+        if rank_slice:
+            # what ONE rank of the TP=8 group scores (c3-rank): its head slice, its two q-heads
+            # as two shards on two threads (tp_sim.cpp:12-27 at T = 2 over the slice)
+            hps = shp["num_q_heads"] // self.TP
+            shp["num_kv_heads"] = max(1, shp["num_kv_heads"] * hps // shp["num_q_heads"])
+            shp["num_q_heads"] = hps
+            self.TP = hps
         self.nproc = os.cpu_count() or 1
         # distinct request lengths of the config, longest first (one input set per length)
         self.lengths = sorted(set(lengths), reverse=True)[:4]
@@ -316,7 +323,9 @@ class CpuReferenceUnits:
         # hidden-state values do not change the reference's work: one shared bf16-exact buffer
         self.hidden = _bf16_exact(rng.standard_normal((N, HID), dtype=np.float32))
         self.desc = (f"(request, drop layer) units of the workload at their real lengths "
-                     f"{self.lengths} ({model} shape, {regime} bf16-exact inputs from numpy): the reference "
+                     f"{self.lengths} ({model} shape{' -- one TP=8 rank slice' if rank_slice else ''}, "
+                     f"{shp['num_q_heads']} q-heads / {shp['num_kv_heads']} kv-heads, {regime} bf16-exact inputs "
+                     f"from numpy): the reference "
                      f"(oracle/_ref) score -> top_p_select -> apply_drop -> patch_metadata; {self.units} "
                      f"concurrent unit(s) per step, each scored through the reference's TP={self.TP} path "
                      f"(sharded_block_scores + allreduce_scores) with one shard per thread = {self.threads} "
@@ -368,7 +377,7 @@ def run_reference_arm(args):
         lengths = loguniform_lengths_ref(int(count), int(lo), int(hi), int(seed))
     else:
         lengths = list(lspec)
-    units = CpuReferenceUnits(model, lengths, cfg, args.regime)
+    units = CpuReferenceUnits(model, lengths, cfg, args.regime, rank_slice=CONFIGS[args.config][4] == "tp-rank")
     vals = []
     for i in range(args.warmup + args.steps):
         v, _, _ = units.step()
@@ -964,9 +973,9 @@ def run_ours(args):
 
     # ---- CPU baseline (rank 0 only, N=1 semantics) ----
     cpu = None
-    if rank == 0 and ws == 1 and not args.skip_cpu and mode != "tp-rank":  # reported at N=1 only
+    if rank == 0 and ws == 1 and not args.skip_cpu:  # reported at N=1 only
         try:  # one step of the reference arm's units (all cores) + one unit on one core
-            units = CpuReferenceUnits(model, all_lengths, cfgd, args.regime)
+            units = CpuReferenceUnits(model, all_lengths, cfgd, args.regime, rank_slice=mode == "tp-rank")
             cpu = cpu_reference_report(units, [units.step()[0]], units.single_core())
             del units
         except Exception as exc:  # the baseline is reported, never fatal
