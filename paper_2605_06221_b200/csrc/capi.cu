@@ -132,16 +132,16 @@ int q_tiles(const up_score_config* c) {
 // Query-row packing: a window of n <= 64 rows leaves most of a 128-row S tile empty, so P
 // q-heads of one kv-group share it -- virtual head v holds q-heads [vP, vP + P), row r
 // being window row r % (128/P) of q-head vP + r / (128/P).  Served by score_tcw's TS
-// variant (Q loaded row by row by the epilogue threads), i.e. two virtual heads per
-// kv-head at D >= 128: P = the largest power of two with P * npad <= 128 and 2P | gqa.
+// variants (Q loaded row by row by the epilogue threads: one or two virtual heads per
+// kv-head at D >= 128): P = the largest power of two with P * npad <= 128 dividing the
+// kv-group and the head slice.
 int q_pack(const up_heads* h, const up_score_config* c, int shard_heads) {
     const int n = c->query_window_n;
     if (n > 64 || h->head_dim < 128) return 1;
     int npad = 1;
     while (npad < n) npad <<= 1;
     int P = kRows / npad;
-    while (P > 1 && (h->gqa_group % (2 * P) || h->num_q_heads % P || h->q_head_offset % P || shard_heads % (2 * P)))
-        P >>= 1;
+    while (P > 1 && (h->gqa_group % P || h->num_q_heads % P || h->q_head_offset % P || shard_heads % P)) P >>= 1;
     return P;
 }
 up_heads packed_heads(const up_heads* h, int P) {
@@ -168,8 +168,9 @@ Layout layout_for(const up_batch* b, const up_heads* h, const up_score_config* c
     const int64_t H = h ? static_cast<int64_t>(h->num_q_heads) * q_tiles(c) : 0;
     L.max_blocks = T / G + R + 1;
     // Σ_r ceil(N_r / unit) * num_hgroups * HPC * npar <= Hq * npar * (T / 128 + R): bounds
-    // the item statistics rows (npar = 2 for the two-warpgroups-per-head scorer).
-    const int64_t npar = h ? (tc2_enabled() ? 4 : 2) : 1;  // score_tc2 keeps four statistics rows per head
+    // the item statistics rows; npar <= 4 (score_tcw HPC = 1 and score_tc2 keep four
+    // statistics rows per head, the HPC = 2 / SPLIT epilogues two)
+    const int64_t npar = h ? 4 : 1;
     L.max_units = (H > 0 ? H : 1) * npar * (T / kTileKeys + R + 1);
     const int64_t n = c->query_window_n < T ? c->query_window_n : T;
     L.simt_n = static_cast<int32_t>(n > 0 ? n : 1);
@@ -286,16 +287,17 @@ int score_grid() {
     return grid_override > 0 ? (grid_override < 1024 ? grid_override : 1024) : num_sms();
 }
 
-TcPlan tc_plan(const up_batch* b, const up_heads* h, const up_score_config* c, int shard_heads) {
+TcPlan tc_plan(const up_batch* b, const up_heads* h, const up_score_config* c, int shard_heads, int hpc_cap = 4) {
     const int D = h->head_dim;
     TcPlan t{};
     static const int max_hpc_env = [] {  // dev sweeps only
         const char* s = std::getenv("UP_MAX_HPC");
         return s ? std::atoi(s) : 0;
     }();
-    t.hpc = pick_hpc(h, max_hpc_env > 0 ? max_hpc_env : (D == 256 ? 2 : 4), shard_heads);
+    const int want = max_hpc_env > 0 ? max_hpc_env : (D == 256 ? 2 : 4);
+    t.hpc = pick_hpc(h, want < hpc_cap ? want : hpc_cap, shard_heads);
     t.pair = tc2_supported(D, t.hpc, c->block_size_g, b->num_requests);
-    t.wide = !t.pair && (t.hpc == 4 || t.hpc == 2) && tcw_supported(D, t.hpc, c->block_size_g, b->num_requests);
+    t.wide = !t.pair && tcw_supported(D, t.hpc, c->block_size_g, b->num_requests);
     if (!t.wide && !t.pair) t.hpc = pick_hpc(h, tc_max_hpc(D), shard_heads);
     t.npar = t.pair ? 4
                     : (t.wide ? tcw_npar(D, t.hpc, c->block_size_g, b->max_tokens, h->num_q_heads / t.hpc,
@@ -384,8 +386,8 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     const int Tt = q_tiles(c);
     int Pk = Tt == 1 && !std::getenv("UP_NO_QPACK") ? q_pack(h, c, h->num_q_heads / tp) : 1;
     up_heads hv = Pk > 1 ? packed_heads(h, Pk) : virtual_heads(h, Tt);
-    TcPlan plan = tc_plan(b, &hv, c, hv.num_q_heads / tp);
-    if (Pk > 1 && !(plan.wide && plan.hpc == 2)) {  // packing needs score_tcw's TS variant
+    TcPlan plan = tc_plan(b, &hv, c, hv.num_q_heads / tp, Pk > 1 ? 2 : 4);
+    if (Pk > 1 && !(plan.wide && plan.hpc <= 2)) {  // packing needs score_tcw's TS variants
         Pk = 1;
         hv = *h;
         plan = tc_plan(b, &hv, c, hv.num_q_heads / tp);

@@ -53,7 +53,9 @@ struct TcwCfg {
     // TS: with two q-heads per CTA, Q lives in TMEM (tcgen05.mma A operand from tensor
     // memory): the MMA then reads only K from shared memory, which keeps the D = 256
     // MMA math-bound instead of shared-memory-bound, and frees the 128 KB Q tile.
-    static constexpr bool TS = HPC == 2 && D >= 128;
+    // (HPC = 1: one q-head per kv-head -- MHA shapes, or packed query rows -- is TS too: an
+    // SS N = 64 MMA would read 6 KB of shared memory per 32 cycles)
+    static constexpr bool TS = (HPC == 2 || HPC == 1) && D >= 128;
     static constexpr int SK = TS ? 128 : (D <= 128 ? UP_TCW_STAGE_KEYS_D128 : 64);  // keys per K stage
     // keys per MMA / TMEM region (UP_TCW_SUBN_HPC4 = 128: one N = 128 region per head)
     static constexpr int SUBN = HPC == 4 ? UP_TCW_SUBN_HPC4 : 64;
@@ -488,16 +490,28 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 constexpr int COLS = D / 2 / NPAR;  // 64 at D = 256, 32 at D = 128
                 const __nv_bfloat16* qsrc = p.q + static_cast<int64_t>(seg0 + N - neff + jr) * p.q_row_stride +
                                             static_cast<int64_t>(qhead) * D + par * COLS * 2;
+                if constexpr (COLS >= 32) {
 #pragma unroll
-                for (int c0 = 0; c0 < COLS; c0 += 32) {
-                    uint32_t v[32];
+                    for (int c0 = 0; c0 < COLS; c0 += 32) {
+                        uint32_t v[32];
 #pragma unroll
-                    for (int x = 0; x < 8; ++x) {
+                        for (int x = 0; x < 8; ++x) {
+                            uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                            if (row_valid) w = __ldg(reinterpret_cast<const uint4*>(qsrc + c0 * 2) + x);
+                            v[4 * x + 0] = w.x; v[4 * x + 1] = w.y; v[4 * x + 2] = w.z; v[4 * x + 3] = w.w;
+                        }
+                        tmem_st32(tmem_base + lane_base + hh * (D / 2) + par * COLS + c0, v);
+                    }
+                } else {  // HPC = 1 at D = 128: four warpgroups, 16 columns each
+                    static_assert(COLS == 16, "TS Q slice");
+                    uint32_t v[16];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
                         uint4 w = make_uint4(0u, 0u, 0u, 0u);
-                        if (row_valid) w = __ldg(reinterpret_cast<const uint4*>(qsrc + c0 * 2) + x);
+                        if (row_valid) w = __ldg(reinterpret_cast<const uint4*>(qsrc) + x);
                         v[4 * x + 0] = w.x; v[4 * x + 1] = w.y; v[4 * x + 2] = w.z; v[4 * x + 3] = w.w;
                     }
-                    tmem_st32(tmem_base + lane_base + hh * (D / 2) + par * COLS + c0, v);
+                    tmem_st16(tmem_base + lane_base + hh * (D / 2) + par * COLS, v);
                 }
                 tmem_st_wait();
                 tc_fence_before();
@@ -513,7 +527,11 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
 
 #pragma unroll 1
             for (int t = 0; t < nsub; ++t, ++u) {
-                if (NPAR > 1 && (t % NPAR) != par) continue;  // the other warpgroup's subtile
+                // the other warpgroups' subtiles: parity of the subtile's position in the
+                // request (key0 / SUBN + t), as pair_weights / block_combine derive it from a
+                // block's start key -- an item may start at any 128-key unit, so with four
+                // parities (HPC = 1) the item-relative t alone would disagree
+                if (NPAR > 1 && ((key0 / C::SUBN + t) % NPAR) != par) continue;
                 const int cbase = key0 + t * C::SUBN;
                 const uint32_t reg = hh * NB + u % NB;
                 if constexpr (NPAR == 1 && C::NG == 4) {
@@ -750,6 +768,9 @@ bool tcw_supported(int D, int HPC, int G, int R) {
     if (R > kTcwMaxRequests || G % 32 != 0) return false;
     if (HPC == 4) return D == 64 || D == 128;
     if (HPC == 2) return (D == 64 || D == 128 || D == 256) && (G == 32 || G == 64);
+#ifndef UP_NO_TCW_HPC1  // dev A/B: MHA shapes back on score_tc
+    if (HPC == 1) return (D == 128 || D == 256) && (G == 32 || G == 64);  // TS, four parity warpgroups
+#endif
     return false;
 }
 
@@ -764,6 +785,8 @@ cudaError_t launch_score_tcw(int D, int HPC, const CUtensorMap& qm, const CUtens
     if (D == 128 && HPC == 4) return launch_tcw<128, 4>(qm, km, p, grid, stream);
     if (D == 128 && HPC == 2) return launch_tcw<128, 2>(qm, km, p, grid, stream);
     if (D == 256 && HPC == 2) return launch_tcw<256, 2>(qm, km, p, grid, stream);
+    if (D == 128 && HPC == 1) return launch_tcw<128, 1>(qm, km, p, grid, stream);
+    if (D == 256 && HPC == 1) return launch_tcw<256, 1>(qm, km, p, grid, stream);
     return cudaErrorInvalidValue;
 }
 

@@ -41,7 +41,9 @@ def _assert_blocks_close(got, want):
     (4, 1, 128, [300, 1], 128, 64),        # single-token segment
     (8, 1, 64, [1500], 128, 64),           # D=64, HPC 8
     (4, 2, 256, [900, 333], 128, 64),      # D=256 (Gemma / Qwen head dim)
-    (4, 4, 128, [777], 128, 64),           # MHA, HPC 1
+    (4, 4, 128, [777], 128, 64),           # MHA, HPC 1 (score_tcw TS, four parity warpgroups)
+    (8, 8, 128, [2000, 64, 900], 128, 32), # MHA varlen, G=32
+    (4, 4, 256, [1500, 300], 128, 64),     # MHA at D=256
     (8, 2, 128, [1024, 513], 64, 32),      # n=64, G=32
     (8, 2, 128, [2048], 128, 128),         # G=128
     (8, 2, 128, [1300], 100, 96),          # n < 128, G not a power of two

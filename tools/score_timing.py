@@ -11,6 +11,8 @@ SHAPES = {  # Hq, Hkv, D, lengths, tp
     "gemma": (16, 8, 256, [65536] * 4, 1),
     "qwen": (16, 2, 256, [131072], 1),
     "qwen-tp8": (16, 2, 256, [131072], 8),
+    "mha": (32, 32, 128, [32768] * 4, 1),
+    "mha256": (16, 16, 256, [65536] * 2, 1),
 }
 Hq, Hkv, D, L, tp = SHAPES[os.environ.get("SHAPE", "llama")]
 sb = make_batch(L, Hq, Hkv, D, 64, regime=os.environ.get("REGIME", "planted"), seed=1, device="cuda", with_v=False)
