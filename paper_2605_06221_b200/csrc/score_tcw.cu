@@ -1,6 +1,8 @@
-// score_tcw.cu -- tensor-core block scorer with four epilogue warpgroups for HPC = 4 or 2
-// q-heads per kv-head (LLaMA-3.1-8B: D = 128, HPC = 4; Gemma-3 / Qwen3-Next full-attention
-// layers: D = 256, HPC = 2).
+// score_tcw.cu -- tensor-core block scorer with four epilogue warpgroups for HPC = 4, 2 or
+// 1 (virtual) q-heads per kv-head (LLaMA-3.1-8B: D = 128, HPC = 4; Gemma-3 / Qwen3-Next
+// full-attention layers: D = 256, HPC = 2; MHA shapes: HPC = 1).  A "head" here is a
+// virtual head of 128 query rows: a query tile of a longer window (n > 128, q_tiles) or
+// several q-heads' short windows packed together (n <= 64, q_pack) -- see params.cuh.
 //
 // Same math, work partition and per-item statistics as score_tc.cu (its header restates
 // importance.cpp:17-132 as a single pass over K); pair_weights_kernel and
@@ -8,10 +10,10 @@
 // because the exp2 epilogue (MUFU, 16/clk/SM) -- not the tensor core -- bounds the scorer:
 //  * 18 warps: warp 0 TMA, warp 1 MMA, warps 2..17 = four epilogue warpgroups, so every
 //    SMSP runs four exp2 streams.  Warpgroup wg drains head hh = wg / NPAR and, with
-//    HPC = 2 (NPAR = 2), only the 64-key subtiles whose parity is wg % NPAR: the two
-//    warpgroups of a head keep separate running statistics, recorded as separate
-//    "virtual heads" vh = hh * NPAR + par in the item statistics (requires G in {32, 64}
-//    so that every block lies inside one subtile);
+//    HPC = 2 / 1 (NPAR = 2 / 4), only the 64-key subtiles whose parity (position in the
+//    request mod NPAR) is wg % NPAR: the warpgroups of a head keep separate running
+//    statistics, recorded as separate rows vh = hh * NPAR + par in the item statistics
+//    (requires G in {32, 64} so that every block lies inside one subtile);
 //  * K is streamed in stages of SK keys (128 x 2 stages at D <= 128, 64 x 3 at D = 256)
 //    next to the resident Q of the HPC heads (128 KB), so the kv-head's K tile is read
 //    from HBM once for all HPC heads;
