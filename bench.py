@@ -920,14 +920,42 @@ def run_ours(args):
         host_row_bytes = HID * 2 + runner.Hkv_local * D * 2 + 8  # hidden + V + position per retained row
         d2h = o_keep.numel() + o_cu.numel() * 4 + o_cut.numel() * 8
         L0 = runner.layer
+        # Double-buffered inputs: the next layer's query-window rows, K and cu_seqlens are
+        # copied H2D on a side stream while this layer scores, compacts and scatters (the
+        # scatter's zero-copy writes travel D2H, so the copy engines and the PCIe link run
+        # both directions at once); a buffer is refilled only after the layer using it has
+        # compacted (its K plane is a compaction source).
+        bufs = [d_in, type(src)(torch.empty_like(src.q), torch.empty_like(src.k), h_v, h_hid, h_pos,
+                                torch.empty_like(cu), src.lengths)]
+        cs = torch.cuda.Stream(device=dev)
+        ev_copied = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_free = [torch.cuda.Event(), torch.cuda.Event()]
+        for ev in ev_free:
+            ev.record(stream)
+
+        def copy_in(i):
+            buf = bufs[i]
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_free[i])
+                for (a, b), t in zip(tails, h_qt):
+                    buf.q[a:b].copy_(t, non_blocking=True)
+                buf.k.copy_(h_k, non_blocking=True)
+                buf.cu_seqlens.copy_(h_cu, non_blocking=True)
+                ev_copied[i].record(cs)
 
         def e2e_step():
+            start = torch.cuda.Event()
+            start.record(stream)
+            cs.wait_event(start)  # this step's copies start after the step does
+            copy_in(0)
             for l in range(layers):
-                for (a, b), t in zip(tails, h_qt):
-                    d_in.q[a:b].copy_(t, non_blocking=True)
-                d_in.k.copy_(h_k, non_blocking=True)
-                d_in.cu_seqlens.copy_(h_cu, non_blocking=True)
-                runner(d_in, d_in.cu_seqlens)
+                i = l % 2
+                if l + 1 < layers:
+                    copy_in((l + 1) % 2)
+                stream.wait_event(ev_copied[i])
+                buf = bufs[i]
+                runner(buf, buf.cu_seqlens)
+                ev_free[i].record(stream)
                 if block_spec["reconstitute"]:
                     up.scatter_rows(L0.out.retained_index, [L0.out.planes[0]], [h_hid], num_rows=L0.out.num_out)
                 o_keep.copy_(L0.sel.keep, non_blocking=True)
@@ -966,7 +994,8 @@ def run_ours(args):
                "steps": args.e2e_steps,
                "pcie_gbs": (h2d + d2h_all) * layers / (ems / args.e2e_steps / 1e3) / 1e9,
                "note": "per layer: H2D copies of the query-window rows, K and cu_seqlens from pinned host "
-                       "memory; residual stream, V and positions read in place from pinned host memory by the "
+                       "memory (double-buffered on a side stream: the next layer's copy overlaps this layer); "
+                       "residual stream, V and positions read in place from pinned host memory by the "
                        "compaction kernel (retained rows only); reconstitution scatters the retained hidden "
                        "rows back into the pinned host residual stream; D2H of keep mask, new cu_seqlens, "
                        "cutoff ranks"}

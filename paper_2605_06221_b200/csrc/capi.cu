@@ -28,6 +28,7 @@ bool tcw_supported(int D, int HPC, int G, int R);
 int tcw_stage_keys(int D);
 bool tc2_enabled();
 int tcw_npar(int D, int HPC, int G, int64_t max_tokens, int nhg, int grid);
+int tcw_par_shift_for(int G);
 bool tc2_supported(int D, int HPC, int G, int R);
 int tc2_stage_keys();
 int tc2_grid(int num_sms);
@@ -393,6 +394,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
         plan = tc_plan(b, &hv, c, hv.num_q_heads / tp);
     }
     if (Tt > 1 && !plan.wide) return UP_ERR_UNSUPPORTED;  // query tiles: score_tcw only (nothing enqueued)
+    if (L.max_units >= (int64_t{1} << kUsidParShift)) return UP_ERR_CONTRACT;  // item ids share unit_sid with a parity
     const int hpc = plan.hpc;
     const int nhg = hv.num_q_heads / hpc;
     CUtensorMap qm, km;
@@ -474,7 +476,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     bp.num_shards = tp;
     bp.hpc = hpc;
     bp.npar = plan.npar;
-    bp.par_shift = plan.pair ? 7 : 6;
+    bp.par_shift = plan.pair ? 7 : tcw_par_shift_for(G);
     bp.block_size_g = G;
     bp.unit_keys = p.unit_keys;
     if (peer != nullptr) {  // fused with the TP all-reduce over peer memory

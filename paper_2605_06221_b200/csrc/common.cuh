@@ -28,6 +28,7 @@ enum : uint32_t {
 
 constexpr int kMaxSortBlocks = 16384;  // per-request blocks the select kernel sorts on chip
 constexpr int kTileKeys = 128;          // keys per tcgen05 S tile (UMMA N)
+constexpr int kUsidParShift = 28;       // unit_sid: item id below, statistics parity above (score_common.cuh)
 constexpr int kRows = 128;              // query rows per S tile (UMMA M) -> max n for tcgen05
 
 // Workspace carve-up (byte offsets), identical on host and device.

@@ -62,6 +62,18 @@ __device__ __forceinline__ Item make_item(const Part& P, int64_t pos, int64_t en
     return it;
 }
 
+// unit_sid entries: the item id (its first unit's position, < 2^28) in the low 28 bits and,
+// for the scorers whose statistics parity is not a function of the key position alone
+// (score_tcw, score_tc2), the parity of the unit's first subtile in the top 4 bits.
+__host__ __device__ __forceinline__ int32_t tcw_usid(int32_t sid, int par0) {
+    return sid | static_cast<int32_t>(static_cast<uint32_t>(par0) << kUsidParShift);
+}
+__device__ __forceinline__ int64_t usid_item(int32_t v) { return v & ((1 << kUsidParShift) - 1); }
+// statistics parity of a block whose first key is `off` parity units into its 128-key unit
+__device__ __forceinline__ int usid_par(int32_t v, int off, int npar) {
+    return npar > 1 ? static_cast<int>(((static_cast<uint32_t>(v) >> kUsidParShift) + off) % npar) : 0;
+}
+
 // ---------------------------------------------------------------- pair statistics
 __device__ __forceinline__ void lse_merge(float& M, float& L, float mc, float lc) {
     if (mc == -INFINITY) return;

@@ -172,9 +172,10 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
         const int size = min(p.block_size_g, N - g * p.block_size_g);
         const int u = (g * p.block_size_g) / p.unit_keys;
         const int64_t pair0 = static_cast<int64_t>(p.cu_units[r]) * nhg;
-        // statistics row of head hh: hh * npar + (parity of the block's subtile: 64 keys in
-        // score_tcw, 128 in score_tc2)
-        const int par = p.npar > 1 ? ((g * p.block_size_g) >> p.par_shift) % p.npar : 0;
+        // statistics row of head hh: hh * npar + parity, the parity of the unit's first
+        // subtile (top bits of unit_sid) plus the block's offset in the unit in parity units
+        // (64 keys in score_tcw, 128 in score_tc2 / score_tcw at G = 128)
+        const int poff = ((g * p.block_size_g) % p.unit_keys) >> p.par_shift;
         const int hpcv = p.hpc * p.npar;
         if (T > 1) {
             // Sharded: every head's dot product is reduced across the warp and added, in
@@ -191,7 +192,9 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
                     for (int x = 0; x < 8; ++x) {
                         const int hx = min(h + x, h_end - 1);
                         const int hgx = hx / p.hpc;
-                        const int64_t sid = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
+                        const int32_t us = __shfl_sync(0xffffffffu, my_sid, hgx - hg0);
+                        const int64_t sid = usid_item(us);
+                        const int par = usid_par(us, poff, p.npar);
                         const float4 pv = __ldcs(reinterpret_cast<const float4*>(
                             p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
                         const float4 wv = __ldg(reinterpret_cast<const float4*>(
@@ -220,6 +223,9 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
         // the same arithmetic as block_combine_chunked (so the peer-fused combine, which runs
         // this path, stays bitwise the ascending sum of the plain scorer's partials).
         float red = 0.f;
+        // item ids of up to 32 head groups, one per lane, broadcast by shuffles (one
+        // round trip ahead of the chunks instead of one per chunk)
+        const int my_sid = lane < nhg ? p.unit_sid[pair0 + static_cast<int64_t>(lane) * units_r + u] : 0;
         for (int h0 = 0; h0 < p.num_heads; h0 += 8) {
             const int h1 = min(h0 + 8, p.num_heads);
             float4 pv[8], wv[8];
@@ -227,7 +233,14 @@ __device__ __forceinline__ void block_combine_run(const BlockCombineParams& p, i
             for (int x = 0; x < 8; ++x) {
                 const int hx = min(h0 + x, h1 - 1);
                 const int hgx = hx / p.hpc;
-                const int64_t sid = p.unit_sid[pair0 + static_cast<int64_t>(hgx) * units_r + u];
+#ifdef UP_COMBINE_SID_PER_HEAD  // dev A/B
+                const int32_t us = p.unit_sid[pair0 + static_cast<int64_t>(hgx) * units_r + u];
+#else
+                const int32_t us = nhg <= 32 ? __shfl_sync(0xffffffffu, my_sid, hgx & 31)
+                                             : p.unit_sid[pair0 + static_cast<int64_t>(hgx) * units_r + u];
+#endif
+                const int64_t sid = usid_item(us);
+                const int par = usid_par(us, poff, p.npar);
                 pv[x] = __ldcs(reinterpret_cast<const float4*>(p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
                 wv[x] = __ldg(reinterpret_cast<const float4*>(
                             p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);
@@ -277,14 +290,16 @@ __device__ __forceinline__ void block_combine_chunked(const BlockCombineParams& 
                 size = min(p.block_size_g, N - g * p.block_size_g);
                 const int u = (g * p.block_size_g) / p.unit_keys;
                 const int64_t pair0 = static_cast<int64_t>(p.cu_units[r]) * nhg;
-                const int par = p.npar > 1 ? ((g * p.block_size_g) >> p.par_shift) % p.npar : 0;
+                const int poff = ((g * p.block_size_g) % p.unit_keys) >> p.par_shift;
                 const int h0 = ch * 8, h1 = min(h0 + 8, p.num_heads);
                 float4 pv[8], wv[8];
 #pragma unroll
                 for (int x = 0; x < 8; ++x) {
                     const int hx = min(h0 + x, h1 - 1);
                     const int hgx = hx / p.hpc;
-                    const int64_t sid = p.unit_sid[pair0 + static_cast<int64_t>(hgx) * units_r + u];
+                    const int32_t us = p.unit_sid[pair0 + static_cast<int64_t>(hgx) * units_r + u];
+                    const int64_t sid = usid_item(us);
+                    const int par = usid_par(us, poff, p.npar);
                     pv[x] = __ldcs(reinterpret_cast<const float4*>(p.P + (static_cast<int64_t>(hx) * p.max_blocks + gb) * kRows) + lane);
                     wv[x] = __ldg(reinterpret_cast<const float4*>(
                                 p.stat_w + (sid * hpcv + (hx - hgx * p.hpc) * p.npar + par) * kRows) + lane);

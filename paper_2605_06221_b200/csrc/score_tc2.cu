@@ -494,7 +494,8 @@ score_tc2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 p.stat_l[x] = row_valid ? ll[s] : 0.f;
             }
             if (rank == 0)
-                for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
+                for (int uu = it.u0 + etid; uu < it.u1; uu += 512)  // unit = 128-key subtile uu, parity uu % 4
+                    p.unit_sid[it.seg_start + uu] = tcw_usid(static_cast<int32_t>(it.sid), uu % 4);
         }
     }
 

@@ -85,12 +85,27 @@ struct TcwCfg {
     static_assert(!SPLIT || (HPC == 4 && SUBN == 128 && NB == 1), "SPLIT drains one 128-column region per head");
 };
 
+// Parity of the NPAR > 1 epilogues.  Subtile u of the CTA (the counter the MMA warp's TMEM
+// ring runs on) goes to warpgroup (u >> ushift) % NPAR: one 64-key subtile per parity unit,
+// or pairs of them when a block spans two (G = 128, ushift = 1), so that every block belongs
+// to one warpgroup.  Counting in the CTA's own sequence -- not by key position -- keeps a
+// warpgroup's consecutive waits on the ring at most NPAR (pairs: 2 NPAR - 1) subtiles apart,
+// within the NB regions one mbarrier parity can tell apart, whatever items the CTA walks
+// (a key-position parity lets a warpgroup skip whole short items and then wait on a region
+// two phases ahead).  The parity of each 128-key unit's first subtile travels to
+// block_combine in the top bits of unit_sid (tcw_usid); block_combine adds the block's
+// offset in the unit at par_shift granularity.
+__host__ __device__ constexpr int tcw_par_shift(int G) { return G > 64 ? 7 : 6; }
+__host__ __device__ constexpr int tcw_ushift(int G) { return G > 64 ? 1 : 0; }
+
 // Rebase (cold): rescale the partials this thread already wrote for the item -- blocks
-// [g0, g1) that lie in subtiles of this warpgroup's parity.
+// [g0, g1) in parity units of this warpgroup (subtile index u0 + (g G - key0) / 64).
 static __device__ __noinline__ void rescale_rows_par(float* prow, int g0, int g1, int G, int npar, int par,
-                                                     float f) {
+                                                     float f, int key0, uint32_t u0) {
+    const int us = tcw_ushift(G);
     for (int g = g0; g < g1; ++g)
-        if (((g * G) >> 6) % npar == par) prow[static_cast<int64_t>(g) * kRows] *= f;
+        if (((u0 + static_cast<uint32_t>((g * G - key0) >> 6)) >> us) % npar == static_cast<uint32_t>(par))
+            prow[static_cast<int64_t>(g) * kRows] *= f;
 }
 
 // UP_SCORE_DEBUG phase clocks (second region of the debug buffer): slot k of this CTA
@@ -409,7 +424,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                                     l[e] *= f;
                                     gs0 *= f;  // the half's first group when q2 = 1
                                     // blocks of this half already written for the item
-                                    rescale_rows_par(Prow[e], blk0, cb >> gshift, G, 2, c, f);
+                                    rescale_rows_par(Prow[e], blk0, cb >> gshift, G, 2, c, f, key0, 0u);  // parity = key half
                                 }
                                 m[e] = mnew;
                                 gs = 0.f;
@@ -522,18 +537,18 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             }
             float m = -INFINITY, l = 0.f, bsum = 0.f;
             // block bookkeeping: NPAR = 1 walks every group in order (counters, any G that
-            // is a multiple of 32); NPAR = 2 sees every other subtile (G = 32 or 64: shifts)
+            // is a multiple of 32); NPAR > 1 sees its parity units only (G = 32, 64, 128: shifts)
             const int gpb = G >> 5;
-            const int gshift = G == 64 ? 1 : 0;
+            const int gshift = G == 128 ? 2 : (G == 64 ? 1 : 0);
+            const int ushift = tcw_ushift(G);
+            const uint32_t u_item0 = u;  // the CTA's subtile counter at this item's first subtile
             int gib = 0, blk = blk0;
 
 #pragma unroll 1
             for (int t = 0; t < nsub; ++t, ++u) {
-                // the other warpgroups' subtiles: parity of the subtile's position in the
-                // request (key0 / SUBN + t), as pair_weights / block_combine derive it from a
-                // block's start key -- an item may start at any 128-key unit, so with four
-                // parities (HPC = 1) the item-relative t alone would disagree
-                if (NPAR > 1 && ((key0 / C::SUBN + t) % NPAR) != par) continue;
+                // the other warpgroups' subtiles (parity of the CTA's subtile counter, see
+                // tcw_par_shift)
+                if (NPAR > 1 && ((u >> ushift) % NPAR) != static_cast<uint32_t>(par)) continue;
                 const int cbase = key0 + t * C::SUBN;
                 const uint32_t reg = hh * NB + u % NB;
                 if constexpr (NPAR == 1 && C::NG == 4) {
@@ -656,7 +671,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                                 gs1 *= f;
                                 gs2 *= f;
                                 rescale_rows_par(Prow, blk0, NPAR == 1 ? blk : cbase >> (5 + gshift), G, NPAR,
-                                                 par, f);
+                                                 par, f, key0, u_item0);
                             }
                             m = mnew;
                             gs = 0.f;
@@ -705,7 +720,13 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 p.stat_m[x] = row_valid ? m : -INFINITY;
                 p.stat_l[x] = row_valid ? l : 0.f;
             }
-            for (int uu = it.u0 + etid; uu < it.u1; uu += 512) p.unit_sid[it.seg_start + uu] = static_cast<int32_t>(it.sid);
+            {
+                constexpr int spu = kTileKeys / C::SUBN;  // subtiles per 128-key unit
+                for (int uu = it.u0 + etid; uu < it.u1; uu += 512) {
+                    const uint32_t par0 = NPAR > 1 ? ((u_item0 + (uu - it.u0) * spu) >> ushift) % NPAR : 0u;
+                    p.unit_sid[it.seg_start + uu] = tcw_usid(static_cast<int32_t>(it.sid), static_cast<int>(par0));
+                }
+            }
             if (warp == 2 && lane == 0) TCW_PHASE(2)
         }
     }
@@ -756,6 +777,8 @@ bool tcw_split(int D, int HPC, int G, int64_t max_tokens, int nhg, int grid) {
     return (max_tokens / kTileKeys + 1) * nhg <= 4LL * grid;
 }
 
+int tcw_par_shift_for(int G) { return tcw_par_shift(G); }
+
 // statistics rows per head the tail kernels must merge
 int tcw_npar(int D, int HPC, int G, int64_t max_tokens, int nhg, int grid) {
     return tcw_split(D, HPC, G, max_tokens, nhg, grid) ? 2 : 4 / HPC;
@@ -769,9 +792,12 @@ int tcw_stage_keys(int D) { return D <= 128 ? TcwCfg<128, 4>::SK : TcwCfg<256, 2
 bool tcw_supported(int D, int HPC, int G, int R) {
     if (R > kTcwMaxRequests || G % 32 != 0) return false;
     if (HPC == 4) return D == 64 || D == 128;
-    if (HPC == 2) return (D == 64 || D == 128 || D == 256) && (G == 32 || G == 64);
+    // G = 128 pairs subtiles per parity unit: a warpgroup's waits on the TMEM ring are then
+    // up to 2 NPAR - 1 subtiles apart, which needs NB >= 2 NPAR - 1 regions per head
+    // (HPC 2 at D <= 128: NB 3-4; HPC 1 at D = 128: NB 7; not D = 256, where TS Q leaves 2 / 6)
+    if (HPC == 2) return (D == 64 || D == 128 || D == 256) && (G == 32 || G == 64 || (G == 128 && D <= 128));
 #ifndef UP_NO_TCW_HPC1  // dev A/B: MHA shapes back on score_tc
-    if (HPC == 1) return (D == 128 || D == 256) && (G == 32 || G == 64);  // TS, four parity warpgroups
+    if (HPC == 1) return (D == 128 || D == 256) && (G == 32 || G == 64 || (G == 128 && D == 128));  // TS, four parity warpgroups
 #endif
     return false;
 }

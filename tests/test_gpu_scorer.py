@@ -44,6 +44,16 @@ def _assert_blocks_close(got, want):
     (4, 4, 128, [777], 128, 64),           # MHA, HPC 1 (score_tcw TS, four parity warpgroups)
     (8, 8, 128, [2000, 64, 900], 128, 32), # MHA varlen, G=32
     (4, 4, 256, [1500, 300], 128, 64),     # MHA at D=256
+    (16, 8, 256, [3000, 700], 128, 128),   # Gemma-3 layout at G=128 (score_tc: D=256 leaves too few TMEM regions)
+    (4, 4, 128, [1500, 90], 128, 128),     # MHA at G=128 (HPC 1, paired-subtile parity units)
+    (8, 2, 128, [2048, 300], 32, 128),     # packed rows (P = 4, HPC 1) at G=128
+    (16, 4, 128, [2500, 128, 900], 128, 128),  # GQA 4 at G=128 (HPC 2, D=128)
+    # many one-unit items ahead of long ones (~15 items per CTA): a parity warpgroup of the
+    # CTA at the boundary sees a run of items that never reach its parity, then a long item
+    # (TMEM ring phases, HPC 1)
+    (8, 8, 128, [100] * 200 + [6000, 700], 128, 64),
+    (4, 4, 256, [90] * 300 + [4000], 128, 32),
+    (8, 8, 128, [120] * 200 + [6000], 128, 128),
     (8, 2, 128, [1024, 513], 64, 32),      # n=64, G=32
     (8, 2, 128, [2048], 128, 128),         # G=128
     (8, 2, 128, [1300], 100, 96),          # n < 128, G not a power of two

@@ -13,10 +13,12 @@ SHAPES = {  # Hq, Hkv, D, lengths, tp
     "qwen-tp8": (16, 2, 256, [131072], 8),
     "mha": (32, 32, 128, [32768] * 4, 1),
     "mha256": (16, 16, 256, [65536] * 2, 1),
+    "gqa2": (32, 16, 128, [32768] * 4, 1),
+    "mixed": (32, 32, 128, [100] * 2000 + [65536], 1),
 }
 Hq, Hkv, D, L, tp = SHAPES[os.environ.get("SHAPE", "llama")]
 sb = make_batch(L, Hq, Hkv, D, 64, regime=os.environ.get("REGIME", "planted"), seed=1, device="cuda", with_v=False)
-cfg = up.ScoreConfig(); h = up.HeadLayout(Hq, Hkv, D)
+cfg = up.ScoreConfig(block_size_g=int(os.environ.get("G", "64")), query_window_n=int(os.environ.get("NQ", "128"))); h = up.HeadLayout(Hq, Hkv, D)
 run = (lambda: up.score_blocks_tp(sb.q, sb.k, sb.cu_seqlens, cfg, tp, h, out=out)) if tp > 1 else \
       (lambda: up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, cfg, h, out=out))
 out = None
@@ -33,5 +35,5 @@ with torch.cuda.stream(s):
     e0.record(s); g.replay(); e1.record(s)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
-flops = sum(2 * min(128, n) * n * D * Hq for n in L)
+flops = sum(2 * min(cfg.query_window_n, n) * n * D * Hq for n in L)
 print(f"{os.environ.get('SHAPE', 'llama')}: {ms:.4f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
