@@ -456,7 +456,7 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     wp.q_tiles = Tt;
     wp.q_pack = Pk;
     const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
-    const int wgrid = static_cast<int>(wtasks < num_sms() * 8 ? wtasks : num_sms() * 8);
+    const int wgrid = static_cast<int>(wtasks < num_sms() * 16 ? wtasks : num_sms() * 16);
     // CTAs one (request, head-group) pair spans, for equal-length requests
     const int items_est = ranges / (R * nhg > 0 ? R * nhg : 1) + 2;
     if ((e = launch_pair_weights(wp, wgrid, items_est, stream)) != cudaSuccess) return UP_ERR_CUDA;

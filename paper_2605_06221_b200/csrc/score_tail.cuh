@@ -17,7 +17,7 @@ namespace up {
 // denominators.  One CTA per (pair, head, 32-row chunk): warp w folds items w, w+W, ...
 // (lane = row, coalesced; 4 items' loads in flight per warp), the W partial (M, L) are
 // merged in warp order (deterministic), then the warps write the weights.
-constexpr int kPwWarps = 32;
+constexpr int kPwWarps = 16;  // 512 threads: 128 registers, no spills in the warp path
 
 
 // Pair weights for tasks t0, t0 + tstep, ... (task = (pair, head, 32-row chunk)); every
@@ -28,8 +28,15 @@ constexpr int kPwWarps = 32;
 // request spread over 148 items).
 constexpr int kPwMaxRanges = 1024;
 
+// Pairs that span at most kPwWarpItems scorer CTAs (short requests: one item) are done by
+// one warp per task with no CTA barriers, in the same arithmetic as the CTA path (each
+// item's rows folded from (-inf, 0), the item partials merged in item order); the CTA path
+// is left to pairs spread over many CTAs (measured: 2000 requests of 100 tokens, LLaMA
+// layout, spent ~1 ms in per-task CTA barriers).
+constexpr int kPwWarpItems = 2;
+
 __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int64_t t0, int64_t tstep, int nwarps,
-                                                 float (*sM)[32], float (*sL)[32], int64_t* rb) {
+                                                 float* sM, float* sL, int64_t* rb) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int R = p.num_requests, hpc = p.hpc, nhg = p.num_hgroups, npar = p.npar;
     Part P;
@@ -42,19 +49,111 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
     for (int c = threadIdx.x; c <= P.grid; c += blockDim.x) rb[c] = range_begin(P, c);
     __syncthreads();
     const int64_t tasks = static_cast<int64_t>(R) * nhg * hpc * 4;
-    for (int64_t t = t0; t < tasks; t += tstep) {
+    // ---- warp path: pairs spanning <= kPwWarpItems CTAs.  Warp task = one pair: its index
+    // chain once, then its hpc * 4 (head, 32-row chunk) sub-tasks two at a time (both
+    // sub-tasks' statistics loads in flight together).
+    if (warp < nwarps) {
+        const int64_t pairs = static_cast<int64_t>(R) * nhg;
+        for (int64_t pr = t0 * nwarps + warp; pr < pairs; pr += tstep * nwarps) {
+            const int r = static_cast<int>(pr / nhg), hg = static_cast<int>(pr - static_cast<int64_t>(r) * nhg);
+            const int units_r = p.cu_units[r + 1] - p.cu_units[r];
+            if (units_r == 0) continue;
+            const int64_t seg_start = static_cast<int64_t>(p.cu_units[r]) * nhg + static_cast<int64_t>(hg) * units_r;
+            const int c_first = cta_of(P, seg_start);
+            const int n_items = cta_of(P, seg_start + units_r - 1) - c_first + 1;
+            if (n_items > kPwWarpItems) continue;  // the CTA path below
+            const int N = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
+            const int neff = min(p.query_window_n, N);
+            int64_t sid[kPwWarpItems];
+#pragma unroll
+            for (int k = 0; k < kPwWarpItems; ++k) {
+                sid[k] = -1;
+                if (k < n_items) {
+                    const int64_t b = rb[c_first + k];
+                    sid[k] = (k > 0 && b == rb[c_first + k + 1]) ? -1 : (b > seg_start ? b : seg_start);
+                }
+            }
+#pragma unroll 1
+            for (int st = 0; st < hpc * 4; st += 2) {
+                float mc[2][kPwWarpItems * 4], lc[2][kPwWarpItems * 4];
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    const int hh = (st + x) >> 2, j = ((st + x) & 3) * 32 + lane;
+#pragma unroll
+                    for (int y = 0; y < kPwWarpItems * 4; ++y) {
+                        const int k = y >> 2, q = y & 3;
+                        const bool on = sid[k] >= 0 && q < npar;
+                        const int64_t xx = ((sid[k] * hpc + hh) * npar + q) * kRows + j;
+                        mc[x][y] = on ? __ldcg(&p.stat_m[xx]) : -INFINITY;
+                        lc[x][y] = on ? __ldcg(&p.stat_l[xx]) : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    const int hh = (st + x) >> 2, j = ((st + x) & 3) * 32 + lane;
+                    // each item's rows folded from (-inf, 0), then the items in order: the
+                    // CTA path's arithmetic (one item per warp, warp partials in order)
+                    float M = -INFINITY, L = 0.f;
+#pragma unroll
+                    for (int k = 0; k < kPwWarpItems; ++k) {
+                        float Mk = -INFINITY, Lk = 0.f;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) lse_merge(Mk, Lk, mc[x][k * 4 + q], lc[x][k * 4 + q]);
+                        lse_merge(M, L, Mk, Lk);
+                    }
+                    const int tile = p.q_tiles > 1 ? static_cast<int>((static_cast<int64_t>(hg) * hpc + hh) % p.q_tiles) : 0;
+                    const int jr = p.q_pack > 1 ? j % (kRows / p.q_pack) : tile * kRows + j;  // window row
+                    const bool valid = jr < neff;
+                    if (valid && !(L > 0.f)) raise_error(p.err, kErrMaskedRow);
+                    const float inv = valid && L > 0.f ? 1.f / (L * static_cast<float>(neff)) : 0.f;
+#pragma unroll
+                    for (int y = 0; y < kPwWarpItems * 4; ++y) {
+                        const int k = y >> 2, q = y & 3;
+                        if (sid[k] >= 0 && q < npar)
+                            p.stat_w[((sid[k] * hpc + hh) * npar + q) * kRows + j] =
+                                mc[x][y] != -INFINITY ? ex2_approx(mc[x][y] - M) * inv : 0.f;
+                    }
+                }
+            }
+        }
+    }
+    // ---- CTA path: pairs spread over many CTAs.  With many pairs (continuous batches of
+    // short requests) the tasks are enumerated by candidate instead of by pair: a pair
+    // spread over several CTAs holds the first unit of the range of every CTA after its
+    // first, so the candidates are the pairs holding rb[c] (c < score_grid), each taken at
+    // its smallest c -- grid * hpc * 4 tasks instead of a walk over every pair.
+    const int64_t ctasks = static_cast<int64_t>(P.grid) * hpc * 4;
+    const bool by_pair = tasks <= ctasks;
+    const int64_t ntasks = by_pair ? tasks : ctasks;
+    for (int64_t t = t0; t < ntasks; t += tstep) {
         const int chunk = static_cast<int>(t & 3);
         const int hh = static_cast<int>((t >> 2) % hpc);
-        const int64_t pair = (t >> 2) / hpc;
-        const int r = static_cast<int>(pair / nhg), hg = static_cast<int>(pair - static_cast<int64_t>(r) * nhg);
-        const int units_r = p.cu_units[r + 1] - p.cu_units[r];
-        if (units_r == 0) continue;  // block-uniform
+        int r, hg, units_r;
+        int64_t seg_start;
+        if (by_pair) {
+            const int64_t pair = (t >> 2) / hpc;
+            r = static_cast<int>(pair / nhg);
+            hg = static_cast<int>(pair - static_cast<int64_t>(r) * nhg);
+            units_r = p.cu_units[r + 1] - p.cu_units[r];
+            if (units_r == 0) continue;  // CTA-uniform
+            seg_start = static_cast<int64_t>(p.cu_units[r]) * nhg + static_cast<int64_t>(hg) * units_r;
+        } else {
+            const int cand = static_cast<int>((t >> 2) / hpc);
+            const int64_t pos = rb[cand];
+            if (pos >= P.U) continue;  // CTA-uniform
+            const Item at = make_item(P, pos, P.U);
+            r = at.r;
+            hg = at.hg;
+            units_r = at.units_r;
+            seg_start = at.seg_start;
+            if (cand > 0 && rb[cand - 1] >= seg_start) continue;  // not the pair's first candidate
+        }
         const int N = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
         const int neff = min(p.query_window_n, N);
-        const int64_t seg_start = static_cast<int64_t>(p.cu_units[r]) * nhg + static_cast<int64_t>(hg) * units_r;
         const int64_t seg_end = seg_start + units_r;
         const int c_first = cta_of(P, seg_start);
         const int n_items = cta_of(P, seg_end - 1) - c_first + 1;  // CTAs spanned
+        if (n_items <= kPwWarpItems) continue;  // done by the warp path (CTA-uniform)
         const int j = chunk * 32 + lane;
         // Item k = the part of the pair in CTA c_first + k; CTAs with empty ranges (more
         // CTAs than units) hold no item.
@@ -92,20 +191,20 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
             for (int y = 0; y < KB * 4; ++y) lse_merge(M, L, mc[y], lc[y]);
         }
         if (warp < nwarps) {
-            sM[warp][lane] = M;
-            sL[warp][lane] = L;
+            sM[warp * 32 + lane] = M;
+            sL[warp * 32 + lane] = L;
         }
         __syncthreads();
         if (warp == 0) {  // one warp merges the warp partials (in warp order) for every warp
             M = -INFINITY;
             L = 0.f;
-            for (int w = 0; w < nwarps; ++w) lse_merge(M, L, sM[w][lane], sL[w][lane]);
-            sM[0][lane] = M;
-            sL[0][lane] = L;
+            for (int w = 0; w < nwarps; ++w) lse_merge(M, L, sM[w * 32 + lane], sL[w * 32 + lane]);
+            sM[lane] = M;
+            sL[lane] = L;
         }
         __syncthreads();
-        M = sM[0][lane];
-        L = sL[0][lane];
+        M = sM[lane];
+        L = sL[lane];
         __syncthreads();  // sM / sL are rewritten by the next task
         // row j of this virtual head's query tile is window row 128 t + j
         const int tile = p.q_tiles > 1 ? static_cast<int>((static_cast<int64_t>(hg) * hpc + hh) % p.q_tiles) : 0;

@@ -392,16 +392,20 @@ __global__ void __launch_bounds__(kPwWarps * 32)
 pair_weights_kernel(const PairWeightsParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
-    __shared__ float sM[kPwWarps][32], sL[kPwWarps][32];
-    __shared__ int64_t rb[kPwMaxRanges + 1];
-    pair_weights_run(p, blockIdx.x, gridDim.x, blockDim.x >> 5, sM, sL, rb);
+    // dynamic shared memory: rb[score_grid + 1], then sM / sL [warps][32]
+    extern __shared__ __align__(16) unsigned char pw_smem[];
+    const int nw = blockDim.x >> 5;
+    int64_t* rb = reinterpret_cast<int64_t*>(pw_smem);
+    float* sM = reinterpret_cast<float*>(rb + p.score_grid + 1);
+    pair_weights_run(p, blockIdx.x, gridDim.x, nw, sM, sM + nw * 32, rb);
 }
 
 // items_per_pair: the launcher's estimate of the CTAs one pair spans (sizes the CTA).
 cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream) {
     int warps = 2;
     while (warps < kPwWarps && 4 * warps < items_per_pair) warps *= 2;  // 4 items per warp step
-    return launch_k(kPdlScore, pair_weights_kernel, grid, warps * 32, 0, stream, p);
+    const size_t smem = sizeof(int64_t) * (p.score_grid + 1) + sizeof(float) * 2 * warps * 32;
+    return launch_k(kPdlScore, pair_weights_kernel, grid, warps * 32, smem, stream, p);
 }
 
 __global__ void __launch_bounds__(256)

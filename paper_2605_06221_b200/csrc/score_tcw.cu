@@ -108,6 +108,19 @@ static __device__ __noinline__ void rescale_rows_par(float* prow, int g0, int g1
             prow[static_cast<int64_t>(g) * kRows] *= f;
 }
 
+#ifndef UP_TCW_FIRST_REF  // dev A/B: 0 = an item's first subtile tries the fast path and rebases
+#define UP_TCW_FIRST_REF 1
+#endif
+// First reference m of a row: the maximum of the group's valid columns (k <= lim), scaled
+// -- what the overflow rebase from m = -inf produced, without the wasted first pass.
+static __device__ __forceinline__ float first_ref(const uint32_t (&v)[32], int lim, float sc) {
+    float gmax = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        if (k <= lim) gmax = fmaxf(gmax, __uint_as_float(v[k]));
+    return fmaxf(-INFINITY, gmax * sc);
+}
+
 // UP_SCORE_DEBUG phase clocks (second region of the debug buffer): slot k of this CTA
 #define TCW_PHASE(k)                                                                   \
     if (p.dbg != nullptr) {                                                            \
@@ -377,8 +390,9 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                     const uint32_t taddr = tmem_base + lane_base + reg * C::SUBN + 64 * c;
                     float gs0 = 0.f, gs1 = 0.f;
                     bool redo;
-                    if (cb + 64 <= N - neff + 1) {
+                    if (cb + 64 <= N - neff + 1 && !(UP_TCW_FIRST_REF && __any_sync(0xffffffffu, row_valid && m[e] == -INFINITY))) {
                         // whole half inside the segment and left of every row's causal limit
+                        // (and a reference m set: the item's first half goes the generic way)
                         uint32_t va[32], vb[32];
                         tmem_ld32(taddr, va);
                         tmem_ld_wait();
@@ -401,6 +415,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                             tmem_ld32(taddr + q2 * 32, v);
                             tmem_ld_wait();
                             float gs = 0.f;
+                            if (UP_TCW_FIRST_REF && lim >= 0 && m[e] == -INFINITY) m[e] = first_ref(v, lim, sc);
                             if (lim >= 0) {
                                 float a0 = 0.f, a1 = 0.f;
 #pragma unroll
@@ -554,7 +569,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 if constexpr (NPAR == 1 && C::NG == 4) {
                     // Lean fast path: the whole subtile inside the segment and left of every
                     // row's causal limit (warp-uniform), blocks [blk, blk+2) complete here.
-                    if (lean && cbase + C::SUBN <= N - neff + 1) {
+                    if (lean && cbase + C::SUBN <= N - neff + 1 && !(UP_TCW_FIRST_REF && __any_sync(0xffffffffu, row_valid && m == -INFINITY))) {
                         mbar_wait_u32(tfull_addr + reg * 8, (u / NB) & 1);
                         tc_fence_after();
                         const uint32_t taddr = tmem_base + lane_base + C::Q_COLS + reg * C::SUBN;
@@ -596,7 +611,10 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                 // row's causal limit -> two packed group sums and one overflow check.  The
                 // region goes back to the MMA warp after the check, so the generic path can
                 // re-read it.
-                const bool fast = cbase + C::SUBN <= N - neff + 1 && UP_TCW_DIAG != 1;
+                // (an item's first subtile has no reference m yet: the generic path sets it
+                // from the first group's maximum instead of overflowing and rebasing)
+                const bool fast = cbase + C::SUBN <= N - neff + 1 && UP_TCW_DIAG != 1 &&
+                                  !(UP_TCW_FIRST_REF && __any_sync(0xffffffffu, row_valid && m == -INFINITY));
                 float gs0 = 0.f, gs1 = 0.f, gs2 = 0.f, gs3 = 0.f;
                 bool redo = !fast && cbase < N && UP_TCW_DIAG != 1;
                 if (fast) {
@@ -644,6 +662,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                         tmem_ld32(taddr + q2 * 32, v);
                         tmem_ld_wait();
                         float gs = 0.f;
+                        if (UP_TCW_FIRST_REF && lim >= 0 && m == -INFINITY) m = first_ref(v, lim, sc);
                         if (lim >= 0) {
                             float a0 = 0.f, a1 = 0.f;
 #pragma unroll

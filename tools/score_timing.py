@@ -15,6 +15,8 @@ SHAPES = {  # Hq, Hkv, D, lengths, tp
     "mha256": (16, 16, 256, [65536] * 2, 1),
     "gqa2": (32, 16, 128, [32768] * 4, 1),
     "mixed": (32, 32, 128, [100] * 2000 + [65536], 1),
+    "mixed-llama": (32, 8, 128, [100] * 2000 + [65536], 1),
+    "short-mha": (32, 32, 128, [100] * 2000, 1),
 }
 Hq, Hkv, D, L, tp = SHAPES[os.environ.get("SHAPE", "llama")]
 sb = make_batch(L, Hq, Hkv, D, 64, regime=os.environ.get("REGIME", "planted"), seed=1, device="cuda", with_v=False)
