@@ -866,11 +866,21 @@ def run_ours(args):
         comp_bytes = mean_in * 1 + (R + 1) * 4 * 2 + mean_kept * (2 * runner.row_bytes + 4)
         score_ach = flops / (stages["score"] / 1e3) / 1e12
         comp_ach = comp_bytes / (stages["compact"] / 1e3) / 1e9
+        # The scorer's second bound: one exp2 per (row, key, head) logit -- flops / (2 D) --
+        # against MUFU.EX2 at 16 / clk / SM (the epilogue moves part of them to the FMA
+        # pipe at D = 128, so frac may approach or pass 1 without being wrong).
+        f_mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
+        exps = flops / (2 * D)
+        exp_ach = exps / (stages["score"] / 1e3) / 1e9
+        exp_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 16 * f_mhz * 1e6 / 1e9
         stage_info = {
             "score": {"bound": "tensor", "achieved": score_ach, "peak": tf_peak, "unit": "TFLOP/s",
                       "frac": score_ach / tf_peak, "ms_per_layer": stages["score"],
                       "algorithmic_flops_per_layer": flops,
-                      "traffic": prof_traffic("score_tcw")},
+                      "traffic": prof_traffic("score_tcw"),
+                      "exp2": {"bound": "mufu", "achieved": exp_ach, "peak": exp_peak, "unit": "Gexp2/s",
+                               "frac": exp_ach / exp_peak, "exp2_per_layer": exps,
+                               "peak_basis": f"SMs x 16 MUFU.EX2/clk x {f_mhz:.0f} MHz (sampled SM clock)"}},
             "select": {"bound": "latency", "us_per_event": stages["select"] * 1e3, "requests": R},
             "compact": {"bound": "hbm", "achieved": comp_ach, "peak": hbm_peak, "unit": "GB/s",
                         "frac": comp_ach / hbm_peak, "ms_per_layer": stages["compact"],

@@ -132,6 +132,9 @@ compact_index_kernel(const CompactParams p) {
 
 // One warp copies row src_row of plane pl to row dst_row: 16-byte streaming vectors, a
 // batch of 8 in flight per lane (scalar fallbacks for unaligned planes).
+// U = 16-byte vectors per lane in flight per step (the one-launch small-batch kernel uses
+// 16: a whole 8 KB hidden row in one round trip)
+template <int U = 8>
 __device__ __forceinline__ void copy_row_plane(const CompactParams& p, int pl, int64_t src_row, int64_t dst_row,
                                                int lane) {
     {
@@ -144,19 +147,19 @@ __device__ __forceinline__ void copy_row_plane(const CompactParams& p, int pl, i
             int4* d = reinterpret_cast<int4*>(dst);
             const int64_t nv = rb >> 4;
             int64_t v = lane;
-            for (; v + 7 * 32 < nv; v += 8 * 32) {
-                int4 x[8];
+            for (; v + (U - 1) * 32 < nv; v += U * 32) {
+                int4 x[U];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) x[u] = __ldcs(s + v + u * 32);
+                for (int u = 0; u < U; ++u) x[u] = __ldcs(s + v + u * 32);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) __stcs(d + v + u * 32, x[u]);
+                for (int u = 0; u < U; ++u) __stcs(d + v + u * 32, x[u]);
             }
-            int4 x[8];
+            int4 x[U];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < U; ++u)
                 if (v + u * 32 < nv) x[u] = __ldcs(s + v + u * 32);
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < U; ++u)
                 if (v + u * 32 < nv) __stcs(d + v + u * 32, x[u]);
         } else if (((rb | static_cast<int64_t>(align)) & 3) == 0) {
             for (int64_t b = lane * 4; b < rb; b += 32 * 4)
@@ -211,6 +214,9 @@ scatter_rows_kernel(const CompactParams p) {
 // publishes retained_index, cu_seqlens_out and num_out -- then copies its share of the
 // output rows exactly as compact_copy_kernel does.
 constexpr int kSmallCompactRows = 8192;
+#ifndef UP_SMALL_COPY_UNROLL
+#define UP_SMALL_COPY_UNROLL 16
+#endif
 
 __global__ void __launch_bounds__(kCopyThreads)
 compact_small_kernel(const CompactParams p) {
@@ -285,7 +291,7 @@ compact_small_kernel(const CompactParams p) {
     const int nw = (gridDim.x * kCopyThreads) >> 5;
     for (int t = gw; t < carry * p.num_planes; t += nw) {
         const int o = t / p.num_planes;
-        copy_row_plane(p, t - o * p.num_planes, idx[o], o, lane);
+        copy_row_plane<UP_SMALL_COPY_UNROLL>(p, t - o * p.num_planes, idx[o], o, lane);
     }
 }
 

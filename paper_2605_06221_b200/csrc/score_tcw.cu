@@ -133,7 +133,6 @@ template <int D, int HPC, bool SPLIT>
 __global__ void __launch_bounds__(576, 1)
 score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                  const ScoreTcParams p) {
-    pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     using C = TcwCfg<D, HPC, SPLIT>;
     constexpr int NPAR = C::NPAR, NB = C::NB;
@@ -172,6 +171,9 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         prefetch_tensormap(&kmap);
     }
     if (warp == 1) tmem_alloc(misc, 512);
+    // Barrier init, tensor-map prefetch and the TMEM allocation overlap the predecessor's
+    // tail (PDL); everything from the plan on reads its outputs.
+    pdl_wait();
     if (warp == 2) {
         // Plan from cu_seqlens (PackedBatch::validate, scheduler.cpp:33-48).
         bool ok = p.cu_seqlens[0] == 0;

@@ -291,6 +291,12 @@ __device__ __forceinline__ bool crossing_certain(bool reached, int rc, double ra
 // the 512-thread class (<= 2048 blocks) the CUB sort stays: there the select measured slower
 // (1 x 2048 blocks 19.0 vs 20.0 us, the 64-request stream 36.3 vs 41.0 us).
 // -DUP_SELECT_ALWAYS_SORT: always sort (A/B timing).
+// Requests of <= kSelBruteBlocks blocks (C1: 64) rank every block directly (2o in
+// select_radix_kernel).  -DUP_SELECT_BRUTE=0: radix select for them too (A/B).
+constexpr int kSelBruteBlocks = 128;
+#ifndef UP_SELECT_BRUTE
+#define UP_SELECT_BRUTE 1
+#endif
 #ifndef UP_SELECT_RADIX_MAX_THREADS
 #define UP_SELECT_RADIX_MAX_THREADS 128
 #endif
@@ -567,6 +573,46 @@ select_radix_kernel(const SelectParams p) {
     } else {
         SEL_STAMP(1)
         const double p_d = static_cast<double>(p.top_p);
+        // 2o. <= 128 blocks: every block's rank in the sorted order (descending phi, ties by
+        //     ascending block index) and its inclusive mass by a pass over all blocks -- one
+        //     block per thread, no sort, no histogram levels -- under the same
+        //     crossing_certain guard (the masses are summed in block order).
+        if (use_radix_select<THREADS>() && nb <= kSelBruteBlocks && THREADS >= kSelBruteBlocks && UP_SELECT_BRUTE) {
+            uint32_t* s_key = reinterpret_cast<uint32_t*>(&u.sel);
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i)
+                if (val[i] >= 0) s_key[val[i]] = key[i];
+            if (tid == 0) { s_kstar = nb + 1; s_ratio[0] = -1.0; s_ratio[1] = -1.0; }
+            __syncthreads();
+            int rank = 0;
+            double cum = 0.0;
+            if (tid < nb) {
+                const uint32_t kg = s_key[tid];
+                for (int j = 0; j < nb; ++j) {
+                    const uint32_t kj = s_key[j];
+                    const bool before = kj > kg || (kj == kg && j < tid);
+                    rank += before ? 1 : 0;
+                    if (before || j == tid) cum += static_cast<double>(sc[j]);
+                }
+                if (cum / total >= p_d) atomicMin(&s_kstar, rank + 1);
+            }
+            __syncthreads();
+            const int kpar = s_kstar;
+            const bool reached = kpar <= nb;
+            const int rc = reached ? kpar - 1 : nb - 1;
+            if (tid < nb && rank == rc) s_ratio[0] = cum / total;
+            if (tid < nb && rank == rc - 1) s_ratio[1] = cum / total;
+            __syncthreads();
+            if (crossing_certain(reached, rc, s_ratio[0], s_ratio[1], p_d, nb)) {
+                if (tid < nb) blk[tid] = rank < kpar ? 1 : 0;
+                __syncthreads();
+                SEL_STAMP(4)
+                finish_request(p, r, seg0, N, nb, neff, blk, sc, kpar, degenerate, total, red_d, red_i);
+                SEL_STAMP(5)
+                return;
+            }
+            __syncthreads();  // s_key (u) is reused below
+        }
         // 2a. radix select of the crossing key K* and its rank t inside the tie group
         float dsc[ITEMS];
 #pragma unroll
