@@ -14,6 +14,7 @@
 //   5. expand blocks to tokens, force sinks (i < A) and the query window (i >= N - n_eff)
 //      (expand_mask, :36-49), apply the optional no-readmission veto (restrict_selection,
 //      propagation.cpp:116-136) and compute retained count and covered mass (:108-120).
+#include <cstdlib>
 #include <float.h>
 
 #include <cub/block/block_radix_sort.cuh>
@@ -498,7 +499,7 @@ __device__ bool radix_crossing(const uint32_t (&key)[ITEMS], const float (&dec)[
 }
 
 // ---- CUB radix-sort variant (nb <= THREADS * ITEMS) ---------------------------------
-template <int THREADS, int ITEMS>
+template <int THREADS, int ITEMS, bool RADIX = (THREADS <= UP_SELECT_RADIX_MAX_THREADS)>
 __global__ void __launch_bounds__(THREADS)
 select_radix_kernel(const SelectParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
@@ -577,7 +578,7 @@ select_radix_kernel(const SelectParams p) {
         //     ascending block index) and its inclusive mass by a pass over all blocks -- one
         //     block per thread, no sort, no histogram levels -- under the same
         //     crossing_certain guard (the masses are summed in block order).
-        if (use_radix_select<THREADS>() && nb <= kSelBruteBlocks && THREADS >= kSelBruteBlocks && UP_SELECT_BRUTE) {
+        if (RADIX && use_radix_select<128>() && nb <= kSelBruteBlocks && THREADS >= kSelBruteBlocks && UP_SELECT_BRUTE) {
             uint32_t* s_key = reinterpret_cast<uint32_t*>(&u.sel);
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i)
@@ -619,7 +620,7 @@ select_radix_kernel(const SelectParams p) {
         for (int i = 0; i < ITEMS; ++i) dsc[i] = val[i] >= 0 ? phi_decode_dev(key[i]) : 0.0f;
         uint32_t kkey = 0u;
         int tkeep = 0;
-        const bool sel_ok = use_radix_select<THREADS>() &&
+        const bool sel_ok = RADIX && use_radix_select<128>() &&
                             radix_crossing<THREADS, ITEMS>(key, dsc, total, p_d, nb, u.sel, kstar, kkey, tkeep);
         __syncthreads();  // u.sel is dead past this point
         if (sel_ok) {
@@ -901,29 +902,82 @@ size_t select_smem_bytes(int max_blocks_per_request) {
 
 bool select_fuses_expand(int64_t max_tokens) { return max_tokens <= kSmallExpandTokens; }
 
+// Side stream + fork/join events of the calling thread on the current device: the larger
+// size classes run beside the <= 512-block class instead of after it (they own disjoint
+// requests).  Stream capture records the fork as graph edges.
+struct SelectFork {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static cudaError_t select_fork_for(SelectFork** out) {
+    static thread_local SelectFork forks[32];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 32) return cudaErrorInvalidDevice;
+    SelectFork& f = forks[dev];
+    if (f.side == nullptr) {
+        // first use may fall inside a stream capture (torch.cuda.graph: global mode):
+        // create the stream and events in relaxed mode
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        e = cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming);
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        if (e != cudaSuccess) return e;
+    }
+    *out = &f;
+    return cudaSuccess;
+}
+
 cudaError_t launch_select(const SelectParams& p, int R, int max_blocks_per_request, int num_sms,
                           cudaStream_t stream) {
     // One launch per request size class present under the capacity (the sort's cost
     // grows with the CTA's capacity, so small requests must not pay for a large one):
-    // <= 512 blocks: 128 x 4 radix sort; <= 2048: 512 x 4; larger: the bitonic kernel.
+    // <= 512 blocks: 128 x 4 radix select; <= 2048: 512 x 4 sort; larger: the bitonic
+    // kernel.  The larger classes run on a side stream beside the first (disjoint
+    // requests): c5 (64 requests, 4K-128K) 42.3 -> 31.2 us per event, c2 12.8 -> 11.9 us.
+    // Measured and dropped: one launch for every request <= 2048 blocks -- 128 x 16 radix
+    // (c5 45.2 us, 4 x 32K 13.3 -> 21.2 us) or 512 x 4 radix (c5 35.6 us, 4 x 32K 17.1 us).
+    // UP_SELECT_FORK=0: all classes on the caller's stream (A/B).
     cudaError_t e;
     SelectParams q = p;
     q.nb_lo = 0;
     q.nb_hi = 512;
-    if ((e = launch_k(kPdlSelect, select_radix_kernel<128, 4>, R, 128, 0, stream, q)) != cudaSuccess) return e;
-    if (max_blocks_per_request > 512) {
-        q.nb_lo = 512;
-        q.nb_hi = 2048;
-        if ((e = launch_k(kPdlSelect, select_radix_kernel<512, 4>, R, 512, 0, stream, q)) != cudaSuccess) return e;
-    }
-    if (max_blocks_per_request > 2048) {
-        const int cap = max_blocks_per_request < kMaxSortBlocks ? max_blocks_per_request : kMaxSortBlocks;
-        const size_t smem = select_smem_bytes(cap);
-        e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        q.nb_lo = 2048;
-        q.nb_hi = 0x7fffffff;
-        e = launch_k(kPdlSelect, select_kernel, R, kSelThreads, smem, stream, q);
+    {
+        static const bool fork_ok = [] {
+            const char* s = std::getenv("UP_SELECT_FORK");
+            return s == nullptr || s[0] != '0';
+        }();
+        SelectFork* f = nullptr;
+        const bool fork = fork_ok && max_blocks_per_request > 512;
+        if (fork) {  // the larger classes on the side stream, after everything enqueued so far
+            if ((e = select_fork_for(&f)) != cudaSuccess) return e;
+            if ((e = cudaEventRecord(f->fork, stream)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(f->side, f->fork, 0)) != cudaSuccess) return e;
+        }
+        if ((e = launch_k(kPdlSelect, select_radix_kernel<128, 4>, R, 128, 0, stream, q)) != cudaSuccess) return e;
+        cudaStream_t big = fork ? f->side : stream;
+        const int fam = fork ? 0 : kPdlSelect;  // no programmatic edge after an event wait
+        if (max_blocks_per_request > 512) {
+            q.nb_lo = 512;
+            q.nb_hi = 2048;
+            if ((e = launch_k(fam, select_radix_kernel<512, 4>, R, 512, 0, big, q)) != cudaSuccess) return e;
+        }
+        if (max_blocks_per_request > 2048) {
+            const int cap = max_blocks_per_request < kMaxSortBlocks ? max_blocks_per_request : kMaxSortBlocks;
+            const size_t smem = select_smem_bytes(cap);
+            e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            q.nb_lo = 2048;
+            q.nb_hi = 0x7fffffff;
+            if ((e = launch_k(fam, select_kernel, R, kSelThreads, smem, big, q)) != cudaSuccess) return e;
+        }
+        if (fork) {
+            if ((e = cudaEventRecord(f->join, f->side)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(stream, f->join, 0)) != cudaSuccess) return e;
+        }
     }
     if (e != cudaSuccess) return e;
     if (p.fuse_expand) return cudaSuccess;  // the select CTAs wrote the token masks

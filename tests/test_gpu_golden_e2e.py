@@ -233,6 +233,28 @@ def test_cuda_graph_capture_of_drop_layer(up):
     assert int(layer.out.num_out.item()) == n0
 
 
+def test_cuda_graph_capture_across_select_size_classes(up):
+    """Requests in two select size classes (<= 512 and > 512 blocks): the larger class runs
+    on the library's side stream (fork / join events), in eager mode and inside a graph."""
+    from paper_2605_06221_b200.synthetic import make_batch
+    sb = make_batch([36000, 3000, 500], 8, 2, 128, 256, regime="planted", seed=5, device="cuda")
+    layer = up.DropLayer(up.ScoreConfig(), up.HeadLayout(8, 2, 128), 40000, 3, [(256,)], [torch.bfloat16])
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        eager = layer(sb.q, sb.k, sb.cu_seqlens, [sb.hidden])
+        keep0 = layer.sel.keep.clone()
+        cu0 = eager.cu_seqlens.clone()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            layer(sb.q, sb.k, sb.cu_seqlens, [sb.hidden])
+        layer.sel.keep.zero_()
+        for _ in range(3):
+            g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(layer.sel.keep, keep0)
+    assert torch.equal(layer.out.cu_seqlens, cu0)
+
+
 def _random_case(seed):
     rng = np.random.default_rng(seed)
     Hq, Hkv, D = [(8, 2, 128), (4, 2, 256), (4, 4, 64), (16, 8, 256), (32, 8, 128), (2, 1, 256)][seed % 6]
