@@ -150,7 +150,9 @@ up_status up_reduce_block_scores(void* stream, const float* const* shards, int32
 
 /* Top-p keep mask (a9-a13).  block_scores / cu_blocks as produced by up_score_blocks
  * (after any TP reduction).  veto: device uint8[max_tokens] or NULL -- rows that may not
- * be re-admitted.  Writes keep[max_tokens] (1 = retained; pass-through segments all 1). */
+ * be re-admitted.  Writes keep[max_tokens] (1 = retained; pass-through segments all 1).
+ * Stream-ordered: requests of more than 512 blocks are selected on a library-owned side
+ * stream forked from and joined back into `stream` by events (capture-safe). */
 up_status up_select(void* stream, const up_batch* batch, const up_score_config* cfg,
                     const float* block_scores, const int32_t* cu_blocks, const uint8_t* veto,
                     uint8_t* keep, const up_selection_out* out, void* workspace,

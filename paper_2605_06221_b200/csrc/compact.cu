@@ -12,6 +12,7 @@
 //                           loads/stores, a batch of 8 vectors in flight per lane.  Out of
 //                           place: the pre-drop buffer keeps the parked rows
 //                           (propagation.cpp:64-67).
+#include <cstdlib>
 #include "params.cuh"
 
 namespace up {
@@ -223,7 +224,7 @@ compact_small_kernel(const CompactParams p) {
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     constexpr int PER = 16;  // rows per thread per chunk: one 16-byte load of the keep mask
     constexpr int CHUNK = kCopyThreads * PER;
-    __shared__ int32_t idx[kSmallCompactRows];
+    extern __shared__ int32_t idx[];  // [max_tokens] (dynamic: the capacity, <= kSmallCompactRows)
     __shared__ int warp_tot[kCopyThreads / 32];
     const bool lead = blockIdx.x == 0;
     if (!cta_batch_valid(p.cu_seqlens, p.num_requests, p.max_tokens)) {  // empty result, as compact_index
@@ -319,10 +320,14 @@ cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t str
     const int64_t tiles = (p.max_tokens + kCompactTile - 1) / kCompactTile;
     cudaError_t e = cudaSuccess;
     if (compact_is_small(p.max_tokens)) {
+        static const int per_sm = [] {
+            const char* s = std::getenv("UP_SMALL_COMPACT_CTAS_PER_SM");  // dev A/B
+            return s == nullptr ? 4 : std::atoi(s);
+        }();
         int64_t grid = (p.max_tokens * p.num_planes + kCopyThreads / 32 - 1) / (kCopyThreads / 32);  // warp per (row, plane)
-        if (grid > 4LL * num_sms) grid = 4LL * num_sms;
+        if (grid > per_sm * static_cast<int64_t>(num_sms)) grid = per_sm * static_cast<int64_t>(num_sms);
         return launch_k(kPdlCompact, compact_small_kernel, static_cast<unsigned>(grid < 1 ? 1 : grid), kCopyThreads,
-                        0, stream, p);
+                        sizeof(int32_t) * static_cast<size_t>(p.max_tokens), stream, p);
     }
     if (!counts_ready &&
         (e = launch_k(kPdlCompactScan, compact_count_kernel, static_cast<unsigned>(tiles), kCompactThreads, 0, stream, p)) !=

@@ -251,7 +251,8 @@ def test_cuda_graph_capture_across_select_size_classes(up):
         for _ in range(3):
             g.replay()
     torch.cuda.synchronize()
-    assert torch.equal(layer.sel.keep, keep0)
+    T = 36000 + 3000 + 500  # keep past the batch (capacity 40000) is not written
+    assert torch.equal(layer.sel.keep[:T], keep0[:T])
     assert torch.equal(layer.out.cu_seqlens, cu0)
 
 
