@@ -873,6 +873,9 @@ def run_ours(args):
         exps = flops / (2 * D)
         exp_ach = exps / (stages["score"] / 1e3) / 1e9
         exp_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 16 * f_mhz * 1e6 / 1e9
+        # and its third: every shard scored reads its kv-heads' K once (HBM)
+        k_bytes = mean_in * sum(ske - skb for _, (skb, ske) in runner.shards) * D * 2
+        k_ach = k_bytes / (stages["score"] / 1e3) / 1e9
         stage_info = {
             "score": {"bound": "tensor", "achieved": score_ach, "peak": tf_peak, "unit": "TFLOP/s",
                       "frac": score_ach / tf_peak, "ms_per_layer": stages["score"],
@@ -880,7 +883,9 @@ def run_ours(args):
                       "traffic": prof_traffic("score_tcw"),
                       "exp2": {"bound": "mufu", "achieved": exp_ach, "peak": exp_peak, "unit": "Gexp2/s",
                                "frac": exp_ach / exp_peak, "exp2_per_layer": exps,
-                               "peak_basis": f"SMs x 16 MUFU.EX2/clk x {f_mhz:.0f} MHz (sampled SM clock)"}},
+                               "peak_basis": f"SMs x 16 MUFU.EX2/clk x {f_mhz:.0f} MHz (sampled SM clock)"},
+                      "k_stream": {"bound": "hbm", "achieved": k_ach, "peak": hbm_peak, "unit": "GB/s",
+                                   "frac": k_ach / hbm_peak, "k_bytes_per_layer": k_bytes}},
             "select": {"bound": "latency", "us_per_event": stages["select"] * 1e3, "requests": R},
             "compact": {"bound": "hbm", "achieved": comp_ach, "peak": hbm_peak, "unit": "GB/s",
                         "frac": comp_ach / hbm_peak, "ms_per_layer": stages["compact"],

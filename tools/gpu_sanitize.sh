@@ -12,3 +12,4 @@ run $CS --tool memcheck python -m pytest -q -x tests/test_gpu_golden_e2e.py
 run $CS --tool synccheck python -c 'import __graft_entry__ as g; g.smoke()'
 run $CS --tool racecheck python -m pytest -q -x tests/test_gpu_select.py -k "worked or random or varlen or c3_sample"
 run $CS --tool racecheck python -m pytest -q -x tests/test_gpu_compact.py -k small_capacity
+run $CS --tool racecheck python -m pytest -q -x tests/test_gpu_scorer.py -k "many_requests"
