@@ -17,7 +17,7 @@ namespace up {
 // denominators.  One CTA per (pair, head, 32-row chunk): warp w folds items w, w+W, ...
 // (lane = row, coalesced; 4 items' loads in flight per warp), the W partial (M, L) are
 // merged in warp order (deterministic), then the warps write the weights.
-constexpr int kPwWarps = 16;  // 512 threads: 128 registers, no spills in the warp path
+constexpr int kPwWarps = 32;
 
 
 // Pair weights for tasks t0, t0 + tstep, ... (task = (pair, head, 32-row chunk)); every

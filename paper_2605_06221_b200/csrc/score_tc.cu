@@ -388,24 +388,32 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
     }
 }
 
-__global__ void __launch_bounds__(kPwWarps * 32)
+template <int NW>
+__global__ void __launch_bounds__(NW * 32)
 pair_weights_kernel(const PairWeightsParams p) {
     pdl_wait();     // predecessor's outputs are visible past this point
     pdl_trigger();  // let the dependent kernel's CTAs launch while this one runs
     // dynamic shared memory: rb[score_grid + 1], then sM / sL [warps][32]
     extern __shared__ __align__(16) unsigned char pw_smem[];
-    const int nw = blockDim.x >> 5;
     int64_t* rb = reinterpret_cast<int64_t*>(pw_smem);
     float* sM = reinterpret_cast<float*>(rb + p.score_grid + 1);
-    pair_weights_run(p, blockIdx.x, gridDim.x, nw, sM, sM + nw * 32, rb);
+    pair_weights_run(p, blockIdx.x, gridDim.x, NW, sM, sM + NW * 32, rb);
 }
 
-// items_per_pair: the launcher's estimate of the CTAs one pair spans (sizes the CTA).
+// items_per_pair: the launcher's estimate of the CTAs one pair spans (sizes the CTA: 4
+// items per warp step, up to 32 warps -- the register budget follows the CTA size, so the
+// small-CTA variants keep the warp path spill-free).
 cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream) {
     int warps = 2;
-    while (warps < kPwWarps && 4 * warps < items_per_pair) warps *= 2;  // 4 items per warp step
+    while (warps < kPwWarps && 4 * warps < items_per_pair) warps *= 2;
     const size_t smem = sizeof(int64_t) * (p.score_grid + 1) + sizeof(float) * 2 * warps * 32;
-    return launch_k(kPdlScore, pair_weights_kernel, grid, warps * 32, smem, stream, p);
+    switch (warps) {
+        case 2: return launch_k(kPdlScore, pair_weights_kernel<2>, grid, 64, smem, stream, p);
+        case 4: return launch_k(kPdlScore, pair_weights_kernel<4>, grid, 128, smem, stream, p);
+        case 8: return launch_k(kPdlScore, pair_weights_kernel<8>, grid, 256, smem, stream, p);
+        case 16: return launch_k(kPdlScore, pair_weights_kernel<16>, grid, 512, smem, stream, p);
+        default: return launch_k(kPdlScore, pair_weights_kernel<32>, grid, 1024, smem, stream, p);
+    }
 }
 
 __global__ void __launch_bounds__(256)
