@@ -455,6 +455,14 @@ static up_status score_tc_path(cudaStream_t stream, const up_batch* b, const up_
     wp.query_window_n = c->query_window_n;
     wp.q_tiles = Tt;
     wp.q_pack = Pk;
+    {
+        // UP_PW_WARP_ITEMS: test hook -- 0 sends every pair down the CTA path (same arithmetic)
+        static const int wi = [] {
+            const char* e = std::getenv("UP_PW_WARP_ITEMS");
+            return e == nullptr ? kPwWarpItems : std::atoi(e);
+        }();
+        wp.warp_items = wi < 0 ? 0 : (wi > kPwWarpItems ? kPwWarpItems : wi);
+    }
     const int64_t wtasks = static_cast<int64_t>(R) * nhg * hpc * 4;
     const int wgrid = static_cast<int>(wtasks < num_sms() * 16 ? wtasks : num_sms() * 16);
     // CTAs one (request, head-group) pair spans, for equal-length requests

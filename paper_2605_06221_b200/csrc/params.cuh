@@ -42,6 +42,8 @@ struct ScoreTcParams {
     unsigned long long* dbg;  // optional per-CTA timing [grid][4] (UP_SCORE_DEBUG), else null
 };
 
+constexpr int kPwWarpItems = 2;  // pair_weights: warp path for pairs over <= 2 scorer CTAs (score_tail.cuh)
+
 struct PairWeightsParams {
     const int32_t* cu_seqlens;
     const int32_t* cu_units;  // [R+1] from the scorer
@@ -57,6 +59,7 @@ struct PairWeightsParams {
     int32_t query_window_n;
     int32_t q_tiles;          // query tiles per q-head (virtual head = h * q_tiles + t)
     int32_t q_pack;           // q-heads packed per virtual head (row r -> window row r % (128 / q_pack))
+    int32_t warp_items;       // pairs over <= this many scorer CTAs take the warp path (0: none)
 };
 
 struct BlockCombineParams {

@@ -33,7 +33,6 @@ constexpr int kPwMaxRanges = 1024;
 // item's rows folded from (-inf, 0), the item partials merged in item order); the CTA path
 // is left to pairs spread over many CTAs (measured: 2000 requests of 100 tokens, LLaMA
 // layout, spent ~1 ms in per-task CTA barriers).
-constexpr int kPwWarpItems = 2;
 
 __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int64_t t0, int64_t tstep, int nwarps,
                                                  float* sM, float* sL, int64_t* rb) {
@@ -61,7 +60,7 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
             const int64_t seg_start = static_cast<int64_t>(p.cu_units[r]) * nhg + static_cast<int64_t>(hg) * units_r;
             const int c_first = cta_of(P, seg_start);
             const int n_items = cta_of(P, seg_start + units_r - 1) - c_first + 1;
-            if (n_items > kPwWarpItems) continue;  // the CTA path below
+            if (n_items > p.warp_items) continue;  // the CTA path below
             const int N = p.cu_seqlens[r + 1] - p.cu_seqlens[r];
             const int neff = min(p.query_window_n, N);
             int64_t sid[kPwWarpItems];
@@ -123,7 +122,8 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
     // first, so the candidates are the pairs holding rb[c] (c < score_grid), each taken at
     // its smallest c -- grid * hpc * 4 tasks instead of a walk over every pair.
     const int64_t ctasks = static_cast<int64_t>(P.grid) * hpc * 4;
-    const bool by_pair = tasks <= ctasks;
+    // (candidates cover every pair over >= 2 CTAs; pairs inside one CTA need the warp path)
+    const bool by_pair = tasks <= ctasks || p.warp_items < 1;
     const int64_t ntasks = by_pair ? tasks : ctasks;
     for (int64_t t = t0; t < ntasks; t += tstep) {
         const int chunk = static_cast<int>(t & 3);
@@ -153,7 +153,7 @@ __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int
         const int64_t seg_end = seg_start + units_r;
         const int c_first = cta_of(P, seg_start);
         const int n_items = cta_of(P, seg_end - 1) - c_first + 1;  // CTAs spanned
-        if (n_items <= kPwWarpItems) continue;  // done by the warp path (CTA-uniform)
+        if (n_items <= p.warp_items) continue;  // done by the warp path (CTA-uniform)
         const int j = chunk * 32 + lane;
         // Item k = the part of the pair in CTA c_first + k; CTAs with empty ranges (more
         // CTAs than units) hold no item.

@@ -392,3 +392,39 @@ def test_short_query_window_packs_heads_into_one_tile(up):
     assert out.returncode == 0, out.stderr[-2000:]
     assert "pack=1" not in out.stderr and "pack=" in out.stderr
     assert "PACK_BAD []" in out.stdout, out.stdout[-2000:]
+
+
+_PW_CHILD = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2605_06221_b200 as up
+from paper_2605_06221_b200.synthetic import make_batch
+out = []
+for Hq, Hkv, D, lengths in [(32, 8, 128, [100] * 300 + [9000]),     # HPC 4: one-item pairs + a spread pair
+                            (8, 8, 128, [90] * 200 + [130, 5000]),  # HPC 1, four parity rows
+                            (16, 2, 256, [200] * 50 + [3000])]:     # HPC 2 TS
+    sb = make_batch(lengths, Hq, Hkv, D, 64, regime="planted", seed=len(lengths) + D)
+    res = up.score_blocks_varlen(sb.q, sb.k, sb.cu_seqlens, up.ScoreConfig(), up.HeadLayout(Hq, Hkv, D), check=True)
+    torch.cuda.synchronize()
+    out.append(res.block_scores[:int(res.cu_blocks[-1])].cpu().numpy().view(np.uint32))
+np.save(sys.argv[2], np.concatenate(out))
+'''
+
+
+def test_pair_weights_warp_path_is_bitwise_the_cta_path(up, tmp_path):
+    """pair_weights does pairs held by <= 2 scorer CTAs one warp each and wider pairs one
+    CTA each, with the same arithmetic (each item's parity rows folded from (-inf, 0), the
+    items merged in order): block scores are bitwise identical when every pair is forced
+    down the CTA path (UP_PW_WARP_ITEMS=0, child processes: read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    got = {}
+    for wi in ("2", "0"):
+        f = str(tmp_path / f"pw_{wi}.npy")
+        r = subprocess.run([sys.executable, "-c", _PW_CHILD, root, f], capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, UP_PW_WARP_ITEMS=wi))
+        assert r.returncode == 0, r.stderr[-2000:]
+        got[wi] = np.load(f)
+    assert got["2"].size > 0 and np.array_equal(got["2"], got["0"])
