@@ -46,6 +46,9 @@ namespace up {
 #ifndef UP_TCW_LD_PIPE
 #define UP_TCW_LD_PIPE 1
 #endif
+#ifndef UP_TCW_LEAN2  // lean path of the parity epilogues (NPAR > 1, 64-key subtiles, G = 64)
+#define UP_TCW_LEAN2 1
+#endif
 #ifndef UP_TCW_LEAN
 #define UP_TCW_LEAN 1
 #endif
@@ -493,6 +496,8 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
         // addresses held in registers, static block bookkeeping, no per-group branches.
         const uint32_t tfull_addr = smem_u32(t_full), tempty_addr = smem_u32(t_empty);
         const bool lean = NPAR == 1 && C::NG == 4 && G == 64 && UP_TCW_DIAG == 0 && UP_TCW_LEAN;
+        // parity epilogues (HPC 2 / 1): every 64-key subtile is one G = 64 block
+        const bool lean2 = NPAR > 1 && C::NG == 2 && G == 64 && UP_TCW_DIAG == 0 && UP_TCW_LEAN2;
         uint32_t u = 0;
         uint32_t qiter = 0;
         for (int64_t pos = my_begin; pos < my_end;) {
@@ -603,6 +608,34 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                         }
                         // some row must rebase: the general path below redoes this subtile
                         // (its wait returns at once, the region is still held)
+                    }
+                }
+                if constexpr (NPAR > 1 && C::NG == 2) {
+                    // Lean path: the subtile (= block cbase / 64) inside the segment and left of
+                    // every row's causal limit, a reference m set -- two group sums, one vote;
+                    // the same sums the fast path forms ((0 + g0) + g1 = g0 + g1).
+                    if (lean2 && cbase + C::SUBN <= N - neff + 1 &&
+                        !__any_sync(0xffffffffu, row_valid && m == -INFINITY)) {
+                        mbar_wait_u32(tfull_addr + reg * 8, (u / NB) & 1);
+                        tc_fence_after();
+                        const uint32_t taddr = tmem_base + lane_base + C::Q_COLS + reg * C::SUBN;
+                        uint32_t va[32], vb[32];
+                        tmem_ld32(taddr, va);
+                        tmem_ld_wait();
+                        tmem_ld32(taddr + 32, vb);
+                        const float g0 = group_sum_pk<C::NP>(va, pk(sc, sc), pk(-m, -m));
+                        tmem_ld_wait();
+                        const float g1 = group_sum_pk<C::NP>(vb, pk(sc, sc), pk(-m, -m));
+                        const float b0 = g0 + g1;
+                        if (__all_sync(0xffffffffu, !row_valid || b0 <= 0x1p40f)) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_u32(tempty_addr + reg * 8);
+                            Prow[static_cast<int64_t>(cbase >> 6) * kRows] = row_valid ? b0 : 0.f;
+                            l += b0;
+                            continue;
+                        }
+                        // some row must rebase: the general path redoes the subtile
                     }
                 }
                 mbar_wait(&t_full[reg], (u / NB) & 1);
