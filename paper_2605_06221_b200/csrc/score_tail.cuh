@@ -28,11 +28,12 @@ constexpr int kPwWarps = 32;
 // request spread over 148 items).
 constexpr int kPwMaxRanges = 1024;
 
-// Pairs that span at most kPwWarpItems scorer CTAs (short requests: one item) are done by
-// one warp per task with no CTA barriers, in the same arithmetic as the CTA path (each
-// item's rows folded from (-inf, 0), the item partials merged in item order); the CTA path
-// is left to pairs spread over many CTAs (measured: 2000 requests of 100 tokens, LLaMA
-// layout, spent ~1 ms in per-task CTA barriers).
+// Pairs that span at most p.warp_items (kPwWarpItems) scorer CTAs -- short requests: one
+// item -- are done by one warp per pair with no CTA barriers, in the same arithmetic as the
+// CTA path (each item's rows folded from (-inf, 0), the item partials merged in item order;
+// tests/test_gpu_scorer.py checks the two bitwise); the CTA path is left to pairs spread
+// over more CTAs (measured: 2000 requests of 100 tokens, LLaMA layout, spent ~1 ms in
+// per-task CTA barriers; 0.13 ms now).
 
 __device__ __forceinline__ void pair_weights_run(const PairWeightsParams& p, int64_t t0, int64_t tstep, int nwarps,
                                                  float* sM, float* sL, int64_t* rb) {
