@@ -322,7 +322,7 @@ cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t str
     if (compact_is_small(p.max_tokens)) {
         static const int per_sm = [] {
             const char* s = std::getenv("UP_SMALL_COMPACT_CTAS_PER_SM");  // dev A/B
-            return s == nullptr ? 4 : std::atoi(s);
+            return s == nullptr ? 3 : std::atoi(s);  // C1: 2 / 3 / 4 / 6 / 8 -> 8.8 / 8.4 / 10.0 / 10.2 / 11.8 us
         }();
         int64_t grid = (p.max_tokens * p.num_planes + kCopyThreads / 32 - 1) / (kCopyThreads / 32);  // warp per (row, plane)
         if (grid > per_sm * static_cast<int64_t>(num_sms)) grid = per_sm * static_cast<int64_t>(num_sms);
