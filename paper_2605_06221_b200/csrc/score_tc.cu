@@ -29,6 +29,7 @@
 //    statistics become row weights w = 2^(m - M) / (L n_eff), M = max_items m,
 //    L = Σ_items l 2^(m - M);
 //  * block_combine_kernel (score_tail.cuh) -- b_g = (1/|g|) Σ_h Σ_j P[h][g][j] w[item(h,g)][j].
+#include <cstdlib>
 #include "score_tail.cuh"
 #include "peer.cuh"
 
@@ -406,6 +407,11 @@ pair_weights_kernel(const PairWeightsParams p) {
 cudaError_t launch_pair_weights(const PairWeightsParams& p, int grid, int items_per_pair, cudaStream_t stream) {
     int warps = 2;
     while (warps < kPwWarps && 4 * warps < items_per_pair) warps *= 2;
+    static const int force = [] {  // dev A/B: UP_PW_WARPS = 2 / 4 / 8 / 16 / 32
+        const char* e = std::getenv("UP_PW_WARPS");
+        return e == nullptr ? 0 : std::atoi(e);
+    }();
+    if (force == 2 || force == 4 || force == 8 || force == 16 || force == 32) warps = force;
     const size_t smem = sizeof(int64_t) * (p.score_grid + 1) + sizeof(float) * 2 * warps * 32;
     switch (warps) {
         case 2: return launch_k(kPdlScore, pair_weights_kernel<2>, grid, 64, smem, stream, p);
