@@ -565,12 +565,27 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
             const int ushift = tcw_ushift(G);
             const uint32_t u_item0 = u;  // the CTA's subtile counter at this item's first subtile
             int gib = 0, blk = blk0;
+            // This warpgroup's subtiles only (parity of the CTA's subtile counter, see
+            // tcw_par_shift): the first one, then every NPAR-th (pairs: t, t + 1, then
+            // 2 NPAR - 1 on) -- walking and skipping the others cost the NPAR = 4 epilogue
+            // a loop round with a reconvergence point per foreign subtile.
+            // (at D = 256 the strided walk's extra live state costs more spills than the
+            // skips it saves: there the loop visits every subtile and skips; measured MHA
+            // -5.5%, GQA-2 D=128 -6.3%, Gemma / Qwen D=256 +2-3% when strided)
+            constexpr bool kStride = NPAR > 1 && D <= 128;
+            int t = 0;
+            if (kStride) {
+                while (t < 2 * NPAR && (((u_item0 + t) >> ushift) % NPAR) != static_cast<uint32_t>(par)) ++t;
+                u = u_item0 + t;
+            }
+            // step to this warpgroup's next subtile from subtile u
+            auto next_step = [&](uint32_t uu) -> int {
+                return !kStride ? 1 : (ushift == 0 ? NPAR : ((uu & 1u) ? 2 * NPAR - 1 : 1));
+            };
 
 #pragma unroll 1
-            for (int t = 0; t < nsub; ++t, ++u) {
-                // the other warpgroups' subtiles (parity of the CTA's subtile counter, see
-                // tcw_par_shift)
-                if (NPAR > 1 && ((u >> ushift) % NPAR) != static_cast<uint32_t>(par)) continue;
+            for (int st = next_step(u); t < nsub; t += st, u += st, st = next_step(u)) {
+                if (!kStride && NPAR > 1 && ((u >> ushift) % NPAR) != static_cast<uint32_t>(par)) continue;
                 const int cbase = key0 + t * C::SUBN;
                 const uint32_t reg = hh * NB + u % NB;
                 if constexpr (NPAR == 1 && C::NG == 4) {
@@ -769,6 +784,7 @@ score_tcw_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant
                     }
                 }
             }
+            if (kStride) u = u_item0 + nsub;  // the CTA counter past this item (every warpgroup)
             {
                 const int64_t x = (it.sid * (HPC * NPAR) + vh) * kRows + j;
                 p.stat_m[x] = row_valid ? m : -INFINITY;
