@@ -451,7 +451,7 @@ struct StorePeers {
     }
 };
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 block_combine_peer_kernel(const __grid_constant__ BlockCombineParams p, const __grid_constant__ PeerReduceParams pr) {
     pdl_wait();
     __shared__ uint32_t s_epoch;
@@ -558,7 +558,15 @@ cudaError_t launch_block_combine(const BlockCombineParams& p, int grid, int sms,
 
 cudaError_t launch_block_combine_peer(const BlockCombineParams& p, const PeerReduceParams& pr, int grid,
                                       cudaStream_t stream) {
-    return launch_k(kPdlScore, block_combine_peer_kernel, grid, 256, 0, stream, p, pr);
+    // 32 warps per CTA: the grid is one CTA per SM (peer_grid, co-resident for the flag
+    // waits), so more warps put every block of a chunk in flight at once -- c3-rank score
+    // stage 56 -> 51 us against 256 threads (512: 54 us).  UP_PEER_COMBINE_THREADS: A/B.
+    static const int threads = [] {
+        const char* e = std::getenv("UP_PEER_COMBINE_THREADS");
+        const int t = e == nullptr ? 1024 : std::atoi(e);
+        return t == 256 || t == 512 ? t : 1024;
+    }();
+    return launch_k(kPdlScore, block_combine_peer_kernel, grid, threads, 0, stream, p, pr);
 }
 
 }  // namespace up
