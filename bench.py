@@ -907,6 +907,8 @@ def run_ours(args):
         roofline = {"kernel": dominant, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                     "unit": d["unit"], "frac": d["frac"], "traffic": d["traffic"],
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json burst)"}
+        if dominant == "score":  # the scorer's other bounds (stages.score has the details)
+            roofline["also"] = {"mufu_exp2_frac": d["exp2"]["frac"], "k_stream_hbm_frac": d["k_stream"]["frac"]}
         if not runner.local and S == 1:
             stage_info["attention"] = attention_stage(up, runner, sets[0], cu, Hq, D, stream, dev, tf_peak)
             stage_info["attention"]["traffic"] = prof_traffic("attention")
