@@ -54,6 +54,12 @@ def _assert_blocks_close(got, want):
     (8, 8, 128, [100] * 200 + [6000, 700], 128, 64),
     (4, 4, 256, [90] * 300 + [4000], 128, 32),
     (8, 8, 128, [120] * 200 + [6000], 128, 128),
+    # the D <= 128 parity variants walk only their own subtiles (stride NPAR, pairs at
+    # G = 128): GQA-2 and D = 64 with short items ahead of long ones, every G
+    (16, 8, 128, [90] * 150 + [3000, 257], 128, 32),
+    (16, 8, 128, [130] * 120 + [4000], 128, 128),
+    (8, 4, 64, [100] * 100 + [2500], 128, 128),
+    (8, 4, 64, [700, 64, 1900], 128, 64),
     (8, 2, 128, [1024, 513], 64, 32),      # n=64, G=32
     (8, 2, 128, [2048], 128, 128),         # G=128
     (8, 2, 128, [1300], 100, 96),          # n < 128, G not a power of two
