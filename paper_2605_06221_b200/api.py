@@ -284,6 +284,9 @@ def select_varlen(block_scores: torch.Tensor, cu_blocks: torch.Tensor, cu_seqlen
     dev = block_scores.device
     cu = _as_i32_cuda(cu_seqlens, dev)
     R = cu.numel() - 1
+    if max_tokens is None and torch.cuda.is_current_stream_capturing():
+        raise ContractViolation("select_varlen: pass max_tokens (the capacity) when capturing a CUDA graph "
+                                "-- the default reads cu_seqlens[-1] on the host")
     T = int(max_tokens) if max_tokens is not None else int(cu[-1].item())
     en = None if drop_enabled is None else drop_enabled.to(device=dev, dtype=torch.uint8).contiguous()
     b = _batch(cu, T, en)

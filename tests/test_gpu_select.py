@@ -190,6 +190,45 @@ def test_request_beyond_2048_blocks_uses_bitonic_kernel(up, port):
         off += n
 
 
+def test_every_size_class_in_one_batch_eager_and_graph(up, port):
+    """One batch holding every select path: direct ranks (<= 128 blocks), radix select
+    (<= 512), the 512-thread sort (<= 2048, side stream) and the bitonic kernel (> 2048,
+    side stream), plus a single-token request -- bit-exact with the reference eagerly and
+    replayed from a CUDA graph (the side stream's fork / join captured as graph edges)."""
+    rng = np.random.default_rng(33)
+    lengths = [150000, 60000, 20000, 3000, 100, 1]
+    G = 64
+    nbs = [(n + G - 1) // G for n in lengths]
+    scores = (rng.random(sum(nbs)) ** 7).astype(np.float32)
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(lengths)]), dtype=torch.int32, device="cuda")
+    cub = torch.tensor(np.concatenate([[0], np.cumsum(nbs)]), dtype=torch.int32, device="cuda")
+    cfgd = dict(query_window_n=128, block_size_g=G, sink_count_a=128, top_p=0.99)
+    cfg = up.ScoreConfig(**cfgd)
+    d_scores = torch.from_numpy(scores).cuda()
+    sel = up.select_varlen(d_scores, cub, cu, cfg, check=True)
+    want_keep = []
+    for r, n in enumerate(lengths):
+        w = port.top_p_select(scores[sum(nbs[:r]):sum(nbs[:r + 1])], n, **cfgd)
+        want_keep.append(w.keep_mask)
+        assert int(sel.cutoff_rank[r]) == w.cutoff_rank
+    want_keep = np.concatenate(want_keep)
+    T = sum(lengths)
+    assert np.array_equal(sel.keep[:T].cpu().numpy(), want_keep)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        up.select_varlen(d_scores, cub, cu, cfg, out=sel, max_tokens=T)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            with pytest.raises(up.ContractViolation):  # the capacity must come from the caller
+                up.select_varlen(d_scores, cub, cu, cfg, out=sel)
+            up.select_varlen(d_scores, cub, cu, cfg, out=sel, max_tokens=T)
+        sel.keep.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(sel.keep[:T].cpu().numpy(), want_keep)
+
+
 def test_maximum_request_size(up, port):
     """The largest request the on-chip sort holds: 2^20 tokens = 16384 blocks of 64 (a 1M
     context), bit-exact with the reference; one block more raises the sticky
